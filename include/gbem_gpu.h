@@ -1,0 +1,152 @@
+/* gbem_gpu.h — C-ABI boundary of the B200-native GBEM hot path.
+ *
+ * Replaces, for the single-dielectric Galerkin path of the reference
+ * (arxiv 2203.11733 code, /root/reference/proj):
+ *   - u_pair_integral            proj/include/gbem/kernels.hpp:270   -> gbem_u_pair_integrals
+ *   - assemble_single            proj/include/gbem/assembly.hpp:82   -> gbem_assemble_single(_dev)
+ *   - cholesky_solve             proj/include/gbem/solver.hpp:24     -> gbem_spd_solve(_dev)
+ *   - net_charges (Q = eps_r*eps0*X*1e-6 summed per net)
+ *                                proj/include/gbem/extraction.hpp:55 -> gbem_net_charges_dev
+ *   - dump_system_matrix layout  proj/include/gbem/extraction.hpp:83 -> gbem_matrix_download
+ *
+ * Plain C types only.  Every function returns a status code:
+ *   GBEM_OK 0, GBEM_EINVAL 1 (ValidationError, exit 1), GBEM_ENUMERIC 2
+ *   (NumericalError, exit 2: non-finite quadrature sample, non-SPD pivot),
+ *   GBEM_ECUDA 3 (CUDA runtime failure / no device).
+ * The message for the last failure of a context is gbem_last_error(ctx).
+ * Errors mirror proj/include/gbem/errors.hpp:10-20.
+ *
+ * Threading: one context per host thread; calls are stream-ordered on the
+ * context's stream and the host-buffer variants block until their results are
+ * in host memory.  No global state besides the per-device constant tables.
+ */
+#ifndef GBEM_GPU_H
+#define GBEM_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GBEM_OK 0
+#define GBEM_EINVAL 1
+#define GBEM_ENUMERIC 2
+#define GBEM_ECUDA 3
+
+typedef struct gbem_ctx gbem_ctx;
+
+/* Panel list in structure-of-arrays form (Rect, geometry.hpp:52-76): panel k lies
+ * in the plane x[axis[k]] == level[k], spanning [a_lo,a_hi] x [b_lo,b_hi] along
+ * the in-plane axes in axis-index order.  All arrays have n entries.  Host or
+ * device pointers depending on the entry point. */
+typedef struct {
+  const uint8_t* axis;
+  const double* level;
+  const double* a_lo;
+  const double* a_hi;
+  const double* b_lo;
+  const double* b_hi;
+} gbem_panels;
+
+/* QuadratureConfig (quadrature.hpp:12-15) for the near-field Romberg path plus
+ * the far-field split.  Zero-initialised fields take the defaults:
+ * rel_tol 1e-8, max_levels 16, near_ratio 0.75 (pairs with gap < near_ratio *
+ * max diameter use the reference's semi-analytic forms; the rest use the
+ * anisotropic tensor-Gauss rule), far_tol 1e-12 (target relative error of the
+ * far-field rule). */
+typedef struct {
+  double rel_tol;
+  int32_t max_levels;
+  double near_ratio;
+  double far_tol;
+} gbem_quad_config;
+
+typedef struct {
+  int64_t pairs_total;       /* unique pairs evaluated, n(n+1)/2 for a matrix */
+  int64_t pairs_coplanar;    /* closed-form coplanar (incl. self) */
+  int64_t pairs_parallel;    /* near offset-parallel, Romberg */
+  int64_t pairs_orthogonal;  /* near orthogonal, Romberg */
+  int64_t pairs_far;         /* anisotropic tensor Gauss */
+  int64_t not_converged;     /* Romberg hit max_levels (QuadStats::converged) */
+  int64_t nonfinite;         /* non-finite integrand samples (NumericalError) */
+  int64_t near_evals;        /* Romberg integrand samples */
+  int64_t far_evals;         /* Gauss kernel evaluations */
+  double far_flops;          /* algorithmic FP64 flops of the far kernel */
+  double ms_classify, ms_far, ms_near, ms_total; /* device time per phase */
+} gbem_assembly_stats;
+
+typedef struct {
+  int64_t n;
+  int64_t nrhs;
+  int64_t bad_pivot;         /* first non-positive pivot row, -1 if none */
+  double max_residual;       /* max over rhs of ||A x - b|| / ||b|| (solver.hpp:17-21) */
+  double ms_factor, ms_solve, ms_residual;
+} gbem_solve_stats;
+
+/* Context on CUDA device `device` (one process per GPU; ranks pick their own). */
+int gbem_ctx_create(int device, gbem_ctx** out);
+void gbem_ctx_destroy(gbem_ctx* ctx);
+const char* gbem_last_error(const gbem_ctx* ctx);
+/* Run subsequent work on an existing cudaStream_t (NULL: the context's own). */
+int gbem_ctx_set_stream(gbem_ctx* ctx, void* cuda_stream);
+/* Number of this library's kernels launched on the context so far. */
+int64_t gbem_ctx_launch_count(const gbem_ctx* ctx);
+
+/* Batched u_pair_integral (kernels.hpp:270): out[k] = U(I_k, J_k), the
+ * unnormalised integral (um^3); converged[k] (may be NULL) the Romberg flag.
+ * Host buffers. */
+int gbem_u_pair_integrals(gbem_ctx* ctx, const gbem_panels* I, const gbem_panels* J,
+                          int64_t npairs, const gbem_quad_config* cfg, double* out,
+                          int32_t* converged, gbem_assembly_stats* stats);
+
+/* assemble_single (assembly.hpp:82): A[i][j] = U_ij / (|I_i||I_j|) for all
+ * i <= j, mirrored.  The matrix stays on the device inside the context (n x n,
+ * leading dimension = n) and feeds gbem_spd_solve; when A_host != NULL the full
+ * symmetric matrix is also copied to A_host (row-major, lda >= n).
+ * P: host arrays. */
+int gbem_assemble_single(gbem_ctx* ctx, const gbem_panels* P, int64_t n,
+                         const gbem_quad_config* cfg, double* A_host, int64_t lda,
+                         gbem_assembly_stats* stats);
+/* Same with device-resident panel arrays; no host synchronisation except to
+ * read back stats when stats != NULL. */
+int gbem_assemble_single_dev(gbem_ctx* ctx, const gbem_panels* P_dev, int64_t n,
+                             const gbem_quad_config* cfg, gbem_assembly_stats* stats);
+/* Assemble only rows [row_begin, row_end) of the upper triangle (row-block
+ * sharding: no communication; rank r owns a work-balanced row range). */
+int gbem_assemble_rows_dev(gbem_ctx* ctx, const gbem_panels* P_dev, int64_t n,
+                           int64_t row_begin, int64_t row_end, const gbem_quad_config* cfg,
+                           gbem_assembly_stats* stats);
+
+/* Copy the assembled (or factored) matrix to the host: row-major, lda >= n. */
+int gbem_matrix_download(gbem_ctx* ctx, double* A_host, int64_t lda);
+/* Upload an arbitrary symmetric matrix (row-major host, lda >= n) as the
+ * context's matrix, for solver tests independent of assembly. */
+int gbem_matrix_upload(gbem_ctx* ctx, const double* A_host, int64_t n, int64_t lda);
+/* Device pointer / leading dimension of the context matrix (column-major). */
+int gbem_matrix_device(gbem_ctx* ctx, double** A_dev, int64_t* n, int64_t* lda);
+
+/* cholesky_solve (solver.hpp:24) for nrhs right-hand sides: blocked Cholesky of
+ * the context matrix with a DMMA trailing update, then two triangular solves.
+ * B, X: host, column by column (B[r*n + i]).  resid (may be NULL) receives
+ * ||A x_r - b_r|| / ||b_r|| recomputed from the original matrix.
+ * Non-SPD: GBEM_ENUMERIC, message "matrix not positive definite (pivot at row k)". */
+int gbem_spd_solve(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
+                   gbem_solve_stats* stats);
+/* Device-pointer variant; resid_dev may be NULL. */
+int gbem_spd_solve_dev(gbem_ctx* ctx, const double* B_dev, int64_t nrhs, double* X_dev,
+                       double* resid_dev, gbem_solve_stats* stats);
+
+/* net_charges (extraction.hpp:55-79) for the K-RHS system: with net_of_panel[p]
+ * in [0, K) for conductor panels and -1 otherwise (e.g. grounded outer panels),
+ * C[r*K + k] = scale * sum_{p : net_of_panel[p] == k} X[r*n + p], and
+ * outer[r] (may be NULL) the sum over panels with net -1.  scale = eps_r*eps0*1e-6.
+ * Device pointers. */
+int gbem_net_charges_dev(gbem_ctx* ctx, const int32_t* net_of_panel, int64_t n,
+                         const double* X, int64_t nrhs, int32_t K, double scale, double* C,
+                         double* outer);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

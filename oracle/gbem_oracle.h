@@ -1,0 +1,85 @@
+/* gbem_oracle.h — TEST INFRASTRUCTURE ONLY (never linked into the product).
+ *
+ * Plain-C restatement of the reference GBEM single-layer hot path, used as the
+ * parity checker for the B200 kernels.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it.
+ *
+ * Parity pinned against: the frozen single-layer values of
+ * proj/tests/test_kernels.cpp:166-215, the oracle values of
+ * proj/tests/test_oracle.cpp:60-88, the Romberg/t^4 cases of
+ * proj/tests/test_quadrature.cpp:11-79 and, pair by pair, against the
+ * reference headers themselves compiled into oracle/_ref (see oracle/Makefile).
+ */
+#ifndef GBEM_ORACLE_H
+#define GBEM_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Rect (proj/include/gbem/geometry.hpp:52-76): plane x[axis] == level,
+ * span a / span b along the in-plane axes in axis-index order. */
+typedef struct {
+  int axis;
+  double level;
+  double a0, a1, b0, b1;
+} orc_rect;
+
+/* KernelValue (kernels.hpp:16-20). status: 0 ok, 2 non-finite sample
+ * (the reference throws NumericalError there, quadrature.hpp:34-35,46). */
+typedef struct {
+  double value;
+  int converged;
+  long evals;
+  int status;
+} orc_kv;
+
+/* u_pair_integral (kernels.hpp:270-291) with QuadratureConfig{relTol,maxLevels}
+ * (quadrature.hpp:12-15). */
+orc_kv orc_u_pair_integral(const orc_rect* Ii, const orc_rect* Ij, double rel_tol,
+                           int max_levels);
+
+/* Batched form over pair lists (one thread per pair block when nthreads > 1). */
+int orc_u_pairs(int64_t npairs, const orc_rect* a, const orc_rect* b, double rel_tol,
+                int max_levels, double* out, int* converged, int nthreads);
+
+/* Composite tensor 6-point Gauss (the rule of oracle.hpp:45-81 with the nodes of
+ * quadrature.hpp:116-124) with each panel split sub x sub: the far-field
+ * "truth" of SURVEY §8(c). */
+double orc_gauss_pair(const orc_rect* r1, const orc_rect* r2, int sub);
+
+/* oracle_pair_integral(SingleLayer, ...) restated (oracle.hpp:105-131,191-205). */
+double orc_oracle_pair_integral(const orc_rect* Ii, const orc_rect* Ij, int depth);
+
+/* Gap between the closed world extents (rectDistance, geometry.hpp:79-87) and
+ * diameter (geometry.hpp:73). */
+double orc_rect_distance(const orc_rect* a, const orc_rect* b);
+double orc_rect_diameter(const orc_rect* a);
+
+/* assemble_single (assembly.hpp:82-104) on a panel list: A is n x n row-major,
+ * A[i][j] = A[j][i] = U_ij / (|I_i||I_j|).  Returns 0, or 2 on a non-finite
+ * sample; *all_converged receives the AND of the converged flags. */
+int orc_assemble_single(int64_t n, const orc_rect* p, double rel_tol, int max_levels,
+                        double* A, int* all_converged, int nthreads);
+
+/* cholesky_solve (solver.hpp:24-50) in the reference's loop order, on row-major
+ * A (n x n) for nrhs right-hand sides stored column by column (B[r*n + i]).
+ * Returns 0, 1 on bad dims, 2 with *bad_pivot = k for "matrix not positive
+ * definite (pivot at row k)".  resid[r] = ||A x - b|| / ||b|| (solver.hpp:17-21). */
+int orc_cholesky_solve(int64_t n, const double* A, int64_t nrhs, const double* B, double* X,
+                       double* resid, int64_t* bad_pivot);
+
+/* Romberg / integrateSegment on test integrands (quadrature.hpp:27-113), for the
+ * known-answer cases of test_quadrature.cpp. which: 0 x^2, 1 const 1, 2 log1p,
+ * 3 x (empty interval), 4 sin, 5 1/x, 6 1/sqrt(x), 7 log x, 8 1/sqrt(1-x),
+ * 9 1/sqrt(x)+1/sqrt(1-x), 10 1/sqrt(|x|), 11 x^2 (splits). mode: 0 romberg,
+ * 1 integrateSegment(singA, singB), 2 integrateWithSplits. */
+double orc_quad_test(int which, int mode, double a, double b, int singA, int singB,
+                     int* status, int* converged, long* evals);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,212 @@
+"""ctypes bindings of the native libraries (include/gbem_gpu.h, include/gbem_host.h).
+
+The product path is native only: if a library is missing the import of the
+bound function raises, there is no Python or CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_DIR = Path(__file__).resolve().parent / "lib"
+
+GBEM_OK, GBEM_EINVAL, GBEM_ENUMERIC, GBEM_ECUDA = 0, 1, 2, 3
+
+
+class GbemPanels(C.Structure):
+    _fields_ = [("axis", C.POINTER(C.c_uint8)), ("level", C.POINTER(C.c_double)),
+                ("a_lo", C.POINTER(C.c_double)), ("a_hi", C.POINTER(C.c_double)),
+                ("b_lo", C.POINTER(C.c_double)), ("b_hi", C.POINTER(C.c_double))]
+
+
+class GbemQuadConfig(C.Structure):
+    _fields_ = [("rel_tol", C.c_double), ("max_levels", C.c_int32),
+                ("near_ratio", C.c_double), ("far_tol", C.c_double)]
+
+
+class GbemAssemblyStats(C.Structure):
+    _fields_ = [("pairs_total", C.c_int64), ("pairs_coplanar", C.c_int64),
+                ("pairs_parallel", C.c_int64), ("pairs_orthogonal", C.c_int64),
+                ("pairs_far", C.c_int64), ("not_converged", C.c_int64),
+                ("nonfinite", C.c_int64), ("near_evals", C.c_int64), ("far_evals", C.c_int64),
+                ("far_flops", C.c_double), ("ms_classify", C.c_double), ("ms_far", C.c_double),
+                ("ms_near", C.c_double), ("ms_total", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class GbemSolveStats(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nrhs", C.c_int64), ("bad_pivot", C.c_int64),
+                ("max_residual", C.c_double), ("ms_factor", C.c_double),
+                ("ms_solve", C.c_double), ("ms_residual", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+# (name, restype, argtypes) for every symbol of include/gbem_gpu.h
+_P = C.c_void_p
+GPU_SYMBOLS = [
+    ("gbem_ctx_create", C.c_int, [C.c_int, C.POINTER(_P)]),
+    ("gbem_ctx_destroy", None, [_P]),
+    ("gbem_last_error", C.c_char_p, [_P]),
+    ("gbem_ctx_set_stream", C.c_int, [_P, _P]),
+    ("gbem_ctx_launch_count", C.c_int64, [_P]),
+    ("gbem_u_pair_integrals", C.c_int, [_P, C.POINTER(GbemPanels), C.POINTER(GbemPanels), C.c_int64,
+                                        C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats)]),
+    ("gbem_assemble_single", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, C.POINTER(GbemQuadConfig),
+                                       _P, C.c_int64, C.POINTER(GbemAssemblyStats)]),
+    ("gbem_assemble_single_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, C.POINTER(GbemQuadConfig),
+                                           C.POINTER(GbemAssemblyStats)]),
+    ("gbem_assemble_rows_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, C.c_int64, C.c_int64,
+                                         C.POINTER(GbemQuadConfig), C.POINTER(GbemAssemblyStats)]),
+    ("gbem_matrix_download", C.c_int, [_P, _P, C.c_int64]),
+    ("gbem_matrix_upload", C.c_int, [_P, _P, C.c_int64, C.c_int64]),
+    ("gbem_matrix_device", C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("gbem_spd_solve", C.c_int, [_P, _P, C.c_int64, _P, _P, C.POINTER(GbemSolveStats)]),
+    ("gbem_spd_solve_dev", C.c_int, [_P, _P, C.c_int64, _P, _P, C.POINTER(GbemSolveStats)]),
+    ("gbem_net_charges_dev", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_double, _P, _P]),
+]
+
+_gpu = None
+
+
+def gpu_lib() -> C.CDLL:
+    """Load libgbem_gpu.so (raises if it has not been built)."""
+    global _gpu
+    if _gpu is None:
+        path = LIB_DIR / "libgbem_gpu.so"
+        if not path.exists():
+            raise ImportError(f"{path} missing: run `python -m paper_2203_11733_b200.build`")
+        lib = C.CDLL(str(path))
+        for name, res, args in GPU_SYMBOLS:
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _gpu = lib
+    return _gpu
+
+
+def ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+class PanelArrays:
+    """Contiguous SoA copies of a panel list + the gbem_panels view onto them."""
+
+    def __init__(self, axis, level, a0, a1, b0, b1):
+        self.axis = np.ascontiguousarray(axis, dtype=np.uint8)
+        self.level = np.ascontiguousarray(level, dtype=np.float64)
+        self.a0 = np.ascontiguousarray(a0, dtype=np.float64)
+        self.a1 = np.ascontiguousarray(a1, dtype=np.float64)
+        self.b0 = np.ascontiguousarray(b0, dtype=np.float64)
+        self.b1 = np.ascontiguousarray(b1, dtype=np.float64)
+        self.n = len(self.axis)
+
+    @classmethod
+    def from_matrix(cls, m: np.ndarray) -> "PanelArrays":
+        """m: (n, 6) = axis, level, a0, a1, b0, b1."""
+        m = np.asarray(m, dtype=np.float64)
+        return cls(m[:, 0].astype(np.uint8), m[:, 1], m[:, 2], m[:, 3], m[:, 4], m[:, 5])
+
+    def struct(self) -> GbemPanels:
+        d = C.POINTER(C.c_double)
+        return GbemPanels(self.axis.ctypes.data_as(C.POINTER(C.c_uint8)), self.level.ctypes.data_as(d),
+                          self.a0.ctypes.data_as(d), self.a1.ctypes.data_as(d),
+                          self.b0.ctypes.data_as(d), self.b1.ctypes.data_as(d))
+
+
+class GbemError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class Context:
+    """One gbem_ctx on one CUDA device (one process per GPU)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = gpu_lib()
+        h = _P()
+        rc = self.lib.gbem_ctx_create(device, C.byref(h))
+        self.h = h
+        if rc != GBEM_OK:
+            msg = self.lib.gbem_last_error(h).decode() if h else "context creation failed"
+            if h:
+                self.lib.gbem_ctx_destroy(h)
+            self.h = None
+            raise GbemError(rc, msg)
+
+    def close(self):
+        if self.h:
+            self.lib.gbem_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc: int):
+        if rc != GBEM_OK:
+            raise GbemError(rc, self.lib.gbem_last_error(self.h).decode())
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.gbem_ctx_launch_count(self.h))
+
+    def set_stream(self, stream_handle: int | None):
+        self.check(self.lib.gbem_ctx_set_stream(self.h, _P(stream_handle or 0)))
+
+    @staticmethod
+    def quad(rel_tol=1e-8, max_levels=16, near_ratio=0.75, far_tol=1e-12) -> GbemQuadConfig:
+        return GbemQuadConfig(rel_tol, max_levels, near_ratio, far_tol)
+
+    def u_pair_integrals(self, I: PanelArrays, J: PanelArrays, cfg: GbemQuadConfig | None = None):
+        n = I.n
+        out = np.zeros(n)
+        conv = np.zeros(n, dtype=np.int32)
+        st = GbemAssemblyStats()
+        si, sj = I.struct(), J.struct()
+        rc = self.lib.gbem_u_pair_integrals(self.h, C.byref(si), C.byref(sj), n,
+                                            C.byref(cfg or self.quad()), ptr(out), ptr(conv), C.byref(st))
+        self.check(rc)
+        return out, conv.astype(bool), st
+
+    def assemble_single(self, P: PanelArrays, cfg: GbemQuadConfig | None = None, download: bool = True):
+        n = P.n
+        A = np.empty((n, n)) if download else None
+        st = GbemAssemblyStats()
+        sp = P.struct()
+        rc = self.lib.gbem_assemble_single(self.h, C.byref(sp), n, C.byref(cfg or self.quad()),
+                                           ptr(A) if download else None, n, C.byref(st))
+        self.check(rc)
+        return A, st
+
+    def matrix_upload(self, A: np.ndarray):
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        self.check(self.lib.gbem_matrix_upload(self.h, ptr(A), A.shape[0], A.shape[1]))
+
+    def matrix_download(self, n: int) -> np.ndarray:
+        A = np.empty((n, n))
+        self.check(self.lib.gbem_matrix_download(self.h, ptr(A), n))
+        return A
+
+    def spd_solve(self, B: np.ndarray):
+        """B: (n,) or (n, k) right-hand sides; returns X like B, residuals (k,), stats."""
+        B = np.asarray(B, dtype=np.float64)
+        vec = B.ndim == 1
+        Bc = np.ascontiguousarray((B[:, None] if vec else B).T)  # (k, n) rows = rhs columns
+        k = Bc.shape[0]
+        X = np.zeros_like(Bc)
+        res = np.zeros(k)
+        st = GbemSolveStats()
+        rc = self.lib.gbem_spd_solve(self.h, ptr(Bc), k, ptr(X), ptr(res), C.byref(st))
+        self.check(rc)
+        Xo = X.T
+        return (Xo[:, 0] if vec else np.ascontiguousarray(Xo)), res, st

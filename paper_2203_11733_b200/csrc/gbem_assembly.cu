@@ -1,0 +1,736 @@
+// gbem_assembly.cu — Galerkin single-layer assembly on B200 (sm_100a).
+//
+// Replaces the reference's O(n^2/2) loop over u_pair_integral
+// (proj/include/gbem/assembly.hpp:82-104, kernels.hpp:270-291).  Pipeline per
+// chunk of upper-triangle tiles (32 x 32 pairs each):
+//   1. k_classify<false>: per pair, gap/diameter test and class or far-field
+//      Gauss orders; warp-aggregated (__match_any_sync) histogram over 2^16 keys.
+//   2. k_scan: exclusive scan -> per-key queue segments.
+//   3. k_classify<true>: fill the queue; pairs with equal keys are contiguous, so
+//      every evaluation warp below runs one uniform loop structure.
+//   4. k_far: anisotropic tensor Gauss-Legendre on 1/(4 pi r), one thread per
+//      pair (FP64 pipe: DADD + MUFU.RSQ64H + 4 FP64 ops + DFMA per point).
+//      k_coplanar: the reference's 16-corner closed form, one thread per pair.
+//      k_near_warp: offset-parallel / orthogonal Romberg, one warp per pair.
+//   5. k_symmetrize: mirror the lower triangle into the upper (tiled transpose).
+// The matrix is column-major; entry (row j, col i), i <= j, is written at
+// A[i*lda + j] so consecutive lanes (consecutive j) store contiguously.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "gbem_ctx.cuh"
+#include "gbem_near.cuh"
+
+using namespace gbem_gpu;
+
+namespace gbem_gpu {
+__constant__ double c_gx[kQMax + 1][kQMax];
+__constant__ double c_gw[kQMax + 1][kQMax];
+// c_delta[band][q]: far-field order q suffices along a direction of half-length
+// h when gap >= c_delta[band][q] * h (band 0: far_tol, band 1: far_tol/10 for
+// 0.75 <= gap/diam < 1).  Derived from the Bernstein-ellipse bound of the
+// end-on singularity, rho = 1 + d + sqrt(d (2 + d)), error ~ rho^(-2q);
+// calibrated in tools/calib_far.c.
+__constant__ double c_delta[2][kQMax + 1];
+}  // namespace gbem_gpu
+
+namespace {
+
+enum StatIdx {
+  ST_NONCONV = 0,
+  ST_NONFINITE,
+  ST_NEAR_EVALS,
+  ST_FAR_EVALS,
+  ST_FAR_FLOPS,  // stored as double bits
+  ST_COP,
+  ST_PAR,
+  ST_ORTH,
+  ST_FAR,
+  ST_FIRST_BAD,  // first (i << 32 | j) with a non-finite sample, ~0 if none
+  ST_COUNT
+};
+
+constexpr int kTile = 32;
+constexpr int kClassifyThreads = 256;
+
+// Gauss-Legendre nodes on [-1, 1] by Newton on P_q.
+void legendre_table(double gx[kQMax + 1][kQMax], double gw[kQMax + 1][kQMax]) {
+  for (int q = 0; q <= kQMax; ++q)
+    for (int k = 0; k < kQMax; ++k) gx[q][k] = gw[q][k] = 0.0;
+  for (int q = 1; q <= kQMax; ++q) {
+    for (int i = 0; i < q; ++i) {
+      long double x = cosl(3.14159265358979323846264338327950288L * (i + 0.75L) / (q + 0.5L));
+      long double p0 = 1, p1 = x, dp = 1;
+      for (int it = 0; it < 100; ++it) {
+        p0 = 1;
+        p1 = x;
+        for (int k = 2; k <= q; ++k) {
+          long double p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+          p0 = p1;
+          p1 = p2;
+        }
+        if (q == 1) {
+          p1 = x;
+          p0 = 1;
+        }
+        dp = q * (x * p1 - p0) / (x * x - 1);
+        long double dx = p1 / dp;
+        x -= dx;
+        if (fabsl(dx) < 1e-19L) break;
+      }
+      p0 = 1;
+      p1 = x;
+      for (int k = 2; k <= q; ++k) {
+        long double p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (q == 1) {
+        p1 = x;
+        p0 = 1;
+      }
+      dp = q * (x * p1 - p0) / (x * x - 1);
+      // ascending nodes
+      gx[q][q - 1 - i] = (double)x;
+      gw[q][q - 1 - i] = (double)(2.0L / ((1.0L - x * x) * dp * dp));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- classify
+
+__device__ __forceinline__ int far_order(double gap, double h, int band) {
+#pragma unroll 1
+  for (int q = 1; q < kQMax; ++q)
+    if (gap >= c_delta[band][q] * h) return q;
+  return kQMax;
+}
+
+__device__ __forceinline__ uint32_t classify_pair(const DPanel& A, const DPanel& B, bool same,
+                                                  double near_ratio) {
+  if (same) return kClsCoplanar;
+  double gap = panel_gap(A, B);
+  double la = A.a1 - A.a0, lb = A.b1 - A.b0, lc = B.a1 - B.a0, ld = B.b1 - B.b0;
+  double dm = fmax(hypot(la, lb), hypot(lc, ld));
+  bool same_axis = A.axis == B.axis;
+  if (gap < near_ratio * dm) {
+    if (same_axis) return A.level == B.level ? kClsCoplanar : kClsParallel;
+    return kClsOrthogonal;
+  }
+  int band = gap < dm ? 1 : 0;
+  int qs = far_order(gap, 0.5 * la, band), qt = far_order(gap, 0.5 * lb, band);
+  int qu = far_order(gap, 0.5 * lc, band), qv = far_order(gap, 0.5 * ld, band);
+  return far_key(qs, qt, qu, qv);
+}
+
+// Warp-aggregated append of `key` (one atomic per distinct key in the warp).
+template <bool FILL>
+__device__ __forceinline__ void warp_append(bool valid, uint32_t key, uint32_t i, uint32_t j,
+                                            uint32_t* counts, uint32_t* cursors, uint64_t* queue) {
+  unsigned active = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  unsigned peers = __match_any_sync(active, key);
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(peers) - 1;
+  unsigned rank = __popc(peers & ((1u << lane) - 1u));
+  uint32_t base = 0;
+  if (lane == leader) {
+    if (FILL)
+      base = atomicAdd(&cursors[key], (uint32_t)__popc(peers));
+    else
+      atomicAdd(&counts[key], (uint32_t)__popc(peers));
+  }
+  if (FILL) {
+    base = __shfl_sync(peers, base, leader);
+    queue[base + rank] = pack_entry(i, j, key);
+  }
+}
+
+// One CTA per 32x32 tile of the upper triangle restricted to rows [rb, re).
+// tile_row_off[r] = number of tiles in tile rows before r (relative to bi0).
+template <bool FILL>
+__global__ void __launch_bounds__(kClassifyThreads)
+    k_classify(const DPanel* __restrict__ P, int n, int rb, int re, int bi0, int nbt,
+               const long long* __restrict__ tile_row_off, int nrows_t, long long tile_begin,
+               double near_ratio, uint32_t* counts, uint32_t* cursors, uint64_t* queue) {
+  __shared__ DPanel si[kTile], sj[kTile];
+  long long t = tile_begin + blockIdx.x;
+  // binary search the tile row
+  int lo = 0, hi = nrows_t - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_row_off[mid] <= t)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  int bi = bi0 + lo;
+  int bj = bi + (int)(t - tile_row_off[lo]);
+  int tid = threadIdx.x;
+  if (tid < kTile) {
+    int i = bi * kTile + tid;
+    if (i < n) si[tid] = P[i];
+  } else if (tid < 2 * kTile) {
+    int j = bj * kTile + (tid - kTile);
+    if (j < n) sj[tid - kTile] = P[j];
+  }
+  __syncthreads();
+  int lane = tid & 31, warp = tid >> 5;
+  int j = bj * kTile + lane;
+#pragma unroll 1
+  for (int r = warp; r < kTile; r += kClassifyThreads / 32) {
+    int i = bi * kTile + r;
+    bool valid = i >= rb && i < re && j < n && j >= i;
+    uint32_t key = 0;
+    if (valid) key = classify_pair(si[r], sj[lane], i == j, near_ratio);
+    warp_append<FILL>(valid, key, (uint32_t)i, (uint32_t)j, counts, cursors, queue);
+  }
+}
+
+// Pair-list mode: pair k is (panel k, panel npairs + k).
+template <bool FILL>
+__global__ void __launch_bounds__(256)
+    k_classify_list(const DPanel* __restrict__ P, int npairs, double near_ratio, uint32_t* counts,
+                    uint32_t* cursors, uint64_t* queue) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  bool valid = k < npairs;
+  uint32_t key = 0;
+  if (valid) key = classify_pair(P[k], P[npairs + k], false, near_ratio);
+  warp_append<FILL>(valid, key, (uint32_t)k, (uint32_t)(npairs + k), counts, cursors, queue);
+}
+
+// Exclusive scan of kNumKeys counts (one CTA of 1024 threads, 64 keys each);
+// also seeds the fill cursors and accumulates the class totals into stats.
+__global__ void __launch_bounds__(1024)
+    k_scan(const uint32_t* __restrict__ counts, uint32_t* offsets, uint32_t* cursors,
+           unsigned long long* stats) {
+  __shared__ uint32_t part[1024];
+  int t = threadIdx.x;
+  constexpr int per = kNumKeys / 1024;
+  uint32_t s = 0;
+  for (int k = 0; k < per; ++k) s += counts[t * per + k];
+  part[t] = s;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    uint32_t v = t >= off ? part[t - off] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  uint32_t run = t ? part[t - 1] : 0;
+  for (int k = 0; k < per; ++k) {
+    offsets[t * per + k] = run;
+    cursors[t * per + k] = run;
+    run += counts[t * per + k];
+  }
+  if (t == 1023) offsets[kNumKeys] = run;
+  if (t == 0) {
+    atomicAdd(&stats[ST_COP], (unsigned long long)counts[kClsCoplanar]);
+    atomicAdd(&stats[ST_PAR], (unsigned long long)counts[kClsParallel]);
+    atomicAdd(&stats[ST_ORTH], (unsigned long long)counts[kClsOrthogonal]);
+  }
+  __syncthreads();
+  if (t == 0) {
+    // far total = everything from kFarKeyBase on
+    unsigned long long far = (unsigned long long)(offsets[kNumKeys] - offsets[kFarKeyBase]);
+    atomicAdd(&stats[ST_FAR], far);
+  }
+}
+
+// ---------------------------------------------------------------- evaluation
+
+struct OutSpec {
+  double* A;      // matrix mode (nullptr in list mode)
+  long long lda;
+  double* out;    // list mode: out[i]
+  int32_t* conv;  // list mode converged flags (may be null)
+};
+
+__device__ __forceinline__ double panel_area(const DPanel& p) { return (p.a1 - p.a0) * (p.b1 - p.b0); }
+
+__device__ __forceinline__ void store_value(const OutSpec& o, uint32_t i, uint32_t j, const DPanel& Pi,
+                                            const DPanel& Pj, double U) {
+  if (o.A) {
+    o.A[(long long)i * o.lda + j] = U / (panel_area(Pi) * panel_area(Pj));
+  } else {
+    o.out[i] = U;
+  }
+}
+
+__device__ __forceinline__ double sel3(int k, int ai, double lvl, int kS, double xs, double xt) {
+  return k == ai ? lvl : (k == kS ? xs : xt);
+}
+
+// Anisotropic tensor Gauss over I (orders qs, qt along its in-plane axes) and
+// J (order qu along U, QV along V; V is J's direction with the largest order).
+// Equivalent to gaussPair (oracle.hpp:45-81) with per-direction orders.
+template <int QV>
+__device__ __forceinline__ double far_gauss(const DPanel& I, int qs, int qt, const DPanel& J,
+                                            bool v_is_a, int qu, double& flops) {
+  const int ai = I.axis, aj = J.axis;
+  const int kS = ip0(ai);
+  const double cS = 0.5 * (I.a0 + I.a1), hS = 0.5 * (I.a1 - I.a0);
+  const double cT = 0.5 * (I.b0 + I.b1), hT = 0.5 * (I.b1 - I.b0);
+  int kU, kV;
+  double cU, hU, cV, hV;
+  if (v_is_a) {
+    kV = ip0(aj);
+    cV = 0.5 * (J.a0 + J.a1);
+    hV = 0.5 * (J.a1 - J.a0);
+    kU = ip1(aj);
+    cU = 0.5 * (J.b0 + J.b1);
+    hU = 0.5 * (J.b1 - J.b0);
+  } else {
+    kV = ip1(aj);
+    cV = 0.5 * (J.b0 + J.b1);
+    hV = 0.5 * (J.b1 - J.b0);
+    kU = ip0(aj);
+    cU = 0.5 * (J.a0 + J.a1);
+    hU = 0.5 * (J.a1 - J.a0);
+  }
+  double Qv[QV], Wv[QV];
+#pragma unroll
+  for (int v = 0; v < QV; ++v) {
+    Qv[v] = fma(hV, c_gx[QV][v], cV);
+    Wv[v] = hV * c_gw[QV][v];
+  }
+  double acc = 0.0;
+#pragma unroll 1
+  for (int s = 0; s < qs; ++s) {
+    const double xs = fma(hS, c_gx[qs][s], cS);
+    const double ws = hS * c_gw[qs][s];
+#pragma unroll 1
+    for (int t = 0; t < qt; ++t) {
+      const double xt = fma(hT, c_gx[qt][t], cT);
+      const double wst = ws * (hT * c_gw[qt][t]);
+      const double pz = sel3(aj, ai, I.level, kS, xs, xt) - J.level;
+      const double pu = sel3(kU, ai, I.level, kS, xs, xt);
+      const double pv = sel3(kV, ai, I.level, kS, xs, xt);
+      double dv2[QV];
+#pragma unroll
+      for (int v = 0; v < QV; ++v) {
+        double d = pv - Qv[v];
+        dv2[v] = d * d;
+      }
+      const double pz2 = pz * pz;
+      double inner = 0.0;
+#pragma unroll 2
+      for (int u = 0; u < qu; ++u) {
+        const double du = pu - fma(hU, c_gx[qu][u], cU);
+        const double cu = fma(du, du, pz2);
+        double row = 0.0;
+#pragma unroll
+        for (int v = 0; v < QV; ++v) row = fma(Wv[v], rsq64(cu + dv2[v]), row);
+        inner = fma(hU * c_gw[qu][u], row, inner);
+      }
+      acc = fma(wst, inner, acc);
+    }
+  }
+  const double E = (double)qs * qt * qu * QV;
+  flops += 11.0 * E + 8.0 * qs * qt * qu + (9.0 + 2.0 * QV) * qs * qt + 3.0 * qs + 3.0 * QV + 13.0;
+  return acc / kFourPi;
+}
+
+__device__ double far_dispatch(const DPanel& Pi, const DPanel& Pj, uint32_t key, double& flops) {
+  int q[4] = {(int)(key & 15u), (int)((key >> 4) & 15u), (int)((key >> 8) & 15u), (int)(key >> 12)};
+  // Put the largest order in the compile-time (innermost) direction V of panel J.
+  int mi = max(q[0], q[1]), mj = max(q[2], q[3]);
+  const DPanel* I = &Pi;
+  const DPanel* J = &Pj;
+  int qs = q[0], qt = q[1], qja = q[2], qjb = q[3];
+  if (mi > mj) {
+    I = &Pj;
+    J = &Pi;
+    qs = q[2];
+    qt = q[3];
+    qja = q[0];
+    qjb = q[1];
+  }
+  bool v_is_a = qja > qjb;
+  int QV = v_is_a ? qja : qjb;
+  int qu = v_is_a ? qjb : qja;
+  switch (QV) {
+    case 1: return far_gauss<1>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 2: return far_gauss<2>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 3: return far_gauss<3>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 4: return far_gauss<4>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 5: return far_gauss<5>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 6: return far_gauss<6>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 7: return far_gauss<7>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 8: return far_gauss<8>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 9: return far_gauss<9>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 10: return far_gauss<10>(*I, qs, qt, *J, v_is_a, qu, flops);
+    case 11: return far_gauss<11>(*I, qs, qt, *J, v_is_a, qu, flops);
+    default: return far_gauss<12>(*I, qs, qt, *J, v_is_a, qu, flops);
+  }
+}
+
+__device__ __forceinline__ double warp_reduce_d(double x) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+  return x;
+}
+
+__global__ void __launch_bounds__(256)
+    k_far(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
+          const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats) {
+  const uint32_t begin = offsets[kFarKeyBase], end = offsets[kNumKeys];
+  double flops = 0.0, evals = 0.0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  // Warps walk the queue in 32-entry runs so a warp shares one key.
+  for (uint32_t base = begin + (blockIdx.x * blockDim.x + (threadIdx.x & ~31u)); base < end;
+       base += stride) {
+    uint32_t idx = base + (threadIdx.x & 31u);
+    if (idx < end) {
+      uint64_t e = queue[idx];
+      uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e);
+      DPanel Pi = load_panel(P, i), Pj = load_panel(P, j);
+      double U = far_dispatch(Pi, Pj, key, flops);
+      evals += (double)((key & 15u) * ((key >> 4) & 15u) * ((key >> 8) & 15u) * (key >> 12));
+      store_value(o, i, j, Pi, Pj, U);
+      if (!o.A && o.conv) o.conv[i] = 1;
+    }
+  }
+  flops = warp_reduce_d(flops);
+  evals = warp_reduce_d(evals);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(reinterpret_cast<double*>(&stats[ST_FAR_FLOPS]), flops);
+    atomicAdd(&stats[ST_FAR_EVALS], (unsigned long long)evals);
+  }
+}
+
+__global__ void __launch_bounds__(128)
+    k_coplanar(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
+               const uint32_t* __restrict__ offsets, OutSpec o) {
+  const uint32_t begin = offsets[kClsCoplanar], end = offsets[kClsCoplanar + 1];
+  for (uint32_t idx = begin + blockIdx.x * blockDim.x + threadIdx.x; idx < end;
+       idx += gridDim.x * blockDim.x) {
+    uint64_t e = queue[idx];
+    uint32_t i = entry_i(e), j = entry_j(e);
+    DPanel Pi = load_panel(P, i), Pj = load_panel(P, j);
+    // canonical order (kernels.hpp:273-274) so the value matches the reference's rounding
+    const DPanel& a = d_rect_less(Pj, Pi) ? Pj : Pi;
+    const DPanel& b = d_rect_less(Pj, Pi) ? Pi : Pj;
+    double U = d_u_coplanar(a.a0, a.a1, a.b0, a.b1, b.a0, b.a1, b.b0, b.b1);
+    store_value(o, i, j, Pi, Pj, U);
+    if (!o.A && o.conv) o.conv[i] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(128)
+    k_near_warp(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
+                const uint32_t* __restrict__ offsets, OutSpec o, double rel_tol, int max_levels,
+                unsigned long long* stats) {
+  const uint32_t begin = offsets[kClsParallel], end = offsets[kClsOrthogonal + 1];
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  long long evals = 0;
+  for (uint32_t idx = begin + warp; idx < end; idx += nwarps) {
+    uint64_t e = queue[idx];
+    uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e);
+    DPanel Pi = load_panel(P, i), Pj = load_panel(P, j);
+    bool swap = d_rect_less(Pj, Pi);
+    const DPanel& a = swap ? Pj : Pi;
+    const DPanel& b = swap ? Pi : Pj;
+    WarpQuad st;
+    double U = key == kClsParallel ? warp_u_parallel(a, b, rel_tol, max_levels, lane, st)
+                                   : warp_u_orthogonal(a, b, rel_tol, max_levels, lane, st);
+    evals += st.evals;
+    if (lane == 0) {
+      store_value(o, i, j, Pi, Pj, U);
+      if (!o.A && o.conv) o.conv[i] = st.converged ? 1 : 0;
+      if (!st.converged) atomicAdd(&stats[ST_NONCONV], 1ull);
+      if (st.nonfinite) {
+        atomicAdd(&stats[ST_NONFINITE], 1ull);
+        atomicMin(&stats[ST_FIRST_BAD], ((unsigned long long)i << 32) | j);
+      }
+    }
+  }
+  if (lane == 0) atomicAdd(&stats[ST_NEAR_EVALS], (unsigned long long)evals);
+}
+
+// Mirror A[i*lda + j] (j >= i) into A[j*lda + i] over 32x32 tiles (bi <= bj).
+__global__ void __launch_bounds__(256) k_symmetrize(double* A, long long lda, int n, int nbt) {
+  __shared__ double tile[kTile][kTile + 1];
+  // linear upper-triangle tile index -> (bi, bj)
+  long long t = blockIdx.x;
+  int bi = (int)floor((2.0 * nbt + 1.0 - sqrt((2.0 * nbt + 1.0) * (2.0 * nbt + 1.0) - 8.0 * (double)t)) / 2.0);
+  auto rowoff = [nbt](long long b) { return b * nbt - b * (b - 1) / 2; };
+  while (bi > 0 && rowoff(bi) > t) --bi;
+  while (rowoff(bi + 1) <= t) ++bi;
+  int bj = bi + (int)(t - rowoff(bi));
+  int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < kTile; r += 8) {
+    int i = bi * kTile + r, j = bj * kTile + tx;
+    if (i < n && j < n && j >= i) tile[r][tx] = A[(long long)i * lda + j];
+  }
+  __syncthreads();
+  for (int r = ty; r < kTile; r += 8) {
+    int j = bj * kTile + r, i = bi * kTile + tx;
+    if (i < n && j < n && j > i) A[(long long)j * lda + i] = tile[tx][r];
+  }
+}
+
+__global__ void k_pack_panels(const uint8_t* axis, const double* level, const double* a0,
+                              const double* a1, const double* b0, const double* b1, int n,
+                              DPanel* out) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  DPanel p;
+  p.level = level[k];
+  p.a0 = a0[k];
+  p.a1 = a1[k];
+  p.b0 = b0[k];
+  p.b1 = b1[k];
+  p.axis = axis[k];
+  p.pad = 0;
+  out[k] = p;
+}
+
+int grow(gbem_ctx* ctx, void** p, size_t bytes_needed, int64_t* cap_elems, size_t elem) {
+  if ((size_t)*cap_elems * elem >= bytes_needed && *p) return GBEM_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  cudaError_t e = cudaMalloc(p, bytes_needed);
+  if (e != cudaSuccess) {
+    *cap_elems = 0;
+    return ctx->fail(GBEM_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  *cap_elems = (int64_t)(bytes_needed / elem);
+  return GBEM_OK;
+}
+
+int prepare_work(gbem_ctx* ctx, const gbem_quad_config* cfg_in, gbem_quad_config* cfg) {
+  gbem_quad_config c{};
+  if (cfg_in) c = *cfg_in;
+  if (!(c.rel_tol > 0)) c.rel_tol = 1e-8;
+  if (c.max_levels <= 0) c.max_levels = 16;
+  if (c.max_levels > kRombMax) return ctx->fail(GBEM_EINVAL, "max_levels exceeds 20");
+  if (!(c.near_ratio > 0)) c.near_ratio = 0.75;
+  if (!(c.far_tol > 0)) c.far_tol = 1e-12;
+  *cfg = c;
+  if (!ctx->d_counts) {
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_counts, sizeof(uint32_t) * kNumKeys));
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_offsets, sizeof(uint32_t) * (kNumKeys + 1)));
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_cursors, sizeof(uint32_t) * kNumKeys));
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_stats, sizeof(unsigned long long) * ST_COUNT));
+    GBEM_CUDA(ctx, cudaMallocHost(&ctx->h_stats, sizeof(unsigned long long) * ST_COUNT));
+  }
+  // far-field order thresholds
+  double delta[2][kQMax + 1];
+  for (int band = 0; band < 2; ++band) {
+    double tol = band == 0 ? c.far_tol : 0.1 * c.far_tol;
+    delta[band][0] = 1e300;
+    for (int q = 1; q <= kQMax; ++q) {
+      double rho = std::pow(tol, -1.0 / (2.0 * q));
+      delta[band][q] = 0.5 * (rho + 1.0 / rho) - 1.0;
+    }
+  }
+  GBEM_CUDA(ctx, cudaMemcpyToSymbolAsync(c_delta, delta, sizeof(delta), 0, cudaMemcpyHostToDevice,
+                                         ctx->stream));
+  GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, sizeof(unsigned long long) * ST_COUNT, ctx->stream));
+  // ST_FIRST_BAD starts at ~0 (atomicMin target)
+  GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_stats + ST_FIRST_BAD, 0xFF, sizeof(unsigned long long), ctx->stream));
+  return GBEM_OK;
+}
+
+// Evaluate every queued class for the current chunk.
+int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float* ms_far,
+             float* ms_near) {
+  int sms = ctx->num_sms;
+  cudaEventRecord(ctx->ev[2], ctx->stream);
+  k_far<<<sms * 8, 256, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, ctx->d_stats);
+  GBEM_LAUNCH_CHECK(ctx);
+  cudaEventRecord(ctx->ev[3], ctx->stream);
+  k_coplanar<<<sms * 4, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o);
+  GBEM_LAUNCH_CHECK(ctx);
+  k_near_warp<<<sms * 8, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o,
+                                                cfg.rel_tol, cfg.max_levels, ctx->d_stats);
+  GBEM_LAUNCH_CHECK(ctx);
+  cudaEventRecord(ctx->ev[4], ctx->stream);
+  if (ms_far || ms_near) {
+    GBEM_CUDA(ctx, cudaEventSynchronize(ctx->ev[4]));
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&b, ctx->ev[3], ctx->ev[4]);
+    if (ms_far) *ms_far += a;
+    if (ms_near) *ms_near += b;
+  }
+  return GBEM_OK;
+}
+
+int finish_stats(gbem_ctx* ctx, gbem_assembly_stats* stats, int64_t pairs_total) {
+  GBEM_CUDA(ctx, cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, sizeof(unsigned long long) * ST_COUNT,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const unsigned long long* h = ctx->h_stats;
+  if (stats) {
+    stats->pairs_total = pairs_total;
+    stats->pairs_coplanar = (int64_t)h[ST_COP];
+    stats->pairs_parallel = (int64_t)h[ST_PAR];
+    stats->pairs_orthogonal = (int64_t)h[ST_ORTH];
+    stats->pairs_far = (int64_t)h[ST_FAR];
+    stats->not_converged = (int64_t)h[ST_NONCONV];
+    stats->nonfinite = (int64_t)h[ST_NONFINITE];
+    stats->near_evals = (int64_t)h[ST_NEAR_EVALS];
+    stats->far_evals = (int64_t)h[ST_FAR_EVALS];
+    double f;
+    memcpy(&f, &h[ST_FAR_FLOPS], sizeof(double));
+    stats->far_flops = f;
+  }
+  if (h[ST_NONFINITE]) {
+    unsigned long long b = h[ST_FIRST_BAD];
+    return ctx->fail(GBEM_ENUMERIC, "non-finite integrand sample (pair " +
+                                        std::to_string(b >> 32) + "," +
+                                        std::to_string(b & 0xffffffffull) + ")");
+  }
+  return GBEM_OK;
+}
+
+}  // namespace
+
+int gbem_internal_init_tables(gbem_ctx* ctx) {
+  double gx[kQMax + 1][kQMax], gw[kQMax + 1][kQMax];
+  legendre_table(gx, gw);
+  GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_gx, gx, sizeof(gx)));
+  GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_gw, gw, sizeof(gw)));
+  return GBEM_OK;
+}
+
+int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, bool device_ptrs) {
+  if (n < 0 || n >= (1 << 24)) return ctx->fail(GBEM_EINVAL, "panel count out of range");
+  if (n == 0) return GBEM_OK;
+  if (!P || !P->axis || !P->level || !P->a_lo || !P->a_hi || !P->b_lo || !P->b_hi)
+    return ctx->fail(GBEM_EINVAL, "null panel array");
+  int rc = grow(ctx, (void**)&ctx->d_panels, sizeof(DPanel) * (size_t)n, &ctx->panel_cap, sizeof(DPanel));
+  if (rc) return rc;
+  if (device_ptrs) {
+    k_pack_panels<<<(int)((n + 255) / 256), 256, 0, ctx->stream>>>(P->axis, P->level, P->a_lo, P->a_hi,
+                                                                   P->b_lo, P->b_hi, (int)n, ctx->d_panels);
+    GBEM_LAUNCH_CHECK(ctx);
+    return GBEM_OK;
+  }
+  std::vector<DPanel> h((size_t)n);
+  for (int64_t k = 0; k < n; ++k) {
+    if (P->axis[k] > 2) return ctx->fail(GBEM_EINVAL, "panel axis must be 0, 1 or 2");
+    if (!(P->a_lo[k] < P->a_hi[k]) || !(P->b_lo[k] < P->b_hi[k]))
+      return ctx->fail(GBEM_EINVAL, "panel spans must satisfy lo < hi (panel " + std::to_string(k) + ")");
+    DPanel d;
+    d.level = P->level[k];
+    d.a0 = P->a_lo[k];
+    d.a1 = P->a_hi[k];
+    d.b0 = P->b_lo[k];
+    d.b1 = P->b_hi[k];
+    d.axis = P->axis[k];
+    d.pad = 0;
+    h[(size_t)k] = d;
+  }
+  GBEM_CUDA(ctx, cudaMemcpyAsync(ctx->d_panels, h.data(), sizeof(DPanel) * (size_t)n,
+                                 cudaMemcpyHostToDevice, ctx->stream));
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // h is a stack vector
+  return GBEM_OK;
+}
+
+// Assemble rows [row_begin, row_end) of the upper triangle into ctx->d_A.
+int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,
+                           const gbem_quad_config* cfg_in, gbem_assembly_stats* stats, bool symmetrize) {
+  gbem_quad_config cfg;
+  int rc = prepare_work(ctx, cfg_in, &cfg);
+  if (rc) return rc;
+  if (stats) *stats = gbem_assembly_stats{};
+  if (n == 0) return GBEM_OK;
+  const int nbt = (int)((n + kTile - 1) / kTile);
+  const int bi0 = (int)(row_begin / kTile), bi1 = (int)((row_end - 1) / kTile);
+  const int nrows_t = bi1 - bi0 + 1;
+  std::vector<long long> rowoff((size_t)nrows_t + 1);
+  long long total_tiles = 0;
+  for (int r = 0; r < nrows_t; ++r) {
+    rowoff[(size_t)r] = total_tiles;
+    total_tiles += nbt - (bi0 + r);
+  }
+  rowoff[(size_t)nrows_t] = total_tiles;
+  // queue capacity: 2^27 entries (1 GiB) or what the problem needs
+  long long need = std::min<long long>(total_tiles * kTile * kTile, 1ll << 27);
+  rc = grow(ctx, (void**)&ctx->d_queue, sizeof(uint64_t) * (size_t)need, &ctx->queue_cap, sizeof(uint64_t));
+  if (rc) return rc;
+  long long* d_rowoff = nullptr;
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_rowoff, sizeof(long long) * rowoff.size(), ctx->stream));
+  GBEM_CUDA(ctx, cudaMemcpyAsync(d_rowoff, rowoff.data(), sizeof(long long) * rowoff.size(),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+  OutSpec o{ctx->d_A, (long long)ctx->lda, nullptr, nullptr};
+  const long long tiles_per_chunk = std::max<long long>(1, ctx->queue_cap / (kTile * kTile));
+  float ms_cls = 0, ms_far = 0, ms_near = 0;
+  bool timing = stats != nullptr;
+  cudaEventRecord(ctx->ev[0], ctx->stream);
+  for (long long t0 = 0; t0 < total_tiles; t0 += tiles_per_chunk) {
+    long long nt = std::min(tiles_per_chunk, total_tiles - t0);
+    cudaEventRecord(ctx->ev[5], ctx->stream);
+    GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, ctx->stream));
+    k_classify<false><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
+        ctx->d_panels, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue);
+    GBEM_LAUNCH_CHECK(ctx);
+    k_scan<<<1, 1024, 0, ctx->stream>>>(ctx->d_counts, ctx->d_offsets, ctx->d_cursors, ctx->d_stats);
+    GBEM_LAUNCH_CHECK(ctx);
+    k_classify<true><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
+        ctx->d_panels, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue);
+    GBEM_LAUNCH_CHECK(ctx);
+    cudaEventRecord(ctx->ev[6], ctx->stream);
+    if (timing) {
+      GBEM_CUDA(ctx, cudaEventSynchronize(ctx->ev[6]));
+      float a = 0;
+      cudaEventElapsedTime(&a, ctx->ev[5], ctx->ev[6]);
+      ms_cls += a;
+    }
+    rc = run_eval(ctx, o, cfg, timing ? &ms_far : nullptr, timing ? &ms_near : nullptr);
+    if (rc) return rc;
+  }
+  if (symmetrize) {
+    long long ntiles = (long long)nbt * (nbt + 1) / 2;
+    k_symmetrize<<<(unsigned)ntiles, 256, 0, ctx->stream>>>(ctx->d_A, (long long)ctx->lda, (int)n, nbt);
+    GBEM_LAUNCH_CHECK(ctx);
+  }
+  cudaEventRecord(ctx->ev[1], ctx->stream);
+  GBEM_CUDA(ctx, cudaFreeAsync(d_rowoff, ctx->stream));
+  long long pairs = 0;
+  for (int64_t i = row_begin; i < row_end; ++i) pairs += n - i;
+  if (stats) {
+    rc = finish_stats(ctx, stats, pairs);
+    float tot = 0;
+    cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[1]);
+    stats->ms_classify = ms_cls;
+    stats->ms_far = ms_far;
+    stats->ms_near = ms_near;
+    stats->ms_total = tot;
+    return rc;
+  }
+  return GBEM_OK;
+}
+
+int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_config* cfg_in,
+                            double* d_out, int32_t* d_conv, gbem_assembly_stats* stats) {
+  gbem_quad_config cfg;
+  int rc = prepare_work(ctx, cfg_in, &cfg);
+  if (rc) return rc;
+  if (npairs == 0) return GBEM_OK;
+  if (npairs > (1 << 23)) return ctx->fail(GBEM_EINVAL, "at most 2^23 pairs per call");
+  rc = grow(ctx, (void**)&ctx->d_queue, sizeof(uint64_t) * (size_t)npairs, &ctx->queue_cap, sizeof(uint64_t));
+  if (rc) return rc;
+  GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, ctx->stream));
+  int blocks = (int)((npairs + 255) / 256);
+  k_classify_list<false><<<blocks, 256, 0, ctx->stream>>>(ctx->d_panels, (int)npairs, cfg.near_ratio,
+                                                          ctx->d_counts, ctx->d_cursors, ctx->d_queue);
+  GBEM_LAUNCH_CHECK(ctx);
+  k_scan<<<1, 1024, 0, ctx->stream>>>(ctx->d_counts, ctx->d_offsets, ctx->d_cursors, ctx->d_stats);
+  GBEM_LAUNCH_CHECK(ctx);
+  k_classify_list<true><<<blocks, 256, 0, ctx->stream>>>(ctx->d_panels, (int)npairs, cfg.near_ratio,
+                                                         ctx->d_counts, ctx->d_cursors, ctx->d_queue);
+  GBEM_LAUNCH_CHECK(ctx);
+  OutSpec o{nullptr, 0, d_out, d_conv};
+  rc = run_eval(ctx, o, cfg, nullptr, nullptr);
+  if (rc) return rc;
+  return finish_stats(ctx, stats, npairs);
+}

@@ -1,0 +1,294 @@
+// gbem_capi.cu — the extern "C" boundary declared in include/gbem_gpu.h.
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "gbem_ctx.cuh"
+
+namespace {
+
+int ensure_matrix(gbem_ctx* ctx, int64_t n) {
+  int64_t lda = ((n + 7) / 8) * 8;  // 64-byte columns (cp.async alignment)
+  if (lda == 0) lda = 8;
+  size_t need = (size_t)lda * (size_t)(n > 0 ? n : 1);
+  if (ctx->A_cap < need || !ctx->d_A) {
+    if (ctx->d_A) cudaFree(ctx->d_A);
+    ctx->d_A = nullptr;
+    ctx->A_cap = 0;
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_A, need * sizeof(double)));
+    ctx->A_cap = need;
+  }
+  ctx->n = n;
+  ctx->lda = lda;
+  ctx->factored = false;
+  return GBEM_OK;
+}
+
+__global__ void k_net_charges(const int32_t* net, int n, const double* X, int nrhs, int K, double scale,
+                              double* C, double* outer) {
+  // one CTA per rhs; K <= 1024 accumulators in shared memory (deterministic
+  // per-thread partials folded in a fixed order)
+  extern __shared__ double part[];  // [blockDim.x][K + 1]
+  int r = blockIdx.x;
+  const int W = K + 1;
+  for (int k = 0; k < W; ++k) part[threadIdx.x * W + k] = 0.0;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    int k = net[p];
+    double v = X[(long long)r * n + p];
+    part[threadIdx.x * W + (k >= 0 && k < K ? k : K)] += v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < W; k += blockDim.x) {
+    double s = 0.0;
+    for (int t = 0; t < (int)blockDim.x; ++t) s += part[t * W + k];
+    if (k < K)
+      C[(long long)r * K + k] = scale * s;
+    else if (outer)
+      outer[r] = scale * s;
+  }
+}
+
+}  // namespace
+
+int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n) { return ensure_matrix(ctx, n); }
+
+extern "C" {
+
+int gbem_ctx_create(int device, gbem_ctx** out) {
+  if (!out) return GBEM_EINVAL;
+  *out = nullptr;
+  gbem_ctx* ctx = new (std::nothrow) gbem_ctx();
+  if (!ctx) return GBEM_ECUDA;
+  *out = ctx;  // the caller can read gbem_last_error even when creation fails
+  ctx->device = device;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0 || device < 0 || device >= count) {
+    ctx->err = std::string("no CUDA device available: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "device index out of range");
+    *out = ctx;  // caller can still read the message
+    return GBEM_ECUDA;
+  }
+  GBEM_CUDA(ctx, cudaSetDevice(device));
+  cudaDeviceProp prop;
+  GBEM_CUDA(ctx, cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    ctx->err = "this build targets sm_100a (B200); found compute capability " +
+               std::to_string(prop.major) + "." + std::to_string(prop.minor);
+    *out = ctx;
+    return GBEM_ECUDA;
+  }
+  ctx->num_sms = prop.multiProcessorCount;
+  // the warp-cooperative Romberg keeps two tableau rows per lane on the stack
+  GBEM_CUDA(ctx, cudaDeviceSetLimit(cudaLimitStackSize, 8192));
+  GBEM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  ctx->stream = ctx->own_stream;
+  for (auto& ev : ctx->ev) GBEM_CUDA(ctx, cudaEventCreate(&ev));
+  int rc = gbem_internal_init_tables(ctx);
+  *out = ctx;
+  return rc;
+}
+
+void gbem_ctx_destroy(gbem_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+  if (ctx->stream && ctx->stream != ctx->own_stream) cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->d_panels);
+  cudaFree(ctx->d_A);
+  cudaFree(ctx->d_diag);
+  cudaFree(ctx->d_queue);
+  cudaFree(ctx->d_counts);
+  cudaFree(ctx->d_offsets);
+  cudaFree(ctx->d_cursors);
+  cudaFree(ctx->d_stats);
+  cudaFree(ctx->d_work);
+  cudaFree(ctx->d_info);
+  if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
+  if (ctx->h_info) cudaFreeHost(ctx->h_info);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+const char* gbem_last_error(const gbem_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int gbem_ctx_set_stream(gbem_ctx* ctx, void* stream) {
+  if (!ctx) return GBEM_EINVAL;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  return GBEM_OK;
+}
+
+int64_t gbem_ctx_launch_count(const gbem_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int gbem_u_pair_integrals(gbem_ctx* ctx, const gbem_panels* I, const gbem_panels* J, int64_t npairs,
+                          const gbem_quad_config* cfg, double* out, int32_t* converged,
+                          gbem_assembly_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  if (npairs < 0) return ctx->fail(GBEM_EINVAL, "npairs must be >= 0");
+  if (npairs == 0) return GBEM_OK;
+  if (!I || !J || !out) return ctx->fail(GBEM_EINVAL, "null argument");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  // concatenate I and J into one panel list: pair k = (k, npairs + k)
+  std::vector<uint8_t> ax((size_t)(2 * npairs));
+  std::vector<double> lv((size_t)(2 * npairs)), a0(ax.size()), a1(ax.size()), b0(ax.size()), b1(ax.size());
+  for (int64_t k = 0; k < npairs; ++k) {
+    for (int side = 0; side < 2; ++side) {
+      const gbem_panels* S = side ? J : I;
+      size_t d = (size_t)(side * npairs + k);
+      ax[d] = S->axis[k];
+      lv[d] = S->level[k];
+      a0[d] = S->a_lo[k];
+      a1[d] = S->a_hi[k];
+      b0[d] = S->b_lo[k];
+      b1[d] = S->b_hi[k];
+    }
+  }
+  gbem_panels all{ax.data(), lv.data(), a0.data(), a1.data(), b0.data(), b1.data()};
+  int rc = gbem_internal_upload_panels(ctx, &all, 2 * npairs, false);
+  if (rc) return rc;
+  double* d_out = nullptr;
+  int32_t* d_conv = nullptr;
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_out, sizeof(double) * npairs, ctx->stream));
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_conv, sizeof(int32_t) * npairs, ctx->stream));
+  rc = gbem_internal_pair_list(ctx, npairs, cfg, d_out, d_conv, stats);
+  if (rc == GBEM_OK || rc == GBEM_ENUMERIC) {
+    GBEM_CUDA(ctx, cudaMemcpyAsync(out, d_out, sizeof(double) * npairs, cudaMemcpyDeviceToHost, ctx->stream));
+    if (converged)
+      GBEM_CUDA(ctx, cudaMemcpyAsync(converged, d_conv, sizeof(int32_t) * npairs, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+  }
+  cudaFreeAsync(d_out, ctx->stream);
+  cudaFreeAsync(d_conv, ctx->stream);
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return rc;
+}
+
+int gbem_assemble_single(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const gbem_quad_config* cfg,
+                         double* A_host, int64_t lda, gbem_assembly_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  if (A_host && lda < n) return ctx->fail(GBEM_EINVAL, "lda < n");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int rc = gbem_internal_upload_panels(ctx, P, n, false);
+  if (rc) return rc;
+  rc = ensure_matrix(ctx, n);
+  if (rc) return rc;
+  rc = gbem_internal_assemble(ctx, n, 0, n, cfg, stats, true);
+  if (rc) return rc;
+  if (A_host) return gbem_matrix_download(ctx, A_host, lda);
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GBEM_OK;
+}
+
+int gbem_assemble_single_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const gbem_quad_config* cfg,
+                             gbem_assembly_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int rc = gbem_internal_upload_panels(ctx, P, n, true);
+  if (rc) return rc;
+  rc = ensure_matrix(ctx, n);
+  if (rc) return rc;
+  return gbem_internal_assemble(ctx, n, 0, n, cfg, stats, true);
+}
+
+int gbem_assemble_rows_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, int64_t row_begin, int64_t row_end,
+                           const gbem_quad_config* cfg, gbem_assembly_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  if (row_begin < 0 || row_end > n || row_begin > row_end)
+    return ctx->fail(GBEM_EINVAL, "row range out of bounds");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int rc = gbem_internal_upload_panels(ctx, P, n, true);
+  if (rc) return rc;
+  rc = ensure_matrix(ctx, n);
+  if (rc) return rc;
+  if (row_end == row_begin) return GBEM_OK;
+  return gbem_internal_assemble(ctx, n, row_begin, row_end, cfg, stats, false);
+}
+
+int gbem_matrix_download(gbem_ctx* ctx, double* A_host, int64_t lda) {
+  if (!ctx || !A_host) return GBEM_EINVAL;
+  if (lda < ctx->n) return ctx->fail(GBEM_EINVAL, "lda < n");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  // column-major device == row-major host for the symmetric matrix; a factored
+  // matrix comes back as its column-major lower factor transposed.
+  GBEM_CUDA(ctx, cudaMemcpy2DAsync(A_host, sizeof(double) * lda, ctx->d_A, sizeof(double) * ctx->lda,
+                                   sizeof(double) * ctx->n, ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GBEM_OK;
+}
+
+int gbem_matrix_upload(gbem_ctx* ctx, const double* A_host, int64_t n, int64_t lda) {
+  if (!ctx || (!A_host && n > 0)) return GBEM_EINVAL;
+  if (n < 0 || lda < n) return ctx->fail(GBEM_EINVAL, "bad matrix dimensions");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int rc = ensure_matrix(ctx, n);
+  if (rc) return rc;
+  if (n == 0) return GBEM_OK;
+  // row-major host -> column-major device of the transpose (== A when symmetric)
+  GBEM_CUDA(ctx, cudaMemcpy2DAsync(ctx->d_A, sizeof(double) * ctx->lda, A_host, sizeof(double) * lda,
+                                   sizeof(double) * n, n, cudaMemcpyHostToDevice, ctx->stream));
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GBEM_OK;
+}
+
+int gbem_matrix_device(gbem_ctx* ctx, double** A_dev, int64_t* n, int64_t* lda) {
+  if (!ctx) return GBEM_EINVAL;
+  if (A_dev) *A_dev = ctx->d_A;
+  if (n) *n = ctx->n;
+  if (lda) *lda = ctx->lda;
+  return GBEM_OK;
+}
+
+int gbem_spd_solve(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
+                   gbem_solve_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  if (nrhs < 0) return ctx->fail(GBEM_EINVAL, "cholesky_solve: dimension mismatch");
+  if (nrhs > 0 && (!B || !X)) return ctx->fail(GBEM_EINVAL, "null argument");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int64_t n = ctx->n;
+  size_t cnt = (size_t)n * (size_t)nrhs;
+  double *dB = nullptr, *dX = nullptr, *dR = nullptr;
+  if (cnt) {
+    GBEM_CUDA(ctx, cudaMalloc(&dB, cnt * sizeof(double)));
+    GBEM_CUDA(ctx, cudaMalloc(&dX, cnt * sizeof(double)));
+    GBEM_CUDA(ctx, cudaMalloc(&dR, (size_t)nrhs * sizeof(double)));
+    GBEM_CUDA(ctx, cudaMemcpyAsync(dB, B, cnt * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  int rc = gbem_internal_solve(ctx, dB, nrhs, dX, dR, stats);
+  if (rc == GBEM_OK && cnt) {
+    GBEM_CUDA(ctx, cudaMemcpyAsync(X, dX, cnt * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (resid)
+      GBEM_CUDA(ctx, cudaMemcpyAsync(resid, dR, (size_t)nrhs * sizeof(double), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+  }
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(dB);
+  cudaFree(dX);
+  cudaFree(dR);
+  return rc;
+}
+
+int gbem_spd_solve_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
+                       gbem_solve_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  return gbem_internal_solve(ctx, B, nrhs, X, resid, stats);
+}
+
+int gbem_net_charges_dev(gbem_ctx* ctx, const int32_t* net, int64_t n, const double* X, int64_t nrhs,
+                         int32_t K, double scale, double* C, double* outer) {
+  if (!ctx) return GBEM_EINVAL;
+  if (K < 1 || K > 512 || nrhs < 0) return ctx->fail(GBEM_EINVAL, "net count must be in [1, 512]");
+  if (nrhs == 0 || n == 0) return GBEM_OK;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int threads = 64;
+  size_t smem = sizeof(double) * (size_t)threads * (size_t)(K + 1);
+  if (smem > 200 * 1024) return ctx->fail(GBEM_EINVAL, "too many nets for the charge reduction");
+  if (smem > 48 * 1024)
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_net_charges, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_net_charges<<<(unsigned)nrhs, threads, smem, ctx->stream>>>(net, (int)n, X, (int)nrhs, K, scale, C, outer);
+  GBEM_LAUNCH_CHECK(ctx);
+  return GBEM_OK;
+}
+
+}  // extern "C"

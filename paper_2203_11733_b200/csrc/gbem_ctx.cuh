@@ -1,0 +1,80 @@
+// gbem_ctx.cuh — internal context shared by the assembly, solver and C-ABI units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/gbem_gpu.h"
+#include "gbem_common.cuh"
+
+struct gbem_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;      // active stream
+  cudaStream_t own_stream = nullptr;  // created by the context
+  std::string err;
+  int64_t launches = 0;
+  int num_sms = 148;
+
+  // panels (device, 48-byte records)
+  gbem_gpu::DPanel* d_panels = nullptr;
+  int64_t panel_cap = 0;
+
+  // matrix: column-major n x n with leading dimension lda (symmetric after
+  // assembly; lower triangle overwritten by the Cholesky factor)
+  double* d_A = nullptr;
+  int64_t n = 0, lda = 0;
+  size_t A_cap = 0;  // elements
+  double* d_diag = nullptr;  // original diagonal (kept for residuals after factoring)
+  int64_t diag_cap = 0;
+  bool factored = false;
+
+  // assembly work buffers
+  uint64_t* d_queue = nullptr;
+  int64_t queue_cap = 0;
+  uint32_t* d_counts = nullptr;   // per key
+  uint32_t* d_offsets = nullptr;  // exclusive scan of counts (kNumKeys + 1)
+  uint32_t* d_cursors = nullptr;
+  unsigned long long* d_stats = nullptr;  // device counters (see gbem_assembly.cu)
+  unsigned long long* h_stats = nullptr;  // pinned mirror
+
+  // solver work buffers
+  double* d_work = nullptr;
+  size_t work_cap = 0;  // elements
+  int* d_info = nullptr;
+  int* h_info = nullptr;  // pinned
+
+  cudaEvent_t ev[8] = {};
+
+  int fail(int code, const std::string& msg) {
+    err = msg;
+    return code;
+  }
+};
+
+// Wrap a CUDA runtime call inside a C-ABI entry point.
+#define GBEM_CUDA(ctx, call)                                                              \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return (ctx)->fail(GBEM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define GBEM_LAUNCH_CHECK(ctx)                                                            \
+  do {                                                                                    \
+    (ctx)->launches++;                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess)                                                                \
+      return (ctx)->fail(GBEM_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Internal entry points implemented across the units.
+int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n);
+int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, bool device_ptrs);
+int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,
+                           const gbem_quad_config* cfg, gbem_assembly_stats* stats, bool symmetrize);
+int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_config* cfg,
+                            double* d_out, int32_t* d_conv, gbem_assembly_stats* stats);
+int gbem_internal_init_tables(gbem_ctx* ctx);
+int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X,
+                        double* d_resid, gbem_solve_stats* stats);

@@ -1,0 +1,593 @@
+// gbem_solver.cu — dense SPD solve on B200: blocked right-looking Cholesky with
+// an FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) trailing update, K-RHS
+// triangular solves, residual recomputed from the original matrix.
+//
+// Replaces cholesky_solve + residual_norm (proj/include/gbem/solver.hpp:17-50).
+// Same contract: SPD input, "matrix not positive definite (pivot at row k)" on a
+// non-positive pivot (solver.hpp:31-33), relative residual ||Ax-b||/||b||
+// recomputed from the unfactored matrix (solver.hpp:47).
+//
+// Storage: column-major A (lda), lower triangle overwritten by L; the strict
+// upper triangle is left untouched and the original diagonal is saved, so the
+// residual uses the original A.  Block size NB = 128:
+//   k_potrf_diag  : one CTA factors the NB x NB diagonal block in shared memory
+//                   and forms inv(L11) (kept for the solves);
+//   k_gemm_nt<STORE>: L21 = A21 * inv(L11)^T (trsm as a DMMA GEMM, in place);
+//   k_gemm_nt<SUB>  : A22 -= L21 * L21^T on lower 128x128 tiles (the O(n^3) part).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "gbem_ctx.cuh"
+
+namespace {
+
+constexpr int NB = 128;       // Cholesky block size
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
+constexpr int LDS = BM + 8;   // smem row stride in doubles: conflict-free fragment loads
+constexpr int GEMM_THREADS = 256;
+constexpr size_t GEMM_SMEM = (size_t)STAGES * 2 * BK * LDS * sizeof(double);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+enum GemmMode { kSub = 0, kStore = 1 };
+
+// C (M x N) op= A (M x K) * B (N x K)^T, all column-major.
+//   kSub  : C -= A B^T; tiles restricted to the lower triangle when `lower`
+//           (tile (I,J) with I >= J; diagonal tiles write row >= col only).
+//   kStore: C  = A B^T (C may alias A: each CTA owns full rows, BN >= N).
+// Tile 128 x 128, 8 warps as 4 (M) x 2 (N), warp tile 32 x 64 = 4 x 8 DMMA
+// fragments; BK = 16 slabs through a 3-stage cp.async pipeline.
+template <int MODE>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm_nt(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb,
+              int M, int N, int K, int lower) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                       // [STAGES][BK][LDS]
+  double* Bs = smem + STAGES * BK * LDS;   // [STAGES][BK][LDS]
+  int tm, tn;
+  if (lower) {
+    // linear lower-triangle tile index -> (tm >= tn)
+    long long t = blockIdx.x;
+    int r = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while ((long long)(r + 1) * (r + 2) / 2 <= t) ++r;
+    while ((long long)r * (r + 1) / 2 > t) --r;
+    tm = r;
+    tn = (int)(t - (long long)r * (r + 1) / 2);
+  } else {
+    tm = blockIdx.x;
+    tn = blockIdx.y;
+  }
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  double acc[4][8][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KT = (K + BK - 1) / BK;
+  // each stage: A slab BK x BM (1024 x 16B chunks... 16*128/2 = 1024) and B slab
+  auto load_stage = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    double* as = As + st * BK * LDS;
+    double* bs = Bs + st * BK * LDS;
+#pragma unroll
+    for (int c = tid; c < BK * BM / 2; c += GEMM_THREADS) {
+      int kk = c / (BM / 2), mm = (c % (BM / 2)) * 2;
+      int gk = k0 + kk, gm = m0 + mm;
+      int bytes = 0;
+      const double* src = A;
+      if (gk < K && gm < M) {
+        bytes = gm + 1 < M ? 16 : 8;
+        src = A + (long long)gk * lda + gm;
+      }
+      cp_async16(as + kk * LDS + mm, src, bytes);
+    }
+#pragma unroll
+    for (int c = tid; c < BK * BN / 2; c += GEMM_THREADS) {
+      int kk = c / (BN / 2), nn = (c % (BN / 2)) * 2;
+      int gk = k0 + kk, gn = n0 + nn;
+      int bytes = 0;
+      const double* src = B;
+      if (gk < K && gn < N) {
+        bytes = gn + 1 < N ? 16 : 8;
+        src = B + (long long)gk * ldb + gn;
+      }
+      cp_async16(bs + kk * LDS + nn, src, bytes);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    int nxt = kt + STAGES - 1;
+    if (nxt < KT) load_stage(nxt, nxt % STAGES);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * BK * LDS;
+    const double* bs = Bs + (kt % STAGES) * BK * LDS;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[(kk + t4) * LDS + wm * 32 + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bf[j] = bs[(kk + t4) * LDS + wn * 64 + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: fragment (i,j) holds rows m0+wm*32+i*8+g, cols n0+wn*64+j*8+2*t4+{0,1}
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int row = m0 + wm * 32 + i * 8 + g;
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int col = n0 + wn * 64 + j * 8 + 2 * t4 + e;
+        if (col >= N) continue;
+        if (lower && tm == tn && col > row) continue;
+        double* p = C + (long long)col * ldc + row;
+        if (MODE == kSub)
+          *p = *p - acc[i][j][e];
+        else
+          *p = acc[i][j][e];
+      }
+    }
+  }
+}
+
+// Factor the kb x kb diagonal block at A (lda) in shared memory (right-looking,
+// one column per step), write L11 back, then invert L11 in place (column
+// sweep j = kb-1..0, LAPACK dtrti2 order) and write inv(L11) (column-major,
+// ld = NB) into Linv for the GEMM-form trsm and the solves.  info[0] receives
+// the first failing global row (atomicMin); the factorisation continues with a
+// unit pivot so the launch sequence stays fixed.
+__global__ void __launch_bounds__(512)
+    k_potrf_diag(double* A, long long lda, int kb, int row0, double* Linv, int* info) {
+  extern __shared__ __align__(16) double sm[];
+  constexpr int LD = NB + 1;
+  double* a = sm;             // [NB][LD] column-major: a[c*LD + r]
+  double* tmp = sm + NB * LD; // one column
+  __shared__ double s_inv_piv;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (int idx = tid; idx < kb * kb; idx += nth) {
+    int c = idx / kb, r = idx % kb;
+    a[c * LD + r] = r >= c ? A[(long long)c * lda + r] : 0.0;
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int j = 0; j < kb; ++j) {
+    if (tid == 0) {
+      double d = a[j * LD + j];
+      if (!(d > 0.0)) {
+        if (!s_bad) atomicMin(info, row0 + j);
+        s_bad = 1;
+        d = 1.0;
+      }
+      double sq = sqrt(d);
+      a[j * LD + j] = sq;
+      s_inv_piv = 1.0 / sq;
+    }
+    __syncthreads();
+    const double ip = s_inv_piv;
+    for (int r = j + 1 + tid; r < kb; r += nth) a[j * LD + r] *= ip;
+    __syncthreads();
+    const int m = kb - j - 1;
+    for (int idx = tid; idx < m * m; idx += nth) {
+      int c = j + 1 + idx / m, r = j + 1 + idx % m;
+      if (r >= c) a[c * LD + r] -= a[j * LD + r] * a[j * LD + c];
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < kb * kb; idx += nth) {
+    int c = idx / kb, r = idx % kb;
+    if (r >= c) A[(long long)c * lda + r] = a[c * LD + r];
+  }
+  __syncthreads();
+  // in-place inverse: for j = kb-1..0: a[j][j] = 1/a[j][j];
+  // a[j+1:, j] = -a[j][j] * T * a[j+1:, j], T = already-inverted trailing block
+  for (int j = kb - 1; j >= 0; --j) {
+    for (int r = j + 1 + tid; r < kb; r += nth) tmp[r] = a[j * LD + r];
+    __syncthreads();
+    const double ajj = 1.0 / a[j * LD + j];
+    for (int r = j + 1 + tid; r < kb; r += nth) {
+      double s = 0.0;
+      for (int k = j + 1; k <= r; ++k) s += a[k * LD + r] * tmp[k];
+      a[j * LD + r] = -ajj * s;
+    }
+    __syncthreads();
+    if (tid == 0) a[j * LD + j] = ajj;
+    __syncthreads();
+  }
+  for (int idx = tid; idx < NB * NB; idx += nth) {
+    int c = idx / NB, r = idx % NB;
+    Linv[c * NB + r] = (r < kb && c < kb && r >= c) ? a[c * LD + r] : 0.0;
+  }
+}
+
+// Forward step: Y_k = inv(L_kk) B_k (B_k overwritten), rows [k0, k0+kb), all rhs.
+__global__ void k_trsv_diag(const double* Linv, int kb, double* B, long long ldb, int k0, int nrhs,
+                            int transpose) {
+  __shared__ double y[NB];
+  for (int r = blockIdx.x; r < nrhs; r += gridDim.x) {
+    double* b = B + (long long)r * ldb + k0;
+    for (int i = threadIdx.x; i < kb; i += blockDim.x) y[i] = b[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < kb; i += blockDim.x) {
+      double s = 0.0;
+      if (!transpose) {
+        for (int k = 0; k <= i; ++k) s += Linv[k * NB + i] * y[k];  // (Linv)(i,k)
+      } else {
+        for (int k = i; k < kb; ++k) s += Linv[i * NB + k] * y[k];  // (Linv^T)(i,k) = Linv(k,i)
+      }
+      b[i] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// Forward update: B[r] -= sum_{c in block} L(r, c) Y[c] for rows r >= k0+kb.
+// Thread per row (coalesced over r for each c), nrhs accumulators in registers.
+template <int MAXR>
+__global__ void k_fwd_update(const double* A, long long lda, int k0, int kb, int n, double* B,
+                             long long ldb, int nrhs) {
+  __shared__ double ys[NB * MAXR];
+  for (int idx = threadIdx.x; idx < kb * nrhs; idx += blockDim.x) {
+    int c = idx % kb, rr = idx / kb;
+    ys[c * MAXR + rr] = B[(long long)rr * ldb + k0 + c];
+  }
+  __syncthreads();
+  int r = k0 + kb + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double acc[MAXR];
+#pragma unroll
+  for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
+  for (int c = 0; c < kb; ++c) {
+    double l = A[(long long)(k0 + c) * lda + r];
+#pragma unroll
+    for (int q = 0; q < MAXR; ++q) acc[q] = fma(l, ys[c * MAXR + q], acc[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < MAXR; ++q)
+    if (q < nrhs) B[(long long)q * ldb + r] -= acc[q];
+}
+
+// Backward update: Y[r] -= sum_{c in block k} L(c, r) X[c] for rows r < k0.
+// L(c, r) (row c in block k, col r) sits at A[r*lda + c]: a warp reads the
+// kb-long contiguous column segment of row r.
+template <int MAXR>
+__global__ void k_bwd_update(const double* A, long long lda, int k0, int kb, double* B, long long ldb,
+                             int nrhs) {
+  __shared__ double xs[NB * MAXR];
+  for (int idx = threadIdx.x; idx < kb * nrhs; idx += blockDim.x) {
+    int c = idx % kb, rr = idx / kb;
+    xs[c * MAXR + rr] = B[(long long)rr * ldb + k0 + c];
+  }
+  __syncthreads();
+  int lane = threadIdx.x & 31;
+  int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= k0) return;
+  double acc[MAXR];
+#pragma unroll
+  for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
+  for (int c = lane; c < kb; c += 32) {
+    double l = A[(long long)r * lda + k0 + c];
+#pragma unroll
+    for (int q = 0; q < MAXR; ++q) acc[q] = fma(l, xs[c * MAXR + q], acc[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < MAXR; ++q) {
+    double v = acc[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0 && q < nrhs) B[(long long)q * ldb + r] -= v;
+  }
+}
+
+__global__ void k_save_diag(const double* A, long long lda, int n, double* d) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = A[(long long)i * lda + i];
+}
+
+// y = A x with A given by its strict upper triangle (col-major, A[c*lda + r],
+// r < c) and the saved diagonal; 64 x 64 tiles (I <= J), atomics into y.
+template <int MAXR>
+__global__ void k_symv_upper(const double* A, long long lda, const double* diag, int n,
+                             const double* X, long long ldx, int nrhs, double* Y) {
+  constexpr int T = 64;
+  long long t = blockIdx.x;
+  int nbt = (n + T - 1) / T;
+  // upper tile (bi <= bj) from linear index, row-major over bi
+  int bi = 0;
+  long long off = 0;
+  while (off + (nbt - bi) <= t) {
+    off += nbt - bi;
+    ++bi;
+  }
+  int bj = bi + (int)(t - off);
+  __shared__ double xi[T * MAXR], xj[T * MAXR];
+  for (int idx = threadIdx.x; idx < T * nrhs; idx += blockDim.x) {
+    int r = idx % T, q = idx / T;
+    int gi = bi * T + r, gj = bj * T + r;
+    xi[r * MAXR + q] = gi < n ? X[(long long)q * ldx + gi] : 0.0;
+    xj[r * MAXR + q] = gj < n ? X[(long long)q * ldx + gj] : 0.0;
+  }
+  __syncthreads();
+  // thread per column c of the tile (T threads): y_j[c] += sum_r A(r,c) x_i[r];
+  // and per row r: y_i[r] += sum_c A(r,c) x_j[c] (second pass)
+  int tid = threadIdx.x;
+  if (tid < T) {
+    int c = bj * T + tid;
+    if (c < n) {
+      double acc[MAXR];
+#pragma unroll
+      for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
+      for (int rr = 0; rr < T; ++rr) {
+        int r = bi * T + rr;
+        if (r >= n || r >= c) break;
+        double a = A[(long long)c * lda + r];
+#pragma unroll
+        for (int q = 0; q < MAXR; ++q) acc[q] = fma(a, xi[rr * MAXR + q], acc[q]);
+      }
+      if (bi == bj) {
+#pragma unroll
+        for (int q = 0; q < MAXR; ++q) acc[q] = fma(diag[c], xj[tid * MAXR + q], acc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < MAXR; ++q)
+        if (q < nrhs) atomicAdd(&Y[(long long)q * n + c], acc[q]);
+    }
+  } else if (tid < 2 * T) {
+    int rr = tid - T;
+    int r = bi * T + rr;
+    if (r < n) {
+      double acc[MAXR];
+#pragma unroll
+      for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
+      for (int cc = 0; cc < T; ++cc) {
+        int c = bj * T + cc;
+        if (c >= n) break;
+        if (c <= r) continue;
+        double a = A[(long long)c * lda + r];
+#pragma unroll
+        for (int q = 0; q < MAXR; ++q) acc[q] = fma(a, xj[cc * MAXR + q], acc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < MAXR; ++q)
+        if (q < nrhs) atomicAdd(&Y[(long long)q * n + r], acc[q]);
+    }
+  }
+}
+
+// resid[q] = ||Y[:,q] - B[:,q]|| / ||B[:,q]|| (one CTA per rhs)
+__global__ void k_resid_norm(const double* Y, const double* B, int n, double* resid) {
+  int q = blockIdx.x;
+  double rn = 0.0, bn = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double d = Y[(long long)q * n + i] - B[(long long)q * n + i];
+    double b = B[(long long)q * n + i];
+    rn += d * d;
+    bn += b * b;
+  }
+  __shared__ double s1[256], s2[256];
+  s1[threadIdx.x] = rn;
+  s2[threadIdx.x] = bn;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+      s2[threadIdx.x] += s2[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double b = sqrt(s2[0]);
+    resid[q] = sqrt(s1[0]) / (b > 0.0 ? b : 1.0);
+  }
+}
+
+__global__ void k_copy(const double* src, double* dst, long long count) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < count) dst[i] = src[i];
+}
+
+int ensure_work(gbem_ctx* ctx, size_t elems) {
+  if (ctx->work_cap >= elems && ctx->d_work) return GBEM_OK;
+  if (ctx->d_work) cudaFree(ctx->d_work);
+  ctx->d_work = nullptr;
+  ctx->work_cap = 0;
+  GBEM_CUDA(ctx, cudaMalloc(&ctx->d_work, elems * sizeof(double)));
+  ctx->work_cap = elems;
+  return GBEM_OK;
+}
+
+}  // namespace
+
+// Blocked Cholesky of ctx->d_A (n x n) + solves for nrhs columns of d_B (ld n)
+// into d_X; d_resid[nrhs] optional.
+int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
+                        gbem_solve_stats* stats) {
+  const int n = (int)ctx->n;
+  const long long lda = ctx->lda;
+  if (stats) {
+    *stats = gbem_solve_stats{};
+    stats->n = n;
+    stats->nrhs = nrhs;
+    stats->bad_pivot = -1;
+  }
+  if (nrhs < 0 || nrhs > 64) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, 64]");
+  if (n == 0) return GBEM_OK;
+  if (ctx->factored) return ctx->fail(GBEM_EINVAL, "matrix already factored; re-assemble or re-upload");
+  const int nblk = (n + NB - 1) / NB;
+  // workspace: inverses of the diagonal blocks (nblk * NB * NB) + symv result (n * nrhs)
+  size_t need = (size_t)nblk * NB * NB + (size_t)n * (size_t)std::max<int64_t>(nrhs, 1);
+  int rc = ensure_work(ctx, need);
+  if (rc) return rc;
+  double* Linv = ctx->d_work;
+  double* Ysym = ctx->d_work + (size_t)nblk * NB * NB;
+  if (ctx->diag_cap < n) {
+    if (ctx->d_diag) cudaFree(ctx->d_diag);
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_diag, sizeof(double) * n));
+    ctx->diag_cap = n;
+  }
+  if (!ctx->d_info) {
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_info, sizeof(int)));
+    GBEM_CUDA(ctx, cudaMallocHost(&ctx->h_info, sizeof(int)));
+  }
+  static bool attr_done = false;
+  if (!attr_done) {
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kSub>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)((NB + 1) * (NB + 1) * sizeof(double))));
+    attr_done = true;
+  }
+  cudaStream_t s = ctx->stream;
+  int big = 0x7fffffff;
+  GBEM_CUDA(ctx, cudaMemcpyAsync(ctx->d_info, &big, sizeof(int), cudaMemcpyHostToDevice, s));
+  k_save_diag<<<(n + 255) / 256, 256, 0, s>>>(ctx->d_A, lda, n, ctx->d_diag);
+  GBEM_LAUNCH_CHECK(ctx);
+  cudaEventRecord(ctx->ev[0], s);
+  const size_t potrf_smem = (size_t)(NB + 1) * (NB + 1) * sizeof(double);
+  for (int b = 0; b < nblk; ++b) {
+    int k0 = b * NB, kb = std::min(NB, n - k0);
+    double* Akk = ctx->d_A + (long long)k0 * lda + k0;
+    k_potrf_diag<<<1, 512, potrf_smem, s>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
+    GBEM_LAUNCH_CHECK(ctx);
+    int m = n - k0 - kb;
+    if (m <= 0) break;
+    double* A21 = Akk + kb;  // rows k0+kb.., cols k0..
+    // L21 = A21 * inv(L11)^T  (in place)
+    k_gemm_nt<kStore><<<dim3((m + BM - 1) / BM, 1), GEMM_THREADS, GEMM_SMEM, s>>>(
+        A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb, 0);
+    GBEM_LAUNCH_CHECK(ctx);
+    // A22 -= L21 L21^T (lower tiles)
+    int nt = (m + BM - 1) / BM;
+    long long ntiles = (long long)nt * (nt + 1) / 2;
+    double* A22 = ctx->d_A + (long long)(k0 + kb) * lda + (k0 + kb);
+    k_gemm_nt<kSub><<<(unsigned)ntiles, GEMM_THREADS, GEMM_SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m, kb, 1);
+    GBEM_LAUNCH_CHECK(ctx);
+  }
+  cudaEventRecord(ctx->ev[1], s);
+  GBEM_CUDA(ctx, cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GBEM_CUDA(ctx, cudaStreamSynchronize(s));
+  ctx->factored = true;
+  if (*ctx->h_info != big) {
+    if (stats) stats->bad_pivot = *ctx->h_info;
+    return ctx->fail(GBEM_ENUMERIC,
+                     "matrix not positive definite (pivot at row " + std::to_string(*ctx->h_info) + ")");
+  }
+  if (nrhs == 0) return GBEM_OK;
+  // X <- B, then forward / backward substitution in place
+  k_copy<<<(unsigned)(((long long)n * nrhs + 255) / 256), 256, 0, s>>>(d_B, d_X, (long long)n * nrhs);
+  GBEM_LAUNCH_CHECK(ctx);
+  const int R = (int)nrhs;
+  for (int b = 0; b < nblk; ++b) {
+    int k0 = b * NB, kb = std::min(NB, n - k0);
+    k_trsv_diag<<<R, 128, 0, s>>>(Linv + (size_t)b * NB * NB, kb, d_X, n, k0, R, 0);
+    GBEM_LAUNCH_CHECK(ctx);
+    int m = n - k0 - kb;
+    if (m > 0) {
+      dim3 grid((m + 127) / 128);
+      for (int q0 = 0; q0 < R; q0 += 32) {
+        int rq = std::min(32, R - q0);
+        double* Xq = d_X + (long long)q0 * n;
+        if (rq <= 8)
+          k_fwd_update<8><<<grid, 128, 0, s>>>(ctx->d_A, lda, k0, kb, n, Xq, n, rq);
+        else if (rq <= 16)
+          k_fwd_update<16><<<grid, 128, 0, s>>>(ctx->d_A, lda, k0, kb, n, Xq, n, rq);
+        else
+          k_fwd_update<32><<<grid, 128, 0, s>>>(ctx->d_A, lda, k0, kb, n, Xq, n, rq);
+        GBEM_LAUNCH_CHECK(ctx);
+      }
+    }
+  }
+  for (int b = nblk - 1; b >= 0; --b) {
+    int k0 = b * NB, kb = std::min(NB, n - k0);
+    k_trsv_diag<<<R, 128, 0, s>>>(Linv + (size_t)b * NB * NB, kb, d_X, n, k0, R, 1);
+    GBEM_LAUNCH_CHECK(ctx);
+    if (k0 > 0) {
+      dim3 grid((k0 + 7) / 8);
+      for (int q0 = 0; q0 < R; q0 += 32) {
+        int rq = std::min(32, R - q0);
+        double* Xq = d_X + (long long)q0 * n;
+        if (rq <= 8)
+          k_bwd_update<8><<<grid, 256, 0, s>>>(ctx->d_A, lda, k0, kb, Xq, n, rq);
+        else if (rq <= 16)
+          k_bwd_update<16><<<grid, 256, 0, s>>>(ctx->d_A, lda, k0, kb, Xq, n, rq);
+        else
+          k_bwd_update<32><<<grid, 256, 0, s>>>(ctx->d_A, lda, k0, kb, Xq, n, rq);
+        GBEM_LAUNCH_CHECK(ctx);
+      }
+    }
+  }
+  cudaEventRecord(ctx->ev[2], s);
+  if (d_resid) {
+    GBEM_CUDA(ctx, cudaMemsetAsync(Ysym, 0, sizeof(double) * (size_t)n * R, s));
+    int nbt = (n + 63) / 64;
+    long long ntiles = (long long)nbt * (nbt + 1) / 2;
+    for (int q0 = 0; q0 < R; q0 += 32) {
+      int rq = std::min(32, R - q0);
+      const double* Xq = d_X + (long long)q0 * n;
+      double* Yq = Ysym + (long long)q0 * n;
+      if (rq <= 8)
+        k_symv_upper<8><<<(unsigned)ntiles, 128, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      else if (rq <= 16)
+        k_symv_upper<16><<<(unsigned)ntiles, 128, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      else
+        k_symv_upper<32><<<(unsigned)ntiles, 128, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      GBEM_LAUNCH_CHECK(ctx);
+    }
+    k_resid_norm<<<R, 256, 0, s>>>(Ysym, d_B, n, d_resid);
+    GBEM_LAUNCH_CHECK(ctx);
+  }
+  cudaEventRecord(ctx->ev[3], s);
+  if (stats) {
+    GBEM_CUDA(ctx, cudaEventSynchronize(ctx->ev[3]));
+    float a = 0, b2 = 0, c = 0;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&b2, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
+    stats->ms_factor = a;
+    stats->ms_solve = b2;
+    stats->ms_residual = c;
+    if (d_resid) {
+      std::vector<double> r((size_t)R);
+      GBEM_CUDA(ctx, cudaMemcpy(r.data(), d_resid, sizeof(double) * R, cudaMemcpyDeviceToHost));
+      double mx = 0;
+      for (double v : r) mx = std::max(mx, v);
+      stats->max_residual = mx;
+    }
+  }
+  return GBEM_OK;
+}
