@@ -146,6 +146,21 @@ int gbem_net_charges_dev(gbem_ctx* ctx, const int32_t* net_of_panel, int64_t n,
                          const double* X, int64_t nrhs, int32_t K, double scale, double* C,
                          double* outer);
 
+/* Capacitance matrix of a single-dielectric panel set in one call (the shared
+ * K-right-hand-side path of capacitance_matrix, extraction.hpp:162-184):
+ * assemble, factor, solve with B[:, r] = 1 on the panels of net r, and reduce
+ * C[r*K + k] = eps_r * eps0 * 1e-6 * sum_{p in net k} X[p, r] (farads).
+ * net_of_panel[p] in [0, K) for conductor panels, -1 for grounded outer panels.
+ * Host buffers (every host<->device copy happens inside the call). */
+int gbem_extract_cmatrix(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net_of_panel,
+                         int32_t K, double eps_r, const gbem_quad_config* cfg, double* C, double* resid,
+                         gbem_assembly_stats* astats, gbem_solve_stats* sstats);
+/* Device-pointer variant (panels, net_of_panel, C, resid on the device); runs
+ * stream-ordered and only synchronises to read back stats when requested. */
+int gbem_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net_of_panel,
+                             int32_t K, double eps_r, const gbem_quad_config* cfg, double* C, double* resid,
+                             gbem_assembly_stats* astats, gbem_solve_stats* sstats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,6 +70,12 @@ GPU_SYMBOLS = [
     ("gbem_spd_solve", C.c_int, [_P, _P, C.c_int64, _P, _P, C.POINTER(GbemSolveStats)]),
     ("gbem_spd_solve_dev", C.c_int, [_P, _P, C.c_int64, _P, _P, C.POINTER(GbemSolveStats)]),
     ("gbem_net_charges_dev", C.c_int, [_P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_double, _P, _P]),
+    ("gbem_extract_cmatrix", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, _P, C.c_int32, C.c_double,
+                                       C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats),
+                                       C.POINTER(GbemSolveStats)]),
+    ("gbem_extract_cmatrix_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, _P, C.c_int32, C.c_double,
+                                           C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats),
+                                           C.POINTER(GbemSolveStats)]),
 ]
 
 _gpu = None
@@ -187,6 +193,20 @@ class Context:
                                            ptr(A) if download else None, n, C.byref(st))
         self.check(rc)
         return A, st
+
+    def extract_cmatrix(self, P: PanelArrays, net_of_panel: np.ndarray, K: int, eps_r: float,
+                        cfg: GbemQuadConfig | None = None, stats: bool = True):
+        """Host-buffer C-matrix extraction (assemble + factor + K solves + charges)."""
+        net = np.ascontiguousarray(net_of_panel, dtype=np.int32)
+        Cm = np.zeros((K, K))
+        res = np.zeros(K)
+        ast, sst = GbemAssemblyStats(), GbemSolveStats()
+        sp = P.struct()
+        rc = self.lib.gbem_extract_cmatrix(self.h, C.byref(sp), P.n, ptr(net), K, eps_r, C.byref(cfg or self.quad()),
+                                           ptr(Cm), ptr(res), C.byref(ast) if stats else None,
+                                           C.byref(sst) if stats else None)
+        self.check(rc)
+        return Cm, res, ast, sst
 
     def matrix_upload(self, A: np.ndarray):
         A = np.ascontiguousarray(A, dtype=np.float64)

@@ -24,7 +24,7 @@ OBJ = LIB / "obj"
 INCLUDE = ROOT / "include"
 
 NVCC = os.environ.get("NVCC", "nvcc")
-CXX = os.environ.get("CXX", "g++")
+CXX = os.environ.get("GBEM_CXX", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"]
 # Per-file extra flags: the assembly unit keeps the reference's operation order

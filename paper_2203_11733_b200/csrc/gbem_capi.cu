@@ -48,6 +48,40 @@ __global__ void k_net_charges(const int32_t* net, int n, const double* X, int nr
   }
 }
 
+__global__ void k_build_rhs(const int32_t* net, int n, int K, double* B) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)n * K) return;
+  int r = (int)(i / n), p = (int)(i % n);
+  B[i] = net[p] == r ? 1.0 : 0.0;
+}
+
+int extract_impl(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* d_net, int32_t K, double eps_r,
+                 const gbem_quad_config* cfg, double* d_C, double* d_resid, gbem_assembly_stats* as,
+                 gbem_solve_stats* ss, bool device_panels) {
+  if (K < 1 || K > 64) return ctx->fail(GBEM_EINVAL, "K must be in [1, 64]");
+  int rc = gbem_internal_upload_panels(ctx, P, n, device_panels);
+  if (rc) return rc;
+  rc = ensure_matrix(ctx, n);
+  if (rc) return rc;
+  rc = gbem_internal_assemble(ctx, n, 0, n, cfg, as, true);
+  if (rc) return rc;
+  size_t cnt = (size_t)n * (size_t)K;
+  if (ctx->rhs_cap < cnt) {
+    cudaFree(ctx->d_rhs);
+    ctx->d_rhs = nullptr;
+    ctx->rhs_cap = 0;
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_rhs, 2 * cnt * sizeof(double)));
+    ctx->rhs_cap = cnt;
+  }
+  double* dB = ctx->d_rhs;
+  double* dX = ctx->d_rhs + cnt;
+  k_build_rhs<<<(unsigned)((cnt + 255) / 256), 256, 0, ctx->stream>>>(d_net, (int)n, K, dB);
+  GBEM_LAUNCH_CHECK(ctx);
+  rc = gbem_internal_solve(ctx, dB, K, dX, d_resid, ss);
+  if (rc) return rc;
+  return gbem_net_charges_dev(ctx, d_net, n, dX, K, K, eps_r * 8.854187817e-12 * 1e-6, d_C, nullptr);
+}
+
 }  // namespace
 
 int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n) { return ensure_matrix(ctx, n); }
@@ -103,6 +137,7 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   cudaFree(ctx->d_stats);
   cudaFree(ctx->d_work);
   cudaFree(ctx->d_info);
+  cudaFree(ctx->d_rhs);
   if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
   if (ctx->h_info) cudaFreeHost(ctx->h_info);
   for (auto& ev : ctx->ev)
@@ -289,6 +324,38 @@ int gbem_net_charges_dev(gbem_ctx* ctx, const int32_t* net, int64_t n, const dou
   k_net_charges<<<(unsigned)nrhs, threads, smem, ctx->stream>>>(net, (int)n, X, (int)nrhs, K, scale, C, outer);
   GBEM_LAUNCH_CHECK(ctx);
   return GBEM_OK;
+}
+
+int gbem_extract_cmatrix(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net_of_panel, int32_t K,
+                         double eps_r, const gbem_quad_config* cfg, double* C, double* resid,
+                         gbem_assembly_stats* as, gbem_solve_stats* ss) {
+  if (!ctx) return GBEM_EINVAL;
+  if (!P || !net_of_panel || !C || n <= 0) return ctx->fail(GBEM_EINVAL, "null argument or empty panel set");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int32_t* d_net = nullptr;
+  double *d_C = nullptr, *d_res = nullptr;
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_net, sizeof(int32_t) * n, ctx->stream));
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_C, sizeof(double) * K * K + sizeof(double) * 64, ctx->stream));
+  d_res = d_C + (size_t)K * K;
+  GBEM_CUDA(ctx, cudaMemcpyAsync(d_net, net_of_panel, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = extract_impl(ctx, P, n, d_net, K, eps_r, cfg, d_C, d_res, as, ss, false);
+  if (rc == GBEM_OK) {
+    GBEM_CUDA(ctx, cudaMemcpyAsync(C, d_C, sizeof(double) * K * K, cudaMemcpyDeviceToHost, ctx->stream));
+    if (resid) GBEM_CUDA(ctx, cudaMemcpyAsync(resid, d_res, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  cudaFreeAsync(d_net, ctx->stream);
+  cudaFreeAsync(d_C, ctx->stream);
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return rc;
+}
+
+int gbem_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net_of_panel,
+                             int32_t K, double eps_r, const gbem_quad_config* cfg, double* C, double* resid,
+                             gbem_assembly_stats* as, gbem_solve_stats* ss) {
+  if (!ctx) return GBEM_EINVAL;
+  if (!P || !net_of_panel || !C || n <= 0) return ctx->fail(GBEM_EINVAL, "null argument or empty panel set");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  return extract_impl(ctx, P, n, net_of_panel, K, eps_r, cfg, C, resid, as, ss, true);
 }
 
 }  // extern "C"

@@ -43,6 +43,8 @@ struct gbem_ctx {
   size_t work_cap = 0;  // elements
   int* d_info = nullptr;
   int* h_info = nullptr;  // pinned
+  double* d_rhs = nullptr;  // B and X of the K-RHS extraction (2 * rhs_cap)
+  size_t rhs_cap = 0;
 
   cudaEvent_t ev[8] = {};
 

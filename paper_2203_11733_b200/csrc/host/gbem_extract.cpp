@@ -1,0 +1,199 @@
+// gbem_extract.cpp — capacitance extraction driver: the caller of the GPU
+// boundary (include/gbem_gpu.h) in place of assemble_single + cholesky_solve
+// (proj/include/gbem/extraction.hpp:106-184).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "../../../include/gbem_gpu.h"
+#include "gbem_host.hpp"
+
+namespace gbh {
+
+namespace {
+
+void raise(gbem_ctx* ctx, int rc) {
+  if (rc == GBEM_OK) return;
+  std::string msg = gbem_last_error(ctx);
+  if (rc == GBEM_EINVAL) throw ValidationError(msg);
+  if (rc == GBEM_ENUMERIC) throw NumericalError(msg);
+  throw std::runtime_error("CUDA: " + msg);
+}
+
+struct SoA {
+  std::vector<uint8_t> axis;
+  std::vector<double> level, a0, a1, b0, b1;
+  explicit SoA(const PanelSet& ps) {
+    const size_t n = ps.panels.size();
+    axis.resize(n);
+    level.resize(n);
+    a0.resize(n);
+    a1.resize(n);
+    b0.resize(n);
+    b1.resize(n);
+    for (size_t k = 0; k < n; ++k) {
+      const Rect& r = ps.panels[k].r;
+      axis[k] = (uint8_t)r.axis;
+      level[k] = r.level;
+      a0[k] = r.a.lo;
+      a1[k] = r.a.hi;
+      b0[k] = r.b.lo;
+      b1[k] = r.b.hi;
+    }
+  }
+  gbem_panels view() const { return {axis.data(), level.data(), a0.data(), a1.data(), b0.data(), b1.data()}; }
+};
+
+bool single_dielectric(const Scene& s) {
+  if (s.regions.size() != 1) return false;
+  if (s.freespace) return true;
+  for (int b : s.bc)
+    if (b != 0) return false;
+  return true;
+}
+
+gbem_quad_config quad(const Options& o) {
+  gbem_quad_config q{};
+  q.rel_tol = o.rel_tol;
+  q.max_levels = o.max_levels;
+  return q;
+}
+
+}  // namespace
+
+Row capacitance_row(gbem_ctx* ctx, const Scene& s, int main_net, const Params& p, const Options& o) {
+  PanelSet ps = partition_for_net(s, main_net, p);
+  if (!single_dielectric(s))
+    throw ValidationError(
+        "the GPU path solves the single-dielectric all-Dirichlet system (multi-dielectric block system is out of scope)");
+  if (ps.count(kNeumann) || ps.count(kInterface))
+    throw ValidationError("single-dielectric assembly requires one region with an all-Dirichlet boundary");
+  const size_t n = ps.panels.size();
+  Row row;
+  row.main_net = main_net;
+  row.diag.panels = n;
+  row.diag.method = "galerkin-single";
+  SoA soa(ps);
+  gbem_panels view = soa.view();
+  gbem_quad_config q = quad(o);
+  gbem_assembly_stats ast{};
+  auto t0 = std::chrono::steady_clock::now();
+  raise(ctx, gbem_assemble_single(ctx, &view, (int64_t)n, &q, nullptr, 0, &ast));
+  row.diag.converged = ast.not_converged == 0;
+  if (!o.dump_matrix.empty()) {
+    std::vector<double> A(n * n);
+    raise(ctx, gbem_matrix_download(ctx, A.data(), (int64_t)n));
+    dump_matrix_file(o.dump_matrix, A, n);
+  }
+  // knownPotential (assembly.hpp:42-44): 1 on the main net's conductor panels
+  std::vector<double> b(n, 0.0), x(n, 0.0);
+  for (size_t k = 0; k < n; ++k)
+    if (ps.panels[k].kind == kConductor && ps.panels[k].net == main_net) b[k] = 1.0;
+  double resid = 0;
+  gbem_solve_stats sst{};
+  raise(ctx, gbem_spd_solve(ctx, b.data(), 1, x.data(), &resid, &sst));
+  auto t1 = std::chrono::steady_clock::now();
+  row.diag.seconds = std::chrono::duration<double>(t1 - t0).count();
+  row.diag.residual = resid;
+  // net_charges (extraction.hpp:55-79)
+  for (const Net& nn : s.nets) row.cap[nn.id] = 0.0;
+  double outer = 0;
+  for (size_t k = 0; k < n; ++k) {
+    const Panel& pn = ps.panels[k];
+    const Region* reg = s.region(pn.regA);
+    if (!reg) throw ValidationError("missing permittivity for region " + std::to_string(pn.regA));
+    const double qv = reg->eps * kEps0 * x[k] * kUnitScale;
+    if (pn.kind == kConductor)
+      row.cap[pn.net] += qv;
+    else
+      outer += qv;
+  }
+  row.outer = outer;
+  double total = outer;
+  for (const auto& kv : row.cap) total += kv.second;
+  row.diag.neutrality = std::abs(total) / std::max(std::abs(row.cap.at(main_net)), 1e-300);
+  return row;
+}
+
+static void reciprocity(CapMatrix& cm) {
+  cm.reciprocity = 0;
+  for (size_t a = 0; a < cm.rows.size(); ++a)
+    for (size_t b = a + 1; b < cm.rows.size(); ++b) {
+      double cab = cm.rows[a].cap.at(cm.ids[b]), cba = cm.rows[b].cap.at(cm.ids[a]);
+      double den = std::max(std::abs(cab), std::abs(cba));
+      if (den > 0) cm.reciprocity = std::max(cm.reciprocity, std::abs(cab - cba) / den);
+    }
+}
+
+CapMatrix capacitance_matrix(gbem_ctx* ctx, const Scene& s, const Params& p, const Options& o) {
+  CapMatrix cm;
+  for (const Net& n : s.nets) cm.ids.push_back(n.id);
+  for (int id : cm.ids) {
+    Options ro = o;
+    if (!o.dump_matrix.empty()) ro.dump_matrix = o.dump_matrix + "_net" + std::to_string(id);
+    cm.rows.push_back(capacitance_row(ctx, s, id, p, ro));
+  }
+  reciprocity(cm);
+  return cm;
+}
+
+CapMatrix capacitance_matrix_shared(gbem_ctx* ctx, const Scene& s, const PanelSet& ps, const Options& o) {
+  if (!single_dielectric(s))
+    throw ValidationError("the GPU path solves the single-dielectric all-Dirichlet system");
+  const size_t n = ps.panels.size();
+  const size_t K = s.nets.size();
+  if (K == 0) throw ValidationError("scene has no conductors");
+  if (K > 64) throw ValidationError("at most 64 nets per shared solve");
+  std::map<int, size_t> col;
+  for (size_t k = 0; k < K; ++k) col[s.nets[k].id] = k;
+  SoA soa(ps);
+  gbem_panels view = soa.view();
+  gbem_quad_config q = quad(o);
+  gbem_assembly_stats ast{};
+  auto t0 = std::chrono::steady_clock::now();
+  raise(ctx, gbem_assemble_single(ctx, &view, (int64_t)n, &q, nullptr, 0, &ast));
+  if (!o.dump_matrix.empty()) {
+    std::vector<double> A(n * n);
+    raise(ctx, gbem_matrix_download(ctx, A.data(), (int64_t)n));
+    dump_matrix_file(o.dump_matrix, A, n);
+  }
+  std::vector<double> B(n * K, 0.0), X(n * K, 0.0), res(K, 0.0);
+  for (size_t p = 0; p < n; ++p)
+    if (ps.panels[p].kind == kConductor) B[col.at(ps.panels[p].net) * n + p] = 1.0;
+  gbem_solve_stats sst{};
+  raise(ctx, gbem_spd_solve(ctx, B.data(), (int64_t)K, X.data(), res.data(), &sst));
+  auto t1 = std::chrono::steady_clock::now();
+  const double secs = std::chrono::duration<double>(t1 - t0).count();
+  CapMatrix cm;
+  for (const Net& nn : s.nets) cm.ids.push_back(nn.id);
+  for (size_t r = 0; r < K; ++r) {
+    Row row;
+    row.main_net = s.nets[r].id;
+    row.diag.panels = n;
+    row.diag.method = "galerkin-shared";
+    row.diag.seconds = secs;
+    row.diag.residual = res[r];
+    row.diag.converged = ast.not_converged == 0;
+    for (const Net& nn : s.nets) row.cap[nn.id] = 0.0;
+    double outer = 0;
+    for (size_t p = 0; p < n; ++p) {
+      const Panel& pn = ps.panels[p];
+      const Region* reg = s.region(pn.regA);
+      if (!reg) throw ValidationError("missing permittivity for region " + std::to_string(pn.regA));
+      const double qv = reg->eps * kEps0 * X[r * n + p] * kUnitScale;
+      if (pn.kind == kConductor)
+        row.cap[pn.net] += qv;
+      else
+        outer += qv;
+    }
+    row.outer = outer;
+    double total = outer;
+    for (const auto& kv : row.cap) total += kv.second;
+    row.diag.neutrality = s.freespace ? -1.0 : std::abs(total) / std::max(std::abs(row.cap.at(row.main_net)), 1e-300);
+    cm.rows.push_back(row);
+  }
+  reciprocity(cm);
+  return cm;
+}
+
+}  // namespace gbh

@@ -1,0 +1,115 @@
+"""End-to-end extraction on the GPU through the C++ host: reference scene file in,
+capacitance matrix out (proj/README.md:78-84 golden), plus the extraction
+properties of proj/tests/test_extraction.cpp and the CLI contract."""
+import json
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import paper_2203_11733_b200 as g
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+BENCH = ROOT / "tests" / "golden" / "bench_single.gbem"
+CLI = ROOT / "paper_2203_11733_b200" / "lib" / "gbem"
+
+# proj/README.md:80-84 (printed with %.9g)
+README_C = np.array([[2.2471839e-16, -5.80121909e-17], [-5.72842648e-17, 1.80198011e-16]])
+
+
+def test_benchmark_matrix_matches_readme_golden():
+    m = g.parse_model(BENCH.read_text())
+    csv, js = m.extract(net=-1, mode=0)
+    C = np.array([[js["rows"][r]["capacitance"][str(k)] for k in (1, 2)] for r in range(2)])
+    assert np.all(np.abs(C - README_C) <= 5e-9 * np.abs(README_C)), C
+    assert [r["panels"] for r in js["rows"]] == [83, 56]
+    assert "# panels net1=83 net2=56" in csv
+    assert "# method net1=galerkin-single net2=galerkin-single" in csv
+    for r in js["rows"]:
+        assert r["residual"] <= 1e-10
+        assert 0 <= r["neutrality"] <= 0.005
+        assert r["outerCharge"] < 0
+
+
+def test_benchmark_matrix_matches_cpu_oracle_pipeline():
+    """Same panels (reference partition), CPU oracle assembly + dense solve."""
+    m = g.parse_model(BENCH.read_text())
+    _, js = m.extract(net=-1, mode=0)
+    for r, net in enumerate((1, 2)):
+        ps = g.partition_scene(m, net)
+        A, conv, rc = O.assemble("orc", ps.matrix(), nthreads=8)
+        b = ((ps.kind == 0) & (ps.net == net)).astype(float)
+        x = np.linalg.solve(A, b)
+        q = 1.0 * 8.854187817e-12 * x * 1e-6
+        for k in (1, 2):
+            ref = q[(ps.kind == 0) & (ps.net == k)].sum()
+            got = js["rows"][r]["capacitance"][str(k)]
+            assert abs(got - ref) <= 1e-9 * abs(ref)
+
+
+def test_capacitance_scales_linearly_with_permittivity():
+    """test_extraction.cpp:93-109: exact 2x."""
+    base = ("domain lo(-6,-6,0) hi(6,6,6)\nregion 1 {eps} lo(-6,-6,0) hi(6,6,6)\n"
+            "net 1 cuboid lo(-1,-0.5,1) hi(1,0.5,2)\nnet 2 cuboid lo(-0.5,-1,3) hi(0.5,1,4)\nparams 3 4 1 1\n")
+    m1, m2 = g.parse_model(base.format(eps=1.0)), g.parse_model(base.format(eps=2.0))
+    m1.extract(net=1)
+    m2.extract(net=1)
+    assert np.array_equal(m2.last_cap, 2.0 * m1.last_cap)  # bit-exact, like the reference
+    assert np.array_equal(m2.last_outer, 2.0 * m1.last_outer)
+
+
+def test_mirror_symmetric_scene():
+    """test_extraction.cpp:111-132."""
+    text = ("domain lo(-8,-8,0) hi(8,8,5)\nregion 1 1.0 lo(-8,-8,0) hi(8,8,5)\n"
+            "net 1 cuboid lo(-3,-1,1) hi(-1,1,3)\nnet 2 cuboid lo(1,-1,1) hi(3,1,3)\n")
+    js = g.capacitance_matrix(g.parse_model(text))
+    c11, c12 = js["rows"][0]["capacitance"]["1"], js["rows"][0]["capacitance"]["2"]
+    c21, c22 = js["rows"][1]["capacitance"]["1"], js["rows"][1]["capacitance"]["2"]
+    assert abs(c22 - c11) <= 1e-9 * c11 and abs(c21 - c12) <= 1e-9 * abs(c12)
+    assert js["reciprocityDefect"] <= 1e-9
+    assert c11 > 0 and c12 <= 1e-3 * c11
+
+
+def test_config1_shared_matches_oracle():
+    m = g.config_model(1)
+    ps = m.partition(1)
+    _, js = m.extract(net=-1, mode=1)
+    A, conv, rc = O.assemble("orc", ps.matrix(), nthreads=16)
+    B = np.stack([(ps.net == 1), (ps.net == 2)], axis=1).astype(float)
+    X = np.linalg.solve(A, B)
+    for r in range(2):
+        for k in (1, 2):
+            ref = 3.9 * 8.854187817e-12 * 1e-6 * X[ps.net == k, r].sum()
+            got = js["rows"][r]["capacitance"][str(k)]
+            assert abs(got - ref) <= 1e-6 * abs(ref), (r, k, got, ref)
+
+
+def test_cli_extract_and_exit_codes(tmp_path):
+    out = subprocess.run([str(CLI), "extract", "--input", str(BENCH), "--all"], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.startswith("# gbem 1.0.0\n# params p1=1.5 p2=4 p3=1 p5=1\n")
+    assert "net,1,2" in out.stdout
+    js = subprocess.run([str(CLI), "extract", "--input", str(BENCH), "--net", "1", "--format", "json"],
+                        capture_output=True, text=True)
+    assert js.returncode == 0 and '"method": "galerkin-single"' in js.stdout and '"seconds"' in js.stdout
+    bad = subprocess.run([str(CLI), "extract", "--input", str(tmp_path / "missing.gbem")], capture_output=True, text=True)
+    assert bad.returncode == 1 and "cannot open" in bad.stderr
+    both = subprocess.run([str(CLI), "extract", "--input", str(BENCH), "--all", "--net", "1"], capture_output=True,
+                          text=True)
+    assert both.returncode == 1 and "mutually exclusive" in both.stderr
+
+
+def test_matrix_dump_round_trip(tmp_path):
+    """--dump-matrix writes extraction.hpp:83-99's format; it equals the assembled matrix bit for bit."""
+    p = tmp_path / "A.bin"
+    m = g.parse_model(BENCH.read_text())
+    m.extract(net=1, mode=0, dump_matrix=str(p))
+    blob = p.read_bytes()
+    n = int.from_bytes(blob[:8], "little")
+    A = np.frombuffer(blob[8:], dtype="<f8").reshape(n, n)
+    ps = g.partition_scene(m, 1)
+    sysm = g.assemble_single(ps)
+    assert n == len(ps) and np.array_equal(A, sysm.A)

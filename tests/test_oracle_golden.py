@@ -1,0 +1,163 @@
+"""Pins the CPU oracle (oracle/gbem_oracle.c) to the reference's own known answers
+and, pair by pair, to the reference headers compiled in place (oracle/_ref).
+CPU only."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import pairgen as G
+
+GOLDEN_U = [  # proj/tests/test_kernels.cpp:166-215
+    ((2, 0, (0, 1), (0, 1)), (2, 0, (0, 1), (0, 1)), 0.2366005022046692, 1e-9),
+    ((0, 1, (0, 2), (-0.25, 0.25)), (0, 1, (0, 2), (-0.25, 0.25)), 0.21169029935491254, 1e-9),
+    ((2, 0, (0, 1), (0, 1)), (2, 0, (1, 2.3), (0, 0.7)), 0.07287312340623026, 1e-9),
+    ((1, -2, (0, 1.5), (0, 1)), (1, -2, (2, 3), (0.5, 2.5)), 0.12268222523420745, 1e-9),
+    ((2, 1, (0, 1), (0, 1)), (2, 0, (0, 1), (0, 1)), 0.06993383553800263, 1e-6),
+    ((0, 2.5, (-1, 0.5), (0.3, 1.7)), (0, 1, (0.2, 2), (-0.5, 0.9)), 0.18994761567034635, 1e-6),
+    ((2, 0, (0, 1), (0, 1)), (0, 2, (0.5, 1.5), (1, 2)), 0.03625499787837069, 1e-6),
+    ((2, 0, (0, 1), (0, 1)), (1, 0, (0, 1), (0, 1)), 0.10734127519843392, 1e-6),
+    ((2, 0, (0, 2), (-1, 1)), (0, 1, (-0.5, 0.5), (0, 1.5)), 0.4790527168879336, 1e-6),
+]
+
+
+def test_frozen_single_layer_values():
+    L = O.orc()
+    for a, b, v, tol in GOLDEN_U:
+        kv = L.orc_u_pair_integral(C.byref(O.rect(*a)), C.byref(O.rect(*b)), 1e-8, 16)
+        assert kv.status == 0 and kv.converged
+        assert abs(kv.value - v) <= tol * v
+
+
+def test_frozen_values_tight_match():
+    """Coplanar closed forms reproduce the frozen digits; Romberg paths to ~1e-11."""
+    L = O.orc()
+    for a, b, v, tol in GOLDEN_U:
+        kv = L.orc_u_pair_integral(C.byref(O.rect(*a)), C.byref(O.rect(*b)), 1e-8, 16)
+        assert abs(kv.value - v) <= (1e-15 if tol == 1e-9 else 2e-11) * v
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_oracle_bit_exact_vs_compiled_reference(seed):
+    rng = np.random.default_rng(seed)
+    A1, B1 = G.classic_pairs(rng, 400)
+    A2, B2 = G.touching_pairs(rng, 60)
+    A3, B3 = G.small_far_pairs(rng, 200)
+    A = np.vstack([A1, A2, A3]); B = np.vstack([B1, B2, B3])
+    o, oc, os_ = O.u_pairs("orc", A, B, nthreads=4)
+    r, rc_, rs = O.u_pairs("ref", A, B, nthreads=4)
+    assert os_ == rs == 0
+    assert np.array_equal(o, r)            # bit-identical
+    assert np.array_equal(oc, rc_)
+
+
+def test_symmetry_and_positivity():
+    """test_kernels.cpp:118-127 on the oracle."""
+    rng = np.random.default_rng(424242)
+    A, B = G.classic_pairs(rng, 100)
+    u1, _, _ = O.u_pairs("orc", A, B)
+    u2, _, _ = O.u_pairs("orc", B, A)
+    assert np.all(u1 > 0)
+    assert np.array_equal(u1, u2)  # canonical argument order makes it bitwise symmetric
+
+
+def _aitken(v0, v1, v2):
+    den = (v2 - v1) - (v1 - v0)
+    if abs(den) < 1e-14 * max(abs(v2), 1e-300):
+        return v2
+    return v2 - (v2 - v1) ** 2 / den
+
+
+def test_brute_force_oracle_reference_values():
+    """test_oracle.cpp:60-88 on the restated recursive Gauss oracle."""
+    L = O.orc()
+    f = L.orc_oracle_pair_integral
+    f.restype = C.c_double
+    sq = O.rect(2, 0, (0, 1), (0, 1))
+    acc = _aitken(*(f(C.byref(sq), C.byref(sq), d) for d in (3, 4, 5)))
+    assert abs(acc - 0.2366005022046692) <= 1e-5 * 0.2366005022046692
+    a, b = O.rect(2, 1, (0, 1), (0, 1)), O.rect(2, 0, (0, 1), (0, 1))
+    assert abs(f(C.byref(a), C.byref(b), 6) - 0.06993383553800263) <= 1e-8 * 0.0699
+    a, b = O.rect(2, 0, (0, 1), (0, 1)), O.rect(1, 0, (0, 1), (0, 1))
+    acc = _aitken(*(f(C.byref(a), C.byref(b), d) for d in (3, 4, 5)))
+    assert abs(acc - 0.10734127519843392) <= 1e-5 * 0.107
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_brute_force_oracle_matches_reference_oracle():
+    rng = np.random.default_rng(5)
+    A, B = G.classic_pairs(rng, 20)
+    for k in range(len(A)):
+        ra, rb = O.rect(A[k, 0], A[k, 1], A[k, 2:4], A[k, 4:6]), O.rect(B[k, 0], B[k, 1], B[k, 2:4], B[k, 4:6])
+        assert O.orc().orc_oracle_pair_integral(C.byref(ra), C.byref(rb), 3) == \
+            O.ref().ref_oracle_pair_integral(C.byref(ra), C.byref(rb), 3)
+
+
+def test_far_truth_matches_brute_force_oracle():
+    """The composite-Gauss far-field truth agrees with the reference's own
+    brute-force oracle (oracle.hpp:191) to its depth-6 accuracy."""
+    rng = np.random.default_rng(11)
+    A, B = G.ratio_pairs(rng, 30, 1.5, 4.0)
+    t = O.truth_pairs(A, B, sub=2)
+    f = O.orc().orc_oracle_pair_integral
+    for k in range(len(A)):
+        ra, rb = O.rect(A[k, 0], A[k, 1], A[k, 2:4], A[k, 4:6]), O.rect(B[k, 0], B[k, 1], B[k, 2:4], B[k, 4:6])
+        assert abs(f(C.byref(ra), C.byref(rb), 4) - t[k]) <= 1e-10 * t[k]
+
+
+QUAD_CASES = [  # proj/tests/test_quadrature.cpp:11-79: (which, mode, a, b, singA, singB, exact, tol)
+    (0, 0, 0.0, 1.0, 0, 0, 1.0 / 3.0, 1e-12),
+    (1, 0, 0.0, 1.0, 0, 0, 1.0, 0.0),
+    (2, 0, 0.0, 1.0, 0, 0, 2 * np.log(2) - 1, 1e-8 * (2 * np.log(2) - 1)),
+    (3, 0, 2.0, 2.0, 0, 0, 0.0, 0.0),
+    (4, 0, 0.0, 3.1, 0, 0, 1 - np.cos(3.1), 1e-10),
+    (6, 1, 0.0, 1.0, 1, 0, 2.0, 1e-9),
+    (7, 1, 0.0, 1.0, 1, 0, -1.0, 1e-8),
+    (8, 1, 0.0, 1.0, 0, 1, 2.0, 1e-9),
+    (9, 1, 0.0, 1.0, 1, 1, 4.0, 1e-8),
+    (10, 2, -1.0, 1.0, 0, 0, 4.0, 1e-8),
+    (11, 2, -1.0, 2.0, 0, 0, 3.0, 1e-10),
+]
+
+
+@pytest.mark.parametrize("case", QUAD_CASES)
+def test_quadrature_known_answers(case):
+    which, mode, a, b, sa, sb, exact, tol = case
+    st, cv, ev = C.c_int(), C.c_int(), C.c_long()
+    v = O.orc().orc_quad_test(which, mode, a, b, sa, sb, C.byref(st), C.byref(cv), C.byref(ev))
+    assert st.value == 0
+    assert abs(v - exact) <= tol
+
+
+def test_quadrature_nonfinite_is_an_error():
+    st, cv, ev = C.c_int(), C.c_int(), C.c_long()
+    O.orc().orc_quad_test(5, 0, 0.0, 1.0, 0, 0, C.byref(st), C.byref(cv), C.byref(ev))
+    assert st.value == 2  # NumericalError("non-finite integrand sample")
+
+
+def _chol(A, B):
+    n = A.shape[0]
+    Bc = np.ascontiguousarray(np.atleast_2d(B.T))
+    X = np.zeros_like(Bc)
+    res = np.zeros(Bc.shape[0])
+    piv = C.c_int64(-1)
+    rc = O.orc().orc_cholesky_solve(n, np.ascontiguousarray(A).ctypes.data, Bc.shape[0], Bc.ctypes.data,
+                                    X.ctypes.data, res.ctypes.data, C.byref(piv))
+    return rc, X.T, res, piv.value
+
+
+def test_cholesky_restatement():
+    """test_solver.cpp:32-125 on the restated reference loop."""
+    rc, x, res, _ = _chol(np.eye(4), np.arange(4.0)[:, None])
+    assert rc == 0 and np.array_equal(x[:, 0], np.arange(4.0)) and res[0] == 0.0
+    rc, x, _, _ = _chol(np.diag([4.0, 9.0]), np.array([[2.0], [3.0]]))
+    assert abs(x[0, 0] - 0.5) < 1e-15 and abs(x[1, 0] - 1 / 3) < 1e-15
+    rng = np.random.default_rng(11)
+    M = rng.normal(size=(50, 50)); A = M.T @ M + np.eye(50); b = rng.normal(size=(50, 1))
+    rc, x, res, _ = _chol(A, b)
+    assert np.abs(x - np.linalg.solve(A, b)).max() <= 1e-9
+    assert res[0] <= 1e-10
+    rc, _, _, piv = _chol(np.array([[1.0, 2.0], [2.0, 1.0]]), np.ones((2, 1)))
+    assert rc == 2 and piv == 1
