@@ -33,6 +33,9 @@ __constant__ double c_gw[kQMax + 1][kQMax];
 // end-on singularity, rho = 1 + d + sqrt(d (2 + d)), error ~ rho^(-2q);
 // calibrated in tools/calib_far.c.
 __constant__ double c_delta[2][kQMax + 1];
+// Gauss-Legendre nodes / weights of the graded near-field rule (near_nodes(band) entries per band)
+__constant__ double c_nx[kNearBands][48];
+__constant__ double c_nw[kNearBands][48];
 }  // namespace gbem_gpu
 
 namespace {
@@ -53,6 +56,45 @@ enum StatIdx {
 
 constexpr int kTile = 32;
 constexpr int kClassifyThreads = 256;
+
+// n-point Gauss-Legendre nodes (ascending) and weights on [-1, 1] (Newton on P_n).
+void legendre_nodes(int q, double* gx, double* gw) {
+  for (int i = 0; i < q; ++i) {
+    long double x = cosl(3.14159265358979323846264338327950288L * (i + 0.75L) / (q + 0.5L));
+    long double p0 = 1, p1 = x, dp = 1;
+    for (int it = 0; it < 100; ++it) {
+      p0 = 1;
+      p1 = x;
+      for (int k = 2; k <= q; ++k) {
+        long double p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      if (q == 1) {
+        p1 = x;
+        p0 = 1;
+      }
+      dp = q * (x * p1 - p0) / (x * x - 1);
+      long double dx = p1 / dp;
+      x -= dx;
+      if (fabsl(dx) < 1e-19L) break;
+    }
+    p0 = 1;
+    p1 = x;
+    for (int k = 2; k <= q; ++k) {
+      long double p2 = ((2 * k - 1) * x * p1 - (k - 1) * p0) / k;
+      p0 = p1;
+      p1 = p2;
+    }
+    if (q == 1) {
+      p1 = x;
+      p0 = 1;
+    }
+    dp = q * (x * p1 - p0) / (x * x - 1);
+    gx[q - 1 - i] = (double)x;
+    gw[q - 1 - i] = (double)(2.0L / ((1.0L - x * x) * dp * dp));
+  }
+}
 
 // Gauss-Legendre nodes on [-1, 1] by Newton on P_q.
 void legendre_table(double gx[kQMax + 1][kQMax], double gw[kQMax + 1][kQMax]) {
@@ -115,8 +157,19 @@ __device__ __forceinline__ uint32_t classify_pair(const DPanel& A, const DPanel&
   double dm = fmax(hypot(la, lb), hypot(lc, ld));
   bool same_axis = A.axis == B.axis;
   if (gap < near_ratio * dm) {
-    if (same_axis) return A.level == B.level ? kClsCoplanar : kClsParallel;
-    return kClsOrthogonal;
+    if (same_axis && A.level == B.level) return kClsCoplanar;
+    int band;
+    if (gap == 0.0 || gap >= 0.1 * dm)
+      band = 0;
+    else if (gap >= 0.02 * dm)
+      band = 1;
+    else if (gap >= 0.005 * dm)
+      band = 2;
+    else if (gap >= 1e-3 * dm)
+      band = 3;
+    else
+      return same_axis ? kClsParallel : kClsOrthogonal;  // near contact: adaptive Romberg
+    return (same_axis ? kClsParallelGL : kClsOrthogonalGL) + band;
   }
   int band = gap < dm ? 1 : 0;
   int qs = far_order(gap, 0.5 * la, band), qt = far_order(gap, 0.5 * lb, band);
@@ -226,9 +279,14 @@ __global__ void __launch_bounds__(1024)
   }
   if (t == 1023) offsets[kNumKeys] = run;
   if (t == 0) {
+    unsigned long long par = counts[kClsParallel], orth = counts[kClsOrthogonal];
+    for (int b = 0; b < kNearBands; ++b) {
+      par += counts[kClsParallelGL + b];
+      orth += counts[kClsOrthogonalGL + b];
+    }
     atomicAdd(&stats[ST_COP], (unsigned long long)counts[kClsCoplanar]);
-    atomicAdd(&stats[ST_PAR], (unsigned long long)counts[kClsParallel]);
-    atomicAdd(&stats[ST_ORTH], (unsigned long long)counts[kClsOrthogonal]);
+    atomicAdd(&stats[ST_PAR], par);
+    atomicAdd(&stats[ST_ORTH], orth);
   }
   __syncthreads();
   if (t == 0) {
@@ -319,16 +377,20 @@ __device__ __forceinline__ double far_gauss(const DPanel& I, int qs, int qt, con
       for (int u = 0; u < qu; ++u) {
         const double du = pu - fma(hU, c_gx[qu][u], cU);
         const double cu = fma(du, du, pz2);
-        double row = 0.0;
+        // two partial sums break the FMA dependency chain along v
+        double row0 = 0.0, row1 = 0.0;
 #pragma unroll
-        for (int v = 0; v < QV; ++v) row = fma(Wv[v], rsq64(cu + dv2[v]), row);
-        inner = fma(hU * c_gw[qu][u], row, inner);
+        for (int v = 0; v < QV; v += 2) {
+          row0 = fma(Wv[v], rsq64(cu + dv2[v]), row0);
+          if (v + 1 < QV) row1 = fma(Wv[v + 1], rsq64(cu + dv2[v + 1]), row1);
+        }
+        inner = fma(hU * c_gw[qu][u], row0 + row1, inner);
       }
       acc = fma(wst, inner, acc);
     }
   }
   const double E = (double)qs * qt * qu * QV;
-  flops += 11.0 * E + 8.0 * qs * qt * qu + (9.0 + 2.0 * QV) * qs * qt + 3.0 * qs + 3.0 * QV + 13.0;
+  flops += 11.0 * E + 9.0 * qs * qt * qu + (9.0 + 2.0 * QV) * qs * qt + 3.0 * qs + 3.0 * QV + 13.0;
   return acc / kFourPi;
 }
 
@@ -372,7 +434,7 @@ __device__ __forceinline__ double warp_reduce_d(double x) {
   return x;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
     k_far(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
           const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats) {
   const uint32_t begin = offsets[kFarKeyBase], end = offsets[kNumKeys];
@@ -418,11 +480,40 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Graded Gauss-Legendre near field (keys 2..9), one thread per pair.
+__global__ void __launch_bounds__(128)
+    k_near_gl(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
+              const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats) {
+  const uint32_t begin = offsets[kClsParallelGL], end = offsets[kClsOrthogonalGL + kNearBands];
+  long long evals = 0, nonfinite = 0;
+  for (uint32_t idx = begin + blockIdx.x * blockDim.x + threadIdx.x; idx < end; idx += gridDim.x * blockDim.x) {
+    uint64_t e = queue[idx];
+    uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e);
+    DPanel Pi = load_panel(P, i), Pj = load_panel(P, j);
+    bool swap = d_rect_less(Pj, Pi);
+    const DPanel& a = swap ? Pj : Pi;
+    const DPanel& b = swap ? Pi : Pj;
+    bool bad = false;
+    const bool par = key < (uint32_t)kClsOrthogonalGL;
+    const int band = (int)key - (par ? kClsParallelGL : kClsOrthogonalGL);
+    double U = par ? gl_u_parallel(a, b, band, c_nx, c_nw, bad) : gl_u_orthogonal(a, b, band, c_nx, c_nw, bad);
+    evals += 2 * near_nodes(band);
+    store_value(o, i, j, Pi, Pj, U);
+    if (!o.A && o.conv) o.conv[i] = 1;
+    if (bad) {
+      ++nonfinite;
+      atomicMin(&stats[ST_FIRST_BAD], ((unsigned long long)i << 32) | j);
+    }
+  }
+  if (nonfinite) atomicAdd(&stats[ST_NONFINITE], (unsigned long long)nonfinite);
+  atomicAdd(&stats[ST_NEAR_EVALS], (unsigned long long)evals);
+}
+
 __global__ void __launch_bounds__(128)
     k_near_warp(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
                 const uint32_t* __restrict__ offsets, OutSpec o, double rel_tol, int max_levels,
                 unsigned long long* stats) {
-  const uint32_t begin = offsets[kClsParallel], end = offsets[kClsOrthogonal + 1];
+  const uint32_t begin = offsets[kClsParallel], end = offsets[kClsOrthogonal + 1];  // keys 10, 11
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -546,6 +637,8 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
   cudaEventRecord(ctx->ev[3], ctx->stream);
   k_coplanar<<<sms * 4, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o);
   GBEM_LAUNCH_CHECK(ctx);
+  k_near_gl<<<sms * 4, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, ctx->d_stats);
+  GBEM_LAUNCH_CHECK(ctx);
   k_near_warp<<<sms * 8, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o,
                                                 cfg.rel_tol, cfg.max_levels, ctx->d_stats);
   GBEM_LAUNCH_CHECK(ctx);
@@ -596,6 +689,10 @@ int gbem_internal_init_tables(gbem_ctx* ctx) {
   legendre_table(gx, gw);
   GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_gx, gx, sizeof(gx)));
   GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_gw, gw, sizeof(gw)));
+  double nx[kNearBands][48] = {}, nw[kNearBands][48] = {};
+  for (int b = 0; b < kNearBands; ++b) legendre_nodes(near_nodes(b), nx[b], nw[b]);
+  GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_nx, nx, sizeof(nx)));
+  GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_nw, nw, sizeof(nw)));
   return GBEM_OK;
 }
 

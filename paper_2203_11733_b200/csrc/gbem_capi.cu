@@ -142,6 +142,9 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   if (ctx->h_info) cudaFreeHost(ctx->h_info);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
+  if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+  if (ctx->ev_panel) cudaEventDestroy(ctx->ev_panel);
+  if (ctx->ev_col) cudaEventDestroy(ctx->ev_col);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }

@@ -23,8 +23,15 @@ constexpr int kQMax = 12;                                  // max far-field Gaus
 // Pair classes (queue key < kFarKeyBase).  Far keys pack four 4-bit orders.
 enum PairClass : uint32_t {
   kClsCoplanar = 1,   // coplanar closed form (self, touching, near coplanar): kernels.hpp:86-94
-  kClsParallel = 2,   // offset-parallel near pair, Romberg over the tent weight: kernels.hpp:138-153
-  kClsOrthogonal = 3, // orthogonal near pair, 2x Romberg with splits / t^4: kernels.hpp:175-214
+  // offset-parallel / orthogonal near pairs on the reference's reduced 1-D
+  // integrands (kernels.hpp:138-153, 175-214) with graded Gauss-Legendre,
+  // band b = 0..3 -> 20 / 24 / 32 / 48 nodes per half segment
+  kClsParallelGL = 2,    // keys 2..5
+  kClsOrthogonalGL = 6,  // keys 6..9
+  // near-contact pairs (gap < 1e-3 diameters, not touching): the reference's
+  // adaptive Romberg (quadrature.hpp:27-113), one warp per pair
+  kClsParallel = 10,
+  kClsOrthogonal = 11,
   kFarKeyBase = 16,
 };
 constexpr int kNumKeys = 1 << 16;

@@ -47,6 +47,8 @@ struct gbem_ctx {
   size_t rhs_cap = 0;
 
   cudaEvent_t ev[8] = {};
+  cudaStream_t side_stream = nullptr;  // high-priority look-ahead stream of the factorisation
+  cudaEvent_t ev_panel = nullptr, ev_col = nullptr;
 
   int fail(int code, const std::string& msg) {
     err = msg;

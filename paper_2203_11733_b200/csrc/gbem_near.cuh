@@ -382,4 +382,108 @@ __device__ inline double warp_u_orthogonal(const DPanel& A, const DPanel& B, dou
   return (tx + ty) / kFourPi;
 }
 
+// ---------------------------------------------------------------------------
+// Fixed-cost near field: the same reduced integrands, each reference segment
+// split at its midpoint and both halves integrated with x = end -+ t^2 grading
+// toward their outer ends and an n-point Gauss-Legendre rule in t (nodes never
+// touch an endpoint, so endpoint singularities need no probing).  Calibrated in
+// tools/near_gl_experiment.c against the tight-tolerance reference algorithm:
+// touching pairs <= 6e-13 with n = 20; gap/diam >= 0.1: n = 20, >= 0.02: n = 24,
+// >= 0.005: n = 32, >= 1e-3: n = 48 (<= 1e-11 worst).  One thread per pair.
+
+constexpr int kNearBands = 4;
+__host__ __device__ constexpr int near_nodes(int band) {
+  return band == 0 ? 20 : band == 1 ? 24 : band == 2 ? 32 : 48;
+}
+
+template <class F>
+__device__ double gl_graded(const F& f, double a, double b, int band, const double (*nx)[48],
+                            const double (*nw)[48], bool& bad) {
+  if (a == b) return 0.0;
+  const int n = near_nodes(band);
+  const double m = 0.5 * (a + b);
+  double total = 0.0;
+#pragma unroll 1
+  for (int side = 0; side < 2; ++side) {
+    const double base = side ? b : a;
+    const double len = side ? b - m : m - a;
+    const double h = 0.5 * sqrt(len);
+    double part = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < n; ++i) {
+      const double t = fma(h, nx[band][i], h);
+      const double x = side ? base - t * t : base + t * t;
+      const double v = f(x);
+      bad |= !isfinite(v);
+      part = fma(nw[band][i] * t, v, part);
+    }
+    total += 2.0 * h * part;
+  }
+  return total;
+}
+
+// uParallelOffset (kernels.hpp:138-153) with the graded Gauss rule.
+__device__ inline double gl_u_parallel(const DPanel& A, const DPanel& B, int band, const double (*nx)[48],
+                                       const double (*nw)[48], bool& bad) {
+  double off = A.level - B.level;
+  ParIntegrand f;
+  Corners c(A.a0, A.a1, B.a0, B.a1);
+  for (int k = 0; k < 4; ++k) f.val[k] = c.val[k];
+  f.b2 = off * off;
+  double xd = A.b0, xu = A.b1, yd = B.b0, yu = B.b1;
+  double t0 = xd - yu, t3 = xu - yd;
+  double da = xd - yd, db = xu - yu;
+  f.t0 = t0;
+  f.t3 = t3;
+  f.plateau = (yu - yd) < (xu - xd) ? (yu - yd) : (xu - xd);
+  double pts[5] = {t0, db < da ? db : da, da < db ? db : da, t3, 0.0};
+  int n = (t0 < 0.0 && 0.0 < t3) ? 5 : 4;
+  sort5(pts, n);
+  double cuts[5];
+  int count = 0;
+  for (int i = 0; i < n; ++i)
+    if (count == 0 || pts[i] > cuts[count - 1]) cuts[count++] = pts[i];
+  double total = 0.0;
+  for (int i = 0; i + 1 < count; ++i) total += gl_graded(f, cuts[i], cuts[i + 1], band, nx, nw, bad);
+  return total / kFourPi;
+}
+
+template <class F>
+__device__ double gl_split0(const F& f, double a, double b, int band, const double (*nx)[48],
+                            const double (*nw)[48], bool& bad) {
+  if (a < 0.0 && 0.0 < b) return gl_graded(f, a, 0.0, band, nx, nw, bad) + gl_graded(f, 0.0, b, band, nx, nw, bad);
+  return gl_graded(f, a, b, band, nx, nw, bad);
+}
+
+// orthFrame + uOrthogonal (kernels.hpp:175-214, 245-255) with the graded Gauss rule.
+__device__ inline double gl_u_orthogonal(const DPanel& A, const DPanel& B, int band, const double (*nx)[48],
+                                         const double (*nw)[48], bool& bad) {
+  int shared = 3 - A.axis - B.axis;
+  double s1lo, s1hi, t1lo, t1hi, i3lo, i3hi, j2lo, j2hi;
+  panel_extent(A, shared, s1lo, s1hi);
+  panel_extent(B, shared, t1lo, t1hi);
+  panel_extent(A, B.axis, i3lo, i3hi);
+  panel_extent(B, A.axis, j2lo, j2hi);
+  double s3lo = i3lo - B.level, s3hi = i3hi - B.level;
+  double t2lo = j2lo - A.level, t2hi = j2hi - A.level;
+  Corners c(s1lo, s1hi, t1lo, t1hi);
+  double scale = dmax4(s1hi - s1lo, t1hi - t1lo, s3hi - s3lo, t2hi - t2lo);
+  scale = scale < 1e-30 ? 1e-30 : scale;
+  OrthFx fx;
+  OrthFy fy;
+  for (int k = 0; k < 4; ++k) {
+    fx.val[k] = c.val[k];
+    fy.val[k] = c.val[k];
+  }
+  fx.y2d = t2lo;
+  fx.y2u = t2hi;
+  fx.guard = 1e-14 * scale;
+  fy.x3d = s3lo;
+  fy.x3u = s3hi;
+  fy.guard = fx.guard;
+  double tx = gl_split0(fx, s3lo, s3hi, band, nx, nw, bad);
+  double ty = gl_split0(fy, t2lo, t2hi, band, nx, nw, bad);
+  return (tx + ty) / kFourPi;
+}
+
 }  // namespace gbem_gpu

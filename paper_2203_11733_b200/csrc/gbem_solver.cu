@@ -55,19 +55,28 @@ enum GemmMode { kSub = 0, kStore = 1 };
 template <int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_nt(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb,
-              int M, int N, int K, int lower) {
+              int M, int N, int K, int tile_mode) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                       // [STAGES][BK][LDS]
   double* Bs = smem + STAGES * BK * LDS;   // [STAGES][BK][LDS]
+  // tile_mode 0: dense grid (blockIdx.x, blockIdx.y); 1: all lower tiles (tm >= tn);
+  // 2: first tile column only (tn = 0, the look-ahead column); 3: lower tiles with tn >= 1.
   int tm, tn;
-  if (lower) {
-    // linear lower-triangle tile index -> (tm >= tn)
+  const int lower = tile_mode != 0;
+  if (tile_mode == 1 || tile_mode == 3) {
     long long t = blockIdx.x;
     int r = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
     while ((long long)(r + 1) * (r + 2) / 2 <= t) ++r;
     while ((long long)r * (r + 1) / 2 > t) --r;
     tm = r;
     tn = (int)(t - (long long)r * (r + 1) / 2);
+    if (tile_mode == 3) {
+      ++tm;
+      ++tn;
+    }
+  } else if (tile_mode == 2) {
+    tm = blockIdx.x;
+    tn = 0;
   } else {
     tm = blockIdx.x;
     tn = blockIdx.y;
@@ -165,73 +174,86 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-// Factor the kb x kb diagonal block at A (lda) in shared memory (right-looking,
-// one column per step), write L11 back, then invert L11 in place (column
-// sweep j = kb-1..0, LAPACK dtrti2 order) and write inv(L11) (column-major,
-// ld = NB) into Linv for the GEMM-form trsm and the solves.  info[0] receives
-// the first failing global row (atomicMin); the factorisation continues with a
-// unit pivot so the launch sequence stays fixed.
+// Factor the kb x kb diagonal block at A (lda) in shared memory and, in the
+// same column sweep, form X = inv(L11) (forward substitution on the identity
+// interleaved with the factorisation), one __syncthreads per column:
+//   phase j: with s_j = sqrt(a_jj) (column j still unscaled),
+//     a(r,c) -= a(r,j) a(c,j) / a_jj           j < c <= r   (Cholesky trailing update)
+//     S(r,c) -= a(r,j) S(j,c) / a_jj            c < j < r    (X rows, S = X * diag(L))
+//     S(r,j)  = -a(r,j) / a_jj                  j < r
+//   and column j-1 / row j-1 are finalised (scaled by 1/s_{j-1}) in the same
+//   phase, since phase j never touches them.  X's strict lower part is kept
+//   transposed in the strict upper half of the smem tile, its diagonal in xd.
+// L11 goes back to A (lower), X to Linv (column-major, ld = NB) for the
+// GEMM-form trsm and the triangular solves.  info[0] receives the first failing
+// global row (atomicMin); a failed pivot continues as 1 so the launch sequence
+// stays fixed (the caller reports "matrix not positive definite").
 __global__ void __launch_bounds__(512)
     k_potrf_diag(double* A, long long lda, int kb, int row0, double* Linv, int* info) {
   extern __shared__ __align__(16) double sm[];
   constexpr int LD = NB + 1;
-  double* a = sm;             // [NB][LD] column-major: a[c*LD + r]
-  double* tmp = sm + NB * LD; // one column
-  __shared__ double s_inv_piv;
-  __shared__ int s_bad;
-  const int tid = threadIdx.x, nth = blockDim.x;
-  for (int idx = tid; idx < kb * kb; idx += nth) {
+  double* a = sm;               // [NB][LD] column-major: a[c*LD + r]
+  double* isq = sm + NB * LD;   // 1/s_j per column
+  double* sq = isq + NB;        // s_j
+  const int tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5, nty = blockDim.x >> 5;
+  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
     int c = idx / kb, r = idx % kb;
     a[c * LD + r] = r >= c ? A[(long long)c * lda + r] : 0.0;
   }
-  if (tid == 0) s_bad = 0;
   __syncthreads();
+  bool bad = false;
   for (int j = 0; j < kb; ++j) {
-    if (tid == 0) {
-      double d = a[j * LD + j];
-      if (!(d > 0.0)) {
-        if (!s_bad) atomicMin(info, row0 + j);
-        s_bad = 1;
-        d = 1.0;
-      }
-      double sq = sqrt(d);
-      a[j * LD + j] = sq;
-      s_inv_piv = 1.0 / sq;
+    double d = a[j * LD + j];
+    if (!(d > 0.0)) {
+      if (tid == 0 && !bad) atomicMin(info, row0 + j);
+      bad = true;
+      d = 1.0;
     }
-    __syncthreads();
-    const double ip = s_inv_piv;
-    for (int r = j + 1 + tid; r < kb; r += nth) a[j * LD + r] *= ip;
-    __syncthreads();
-    const int m = kb - j - 1;
-    for (int idx = tid; idx < m * m; idx += nth) {
-      int c = j + 1 + idx / m, r = j + 1 + idx % m;
-      if (r >= c) a[c * LD + r] -= a[j * LD + r] * a[j * LD + c];
+    const double sj = sqrt(d), inv_s = 1.0 / sj, inv_d = inv_s * inv_s;
+    if (tid == 0) {
+      isq[j] = inv_s;
+      sq[j] = sj;
+    }
+    // finalise column j-1 of L and row j-1 of X
+    if (j > 0) {
+      const int p = j - 1;
+      const double ip = isq[p];
+      for (int r = p + 1 + tid; r < kb; r += blockDim.x) a[p * LD + r] *= ip;  // L(r,p)
+      for (int c = tid; c < p; c += blockDim.x) a[p * LD + c] *= ip;          // X(p,c) stored at (c,p)
+    }
+    for (int r = j + 1 + ty; r < kb; r += nty) {
+      const double arj = a[j * LD + r] * inv_d;
+      for (int c = tx; c <= r; c += 32) {
+        if (c > j)
+          a[c * LD + r] -= arj * a[j * LD + c];       // trailing Cholesky update
+        else if (c < j)
+          a[r * LD + c] -= arj * a[j * LD + c];       // S(r,c) -= L(r,j) X(j,c)   (stored at (c,r))
+        else
+          a[r * LD + j] = -arj;                        // S(r,j) = -L(r,j) / L(j,j)
+      }
     }
     __syncthreads();
   }
-  for (int idx = tid; idx < kb * kb; idx += nth) {
-    int c = idx / kb, r = idx % kb;
-    if (r >= c) A[(long long)c * lda + r] = a[c * LD + r];
+  if (kb > 0) {
+    const int p = kb - 1;
+    const double ip = isq[p];
+    for (int c = tid; c < p; c += blockDim.x) a[p * LD + c] *= ip;
   }
   __syncthreads();
-  // in-place inverse: for j = kb-1..0: a[j][j] = 1/a[j][j];
-  // a[j+1:, j] = -a[j][j] * T * a[j+1:, j], T = already-inverted trailing block
-  for (int j = kb - 1; j >= 0; --j) {
-    for (int r = j + 1 + tid; r < kb; r += nth) tmp[r] = a[j * LD + r];
-    __syncthreads();
-    const double ajj = 1.0 / a[j * LD + j];
-    for (int r = j + 1 + tid; r < kb; r += nth) {
-      double s = 0.0;
-      for (int k = j + 1; k <= r; ++k) s += a[k * LD + r] * tmp[k];
-      a[j * LD + r] = -ajj * s;
-    }
-    __syncthreads();
-    if (tid == 0) a[j * LD + j] = ajj;
-    __syncthreads();
+  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+    int c = idx / kb, r = idx % kb;
+    if (r > c) A[(long long)c * lda + r] = a[c * LD + r];
+    else if (r == c) A[(long long)c * lda + r] = sq[r];
   }
-  for (int idx = tid; idx < NB * NB; idx += nth) {
+  for (int idx = tid; idx < NB * NB; idx += blockDim.x) {
     int c = idx / NB, r = idx % NB;
-    Linv[c * NB + r] = (r < kb && c < kb && r >= c) ? a[c * LD + r] : 0.0;
+    double v = 0.0;
+    if (r < kb && c < kb) {
+      if (r > c) v = a[r * LD + c];
+      else if (r == c) v = isq[r];
+    }
+    Linv[c * NB + r] = v;
   }
 }
 
@@ -469,7 +491,7 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kSub>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)((NB + 1) * (NB + 1) * sizeof(double))));
+                                        (int)((NB * (NB + 1) + 2 * NB) * sizeof(double))));
     attr_done = true;
   }
   cudaStream_t s = ctx->stream;
@@ -478,25 +500,47 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
   k_save_diag<<<(n + 255) / 256, 256, 0, s>>>(ctx->d_A, lda, n, ctx->d_diag);
   GBEM_LAUNCH_CHECK(ctx);
   cudaEventRecord(ctx->ev[0], s);
-  const size_t potrf_smem = (size_t)(NB + 1) * (NB + 1) * sizeof(double);
+  const size_t potrf_smem = (size_t)(NB * (NB + 1) + 2 * NB) * sizeof(double);
+  // Look-ahead: the diagonal factor + panel trsm of block k+1 run on the
+  // high-priority side stream while the main stream finishes the trailing
+  // update of block k (only block column k+1 has to be updated first).
+  if (!ctx->side_stream) {
+    int lo = 0, hi = 0;
+    GBEM_CUDA(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    GBEM_CUDA(ctx, cudaStreamCreateWithPriority(&ctx->side_stream, cudaStreamNonBlocking, hi));
+    GBEM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_panel, cudaEventDisableTiming));
+    GBEM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_col, cudaEventDisableTiming));
+  }
+  cudaStream_t s1 = ctx->side_stream;
+  GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_col, s));
   for (int b = 0; b < nblk; ++b) {
     int k0 = b * NB, kb = std::min(NB, n - k0);
-    double* Akk = ctx->d_A + (long long)k0 * lda + k0;
-    k_potrf_diag<<<1, 512, potrf_smem, s>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
-    GBEM_LAUNCH_CHECK(ctx);
     int m = n - k0 - kb;
-    if (m <= 0) break;
+    double* Akk = ctx->d_A + (long long)k0 * lda + k0;
     double* A21 = Akk + kb;  // rows k0+kb.., cols k0..
-    // L21 = A21 * inv(L11)^T  (in place)
-    k_gemm_nt<kStore><<<dim3((m + BM - 1) / BM, 1), GEMM_THREADS, GEMM_SMEM, s>>>(
-        A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb, 0);
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ev_col, 0));
+    k_potrf_diag<<<1, 512, potrf_smem, s1>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
     GBEM_LAUNCH_CHECK(ctx);
-    // A22 -= L21 L21^T (lower tiles)
+    if (m > 0) {
+      // L21 = A21 * inv(L11)^T  (in place, one CTA per 128-row strip)
+      k_gemm_nt<kStore><<<dim3((m + BM - 1) / BM, 1), GEMM_THREADS, GEMM_SMEM, s1>>>(
+          A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb, 0);
+      GBEM_LAUNCH_CHECK(ctx);
+    }
+    GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_panel, s1));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_panel, 0));
+    if (m <= 0) break;
+    // A22 -= L21 L21^T: first the next block column (tile column 0), then the rest
     int nt = (m + BM - 1) / BM;
-    long long ntiles = (long long)nt * (nt + 1) / 2;
     double* A22 = ctx->d_A + (long long)(k0 + kb) * lda + (k0 + kb);
-    k_gemm_nt<kSub><<<(unsigned)ntiles, GEMM_THREADS, GEMM_SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m, kb, 1);
+    k_gemm_nt<kSub><<<(unsigned)nt, GEMM_THREADS, GEMM_SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m, kb, 2);
     GBEM_LAUNCH_CHECK(ctx);
+    GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_col, s));
+    if (nt > 1) {
+      long long rest = (long long)(nt - 1) * nt / 2;
+      k_gemm_nt<kSub><<<(unsigned)rest, GEMM_THREADS, GEMM_SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m, kb, 3);
+      GBEM_LAUNCH_CHECK(ctx);
+    }
   }
   cudaEventRecord(ctx->ev[1], s);
   GBEM_CUDA(ctx, cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(int), cudaMemcpyDeviceToHost, s));
