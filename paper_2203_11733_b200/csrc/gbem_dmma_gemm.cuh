@@ -1,0 +1,206 @@
+// gbem_dmma_gemm.cuh — FP64 tensor-core (DMMA) GEMM for the Cholesky trailing
+// update and the GEMM-form trsm: C (M x N) op= A (M x K) * B (N x K)^T, all
+// column-major.  sm_100a has no tcgen05 FP64 kind; the FP64 tensor path is the
+// warp-level mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), measured at 37.1 TFLOP/s
+// (tools/fp64_peaks.cu).
+//
+// CTA tile 128 x BN, 8 warps as 4 (M) x 2 (N), warp tile 32 x BN/2 =
+// 4 x BN/16 DMMA fragments; BK = 16 slabs through a 3-stage cp.async pipeline;
+// shared-memory row stride = tile width + 8 doubles makes the 8-byte fragment
+// loads conflict-free.  BN = 64 is the trailing-update shape: ~100 registers,
+// 80 KB shared memory, two CTAs per SM, so one CTA's epilogue (C read-modify-
+// write) and prologue overlap the other's DMMA main loop.  BN = 128 is the
+// trsm shape (one CTA owns complete rows, so C may alias A).
+//   kSub  : C -= A B^T   (C must not alias A or B)
+//   kStore: C  = A B^T
+// Tile enumeration (tile_mode): 0 dense grid (blockIdx.x, blockIdx.y);
+// 1 every tile touching the lower triangle; 2 tiles with column index < split;
+// 3 lower tiles with column index >= split (the look-ahead split of the
+// Cholesky: block column k+1 first, then the rest).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace gbem_gemm {
+
+constexpr int BM = 128, BK = 16, STAGES = 3;
+constexpr int GEMM_THREADS = 256;
+
+template <int BN>
+struct Shape {
+  static constexpr int LDA = BM + 8;  // smem row stride (doubles) of the A slab
+  static constexpr int LDB = BN + 8;
+  static constexpr int WN = BN / 2;   // warp tile width
+  static constexpr int FN = WN / 8;   // DMMA fragments along N per warp
+  static constexpr size_t SMEM = (size_t)STAGES * BK * (LDA + LDB) * sizeof(double);
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+enum GemmMode { kSub = 0, kStore = 1 };
+
+// Number of 128 x BN tiles touching the lower triangle in tile row tm (BM = r*BN).
+template <int BN>
+__host__ __device__ inline long long lower_tiles_before(long long tm) {
+  constexpr long long r = BM / BN;  // tile columns per tile row step
+  // row tm spans tile columns 0 .. r*tm + r - 1  ->  r*(tm+1) tiles
+  return r * tm * (tm + 1) / 2;
+}
+
+template <int BN>
+__device__ inline void lower_tile(long long t, int split, int mode, int& tm, int& tn) {
+  constexpr int r = BM / BN;
+  if (mode == 1) {
+    // t = r*tm(tm+1)/2 + tn
+    int x = (int)((sqrt(8.0 * (double)t / r + 1.0) - 1.0) * 0.5);
+    while (lower_tiles_before<BN>(x + 1) <= t) ++x;
+    while (lower_tiles_before<BN>(x) > t) --x;
+    tm = x;
+    tn = (int)(t - lower_tiles_before<BN>(x));
+  } else {
+    // mode 3: columns >= split (split = r: one block column of 128), rows tm >= 1
+    // per row tm: tile columns split .. r*tm + r - 1  ->  r*tm + r - split tiles
+    long long lo = 0, hi = 1 << 20;
+    while (lo < hi) {  // smallest tm with cum(tm+1) > t
+      long long mid = (lo + hi) >> 1;
+      long long cum = lower_tiles_before<BN>(mid + 1) - (long long)split * (mid + 1);
+      if (cum > t)
+        hi = mid;
+      else
+        lo = mid + 1;
+    }
+    tm = (int)lo;
+    long long before = lower_tiles_before<BN>(lo) - (long long)split * lo;
+    tn = split + (int)(t - before);
+  }
+}
+
+template <int MODE, int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, BN == 64 ? 2 : 1)
+    k_gemm_nt(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb, int M,
+              int N, int K, int tile_mode, int split) {
+  using S = Shape<BN>;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                           // [STAGES][BK][LDA]
+  double* Bs = smem + STAGES * BK * S::LDA;    // [STAGES][BK][LDB]
+  int tm, tn;
+  if (tile_mode == 0) {
+    tm = blockIdx.x;
+    tn = blockIdx.y;
+  } else if (tile_mode == 2) {
+    tm = blockIdx.x;
+    tn = blockIdx.y;
+  } else {
+    lower_tile<BN>(blockIdx.x, split, tile_mode, tm, tn);
+  }
+  const bool lower = tile_mode != 0;
+  const int m0 = tm * BM, n0 = tn * BN;
+  if (lower && n0 > m0 + BM - 1) return;  // tile entirely above the diagonal
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  double acc[4][S::FN][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < S::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KT = (K + BK - 1) / BK;
+  auto load_stage = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    double* as = As + st * BK * S::LDA;
+    double* bs = Bs + st * BK * S::LDB;
+#pragma unroll
+    for (int c = tid; c < BK * BM / 2; c += GEMM_THREADS) {
+      int kk = c / (BM / 2), mm = (c % (BM / 2)) * 2;
+      int gk = k0 + kk, gm = m0 + mm;
+      int bytes = 0;
+      const double* src = A;
+      if (gk < K && gm < M) {
+        bytes = gm + 1 < M ? 16 : 8;
+        src = A + (long long)gk * lda + gm;
+      }
+      cp_async16(as + kk * S::LDA + mm, src, bytes);
+    }
+#pragma unroll
+    for (int c = tid; c < BK * BN / 2; c += GEMM_THREADS) {
+      int kk = c / (BN / 2), nn = (c % (BN / 2)) * 2;
+      int gk = k0 + kk, gn = n0 + nn;
+      int bytes = 0;
+      const double* src = B;
+      if (gk < K && gn < N) {
+        bytes = gn + 1 < N ? 16 : 8;
+        src = B + (long long)gk * ldb + gn;
+      }
+      cp_async16(bs + kk * S::LDB + nn, src, bytes);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    int nxt = kt + STAGES - 1;
+    if (nxt < KT) load_stage(nxt, nxt % STAGES);
+    cp_async_commit();
+    const double* as = As + (kt % STAGES) * BK * S::LDA;
+    const double* bs = Bs + (kt % STAGES) * BK * S::LDB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[S::FN];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[(kk + t4) * S::LDA + wm * 32 + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < S::FN; ++j) bf[j] = bs[(kk + t4) * S::LDB + wn * S::WN + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < S::FN; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: fragment (i,j) holds rows m0+wm*32+i*8+g, cols n0+wn*WN+j*8+2*t4+{0,1};
+  // loads of a fragment row are issued together before its stores
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm * 32 + i * 8 + g;
+    double cur[S::FN][2];
+    bool ok[S::FN][2];
+#pragma unroll
+    for (int j = 0; j < S::FN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = n0 + wn * S::WN + j * 8 + 2 * t4 + e;
+        ok[j][e] = row < M && col < N && !(lower && col > row);
+        cur[j][e] = (MODE == kSub && ok[j][e]) ? C[(long long)col * ldc + row] : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < S::FN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = n0 + wn * S::WN + j * 8 + 2 * t4 + e;
+        if (ok[j][e]) C[(long long)col * ldc + row] = MODE == kSub ? cur[j][e] - acc[i][j][e] : acc[i][j][e];
+      }
+  }
+}
+
+}  // namespace gbem_gemm

@@ -12,168 +12,19 @@
 // residual uses the original A.  Block size NB = 128:
 //   k_potrf_diag  : one CTA factors the NB x NB diagonal block in shared memory
 //                   and forms inv(L11) (kept for the solves);
-//   k_gemm_nt<STORE>: L21 = A21 * inv(L11)^T (trsm as a DMMA GEMM, in place);
-//   k_gemm_nt<SUB>  : A22 -= L21 * L21^T on lower 128x128 tiles (the O(n^3) part).
+//   k_gemm_nt<STORE,128>: L21 = A21 * inv(L11)^T (trsm as a DMMA GEMM, in place);
+//   k_gemm_nt<SUB,64>   : A22 -= L21 * L21^T on lower 128x64 tiles (the O(n^3) part).
 #include <algorithm>
 #include <cmath>
 #include <vector>
 
 #include "gbem_ctx.cuh"
+#include "gbem_dmma_gemm.cuh"
 
 namespace {
 
+using namespace gbem_gemm;
 constexpr int NB = 128;       // Cholesky block size
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
-constexpr int LDS = BM + 8;   // smem row stride in doubles: conflict-free fragment loads
-constexpr int GEMM_THREADS = 256;
-constexpr size_t GEMM_SMEM = (size_t)STAGES * 2 * BK * LDS * sizeof(double);
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
-enum GemmMode { kSub = 0, kStore = 1 };
-
-// C (M x N) op= A (M x K) * B (N x K)^T, all column-major.
-//   kSub  : C -= A B^T; tiles restricted to the lower triangle when `lower`
-//           (tile (I,J) with I >= J; diagonal tiles write row >= col only).
-//   kStore: C  = A B^T (C may alias A: each CTA owns full rows, BN >= N).
-// Tile 128 x 128, 8 warps as 4 (M) x 2 (N), warp tile 32 x 64 = 4 x 8 DMMA
-// fragments; BK = 16 slabs through a 3-stage cp.async pipeline.
-template <int MODE>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_gemm_nt(double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb,
-              int M, int N, int K, int tile_mode) {
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;                       // [STAGES][BK][LDS]
-  double* Bs = smem + STAGES * BK * LDS;   // [STAGES][BK][LDS]
-  // tile_mode 0: dense grid (blockIdx.x, blockIdx.y); 1: all lower tiles (tm >= tn);
-  // 2: first tile column only (tn = 0, the look-ahead column); 3: lower tiles with tn >= 1.
-  int tm, tn;
-  const int lower = tile_mode != 0;
-  if (tile_mode == 1 || tile_mode == 3) {
-    long long t = blockIdx.x;
-    int r = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-    while ((long long)(r + 1) * (r + 2) / 2 <= t) ++r;
-    while ((long long)r * (r + 1) / 2 > t) --r;
-    tm = r;
-    tn = (int)(t - (long long)r * (r + 1) / 2);
-    if (tile_mode == 3) {
-      ++tm;
-      ++tn;
-    }
-  } else if (tile_mode == 2) {
-    tm = blockIdx.x;
-    tn = 0;
-  } else {
-    tm = blockIdx.x;
-    tn = blockIdx.y;
-  }
-  const int m0 = tm * BM, n0 = tn * BN;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 3, wn = warp >> 2;
-  const int g = lane >> 2, t4 = lane & 3;
-
-  double acc[4][8][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  const int KT = (K + BK - 1) / BK;
-  // each stage: A slab BK x BM (1024 x 16B chunks... 16*128/2 = 1024) and B slab
-  auto load_stage = [&](int kt, int st) {
-    const int k0 = kt * BK;
-    double* as = As + st * BK * LDS;
-    double* bs = Bs + st * BK * LDS;
-#pragma unroll
-    for (int c = tid; c < BK * BM / 2; c += GEMM_THREADS) {
-      int kk = c / (BM / 2), mm = (c % (BM / 2)) * 2;
-      int gk = k0 + kk, gm = m0 + mm;
-      int bytes = 0;
-      const double* src = A;
-      if (gk < K && gm < M) {
-        bytes = gm + 1 < M ? 16 : 8;
-        src = A + (long long)gk * lda + gm;
-      }
-      cp_async16(as + kk * LDS + mm, src, bytes);
-    }
-#pragma unroll
-    for (int c = tid; c < BK * BN / 2; c += GEMM_THREADS) {
-      int kk = c / (BN / 2), nn = (c % (BN / 2)) * 2;
-      int gk = k0 + kk, gn = n0 + nn;
-      int bytes = 0;
-      const double* src = B;
-      if (gk < K && gn < N) {
-        bytes = gn + 1 < N ? 16 : 8;
-        src = B + (long long)gk * ldb + gn;
-      }
-      cp_async16(bs + kk * LDS + nn, src, bytes);
-    }
-  };
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, s);
-    cp_async_commit();
-  }
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    int nxt = kt + STAGES - 1;
-    if (nxt < KT) load_stage(nxt, nxt % STAGES);
-    cp_async_commit();
-    const double* as = As + (kt % STAGES) * BK * LDS;
-    const double* bs = Bs + (kt % STAGES) * BK * LDS;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = as[(kk + t4) * LDS + wm * 32 + i * 8 + g];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) bf[j] = bs[(kk + t4) * LDS + wn * 64 + j * 8 + g];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-  }
-  cp_async_wait<0>();
-
-  // epilogue: fragment (i,j) holds rows m0+wm*32+i*8+g, cols n0+wn*64+j*8+2*t4+{0,1}
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int row = m0 + wm * 32 + i * 8 + g;
-    if (row >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        int col = n0 + wn * 64 + j * 8 + 2 * t4 + e;
-        if (col >= N) continue;
-        if (lower && tm == tn && col > row) continue;
-        double* p = C + (long long)col * ldc + row;
-        if (MODE == kSub)
-          *p = *p - acc[i][j][e];
-        else
-          *p = acc[i][j][e];
-      }
-    }
-  }
-}
-
 // Factor the kb x kb diagonal block at A (lda) in shared memory and, in the
 // same column sweep, form X = inv(L11) (forward substitution on the identity
 // interleaved with the factorisation), one __syncthreads per column:
@@ -488,8 +339,10 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
   }
   static bool attr_done = false;
   if (!attr_done) {
-    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kSub>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
-    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kStore>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kSub, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)Shape<64>::SMEM));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kStore, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)Shape<128>::SMEM));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)((NB * (NB + 1) + 2 * NB) * sizeof(double))));
     attr_done = true;
@@ -523,8 +376,8 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
     GBEM_LAUNCH_CHECK(ctx);
     if (m > 0) {
       // L21 = A21 * inv(L11)^T  (in place, one CTA per 128-row strip)
-      k_gemm_nt<kStore><<<dim3((m + BM - 1) / BM, 1), GEMM_THREADS, GEMM_SMEM, s1>>>(
-          A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb, 0);
+      k_gemm_nt<kStore, 128><<<dim3((m + BM - 1) / BM, 1), GEMM_THREADS, Shape<128>::SMEM, s1>>>(
+          A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb, 0, 0);
       GBEM_LAUNCH_CHECK(ctx);
     }
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_panel, s1));
@@ -533,12 +386,15 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
     // A22 -= L21 L21^T: first the next block column (tile column 0), then the rest
     int nt = (m + BM - 1) / BM;
     double* A22 = ctx->d_A + (long long)(k0 + kb) * lda + (k0 + kb);
-    k_gemm_nt<kSub><<<(unsigned)nt, GEMM_THREADS, GEMM_SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m, kb, 2);
+    constexpr int kSplit = NB / 64;  // block column k+1 = kSplit tile columns of 64
+    k_gemm_nt<kSub, 64><<<dim3(nt, kSplit), GEMM_THREADS, Shape<64>::SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m,
+                                                                               kb, 2, kSplit);
     GBEM_LAUNCH_CHECK(ctx);
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_col, s));
     if (nt > 1) {
-      long long rest = (long long)(nt - 1) * nt / 2;
-      k_gemm_nt<kSub><<<(unsigned)rest, GEMM_THREADS, GEMM_SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m, kb, 3);
+      long long rest = lower_tiles_before<64>(nt) - (long long)kSplit * nt;
+      k_gemm_nt<kSub, 64><<<(unsigned)rest, GEMM_THREADS, Shape<64>::SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m,
+                                                                              kb, 3, kSplit);
       GBEM_LAUNCH_CHECK(ctx);
     }
   }
