@@ -20,11 +20,13 @@
 
 #include "gbem_ctx.cuh"
 #include "gbem_dmma_gemm.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace {
 
 using namespace gbem_gemm;
-constexpr int NB = 128;       // Cholesky block size
+constexpr int NB = 128;       // Cholesky block size (diagonal blocks, trailing-update K)
 // Factor the kb x kb diagonal block at A (lda) in shared memory and, in the
 // same column sweep, form X = inv(L11) (forward substitution on the identity
 // interleaved with the factorisation), one __syncthreads per column:
@@ -39,7 +41,7 @@ constexpr int NB = 128;       // Cholesky block size
 // GEMM-form trsm and the triangular solves.  info[0] receives the first failing
 // global row (atomicMin); a failed pivot continues as 1 so the launch sequence
 // stays fixed (the caller reports "matrix not positive definite").
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
     k_potrf_diag(double* A, long long lda, int kb, int row0, double* Linv, int* info) {
   extern __shared__ __align__(16) double sm[];
   constexpr int LD = NB + 1;
@@ -73,17 +75,41 @@ __global__ void __launch_bounds__(512)
       for (int r = p + 1 + tid; r < kb; r += blockDim.x) a[p * LD + r] *= ip;  // L(r,p)
       for (int c = tid; c < p; c += blockDim.x) a[p * LD + c] *= ip;          // X(p,c) stored at (c,p)
     }
-    for (int r = j + 1 + ty; r < kb; r += nty) {
-      const double arj = a[j * LD + r] * inv_d;
-      for (int c = tx; c <= r; c += 32) {
-        if (c > j)
-          a[c * LD + r] -= arj * a[j * LD + c];       // trailing Cholesky update
-        else if (c < j)
-          a[r * LD + c] -= arj * a[j * LD + c];       // S(r,c) -= L(r,j) X(j,c)   (stored at (c,r))
-        else
-          a[r * LD + j] = -arj;                        // S(r,j) = -L(r,j) / L(j,j)
-      }
+    // element (r, c), r > j, c <= r: c > j trailing update a(r,c); c < j the
+    // X row update S(r,c) (stored at (c,r)); c == j starts S(r,j).  Each thread
+    // owns <= 4 rows x 4 columns; every load of the phase is issued before any
+    // store so the shared-memory latency is paid once per phase.
+    double arj[4], mc[4], t[4][4];
+    int rr[4], cc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      rr[k] = j + 1 + ty + nty * k;
+      cc[k] = tx + 32 * k;
+      arj[k] = rr[k] < kb ? a[j * LD + rr[k]] * inv_d : 0.0;
+      mc[k] = cc[k] < kb ? a[j * LD + cc[k]] : 0.0;
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int r = rr[k], c = cc[m];
+        t[k][m] = 0.0;
+        if (r < kb && c <= r && c != j) t[k][m] = c > j ? a[c * LD + r] : a[r * LD + c];
+      }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int r = rr[k], c = cc[m];
+        if (r < kb && c <= r) {
+          if (c > j)
+            a[c * LD + r] = fma(-arj[k], mc[m], t[k][m]);
+          else if (c < j)
+            a[r * LD + c] = fma(-arj[k], mc[m], t[k][m]);
+          else
+            a[r * LD + j] = -arj[k];
+        }
+      }
     __syncthreads();
   }
   if (kb > 0) {
@@ -105,85 +131,6 @@ __global__ void __launch_bounds__(512)
       else if (r == c) v = isq[r];
     }
     Linv[c * NB + r] = v;
-  }
-}
-
-// Forward step: Y_k = inv(L_kk) B_k (B_k overwritten), rows [k0, k0+kb), all rhs.
-__global__ void k_trsv_diag(const double* Linv, int kb, double* B, long long ldb, int k0, int nrhs,
-                            int transpose) {
-  __shared__ double y[NB];
-  for (int r = blockIdx.x; r < nrhs; r += gridDim.x) {
-    double* b = B + (long long)r * ldb + k0;
-    for (int i = threadIdx.x; i < kb; i += blockDim.x) y[i] = b[i];
-    __syncthreads();
-    for (int i = threadIdx.x; i < kb; i += blockDim.x) {
-      double s = 0.0;
-      if (!transpose) {
-        for (int k = 0; k <= i; ++k) s += Linv[k * NB + i] * y[k];  // (Linv)(i,k)
-      } else {
-        for (int k = i; k < kb; ++k) s += Linv[i * NB + k] * y[k];  // (Linv^T)(i,k) = Linv(k,i)
-      }
-      b[i] = s;
-    }
-    __syncthreads();
-  }
-}
-
-// Forward update: B[r] -= sum_{c in block} L(r, c) Y[c] for rows r >= k0+kb.
-// Thread per row (coalesced over r for each c), nrhs accumulators in registers.
-template <int MAXR>
-__global__ void k_fwd_update(const double* A, long long lda, int k0, int kb, int n, double* B,
-                             long long ldb, int nrhs) {
-  __shared__ double ys[NB * MAXR];
-  for (int idx = threadIdx.x; idx < kb * nrhs; idx += blockDim.x) {
-    int c = idx % kb, rr = idx / kb;
-    ys[c * MAXR + rr] = B[(long long)rr * ldb + k0 + c];
-  }
-  __syncthreads();
-  int r = k0 + kb + blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= n) return;
-  double acc[MAXR];
-#pragma unroll
-  for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
-  for (int c = 0; c < kb; ++c) {
-    double l = A[(long long)(k0 + c) * lda + r];
-#pragma unroll
-    for (int q = 0; q < MAXR; ++q) acc[q] = fma(l, ys[c * MAXR + q], acc[q]);
-  }
-#pragma unroll
-  for (int q = 0; q < MAXR; ++q)
-    if (q < nrhs) B[(long long)q * ldb + r] -= acc[q];
-}
-
-// Backward update: Y[r] -= sum_{c in block k} L(c, r) X[c] for rows r < k0.
-// L(c, r) (row c in block k, col r) sits at A[r*lda + c]: a warp reads the
-// kb-long contiguous column segment of row r.
-template <int MAXR>
-__global__ void k_bwd_update(const double* A, long long lda, int k0, int kb, double* B, long long ldb,
-                             int nrhs) {
-  __shared__ double xs[NB * MAXR];
-  for (int idx = threadIdx.x; idx < kb * nrhs; idx += blockDim.x) {
-    int c = idx % kb, rr = idx / kb;
-    xs[c * MAXR + rr] = B[(long long)rr * ldb + k0 + c];
-  }
-  __syncthreads();
-  int lane = threadIdx.x & 31;
-  int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (r >= k0) return;
-  double acc[MAXR];
-#pragma unroll
-  for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
-  for (int c = lane; c < kb; c += 32) {
-    double l = A[(long long)r * lda + k0 + c];
-#pragma unroll
-    for (int q = 0; q < MAXR; ++q) acc[q] = fma(l, xs[c * MAXR + q], acc[q]);
-  }
-#pragma unroll
-  for (int q = 0; q < MAXR; ++q) {
-    double v = acc[q];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0 && q < nrhs) B[(long long)q * ldb + r] -= v;
   }
 }
 
@@ -289,9 +236,186 @@ __global__ void k_resid_norm(const double* Y, const double* B, int n, double* re
   }
 }
 
-__global__ void k_copy(const double* src, double* dst, long long count) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < count) dst[i] = src[i];
+
+// Forward (L Y = B) and backward (L^T X = Y) block substitution for up to
+// kSolveR right-hand sides in one cooperative launch (one CTA per SM).
+// Step k: the 128 x 128 diagonal-block inverse inv(L_kk) sits in shared memory
+// (cp.async prefetch of the next block overlaps the current step's updates);
+// every CTA forms y = inv(L_kk) w_k (or inv(L_kk)^T) redundantly, CTA 0
+// publishes it, and all CTAs update the remaining rows (right-looking); one
+// grid barrier per step.  Buffers: W = B copy that receives the forward updates
+// and finally the solution X; Out = forward results Y that receive the
+// backward updates.
+constexpr int kSolveThreads = 256;
+constexpr int kSolveR = 16;
+constexpr size_t kSolveSmem = (size_t)(NB * NB + 3 * kSolveR * NB) * sizeof(double);
+
+__device__ __forceinline__ void solve_prefetch_block(double* Ls, const double* Li, int tid) {
+  for (int c = tid; c < NB * NB / 2; c += kSolveThreads) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(Ls + 2 * c);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(Li + 2 * c));
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+}
+
+// ys[q][i] = sum_kk M(i,kk) ws[q][kk] with M = inv(L) (transpose = 0, kk <= i) or
+// inv(L)^T (transpose = 1, kk >= i); two threads per row i, partial sums folded in smem.
+__device__ __forceinline__ void solve_diag(const double* Ls, const double* ws, double* ys, double* part, int kb,
+                                          int R, int transpose, int tid) {
+  static_assert(2 * NB == kSolveThreads, "two threads per diagonal-block row");
+  const int i = tid % NB, half = tid / NB;
+  double acc[kSolveR];
+#pragma unroll
+  for (int q = 0; q < kSolveR; ++q) acc[q] = 0.0;
+  if (i < kb) {
+    const int lo = transpose ? i : 0, hi = transpose ? kb : i + 1;
+    const int mid = (lo + hi) >> 1;
+    const int b0 = half ? mid : lo, b1 = half ? hi : mid;
+    for (int kk = b0; kk < b1; ++kk) {
+      const double m = transpose ? Ls[i * NB + kk] : Ls[kk * NB + i];
+#pragma unroll
+      for (int q = 0; q < kSolveR; ++q)
+        if (q < R) acc[q] = fma(m, ws[q * NB + kk], acc[q]);
+    }
+  }
+  if (half)
+#pragma unroll
+    for (int q = 0; q < kSolveR; ++q)
+      if (q < R) part[q * NB + i] = acc[q];
+  __syncthreads();
+  if (!half && i < kb)
+#pragma unroll
+    for (int q = 0; q < kSolveR; ++q)
+      if (q < R) ys[q * NB + i] = acc[q] + part[q * NB + i];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSolveThreads, 1)
+    k_solve_coop(const double* __restrict__ A, long long lda, const double* __restrict__ Linv, int n, int R,
+                 const double* __restrict__ B, double* W, double* Out) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double sm[];
+  double* Ls = sm;                    // [NB][NB] current diagonal-block inverse
+  double* ws = Ls + NB * NB;          // [kSolveR][NB] right-hand side block
+  double* ys = ws + kSolveR * NB;     // [kSolveR][NB] solved block
+  double* part = ys + kSolveR * NB;   // [kSolveR][NB] partial sums
+  const int nblk = (n + NB - 1) / NB;
+  const long long nR = (long long)n * R;
+  const int tid = threadIdx.x, lane = tid & 31;
+  solve_prefetch_block(Ls, Linv, tid);
+  for (long long i = grid.thread_rank(); i < nR; i += grid.size()) W[i] = B[i];
+  grid.sync();
+  // ---- forward: W holds b - sum_{j<k} L_kj y_j, Out receives y
+  for (int b = 0; b < nblk; ++b) {
+    const int k0 = b * NB, kb = min(NB, n - k0);
+    for (int idx = tid; idx < kb * R; idx += blockDim.x) {
+      const int i = idx % kb, q = idx / kb;
+      ws[q * NB + i] = W[(long long)q * n + k0 + i];
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    solve_diag(Ls, ws, ys, part, kb, R, 0, tid);
+    if (b + 1 < nblk)
+      solve_prefetch_block(Ls, Linv + (size_t)(b + 1) * NB * NB, tid);
+    else
+      solve_prefetch_block(Ls, Linv + (size_t)b * NB * NB, tid);  // backward starts from the last block
+    if (blockIdx.x == 0)
+      for (int idx = tid; idx < kb * R; idx += blockDim.x) {
+        const int i = idx % kb, q = idx / kb;
+        Out[(long long)q * n + k0 + i] = ys[q * NB + i];
+      }
+    // rows below the block: 32-row strips, a warp per strip, strips dealt across
+    // CTAs first so every SM streams; 16-deep unroll keeps 16 loads in flight
+    const int nstrips = (n - k0 - kb + 31) / 32;
+    for (int st = blockIdx.x + gridDim.x * (tid >> 5); st < nstrips; st += gridDim.x * (blockDim.x >> 5)) {
+      const long long r = (long long)k0 + kb + 32LL * st + lane;
+      if (r >= n) continue;
+      double acc[kSolveR];
+#pragma unroll
+      for (int q = 0; q < kSolveR; ++q) acc[q] = 0.0;
+      const double* col = A + (long long)k0 * lda + r;
+      int c = 0;
+      for (; c + 16 <= kb; c += 16) {
+        double l[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) l[u] = col[(long long)(c + u) * lda];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+#pragma unroll
+          for (int q = 0; q < kSolveR; ++q)
+            if (q < R) acc[q] = fma(l[u], ys[q * NB + c + u], acc[q]);
+      }
+      for (; c < kb; ++c) {
+        const double l = col[(long long)c * lda];
+#pragma unroll
+        for (int q = 0; q < kSolveR; ++q)
+          if (q < R) acc[q] = fma(l, ys[q * NB + c], acc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kSolveR; ++q)
+        if (q < R) W[(long long)q * n + r] -= acc[q];
+    }
+    grid.sync();
+  }
+  // ---- backward: Out holds y - sum_{j>k} L_jk^T x_j, W receives x
+  const long long gwarp = blockIdx.x + (long long)gridDim.x * (tid >> 5), nwarps = grid.size() >> 5;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int k0 = b * NB, kb = min(NB, n - k0);
+    for (int idx = tid; idx < kb * R; idx += blockDim.x) {
+      const int i = idx % kb, q = idx / kb;
+      ws[q * NB + i] = Out[(long long)q * n + k0 + i];
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    solve_diag(Ls, ws, ys, part, kb, R, 1, tid);
+    if (b > 0) solve_prefetch_block(Ls, Linv + (size_t)(b - 1) * NB * NB, tid);
+    if (blockIdx.x == 0)
+      for (int idx = tid; idx < kb * R; idx += blockDim.x) {
+        const int i = idx % kb, q = idx / kb;
+        W[(long long)q * n + k0 + i] = ys[q * NB + i];
+      }
+    // rows r < k0: Out[r] -= sum_{c in block} L(k0+c, r) x_c; L(c,r) sits at A[r*lda + c]
+    // (contiguous in c): a warp per row, 4 rows per pass (16 loads in flight per lane)
+    for (long long r0 = gwarp * 4; r0 < k0; r0 += nwarps * 4) {
+      double acc[4][kSolveR];
+      double l[4][4];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+#pragma unroll
+        for (int q = 0; q < kSolveR; ++q) acc[rr][q] = 0.0;
+        const long long r = r0 + rr;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = lane + 32 * j;
+          l[rr][j] = (r < k0 && c < kb) ? A[r * lda + k0 + c] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int c = lane + 32 * j;
+          if (c < kb) {
+#pragma unroll
+            for (int q = 0; q < kSolveR; ++q)
+              if (q < R) acc[rr][q] = fma(l[rr][j], ys[q * NB + c], acc[rr][q]);
+          }
+        }
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const long long r = r0 + rr;
+#pragma unroll
+        for (int q = 0; q < kSolveR; ++q) {
+          if (q >= R) continue;
+          double v = acc[rr][q];
+#pragma unroll
+          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+          if (lane == 0 && r < k0) Out[(long long)q * n + r] -= v;
+        }
+      }
+    }
+    grid.sync();
+  }
 }
 
 int ensure_work(gbem_ctx* ctx, size_t elems) {
@@ -323,7 +447,7 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
   if (ctx->factored) return ctx->fail(GBEM_EINVAL, "matrix already factored; re-assemble or re-upload");
   const int nblk = (n + NB - 1) / NB;
   // workspace: inverses of the diagonal blocks (nblk * NB * NB) + symv result (n * nrhs)
-  size_t need = (size_t)nblk * NB * NB + (size_t)n * (size_t)std::max<int64_t>(nrhs, 1);
+  size_t need = (size_t)nblk * NB * NB + 2 * (size_t)n * (size_t)std::max<int64_t>(nrhs, 1);
   int rc = ensure_work(ctx, need);
   if (rc) return rc;
   double* Linv = ctx->d_work;
@@ -341,8 +465,8 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
   if (!attr_done) {
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kSub, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)Shape<64>::SMEM));
-    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kStore, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)Shape<128>::SMEM));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kStore, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)Shape<NB>::SMEM));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)((NB * (NB + 1) + 2 * NB) * sizeof(double))));
     attr_done = true;
@@ -372,11 +496,11 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
     double* Akk = ctx->d_A + (long long)k0 * lda + k0;
     double* A21 = Akk + kb;  // rows k0+kb.., cols k0..
     GBEM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ev_col, 0));
-    k_potrf_diag<<<1, 512, potrf_smem, s1>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
+    k_potrf_diag<<<1, 1024, potrf_smem, s1>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
     GBEM_LAUNCH_CHECK(ctx);
     if (m > 0) {
       // L21 = A21 * inv(L11)^T  (in place, one CTA per 128-row strip)
-      k_gemm_nt<kStore, 128><<<dim3((m + BM - 1) / BM, 1), GEMM_THREADS, Shape<128>::SMEM, s1>>>(
+      k_gemm_nt<kStore, NB><<<dim3((m + BM - 1) / BM, 1), GEMM_THREADS, Shape<NB>::SMEM, s1>>>(
           A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb, 0, 0);
       GBEM_LAUNCH_CHECK(ctx);
     }
@@ -408,47 +532,24 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
                      "matrix not positive definite (pivot at row " + std::to_string(*ctx->h_info) + ")");
   }
   if (nrhs == 0) return GBEM_OK;
-  // X <- B, then forward / backward substitution in place
-  k_copy<<<(unsigned)(((long long)n * nrhs + 255) / 256), 256, 0, s>>>(d_B, d_X, (long long)n * nrhs);
-  GBEM_LAUNCH_CHECK(ctx);
+  // forward + backward substitution in one cooperative kernel (a grid barrier
+  // per block step instead of four launches per block step)
   const int R = (int)nrhs;
-  for (int b = 0; b < nblk; ++b) {
-    int k0 = b * NB, kb = std::min(NB, n - k0);
-    k_trsv_diag<<<R, 128, 0, s>>>(Linv + (size_t)b * NB * NB, kb, d_X, n, k0, R, 0);
-    GBEM_LAUNCH_CHECK(ctx);
-    int m = n - k0 - kb;
-    if (m > 0) {
-      dim3 grid((m + 127) / 128);
-      for (int q0 = 0; q0 < R; q0 += 32) {
-        int rq = std::min(32, R - q0);
-        double* Xq = d_X + (long long)q0 * n;
-        if (rq <= 8)
-          k_fwd_update<8><<<grid, 128, 0, s>>>(ctx->d_A, lda, k0, kb, n, Xq, n, rq);
-        else if (rq <= 16)
-          k_fwd_update<16><<<grid, 128, 0, s>>>(ctx->d_A, lda, k0, kb, n, Xq, n, rq);
-        else
-          k_fwd_update<32><<<grid, 128, 0, s>>>(ctx->d_A, lda, k0, kb, n, Xq, n, rq);
-        GBEM_LAUNCH_CHECK(ctx);
-      }
-    }
-  }
-  for (int b = nblk - 1; b >= 0; --b) {
-    int k0 = b * NB, kb = std::min(NB, n - k0);
-    k_trsv_diag<<<R, 128, 0, s>>>(Linv + (size_t)b * NB * NB, kb, d_X, n, k0, R, 1);
-    GBEM_LAUNCH_CHECK(ctx);
-    if (k0 > 0) {
-      dim3 grid((k0 + 7) / 8);
-      for (int q0 = 0; q0 < R; q0 += 32) {
-        int rq = std::min(32, R - q0);
-        double* Xq = d_X + (long long)q0 * n;
-        if (rq <= 8)
-          k_bwd_update<8><<<grid, 256, 0, s>>>(ctx->d_A, lda, k0, kb, Xq, n, rq);
-        else if (rq <= 16)
-          k_bwd_update<16><<<grid, 256, 0, s>>>(ctx->d_A, lda, k0, kb, Xq, n, rq);
-        else
-          k_bwd_update<32><<<grid, 256, 0, s>>>(ctx->d_A, lda, k0, kb, Xq, n, rq);
-        GBEM_LAUNCH_CHECK(ctx);
-      }
+  double* scratch = Ysym + (size_t)n * R;
+  {
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSolveSmem));
+    const double* cA = ctx->d_A;
+    const double* cL = Linv;
+    int nn = n;
+    for (int q0 = 0; q0 < R; q0 += kSolveR) {
+      int RR = std::min(kSolveR, R - q0);
+      const double* Bq = d_B + (size_t)q0 * n;
+      double* Xq = d_X + (size_t)q0 * n;
+      double* Sq = scratch;  // scratch holds n * R >= n * RR
+      void* args[] = {(void*)&cA, (void*)&lda, (void*)&cL, (void*)&nn, (void*)&RR, (void*)&Bq, (void*)&Xq, (void*)&Sq};
+      GBEM_CUDA(ctx, cudaLaunchCooperativeKernel((void*)k_solve_coop, dim3(ctx->num_sms), dim3(kSolveThreads), args,
+                                                 kSolveSmem, s));
+      GBEM_LAUNCH_CHECK(ctx);
     }
   }
   cudaEventRecord(ctx->ev[2], s);
