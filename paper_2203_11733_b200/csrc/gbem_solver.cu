@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "gbem_ctx.cuh"
+#include "gbem_common.cuh"
 #include "gbem_dmma_gemm.cuh"
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
@@ -27,108 +28,207 @@ namespace {
 
 using namespace gbem_gemm;
 constexpr int NB = 128;       // Cholesky block size (diagonal blocks, trailing-update K)
-// Factor the kb x kb diagonal block at A (lda) in shared memory and, in the
-// same column sweep, form X = inv(L11) (forward substitution on the identity
-// interleaved with the factorisation), one __syncthreads per column:
-//   phase j: with s_j = sqrt(a_jj) (column j still unscaled),
-//     a(r,c) -= a(r,j) a(c,j) / a_jj           j < c <= r   (Cholesky trailing update)
-//     S(r,c) -= a(r,j) S(j,c) / a_jj            c < j < r    (X rows, S = X * diag(L))
-//     S(r,j)  = -a(r,j) / a_jj                  j < r
-//   and column j-1 / row j-1 are finalised (scaled by 1/s_{j-1}) in the same
-//   phase, since phase j never touches them.  X's strict lower part is kept
-//   transposed in the strict upper half of the smem tile, its diagonal in xd.
-// L11 goes back to A (lower), X to Linv (column-major, ld = NB) for the
-// GEMM-form trsm and the triangular solves.  info[0] receives the first failing
-// global row (atomicMin); a failed pivot continues as 1 so the launch sequence
-// stays fixed (the caller reports "matrix not positive definite").
-__global__ void __launch_bounds__(1024)
+// Factor the kb x kb (kb <= NB = 128) diagonal block and invert its factor, in
+// shared memory, by 32-column panels:
+//   1. warp 0 factors the 32 x 32 diagonal sub-block in registers (lane i owns
+//      row i; pivots and column entries move by __shfl_sync, no block barriers)
+//      and inverts it the same way;
+//   2. all warps form the panel rows below: L_rp = A_rp * inv(L_pp)^T;
+//   3. all warps apply the rank-32 update to the trailing sub-block (4 x 4
+//      register tiles);
+// then the off-diagonal 32 x 32 blocks of X = inv(L) follow from
+// X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp.  L goes back to A (lower), X to Linv
+// (column-major, ld = NB) for the GEMM-form trsm and the triangular solves.
+// X(r,c), r > c, is kept at a[r*LD + c] (the strict upper half), its diagonal
+// in xd.  info[0] receives the first failing global row (atomicMin); a failed
+// pivot continues as 1 so the launch sequence stays fixed.
+#ifdef GBEM_POTRF_TIMING
+__device__ long long g_potrf_clk[64];
+#define POTRF_TICK(k) \
+  if (threadIdx.x == 0) g_potrf_clk[k] = clock64();
+#else
+#define POTRF_TICK(k)
+#endif
+constexpr int kPotrfThreads = 512;
+constexpr int kPanel = 32;
+constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + 2 * NB + 3 * kPanel * kPanel) * sizeof(double);
+
+__global__ void __launch_bounds__(kPotrfThreads)
     k_potrf_diag(double* A, long long lda, int kb, int row0, double* Linv, int* info) {
   extern __shared__ __align__(16) double sm[];
   constexpr int LD = NB + 1;
-  double* a = sm;               // [NB][LD] column-major: a[c*LD + r]
-  double* isq = sm + NB * LD;   // 1/s_j per column
-  double* sq = isq + NB;        // s_j
-  const int tid = threadIdx.x;
-  const int tx = tid & 31, ty = tid >> 5, nty = blockDim.x >> 5;
-  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
-    int c = idx / kb, r = idx % kb;
-    a[c * LD + r] = r >= c ? A[(long long)c * lda + r] : 0.0;
+  double* a = sm;              // [NB][LD] column-major: a[c*LD + r]
+  double* xd = a + NB * LD;    // diag of X (= 1 / diag of L)
+  double* sqd = xd + NB;       // diag of L
+  double* tmp = sqd + NB;      // [3][32*32] products of the X assembly
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < NB * NB; idx += kPotrfThreads) {
+    int c = idx / NB, r = idx % NB;
+    double v = 0.0;
+    if (r < kb && c < kb) v = r >= c ? A[(long long)c * lda + r] : 0.0;
+    else if (r == c) v = 1.0;  // pad the ragged last block with the identity
+    a[c * LD + r] = v;
   }
   __syncthreads();
+  POTRF_TICK(0);
+  const int npan = (kb + kPanel - 1) / kPanel;
   bool bad = false;
-  for (int j = 0; j < kb; ++j) {
-    double d = a[j * LD + j];
-    if (!(d > 0.0)) {
-      if (tid == 0 && !bad) atomicMin(info, row0 + j);
-      bad = true;
-      d = 1.0;
-    }
-    const double sj = sqrt(d), inv_s = 1.0 / sj, inv_d = inv_s * inv_s;
-    if (tid == 0) {
-      isq[j] = inv_s;
-      sq[j] = sj;
-    }
-    // finalise column j-1 of L and row j-1 of X
-    if (j > 0) {
-      const int p = j - 1;
-      const double ip = isq[p];
-      for (int r = p + 1 + tid; r < kb; r += blockDim.x) a[p * LD + r] *= ip;  // L(r,p)
-      for (int c = tid; c < p; c += blockDim.x) a[p * LD + c] *= ip;          // X(p,c) stored at (c,p)
-    }
-    // element (r, c), r > j, c <= r: c > j trailing update a(r,c); c < j the
-    // X row update S(r,c) (stored at (c,r)); c == j starts S(r,j).  Each thread
-    // owns <= 4 rows x 4 columns; every load of the phase is issued before any
-    // store so the shared-memory latency is paid once per phase.
-    double arj[4], mc[4], t[4][4];
-    int rr[4], cc[4];
+  for (int p = 0; p < npan; ++p) {
+    const int c0 = p * kPanel;
+    // ---- 1. panel factorisation, one barrier per pivot: phase j applies the
+    // pivot to the panel columns (j, c0+32) on every row below (unscaled column
+    // j, scaled by 1/a_jj on the fly), runs the in-panel forward substitution
+    // of X = inv(L_pp) (S = X diag(L), stored transposed in the upper half), and
+    // finalises column j-1 / X row j-1, which phase j never reads.
+    for (int j = c0; j < c0 + kPanel; ++j) {
+      double d = a[j * LD + j];
+      if (!(d > 0.0)) {
+        if (tid == 0 && !bad && j < kb) atomicMin(info, row0 + j);
+        bad = true;
+        d = 1.0;
+      }
+      const double is = gbem_gpu::rsq64(d), isd = is * is;
+      if (tid == 0) {
+        xd[j] = is;
+        sqd[j] = d * is;
+      }
+      if (j > c0) {
+        const int q = j - 1;
+        const double iq = xd[q];
+        for (int r = q + 1 + tid; r < NB; r += kPotrfThreads) a[q * LD + r] *= iq;          // L(r, q)
+        if (tid < q - c0) a[q * LD + c0 + tid] *= iq;                                      // X(q, c0+tid)
+      }
+      // Cholesky update of the panel columns, rows r >= c: lane -> column, warp -> rows
+      const int cc = c0 + lane;
+      const bool colv = cc > j;
+      const double acj = colv ? a[j * LD + cc] * isd : 0.0;
+      double tv[8], arj[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      rr[k] = j + 1 + ty + nty * k;
-      cc[k] = tx + 32 * k;
-      arj[k] = rr[k] < kb ? a[j * LD + rr[k]] * inv_d : 0.0;
-      mc[k] = cc[k] < kb ? a[j * LD + cc[k]] : 0.0;
-    }
+      for (int k = 0; k < 8; ++k) {
+        const int r = j + 1 + warp + 16 * k;
+        const bool ok = colv && r < NB && r >= cc;
+        tv[k] = ok ? a[cc * LD + r] : 0.0;
+        arj[k] = ok ? a[j * LD + r] : 0.0;
+      }
+      // in-panel X rows: S(i,k) -= L(i,j) X(j,k), i in (j, c0+32), k in [c0, j]
+      const int kx = c0 + lane;
+      bool xv[2];
+      double sv[2], lij[2];
+      const double xjk = kx == j ? is : (kx < j ? a[j * LD + kx] * is : 0.0);
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+      for (int h = 0; h < 2; ++h) {
+        const int ix = j + 1 + warp + 16 * h;
+        xv[h] = kx <= j && ix < c0 + kPanel;
+        sv[h] = xv[h] && kx < j ? a[ix * LD + kx] : 0.0;
+        lij[h] = xv[h] ? a[j * LD + ix] * is : 0.0;
+      }
+      // (no barrier needed here: phase j never writes column j, and every
+      // element it writes is read only by the thread that writes it)
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int r = rr[k], c = cc[m];
-        t[k][m] = 0.0;
-        if (r < kb && c <= r && c != j) t[k][m] = c > j ? a[c * LD + r] : a[r * LD + c];
+      for (int k = 0; k < 8; ++k) {
+        const int r = j + 1 + warp + 16 * k;
+        if (colv && r < NB && r >= cc) a[cc * LD + r] = fma(-arj[k], acj, tv[k]);
       }
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+      for (int h = 0; h < 2; ++h)
+        if (xv[h]) a[(j + 1 + warp + 16 * h) * LD + kx] = fma(-lij[h], xjk, sv[h]);
+      __syncthreads();
+    }
+    {  // finalise the last panel column and X row
+      const int q = c0 + kPanel - 1;
+      const double iq = xd[q];
+      for (int r = q + 1 + tid; r < NB; r += kPotrfThreads) a[q * LD + r] *= iq;
+      if (tid < q - c0) a[q * LD + c0 + tid] *= iq;
+      if (tid < kPanel) a[(c0 + tid) * LD + c0 + tid] = sqd[c0 + tid];
+    }
+    __syncthreads();
+    POTRF_TICK(1 + 3 * p);
+    const int r0 = c0 + kPanel, mrest = NB - r0;  // padded rows below the panel
+    if (mrest <= 0) break;
+    POTRF_TICK(2 + 3 * p);
+    // ---- 3. rank-32 update of the trailing lower part, 4 x 4 register tiles
+    {
+      const int nb4 = mrest / 4;
+      const int ntile = nb4 * (nb4 + 1) / 2;
+      for (int t = tid; t < ntile; t += kPotrfThreads) {
+        int tr = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+        while ((tr + 1) * (tr + 2) / 2 <= t) ++tr;
+        while (tr * (tr + 1) / 2 > t) --tr;
+        const int tc = t - tr * (tr + 1) / 2;
+        const int rb = r0 + 4 * tr, cb = r0 + 4 * tc;
+        double acc[4][4] = {};
+#pragma unroll 4
+        for (int k = 0; k < kPanel; ++k) {
+          double lr[4], lc[4];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int r = rr[k], c = cc[m];
-        if (r < kb && c <= r) {
-          if (c > j)
-            a[c * LD + r] = fma(-arj[k], mc[m], t[k][m]);
-          else if (c < j)
-            a[r * LD + c] = fma(-arj[k], mc[m], t[k][m]);
-          else
-            a[r * LD + j] = -arj[k];
+          for (int u = 0; u < 4; ++u) {
+            lr[u] = a[(c0 + k) * LD + rb + u];
+            lc[u] = a[(c0 + k) * LD + cb + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(lr[u], lc[v], acc[u][v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            if (cb + v <= rb + u) a[(cb + v) * LD + rb + u] -= acc[u][v];
+      }
+    }
+    __syncthreads();
+    POTRF_TICK(3 + 3 * p);
+  }
+  POTRF_TICK(20);
+  // ---- off-diagonal blocks of X = inv(L): X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp.
+  // Each thread computes 4 adjacent columns of one row (4 independent chains).
+  for (int rbk = 1; rbk < npan; ++rbk) {
+    const int R0 = rbk * kPanel;
+    const int ntask = rbk * kPanel * (kPanel / 4);
+    for (int t = tid; t < ntask; t += kPotrfThreads) {
+      const int i = t % kPanel, k4 = (t / kPanel) % (kPanel / 4), pb = t / (kPanel * (kPanel / 4));
+      const int col = pb * kPanel + 4 * k4;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int m = col; m < R0; ++m) {
+        const double lrm = a[m * LD + R0 + i];  // L(R0+i, m)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int c = col + v;
+          const double xmc = m == c ? xd[m] : (m > c ? a[m * LD + c] : 0.0);  // X(m, c)
+          acc[v] = fma(lrm, xmc, acc[v]);
         }
       }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) tmp[pb * kPanel * kPanel + (4 * k4 + v) * kPanel + i] = acc[v];
+    }
+    __syncthreads();
+    for (int t = tid; t < ntask; t += kPotrfThreads) {
+      const int i = t % kPanel, k4 = (t / kPanel) % (kPanel / 4), pb = t / (kPanel * (kPanel / 4));
+      const int col = pb * kPanel + 4 * k4;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int m = 0; m <= i; ++m) {
+        const double xim = m == i ? xd[R0 + i] : a[(R0 + i) * LD + R0 + m];  // X(R0+i, R0+m)
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          acc[v] = fma(xim, tmp[pb * kPanel * kPanel + (4 * k4 + v) * kPanel + m], acc[v]);
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) a[(R0 + i) * LD + col + v] = -acc[v];  // X(R0+i, col+v)
+    }
     __syncthreads();
   }
-  if (kb > 0) {
-    const int p = kb - 1;
-    const double ip = isq[p];
-    for (int c = tid; c < p; c += blockDim.x) a[p * LD + c] *= ip;
-  }
-  __syncthreads();
-  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+  POTRF_TICK(21);
+  for (int idx = tid; idx < kb * kb; idx += kPotrfThreads) {
     int c = idx / kb, r = idx % kb;
-    if (r > c) A[(long long)c * lda + r] = a[c * LD + r];
-    else if (r == c) A[(long long)c * lda + r] = sq[r];
+    if (r >= c) A[(long long)c * lda + r] = a[c * LD + r];
   }
-  for (int idx = tid; idx < NB * NB; idx += blockDim.x) {
+  for (int idx = tid; idx < NB * NB; idx += kPotrfThreads) {
     int c = idx / NB, r = idx % NB;
     double v = 0.0;
     if (r < kb && c < kb) {
       if (r > c) v = a[r * LD + c];
-      else if (r == c) v = isq[r];
+      else if (r == c) v = xd[r];
     }
     Linv[c * NB + r] = v;
   }
@@ -468,7 +568,7 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kStore, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)Shape<NB>::SMEM));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)((NB * (NB + 1) + 2 * NB) * sizeof(double))));
+                                        (int)kPotrfSmem));
     attr_done = true;
   }
   cudaStream_t s = ctx->stream;
@@ -477,7 +577,6 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
   k_save_diag<<<(n + 255) / 256, 256, 0, s>>>(ctx->d_A, lda, n, ctx->d_diag);
   GBEM_LAUNCH_CHECK(ctx);
   cudaEventRecord(ctx->ev[0], s);
-  const size_t potrf_smem = (size_t)(NB * (NB + 1) + 2 * NB) * sizeof(double);
   // Look-ahead: the diagonal factor + panel trsm of block k+1 run on the
   // high-priority side stream while the main stream finishes the trailing
   // update of block k (only block column k+1 has to be updated first).
@@ -496,7 +595,7 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
     double* Akk = ctx->d_A + (long long)k0 * lda + k0;
     double* A21 = Akk + kb;  // rows k0+kb.., cols k0..
     GBEM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ev_col, 0));
-    k_potrf_diag<<<1, 1024, potrf_smem, s1>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
+    k_potrf_diag<<<1, kPotrfThreads, kPotrfSmem, s1>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
     GBEM_LAUNCH_CHECK(ctx);
     if (m > 0) {
       // L21 = A21 * inv(L11)^T  (in place, one CTA per 128-row strip)
