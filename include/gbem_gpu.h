@@ -51,7 +51,7 @@ typedef struct {
 
 /* QuadratureConfig (quadrature.hpp:12-15) for the near-field Romberg path plus
  * the far-field split.  Zero-initialised fields take the defaults:
- * rel_tol 1e-8, max_levels 16, near_ratio 0.75 (pairs with gap < near_ratio *
+ * rel_tol 1e-8, max_levels 16, near_ratio 1.0 (>= 1; pairs with gap < near_ratio *
  * max diameter use the reference's semi-analytic forms; the rest use the
  * anisotropic tensor-Gauss rule), far_tol 1e-12 (target relative error of the
  * far-field rule). */

@@ -170,7 +170,7 @@ class Context:
         self.check(self.lib.gbem_ctx_set_stream(self.h, _P(stream_handle or 0)))
 
     @staticmethod
-    def quad(rel_tol=1e-8, max_levels=16, near_ratio=0.75, far_tol=1e-12) -> GbemQuadConfig:
+    def quad(rel_tol=1e-8, max_levels=16, near_ratio=1.0, far_tol=1e-12) -> GbemQuadConfig:
         return GbemQuadConfig(rel_tol, max_levels, near_ratio, far_tol)
 
     def u_pair_integrals(self, I: PanelArrays, J: PanelArrays, cfg: GbemQuadConfig | None = None):

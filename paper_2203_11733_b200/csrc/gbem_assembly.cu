@@ -27,12 +27,12 @@ using namespace gbem_gpu;
 namespace gbem_gpu {
 __constant__ double c_gx[kQMax + 1][kQMax];
 __constant__ double c_gw[kQMax + 1][kQMax];
-// c_delta[band][q]: far-field order q suffices along a direction of half-length
-// h when gap >= c_delta[band][q] * h (band 0: far_tol, band 1: far_tol/10 for
-// 0.75 <= gap/diam < 1).  Derived from the Bernstein-ellipse bound of the
+// c_delta[q]: far-field order q suffices along a direction of half-length h
+// when gap >= c_delta[q] * h.  Derived from the Bernstein-ellipse bound of the
 // end-on singularity, rho = 1 + d + sqrt(d (2 + d)), error ~ rho^(-2q);
-// calibrated in tools/calib_far.c.
-__constant__ double c_delta[2][kQMax + 1];
+// calibrated in tools/calib_far.c (far pairs have gap >= diam, so q <= 8 at
+// far_tol = 1e-12).
+__constant__ double c_delta[kQMax + 1];
 // Gauss-Legendre nodes / weights of the graded near-field rule (near_nodes(band) entries per band)
 __constant__ double c_nx[kNearBands][48];
 __constant__ double c_nw[kNearBands][48];
@@ -142,10 +142,10 @@ void legendre_table(double gx[kQMax + 1][kQMax], double gw[kQMax + 1][kQMax]) {
 
 // ---------------------------------------------------------------- classify
 
-__device__ __forceinline__ int far_order(double gap, double h, int band) {
+__device__ __forceinline__ int far_order(double gap, double h) {
 #pragma unroll 1
   for (int q = 1; q < kQMax; ++q)
-    if (gap >= c_delta[band][q] * h) return q;
+    if (gap >= c_delta[q] * h) return q;
   return kQMax;
 }
 
@@ -171,10 +171,8 @@ __device__ __forceinline__ uint32_t classify_pair(const DPanel& A, const DPanel&
       return same_axis ? kClsParallel : kClsOrthogonal;  // near contact: adaptive Romberg
     return (same_axis ? kClsParallelGL : kClsOrthogonalGL) + band;
   }
-  int band = gap < dm ? 1 : 0;
-  int qs = far_order(gap, 0.5 * la, band), qt = far_order(gap, 0.5 * lb, band);
-  int qu = far_order(gap, 0.5 * lc, band), qv = far_order(gap, 0.5 * ld, band);
-  return far_key(qs, qt, qu, qv);
+  return far_key(far_order(gap, 0.5 * la), far_order(gap, 0.5 * lb), far_order(gap, 0.5 * lc),
+                 far_order(gap, 0.5 * ld));
 }
 
 // Warp-aggregated append of `key` (one atomic per distinct key in the warp).
@@ -323,9 +321,10 @@ __device__ __forceinline__ double sel3(int k, int ai, double lvl, int kS, double
 // Anisotropic tensor Gauss over I (orders qs, qt along its in-plane axes) and
 // J (order qu along U, QV along V; V is J's direction with the largest order).
 // Equivalent to gaussPair (oracle.hpp:45-81) with per-direction orders.
-template <int QV>
+template <int QV, int QU>
 __device__ __forceinline__ double far_gauss(const DPanel& I, int qs, int qt, const DPanel& J,
-                                            bool v_is_a, int qu, double& flops) {
+                                            bool v_is_a, int qu_rt, double& flops) {
+  const int qu = QU > 0 ? QU : qu_rt;
   const int ai = I.axis, aj = J.axis;
   const int kS = ip0(ai);
   const double cS = 0.5 * (I.a0 + I.a1), hS = 0.5 * (I.a1 - I.a0);
@@ -373,8 +372,9 @@ __device__ __forceinline__ double far_gauss(const DPanel& I, int qs, int qt, con
       }
       const double pz2 = pz * pz;
       double inner = 0.0;
-#pragma unroll 2
-      for (int u = 0; u < qu; ++u) {
+#pragma unroll
+      for (int u = 0; u < (QU > 0 ? QU : kQMax); ++u) {
+        if (QU == 0 && u >= qu) break;
         const double du = pu - fma(hU, c_gx[qu][u], cU);
         const double cu = fma(du, du, pz2);
         // two partial sums break the FMA dependency chain along v
@@ -394,50 +394,23 @@ __device__ __forceinline__ double far_gauss(const DPanel& I, int qs, int qt, con
   return acc / kFourPi;
 }
 
-__device__ double far_dispatch(const DPanel& Pi, const DPanel& Pj, uint32_t key, double& flops) {
-  int q[4] = {(int)(key & 15u), (int)((key >> 4) & 15u), (int)((key >> 8) & 15u), (int)(key >> 12)};
-  // Put the largest order in the compile-time (innermost) direction V of panel J.
-  int mi = max(q[0], q[1]), mj = max(q[2], q[3]);
-  const DPanel* I = &Pi;
-  const DPanel* J = &Pj;
-  int qs = q[0], qt = q[1], qja = q[2], qjb = q[3];
-  if (mi > mj) {
-    I = &Pj;
-    J = &Pi;
-    qs = q[2];
-    qt = q[3];
-    qja = q[0];
-    qjb = q[1];
-  }
-  bool v_is_a = qja > qjb;
-  int QV = v_is_a ? qja : qjb;
-  int qu = v_is_a ? qjb : qja;
-  switch (QV) {
-    case 1: return far_gauss<1>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 2: return far_gauss<2>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 3: return far_gauss<3>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 4: return far_gauss<4>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 5: return far_gauss<5>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 6: return far_gauss<6>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 7: return far_gauss<7>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 8: return far_gauss<8>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 9: return far_gauss<9>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 10: return far_gauss<10>(*I, qs, qt, *J, v_is_a, qu, flops);
-    case 11: return far_gauss<11>(*I, qs, qt, *J, v_is_a, qu, flops);
-    default: return far_gauss<12>(*I, qs, qt, *J, v_is_a, qu, flops);
-  }
-}
-
 __device__ __forceinline__ double warp_reduce_d(double x) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
   return x;
 }
 
-__global__ void __launch_bounds__(256, 2)
+// Far field, one kernel per (largest order QV, order qu of J's other direction)
+// segment of the queue (QU = 0: qu at run time): the register footprint and the
+// unrolling follow the orders, so the common small-order pairs run fully
+// unrolled at high occupancy.
+template <int QV, int QU>
+__global__ void __launch_bounds__(256, QV <= 4 ? 3 : 2)
     k_far(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
           const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats) {
-  const uint32_t begin = offsets[kFarKeyBase], end = offsets[kNumKeys];
+  const uint32_t begin = offsets[far_key_first(QV, QU > 0 ? QU : 1)];
+  const uint32_t end = offsets[QU > 0 && QU < QV ? far_key_first(QV, QU + 1)
+                                                 : (QV < kQMax ? far_key_first(QV + 1) : kNumKeys)];
   double flops = 0.0, evals = 0.0;
   const uint32_t stride = gridDim.x * blockDim.x;
   // Warps walk the queue in 32-entry runs so a warp shares one key.
@@ -446,10 +419,13 @@ __global__ void __launch_bounds__(256, 2)
     uint32_t idx = base + (threadIdx.x & 31u);
     if (idx < end) {
       uint64_t e = queue[idx];
-      uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e);
+      uint32_t i = entry_i(e), j = entry_j(e), k = entry_key(e) - 16u;
       DPanel Pi = load_panel(P, i), Pj = load_panel(P, j);
-      double U = far_dispatch(Pi, Pj, key, flops);
-      evals += (double)((key & 15u) * ((key >> 4) & 15u) * ((key >> 8) & 15u) * (key >> 12));
+      const bool swap = (k >> 7) & 1u, v_is_a = (k >> 6) & 1u;
+      const int qu = (int)((k >> 8) & 7u) + 1, qs = (int)((k >> 3) & 7u) + 1, qt = (int)(k & 7u) + 1;
+      double U = swap ? far_gauss<QV, QU>(Pj, qs, qt, Pi, v_is_a, qu, flops)
+                      : far_gauss<QV, QU>(Pi, qs, qt, Pj, v_is_a, qu, flops);
+      evals += (double)(qs * qt * qu * QV);
       store_value(o, i, j, Pi, Pj, U);
       if (!o.A && o.conv) o.conv[i] = 1;
     }
@@ -599,7 +575,8 @@ int prepare_work(gbem_ctx* ctx, const gbem_quad_config* cfg_in, gbem_quad_config
   if (!(c.rel_tol > 0)) c.rel_tol = 1e-8;
   if (c.max_levels <= 0) c.max_levels = 16;
   if (c.max_levels > kRombMax) return ctx->fail(GBEM_EINVAL, "max_levels exceeds 20");
-  if (!(c.near_ratio > 0)) c.near_ratio = 0.75;
+  if (!(c.near_ratio > 0)) c.near_ratio = 1.0;
+  if (c.near_ratio < 1.0) return ctx->fail(GBEM_EINVAL, "near_ratio must be >= 1 (far-field orders are capped at 8)");
   if (!(c.far_tol > 0)) c.far_tol = 1e-12;
   *cfg = c;
   if (!ctx->d_counts) {
@@ -610,14 +587,11 @@ int prepare_work(gbem_ctx* ctx, const gbem_quad_config* cfg_in, gbem_quad_config
     GBEM_CUDA(ctx, cudaMallocHost(&ctx->h_stats, sizeof(unsigned long long) * ST_COUNT));
   }
   // far-field order thresholds
-  double delta[2][kQMax + 1];
-  for (int band = 0; band < 2; ++band) {
-    double tol = band == 0 ? c.far_tol : 0.1 * c.far_tol;
-    delta[band][0] = 1e300;
-    for (int q = 1; q <= kQMax; ++q) {
-      double rho = std::pow(tol, -1.0 / (2.0 * q));
-      delta[band][q] = 0.5 * (rho + 1.0 / rho) - 1.0;
-    }
+  double delta[kQMax + 1];
+  delta[0] = 1e300;
+  for (int q = 1; q <= kQMax; ++q) {
+    double rho = std::pow(c.far_tol, -1.0 / (2.0 * q));
+    delta[q] = 0.5 * (rho + 1.0 / rho) - 1.0;
   }
   GBEM_CUDA(ctx, cudaMemcpyToSymbolAsync(c_delta, delta, sizeof(delta), 0, cudaMemcpyHostToDevice,
                                          ctx->stream));
@@ -632,8 +606,15 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
              float* ms_near) {
   int sms = ctx->num_sms;
   cudaEventRecord(ctx->ev[2], ctx->stream);
-  k_far<<<sms * 8, 256, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, ctx->d_stats);
+#define GBEM_FAR(QV, QU, B) \
+  k_far<QV, QU><<<sms * (B), 256, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, ctx->d_stats); \
   GBEM_LAUNCH_CHECK(ctx);
+  GBEM_FAR(1, 1, 1)
+  GBEM_FAR(2, 1, 1) GBEM_FAR(2, 2, 1)
+  GBEM_FAR(3, 1, 2) GBEM_FAR(3, 2, 2) GBEM_FAR(3, 3, 3)
+  GBEM_FAR(4, 1, 2) GBEM_FAR(4, 2, 3) GBEM_FAR(4, 3, 3) GBEM_FAR(4, 4, 3)
+  GBEM_FAR(5, 0, 2) GBEM_FAR(6, 0, 2) GBEM_FAR(7, 0, 2) GBEM_FAR(8, 0, 2)
+#undef GBEM_FAR
   cudaEventRecord(ctx->ev[3], ctx->stream);
   k_coplanar<<<sms * 4, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o);
   GBEM_LAUNCH_CHECK(ctx);

@@ -18,7 +18,7 @@ struct __align__(16) DPanel {
 };
 
 constexpr double kFourPi = 4.0 * 3.14159265358979323846;  // oracle.hpp:11
-constexpr int kQMax = 12;                                  // max far-field Gauss order per direction
+constexpr int kQMax = 8;                                   // max far-field Gauss order per direction
 
 // Pair classes (queue key < kFarKeyBase).  Far keys pack four 4-bit orders.
 enum PairClass : uint32_t {
@@ -36,8 +36,24 @@ enum PairClass : uint32_t {
 };
 constexpr int kNumKeys = 1 << 16;
 
-__host__ __device__ inline uint32_t far_key(int qs, int qt, int qu, int qv) {
-  return (uint32_t)(qs | (qt << 4) | (qu << 8) | (qv << 12));
+// Far keys are canonical: the largest of the four per-direction orders (QV)
+// sits in direction V of panel J; `swap` says J is the pair's first panel,
+// `v_is_a` that V is J's first in-plane axis.  QV is the most significant field,
+// so the queue segment of one QV is contiguous and runs in its own kernel.
+//   key = kFarKeyBase + ((QV-1) << 11 | (qu-1) << 8 | swap << 7 | v_is_a << 6 | (qs-1) << 3 | (qt-1))
+// (QV, qu) segments are contiguous too: the common small-order cases run fully unrolled.
+__host__ __device__ inline uint32_t far_key(int qa_i, int qb_i, int qa_j, int qb_j) {
+  const int mi = qa_i > qb_i ? qa_i : qb_i, mj = qa_j > qb_j ? qa_j : qb_j;
+  const int swap = mi > mj ? 1 : 0;
+  const int qs = swap ? qa_j : qa_i, qt = swap ? qb_j : qb_i;
+  const int ja = swap ? qa_i : qa_j, jb = swap ? qb_i : qb_j;
+  const int v_is_a = ja > jb ? 1 : 0;
+  const int QV = v_is_a ? ja : jb, qu = v_is_a ? jb : ja;
+  return 16u + (uint32_t)(((QV - 1) << 11) | ((qu - 1) << 8) | (swap << 7) | (v_is_a << 6) | ((qs - 1) << 3) |
+                          (qt - 1));
+}
+__host__ __device__ inline uint32_t far_key_first(int QV, int qu = 1) {
+  return 16u + (uint32_t)(((QV - 1) << 11) | ((qu - 1) << 8));
 }
 
 // Queue entry: i (24 bits) | j (24 bits) | key (16 bits).
