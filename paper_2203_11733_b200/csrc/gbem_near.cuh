@@ -1,6 +1,6 @@
 // gbem_near.cuh — near-field / singular pair integrals on the GPU.
 //
-// These classes (self, edge/corner-touching, and pairs closer than 0.75
+// These classes (self, edge/corner-touching, and pairs closer than one
 // diameters) are evaluated with the reference's own semi-analytic reductions,
 // re-expressed for the GPU:
 //   * coplanar: 16-corner closed form, one thread per pair
@@ -157,6 +157,93 @@ struct OrthFy {
         double x = side == 0 ? x3u : x3d;
         double c2 = x * x + y2;
         acc += Corners::sign(k) * sx * d_mul_log(0.5 * val[k] * x, val[k], c2, guard);
+      }
+    return acc;
+  }
+};
+
+
+// ---- fast forms of the reduced integrands for the fixed-rule near field:
+// log(u + r) for u < 0 as log(c2 / (r - u)) (one log instead of the
+// reference's log(c2) - log(r - u)), and the two mulLog terms of fx that share
+// log(y + sqrt(y^2 + u^2 + x^2)) evaluate it once.  Guards as mulLog: a term
+// whose prefactor is <= guard contributes 0 and its log is not evaluated.
+__device__ __forceinline__ double d_lupr_fast(double u, double c2) {
+  const double r = sqrt(u * u + c2);
+  if (u >= 0.0) {
+    const double arg = u + r;
+    return arg > 0.0 ? log(arg) : -CUDART_INF;
+  }
+  return c2 == 0.0 ? -CUDART_INF : log(c2 / (r - u));
+}
+
+struct ParIntegrandFast {
+  double val[4];
+  double b2, t0, t3, plateau;
+  __device__ double operator()(double v) const {
+    const double c2 = v * v + b2;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double u = val[k];
+      const double r = sqrt(u * u + c2);
+      const double lg = u >= 0.0 ? log(u + r) : log(c2 / (r - u));
+      acc += Corners::sign(k) * (u * lg - r);
+    }
+    double m = v - t0;
+    m = plateau < m ? plateau : m;
+    m = (t3 - v) < m ? (t3 - v) : m;
+    return (0.0 < m ? m : 0.0) * acc;
+  }
+};
+
+struct OrthFxFast {
+  double val[4];
+  double y2d, y2u, guard;
+  __device__ double operator()(double x) const {
+    double acc = 0.0;
+    const double x2 = x * x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double cv = val[k];
+      const double u2 = cv * cv;
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const double y = side == 0 ? y2u : y2d;
+        const double c2 = x2 + y * y;
+        const double p1 = 0.5 * cv * y, p2 = 0.5 * u2, p3 = 0.5 * (x2 + u2);
+        double term = 0.0;
+        if (fabs(p1) > guard) term = p1 * d_lupr_fast(cv, c2);
+        if (fabs(p2) > guard || fabs(p3) > guard) {
+          const double l2 = d_lupr_fast(y, u2 + x2);
+          if (fabs(p2) > guard) term += p2 * l2;
+          term -= fabs(p3) > guard ? p3 * l2 : 0.0;
+        }
+        const double r = sqrt(u2 + c2);
+        const double t = term - 0.5 * y * r;
+        acc += (side == 0 ? Corners::sign(k) : -Corners::sign(k)) * t;
+      }
+    }
+    return acc;
+  }
+};
+
+struct OrthFyFast {
+  double val[4];
+  double x3d, x3u, guard;
+  __device__ double operator()(double y) const {
+    double acc = 0.0;
+    const double y2 = y * y;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const double x = side == 0 ? x3u : x3d;
+        const double p = 0.5 * val[k] * x;
+        if (fabs(p) > guard) {
+          const double t = p * d_lupr_fast(val[k], x * x + y2);
+          acc += (side == 0 ? Corners::sign(k) : -Corners::sign(k)) * t;
+        }
       }
     return acc;
   }
@@ -426,7 +513,7 @@ __device__ double gl_graded(const F& f, double a, double b, int band, const doub
 __device__ inline double gl_u_parallel(const DPanel& A, const DPanel& B, int band, const double (*nx)[48],
                                        const double (*nw)[48], bool& bad) {
   double off = A.level - B.level;
-  ParIntegrand f;
+  ParIntegrandFast f;
   Corners c(A.a0, A.a1, B.a0, B.a1);
   for (int k = 0; k < 4; ++k) f.val[k] = c.val[k];
   f.b2 = off * off;
@@ -469,8 +556,8 @@ __device__ inline double gl_u_orthogonal(const DPanel& A, const DPanel& B, int b
   Corners c(s1lo, s1hi, t1lo, t1hi);
   double scale = dmax4(s1hi - s1lo, t1hi - t1lo, s3hi - s3lo, t2hi - t2lo);
   scale = scale < 1e-30 ? 1e-30 : scale;
-  OrthFx fx;
-  OrthFy fy;
+  OrthFxFast fx;
+  OrthFyFast fy;
   for (int k = 0; k < 4; ++k) {
     fx.val[k] = c.val[k];
     fy.val[k] = c.val[k];
