@@ -112,11 +112,13 @@ int gbem_assemble_single(gbem_ctx* ctx, const gbem_panels* P, int64_t n,
  * read back stats when stats != NULL. */
 int gbem_assemble_single_dev(gbem_ctx* ctx, const gbem_panels* P_dev, int64_t n,
                              const gbem_quad_config* cfg, gbem_assembly_stats* stats);
-/* Assemble only rows [row_begin, row_end) of the upper triangle (row-block
- * sharding: no communication; rank r owns a work-balanced row range). */
+/* Row-block sharded assembly (no communication; rank r owns a work-balanced
+ * row range): rows [row_begin, row_end) of the upper triangle into the caller's
+ * device buffer, entry (i, j >= i) at out[(i - row_begin) * ld_out + j]
+ * (ld_out >= n; entries j < i are not written). */
 int gbem_assemble_rows_dev(gbem_ctx* ctx, const gbem_panels* P_dev, int64_t n,
                            int64_t row_begin, int64_t row_end, const gbem_quad_config* cfg,
-                           gbem_assembly_stats* stats);
+                           double* out, int64_t ld_out, gbem_assembly_stats* stats);
 
 /* Copy the assembled (or factored) matrix to the host: row-major, lda >= n. */
 int gbem_matrix_download(gbem_ctx* ctx, double* A_host, int64_t lda);

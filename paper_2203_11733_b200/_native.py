@@ -63,7 +63,7 @@ GPU_SYMBOLS = [
     ("gbem_assemble_single_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, C.POINTER(GbemQuadConfig),
                                            C.POINTER(GbemAssemblyStats)]),
     ("gbem_assemble_rows_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, C.c_int64, C.c_int64,
-                                         C.POINTER(GbemQuadConfig), C.POINTER(GbemAssemblyStats)]),
+                                         C.POINTER(GbemQuadConfig), _P, C.c_int64, C.POINTER(GbemAssemblyStats)]),
     ("gbem_matrix_download", C.c_int, [_P, _P, C.c_int64]),
     ("gbem_matrix_upload", C.c_int, [_P, _P, C.c_int64, C.c_int64]),
     ("gbem_matrix_device", C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

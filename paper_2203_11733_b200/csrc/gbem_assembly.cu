@@ -713,7 +713,8 @@ int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, 
 
 // Assemble rows [row_begin, row_end) of the upper triangle into ctx->d_A.
 int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,
-                           const gbem_quad_config* cfg_in, gbem_assembly_stats* stats, bool symmetrize) {
+                           const gbem_quad_config* cfg_in, gbem_assembly_stats* stats, bool symmetrize,
+                           double* out, int64_t ld_out) {
   gbem_quad_config cfg;
   int rc = prepare_work(ctx, cfg_in, &cfg);
   if (rc) return rc;
@@ -737,7 +738,13 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
   GBEM_CUDA(ctx, cudaMallocAsync(&d_rowoff, sizeof(long long) * rowoff.size(), ctx->stream));
   GBEM_CUDA(ctx, cudaMemcpyAsync(d_rowoff, rowoff.data(), sizeof(long long) * rowoff.size(),
                                  cudaMemcpyHostToDevice, ctx->stream));
+  // destination: the context matrix (entry (i, j >= i) at A[i*lda + j]) or a
+  // caller row block (entry at out[(i - row_begin)*ld_out + j])
   OutSpec o{ctx->d_A, (long long)ctx->lda, nullptr, nullptr};
+  if (out) {
+    o.A = out - row_begin * ld_out;
+    o.lda = (long long)ld_out;
+  }
   const long long tiles_per_chunk = std::max<long long>(1, ctx->queue_cap / (kTile * kTile));
   float ms_cls = 0, ms_far = 0, ms_near = 0;
   bool timing = stats != nullptr;

@@ -230,17 +230,16 @@ int gbem_assemble_single_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, con
 }
 
 int gbem_assemble_rows_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, int64_t row_begin, int64_t row_end,
-                           const gbem_quad_config* cfg, gbem_assembly_stats* stats) {
+                           const gbem_quad_config* cfg, double* out, int64_t ld_out, gbem_assembly_stats* stats) {
   if (!ctx) return GBEM_EINVAL;
   if (row_begin < 0 || row_end > n || row_begin > row_end)
     return ctx->fail(GBEM_EINVAL, "row range out of bounds");
+  if (!out || ld_out < n) return ctx->fail(GBEM_EINVAL, "row block buffer missing or ld_out < n");
   GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
   int rc = gbem_internal_upload_panels(ctx, P, n, true);
   if (rc) return rc;
-  rc = ensure_matrix(ctx, n);
-  if (rc) return rc;
   if (row_end == row_begin) return GBEM_OK;
-  return gbem_internal_assemble(ctx, n, row_begin, row_end, cfg, stats, false);
+  return gbem_internal_assemble(ctx, n, row_begin, row_end, cfg, stats, false, out, ld_out);
 }
 
 int gbem_matrix_download(gbem_ctx* ctx, double* A_host, int64_t lda) {

@@ -76,7 +76,8 @@ struct gbem_ctx {
 int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n);
 int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, bool device_ptrs);
 int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,
-                           const gbem_quad_config* cfg, gbem_assembly_stats* stats, bool symmetrize);
+                           const gbem_quad_config* cfg, gbem_assembly_stats* stats, bool symmetrize,
+                           double* out = nullptr, int64_t ld_out = 0);
 int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_config* cfg,
                             double* d_out, int32_t* d_conv, gbem_assembly_stats* stats);
 int gbem_internal_init_tables(gbem_ctx* ctx);
