@@ -194,3 +194,14 @@ def test_config5_geometry():
     assert len(ps) == 2000
     assert la.min() >= 0.002 - 1e-15 and la.max() <= 0.2 + 1e-15
     assert np.all(np.abs(ps.level * 1000 - np.round(ps.level * 1000)) < 1e-6)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_config_panel_lists_match_golden_fixture(cfg):
+    """The committed C-matrix fixtures were computed on exactly these panel lists."""
+    import hashlib
+    import json
+    fx = json.loads((ROOT / "tests" / "golden" / f"config{cfg}_cmatrix.json").read_text())
+    P = g.config_model(cfg, seed=fx["seed"]).partition(1).matrix()
+    assert len(P) == fx["panels"]
+    assert hashlib.sha256(np.ascontiguousarray(P).tobytes()).hexdigest() == fx["panels_sha256"]
