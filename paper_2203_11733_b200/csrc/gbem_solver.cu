@@ -43,13 +43,17 @@ constexpr int NB = 128;       // Cholesky block size (diagonal blocks, trailing-
 // in xd.  info[0] receives the first failing global row (atomicMin); a failed
 // pivot continues as 1 so the launch sequence stays fixed.
 #ifdef GBEM_POTRF_TIMING
-__device__ long long g_potrf_clk[64];
+__device__ long long g_potrf_clk[128];
 #define POTRF_TICK(k) \
   if (threadIdx.x == 0) g_potrf_clk[k] = clock64();
 #else
 #define POTRF_TICK(k)
 #endif
 constexpr int kPotrfThreads = 512;
+constexpr int kPotrfWarps = kPotrfThreads / 32;
+constexpr int kRowSlots = NB / kPotrfWarps;          // rows per warp in a pivot phase
+constexpr int kXSlots = 32 / kPotrfWarps;            // in-panel X rows per warp
+constexpr int kFinSlots = (NB + kPotrfThreads - 1) / kPotrfThreads;
 constexpr int kPanel = 32;
 constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + 2 * NB + 3 * kPanel * kPanel) * sizeof(double);
 
@@ -62,12 +66,23 @@ __global__ void __launch_bounds__(kPotrfThreads)
   double* sqd = xd + NB;       // diag of L
   double* tmp = sqd + NB;      // [3][32*32] products of the X assembly
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int idx = tid; idx < NB * NB; idx += kPotrfThreads) {
-    int c = idx / NB, r = idx % NB;
-    double v = 0.0;
-    if (r < kb && c < kb) v = r >= c ? A[(long long)c * lda + r] : 0.0;
-    else if (r == c) v = 1.0;  // pad the ragged last block with the identity
-    a[c * LD + r] = v;
+  // load the block: 8 independent global loads in flight per thread per batch
+  for (int idx0 = tid; idx0 < NB * NB; idx0 += 8 * kPotrfThreads) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = idx0 + u * kPotrfThreads, c = idx / NB, r = idx % NB;
+      v[u] = 0.0;
+      if (idx < NB * NB) {
+        if (r < kb && c < kb) v[u] = r >= c ? A[(long long)c * lda + r] : 0.0;
+        else if (r == c) v[u] = 1.0;  // pad the ragged last block with the identity
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int idx = idx0 + u * kPotrfThreads;
+      if (idx < NB * NB) a[(idx / NB) * LD + idx % NB] = v[u];
+    }
   }
   __syncthreads();
   POTRF_TICK(0);
@@ -81,57 +96,72 @@ __global__ void __launch_bounds__(kPotrfThreads)
     // of X = inv(L_pp) (S = X diag(L), stored transposed in the upper half), and
     // finalises column j-1 / X row j-1, which phase j never reads.
     for (int j = c0; j < c0 + kPanel; ++j) {
+      // (a) every shared load of the phase first (none depends on the pivot) ...
       double d = a[j * LD + j];
+      const int cc = c0 + lane;  // panel column of this lane
+      const bool colv = cc > j;
+      const double acj = colv ? a[j * LD + cc] : 0.0;
+      double tv[kRowSlots], arj[kRowSlots];
+#pragma unroll
+      for (int k = 0; k < kRowSlots; ++k) {
+        const int r = j + 1 + warp + kPotrfWarps * k;
+        const bool ok = colv && r < NB && r >= cc;
+        tv[k] = ok ? a[cc * LD + r] : 0.0;
+        arj[k] = ok ? a[j * LD + r] : 0.0;
+      }
+      const int kx = c0 + lane;  // in-panel X column of this lane
+      const double sjk = kx < j ? a[j * LD + kx] : 0.0;
+      double sv[kXSlots], lij[kXSlots];
+#pragma unroll
+      for (int h = 0; h < kXSlots; ++h) {
+        const int ix = j + 1 + warp + kPotrfWarps * h;
+        const bool ok = kx <= j && ix < c0 + kPanel;
+        sv[h] = ok && kx < j ? a[ix * LD + kx] : 0.0;
+        lij[h] = ok ? a[j * LD + ix] : 0.0;
+      }
+      const int q = j - 1;  // column / X row finalised in this phase
+      const bool fin = j > c0;
+      const double iq = fin ? xd[q] : 0.0;
+      double fl[kFinSlots];
+#pragma unroll
+      for (int k = 0; k < kFinSlots; ++k) {
+        const int r = q + 1 + tid + kPotrfThreads * k;
+        fl[k] = fin && r < NB ? a[q * LD + r] : 0.0;
+      }
+      const double fx = fin && tid < q - c0 ? a[q * LD + c0 + tid] : 0.0;
+      // (b) ... then the pivot ...
       if (!(d > 0.0)) {
         if (tid == 0 && !bad && j < kb) atomicMin(info, row0 + j);
         bad = true;
         d = 1.0;
       }
       const double is = gbem_gpu::rsq64(d), isd = is * is;
+      // (c) ... then every store.  Phase j never writes column j, and each
+      // element it writes is read only by the thread writing it: one barrier.
       if (tid == 0) {
         xd[j] = is;
         sqd[j] = d * is;
       }
-      if (j > c0) {
-        const int q = j - 1;
-        const double iq = xd[q];
-        for (int r = q + 1 + tid; r < NB; r += kPotrfThreads) a[q * LD + r] *= iq;          // L(r, q)
-        if (tid < q - c0) a[q * LD + c0 + tid] *= iq;                                      // X(q, c0+tid)
-      }
-      // Cholesky update of the panel columns, rows r >= c: lane -> column, warp -> rows
-      const int cc = c0 + lane;
-      const bool colv = cc > j;
-      const double acj = colv ? a[j * LD + cc] * isd : 0.0;
-      double tv[8], arj[8];
+      const double acjs = acj * isd;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int r = j + 1 + warp + 16 * k;
-        const bool ok = colv && r < NB && r >= cc;
-        tv[k] = ok ? a[cc * LD + r] : 0.0;
-        arj[k] = ok ? a[j * LD + r] : 0.0;
+      for (int k = 0; k < kRowSlots; ++k) {
+        const int r = j + 1 + warp + kPotrfWarps * k;
+        if (colv && r < NB && r >= cc) a[cc * LD + r] = fma(-arj[k], acjs, tv[k]);   // A(r,c) -= L(r,j) L(c,j)
       }
-      // in-panel X rows: S(i,k) -= L(i,j) X(j,k), i in (j, c0+32), k in [c0, j]
-      const int kx = c0 + lane;
-      bool xv[2];
-      double sv[2], lij[2];
-      const double xjk = kx == j ? is : (kx < j ? a[j * LD + kx] * is : 0.0);
+      const double xjk = kx == j ? is : sjk * is;  // X(j, kx)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int ix = j + 1 + warp + 16 * h;
-        xv[h] = kx <= j && ix < c0 + kPanel;
-        sv[h] = xv[h] && kx < j ? a[ix * LD + kx] : 0.0;
-        lij[h] = xv[h] ? a[j * LD + ix] * is : 0.0;
+      for (int h = 0; h < kXSlots; ++h) {
+        const int ix = j + 1 + warp + kPotrfWarps * h;
+        if (kx <= j && ix < c0 + kPanel) a[ix * LD + kx] = fma(-lij[h] * is, xjk, sv[h]);  // S(i,k) -= L(i,j) X(j,k)
       }
-      // (no barrier needed here: phase j never writes column j, and every
-      // element it writes is read only by the thread that writes it)
+      if (fin) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int r = j + 1 + warp + 16 * k;
-        if (colv && r < NB && r >= cc) a[cc * LD + r] = fma(-arj[k], acj, tv[k]);
+        for (int k = 0; k < kFinSlots; ++k) {
+          const int r = q + 1 + tid + kPotrfThreads * k;
+          if (r < NB) a[q * LD + r] = fl[k] * iq;  // L(r, q)
+        }
+        if (tid < q - c0) a[q * LD + c0 + tid] = fx * iq;  // X(q, c0+tid)
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        if (xv[h]) a[(j + 1 + warp + 16 * h) * LD + kx] = fma(-lij[h], xjk, sv[h]);
       __syncthreads();
     }
     {  // finalise the last panel column and X row
@@ -181,40 +211,57 @@ __global__ void __launch_bounds__(kPotrfThreads)
     POTRF_TICK(3 + 3 * p);
   }
   POTRF_TICK(20);
-  // ---- off-diagonal blocks of X = inv(L): X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp.
-  // Each thread computes 4 adjacent columns of one row (4 independent chains).
+  // ---- off-diagonal blocks of X = inv(L): X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp,
+  // 4 x 4 register tiles (8 shared loads per 16 FMAs).
   for (int rbk = 1; rbk < npan; ++rbk) {
     const int R0 = rbk * kPanel;
-    const int ntask = rbk * kPanel * (kPanel / 4);
+    const int ntask = rbk * 64;  // 64 tiles of 4 x 4 per 32 x 32 block
     for (int t = tid; t < ntask; t += kPotrfThreads) {
-      const int i = t % kPanel, k4 = (t / kPanel) % (kPanel / 4), pb = t / (kPanel * (kPanel / 4));
-      const int col = pb * kPanel + 4 * k4;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int m = col; m < R0; ++m) {
-        const double lrm = a[m * LD + R0 + i];  // L(R0+i, m)
+      const int pb = t / 64, ti = (t % 64) % 8, tk = (t % 64) / 8;
+      const int col0 = pb * kPanel + 4 * tk;
+      double acc[4][4] = {};
+      for (int m = col0; m < R0; ++m) {
+        double lr[4], xc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) lr[u] = a[m * LD + R0 + 4 * ti + u];  // L(R0+i, m)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
-          const int c = col + v;
-          const double xmc = m == c ? xd[m] : (m > c ? a[m * LD + c] : 0.0);  // X(m, c)
-          acc[v] = fma(lrm, xmc, acc[v]);
+          const int c = col0 + v;
+          xc[v] = m == c ? xd[m] : (m > c ? a[m * LD + c] : 0.0);  // X(m, c)
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(lr[u], xc[v], acc[u][v]);
       }
 #pragma unroll
-      for (int v = 0; v < 4; ++v) tmp[pb * kPanel * kPanel + (4 * k4 + v) * kPanel + i] = acc[v];
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) tmp[pb * kPanel * kPanel + (4 * tk + v) * kPanel + 4 * ti + u] = acc[u][v];
     }
     __syncthreads();
     for (int t = tid; t < ntask; t += kPotrfThreads) {
-      const int i = t % kPanel, k4 = (t / kPanel) % (kPanel / 4), pb = t / (kPanel * (kPanel / 4));
-      const int col = pb * kPanel + 4 * k4;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int m = 0; m <= i; ++m) {
-        const double xim = m == i ? xd[R0 + i] : a[(R0 + i) * LD + R0 + m];  // X(R0+i, R0+m)
+      const int pb = t / 64, ti = (t % 64) % 8, tk = (t % 64) / 8;
+      const int col0 = pb * kPanel + 4 * tk;
+      double acc[4][4] = {};
+      for (int m = 0; m < 4 * ti + 4; ++m) {
+        double xr[4], tv[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v)
-          acc[v] = fma(xim, tmp[pb * kPanel * kPanel + (4 * k4 + v) * kPanel + m], acc[v]);
+        for (int u = 0; u < 4; ++u) {
+          const int i = 4 * ti + u;
+          xr[u] = m == i ? xd[R0 + i] : (m < i ? a[(R0 + i) * LD + R0 + m] : 0.0);  // X(R0+i, R0+m)
+        }
+#pragma unroll
+        for (int v = 0; v < 4; ++v) tv[v] = tmp[pb * kPanel * kPanel + (4 * tk + v) * kPanel + m];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(xr[u], tv[v], acc[u][v]);
       }
 #pragma unroll
-      for (int v = 0; v < 4; ++v) a[(R0 + i) * LD + col + v] = -acc[v];  // X(R0+i, col+v)
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) a[(R0 + 4 * ti + u) * LD + col0 + v] = -acc[u][v];  // X(R0+i, col)
     }
     __syncthreads();
   }
