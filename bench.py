@@ -126,7 +126,10 @@ def run_ours(args):
     n = len(ps)
     entries = n * (n + 1) // 2
     ctx = N.Context(local)
-    stream = torch.cuda.current_stream(dev)
+    # one dedicated stream for torch and the library: the CUDA events below time
+    # exactly the work enqueued on it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     # device-resident inputs (panel SoA + net index), outputs
     t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in

@@ -88,7 +88,9 @@ typedef struct {
 int gbem_ctx_create(int device, gbem_ctx** out);
 void gbem_ctx_destroy(gbem_ctx* ctx);
 const char* gbem_last_error(const gbem_ctx* ctx);
-/* Run subsequent work on an existing cudaStream_t (NULL: the context's own). */
+/* Run subsequent work on an existing cudaStream_t (NULL: the context's own
+ * non-blocking stream; pass cudaStreamLegacy, (void*)1, for the legacy default
+ * stream, which is what a framework's "stream 0" handle means). */
 int gbem_ctx_set_stream(gbem_ctx* ctx, void* cuda_stream);
 /* Number of this library's kernels launched on the context so far. */
 int64_t gbem_ctx_launch_count(const gbem_ctx* ctx);
@@ -119,6 +121,24 @@ int gbem_assemble_single_dev(gbem_ctx* ctx, const gbem_panels* P_dev, int64_t n,
 int gbem_assemble_rows_dev(gbem_ctx* ctx, const gbem_panels* P_dev, int64_t n,
                            int64_t row_begin, int64_t row_end, const gbem_quad_config* cfg,
                            double* out, int64_t ld_out, gbem_assembly_stats* stats);
+
+/* As gbem_assemble_rows_dev but for complete rows (all j, the mirrored
+ * entries recomputed locally): entry (i, j) at out[(i - row_begin) * ld_out + j].
+ * This is the row block a sharded solver multiplies with. */
+int gbem_assemble_rows_full_dev(gbem_ctx* ctx, const gbem_panels* P_dev, int64_t n,
+                                int64_t row_begin, int64_t row_end, const gbem_quad_config* cfg,
+                                double* out, int64_t ld_out, gbem_assembly_stats* stats);
+/* Q = Ablk * P for a row block Ablk (rows x n, row i contiguous, leading
+ * dimension ld) and P (n x K row-major: K values per panel, leading dimension
+ * ldp >= K); Q is rows x K row-major with ldq >= K.  Device pointers. */
+int gbem_rowblock_matvec_dev(gbem_ctx* ctx, const double* Ablk, int64_t ld, int64_t rows, int64_t n,
+                             const double* P, int64_t ldp, int64_t K, double* Q, int64_t ldq);
+/* Factor a device SPD matrix (column-major m x m, ldm) into the context and keep
+ * the factor for repeated gbem_spd_solve_factored_dev calls (block-Jacobi
+ * preconditioner of the sharded solver). */
+int gbem_spd_factor_dev(gbem_ctx* ctx, const double* M, int64_t m, int64_t ldm, gbem_solve_stats* stats);
+int gbem_spd_solve_factored_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
+                                gbem_solve_stats* stats);
 
 /* Copy the assembled (or factored) matrix to the host: row-major, lda >= n. */
 int gbem_matrix_download(gbem_ctx* ctx, double* A_host, int64_t lda);

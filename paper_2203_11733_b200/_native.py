@@ -64,6 +64,12 @@ GPU_SYMBOLS = [
                                            C.POINTER(GbemAssemblyStats)]),
     ("gbem_assemble_rows_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, C.c_int64, C.c_int64,
                                          C.POINTER(GbemQuadConfig), _P, C.c_int64, C.POINTER(GbemAssemblyStats)]),
+    ("gbem_assemble_rows_full_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, C.c_int64, C.c_int64,
+                                              C.POINTER(GbemQuadConfig), _P, C.c_int64, C.POINTER(GbemAssemblyStats)]),
+    ("gbem_rowblock_matvec_dev", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int64, _P,
+                                           C.c_int64]),
+    ("gbem_spd_factor_dev", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.POINTER(GbemSolveStats)]),
+    ("gbem_spd_solve_factored_dev", C.c_int, [_P, _P, C.c_int64, _P, _P, C.POINTER(GbemSolveStats)]),
     ("gbem_matrix_download", C.c_int, [_P, _P, C.c_int64]),
     ("gbem_matrix_upload", C.c_int, [_P, _P, C.c_int64, C.c_int64]),
     ("gbem_matrix_device", C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -167,7 +173,11 @@ class Context:
         return int(self.lib.gbem_ctx_launch_count(self.h))
 
     def set_stream(self, stream_handle: int | None):
-        self.check(self.lib.gbem_ctx_set_stream(self.h, _P(stream_handle or 0)))
+        """Order this context's work on a framework stream.  A handle of 0 is the
+        legacy default stream (torch's default stream), passed as cudaStreamLegacy;
+        None returns to the context's own stream."""
+        h = None if stream_handle is None else (stream_handle or 1)
+        self.check(self.lib.gbem_ctx_set_stream(self.h, _P(h)))
 
     @staticmethod
     def quad(rel_tol=1e-8, max_levels=16, near_ratio=1.0, far_tol=1e-12) -> GbemQuadConfig:

@@ -204,7 +204,7 @@ template <bool FILL>
 __global__ void __launch_bounds__(kClassifyThreads)
     k_classify(const DPanel* __restrict__ P, int n, int rb, int re, int bi0, int nbt,
                const long long* __restrict__ tile_row_off, int nrows_t, long long tile_begin,
-               double near_ratio, uint32_t* counts, uint32_t* cursors, uint64_t* queue) {
+               double near_ratio, uint32_t* counts, uint32_t* cursors, uint64_t* queue, int full) {
   __shared__ DPanel si[kTile], sj[kTile];
   long long t = tile_begin + blockIdx.x;
   // binary search the tile row
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kClassifyThreads)
       hi = mid - 1;
   }
   int bi = bi0 + lo;
-  int bj = bi + (int)(t - tile_row_off[lo]);
+  int bj = (full ? 0 : bi) + (int)(t - tile_row_off[lo]);  // full: whole rows (mirrored entries too)
   int tid = threadIdx.x;
   if (tid < kTile) {
     int i = bi * kTile + tid;
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kClassifyThreads)
 #pragma unroll 1
   for (int r = warp; r < kTile; r += kClassifyThreads / 32) {
     int i = bi * kTile + r;
-    bool valid = i >= rb && i < re && j < n && j >= i;
+    bool valid = i >= rb && i < re && j < n && (full || j >= i);
     uint32_t key = 0;
     if (valid) key = classify_pair(si[r], sj[lane], i == j, near_ratio);
     warp_append<FILL>(valid, key, (uint32_t)i, (uint32_t)j, counts, cursors, queue);
@@ -714,7 +714,7 @@ int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, 
 // Assemble rows [row_begin, row_end) of the upper triangle into ctx->d_A.
 int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,
                            const gbem_quad_config* cfg_in, gbem_assembly_stats* stats, bool symmetrize,
-                           double* out, int64_t ld_out) {
+                           double* out, int64_t ld_out, bool full_rows) {
   gbem_quad_config cfg;
   int rc = prepare_work(ctx, cfg_in, &cfg);
   if (rc) return rc;
@@ -727,7 +727,7 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
   long long total_tiles = 0;
   for (int r = 0; r < nrows_t; ++r) {
     rowoff[(size_t)r] = total_tiles;
-    total_tiles += nbt - (bi0 + r);
+    total_tiles += full_rows ? nbt : nbt - (bi0 + r);
   }
   rowoff[(size_t)nrows_t] = total_tiles;
   // queue capacity: 2^27 entries (1 GiB) or what the problem needs
@@ -755,13 +755,13 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
     GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, ctx->stream));
     k_classify<false><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
         ctx->d_panels, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
-        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue);
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
     k_scan<<<1, 1024, 0, ctx->stream>>>(ctx->d_counts, ctx->d_offsets, ctx->d_cursors, ctx->d_stats);
     GBEM_LAUNCH_CHECK(ctx);
     k_classify<true><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
         ctx->d_panels, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
-        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue);
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
     cudaEventRecord(ctx->ev[6], ctx->stream);
     if (timing) {
@@ -781,7 +781,7 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
   cudaEventRecord(ctx->ev[1], ctx->stream);
   GBEM_CUDA(ctx, cudaFreeAsync(d_rowoff, ctx->stream));
   long long pairs = 0;
-  for (int64_t i = row_begin; i < row_end; ++i) pairs += n - i;
+  for (int64_t i = row_begin; i < row_end; ++i) pairs += full_rows ? n : n - i;
   if (stats) {
     rc = finish_stats(ctx, stats, pairs);
     float tot = 0;
@@ -818,4 +818,70 @@ int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_confi
   rc = run_eval(ctx, o, cfg, nullptr, nullptr);
   if (rc) return rc;
   return finish_stats(ctx, stats, npairs);
+}
+
+namespace {
+// Q (rows x K, row-major, ldq) = Ablk (rows x n, row i contiguous, ld) * P (n x K,
+// row-major: one row of K values per panel, ldp).  32 rows per CTA (4 per warp);
+// P is staged through shared memory in 256-panel chunks, KC right-hand sides per
+// pass.  HBM-bound on Ablk (8 B per entry per pass) for K <= KC.
+template <int KC, int RW>
+__global__ void __launch_bounds__(256, 2)
+    k_rowblock_matvec(const double* __restrict__ Ab, long long ld, int rows, int n, const double* __restrict__ P,
+                      long long ldp, int K, int q0, double* __restrict__ Q, long long ldq) {
+  __shared__ double ps[KC * 256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = blockIdx.x * (8 * RW) + warp * RW;
+  const int kc = min(KC, K - q0);
+  double acc[RW][KC];
+#pragma unroll
+  for (int u = 0; u < RW; ++u)
+#pragma unroll
+    for (int q = 0; q < KC; ++q) acc[u][q] = 0.0;
+  for (int j0 = 0; j0 < n; j0 += 256) {
+    const int jn = min(256, n - j0);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 256 * KC; idx += blockDim.x) {
+      const int jj = idx / KC, q = idx % KC;
+      ps[q * 256 + jj] = (jj < jn && q < kc) ? P[(long long)(j0 + jj) * ldp + q0 + q] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int t = 0; t < 8; ++t) {
+      const int c = lane + 32 * t;
+      double pv[KC];
+#pragma unroll
+      for (int q = 0; q < KC; ++q) pv[q] = ps[q * 256 + c];  // one shared load per P value, reused RW times
+      double av[RW];
+#pragma unroll
+      for (int u = 0; u < RW; ++u) av[u] = (c < jn && r0 + u < rows) ? __ldcs(Ab + (long long)(r0 + u) * ld + j0 + c) : 0.0;
+#pragma unroll
+      for (int u = 0; u < RW; ++u)
+#pragma unroll
+        for (int q = 0; q < KC; ++q) acc[u][q] = fma(av[u], pv[q], acc[u][q]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < RW; ++u) {
+    const int r = r0 + u;
+#pragma unroll
+    for (int q = 0; q < KC; ++q) {
+      double v = acc[u][q];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0 && r < rows && q < kc) Q[(long long)r * ldq + q0 + q] = v;
+    }
+  }
+}
+}  // namespace
+
+int gbem_internal_rowblock_matvec(gbem_ctx* ctx, const double* Ab, int64_t ld, int64_t rows, int64_t n,
+                                  const double* P, int64_t ldp, int64_t K, double* Q, int64_t ldq) {
+  if (rows <= 0 || K <= 0) return GBEM_OK;
+  for (int q0 = 0; q0 < K; q0 += 8) {
+    k_rowblock_matvec<8, 4><<<(unsigned)((rows + 31) / 32), 256, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P,
+                                                                                 ldp, (int)K, q0, Q, ldq);
+    GBEM_LAUNCH_CHECK(ctx);
+  }
+  return GBEM_OK;
 }

@@ -138,6 +138,7 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   cudaFree(ctx->d_work);
   cudaFree(ctx->d_info);
   cudaFree(ctx->d_rhs);
+  cudaFree(ctx->d_linv);
   if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
   if (ctx->h_info) cudaFreeHost(ctx->h_info);
   for (auto& ev : ctx->ev)
@@ -240,6 +241,48 @@ int gbem_assemble_rows_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, int64
   if (rc) return rc;
   if (row_end == row_begin) return GBEM_OK;
   return gbem_internal_assemble(ctx, n, row_begin, row_end, cfg, stats, false, out, ld_out);
+}
+
+int gbem_assemble_rows_full_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, int64_t row_begin,
+                                int64_t row_end, const gbem_quad_config* cfg, double* out, int64_t ld_out,
+                                gbem_assembly_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  if (row_begin < 0 || row_end > n || row_begin > row_end)
+    return ctx->fail(GBEM_EINVAL, "row range out of bounds");
+  if (!out || ld_out < n) return ctx->fail(GBEM_EINVAL, "row block buffer missing or ld_out < n");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int rc = gbem_internal_upload_panels(ctx, P, n, true);
+  if (rc) return rc;
+  if (row_end == row_begin) return GBEM_OK;
+  return gbem_internal_assemble(ctx, n, row_begin, row_end, cfg, stats, false, out, ld_out, true);
+}
+
+int gbem_rowblock_matvec_dev(gbem_ctx* ctx, const double* Ablk, int64_t ld, int64_t rows, int64_t n,
+                             const double* P, int64_t ldp, int64_t K, double* Q, int64_t ldq) {
+  if (!ctx) return GBEM_EINVAL;
+  if (!Ablk || !P || !Q || ld < n || rows < 0 || K < 0 || ldp < K || ldq < K)
+    return ctx->fail(GBEM_EINVAL, "bad row-block matvec arguments");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  return gbem_internal_rowblock_matvec(ctx, Ablk, ld, rows, n, P, ldp, K, Q, ldq);
+}
+
+int gbem_spd_factor_dev(gbem_ctx* ctx, const double* M, int64_t m, int64_t ldm, gbem_solve_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  if (m < 0 || (m > 0 && (!M || ldm < m))) return ctx->fail(GBEM_EINVAL, "bad matrix dimensions");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int rc = ensure_matrix(ctx, m);
+  if (rc) return rc;
+  if (m > 0)
+    GBEM_CUDA(ctx, cudaMemcpy2DAsync(ctx->d_A, sizeof(double) * ctx->lda, M, sizeof(double) * ldm, sizeof(double) * m,
+                                     m, cudaMemcpyDeviceToDevice, ctx->stream));
+  return gbem_internal_factor(ctx, stats);
+}
+
+int gbem_spd_solve_factored_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
+                                gbem_solve_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  return gbem_internal_solve_factored(ctx, B, nrhs, X, resid, stats);
 }
 
 int gbem_matrix_download(gbem_ctx* ctx, double* A_host, int64_t lda) {

@@ -43,6 +43,8 @@ struct gbem_ctx {
   size_t work_cap = 0;  // elements
   int* d_info = nullptr;
   int* h_info = nullptr;  // pinned
+  double* d_linv = nullptr;  // inverses of the 128 x 128 diagonal blocks of the factor
+  size_t linv_cap = 0;
   double* d_rhs = nullptr;  // B and X of the K-RHS extraction (2 * rhs_cap)
   size_t rhs_cap = 0;
 
@@ -77,9 +79,14 @@ int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n);
 int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, bool device_ptrs);
 int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,
                            const gbem_quad_config* cfg, gbem_assembly_stats* stats, bool symmetrize,
-                           double* out = nullptr, int64_t ld_out = 0);
+                           double* out = nullptr, int64_t ld_out = 0, bool full_rows = false);
+int gbem_internal_rowblock_matvec(gbem_ctx* ctx, const double* Ab, int64_t ld, int64_t rows, int64_t n,
+                                  const double* P, int64_t ldp, int64_t K, double* Q, int64_t ldq);
 int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_config* cfg,
                             double* d_out, int32_t* d_conv, gbem_assembly_stats* stats);
 int gbem_internal_init_tables(gbem_ctx* ctx);
 int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X,
                         double* d_resid, gbem_solve_stats* stats);
+int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats);
+int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
+                                 gbem_solve_stats* stats);

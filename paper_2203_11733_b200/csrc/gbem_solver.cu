@@ -579,26 +579,30 @@ int ensure_work(gbem_ctx* ctx, size_t elems) {
 
 // Blocked Cholesky of ctx->d_A (n x n) + solves for nrhs columns of d_B (ld n)
 // into d_X; d_resid[nrhs] optional.
-int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
-                        gbem_solve_stats* stats) {
+// Blocked Cholesky of ctx->d_A in place (lower triangle <- L, diagonal saved,
+// strict upper triangle untouched); inverses of the diagonal blocks kept in
+// ctx->d_linv.  Non-SPD: GBEM_ENUMERIC "matrix not positive definite (pivot at row k)".
+int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   const int n = (int)ctx->n;
   const long long lda = ctx->lda;
   if (stats) {
     *stats = gbem_solve_stats{};
     stats->n = n;
-    stats->nrhs = nrhs;
     stats->bad_pivot = -1;
   }
-  if (nrhs < 0 || nrhs > 64) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, 64]");
   if (n == 0) return GBEM_OK;
   if (ctx->factored) return ctx->fail(GBEM_EINVAL, "matrix already factored; re-assemble or re-upload");
   const int nblk = (n + NB - 1) / NB;
-  // workspace: inverses of the diagonal blocks (nblk * NB * NB) + symv result (n * nrhs)
-  size_t need = (size_t)nblk * NB * NB + 2 * (size_t)n * (size_t)std::max<int64_t>(nrhs, 1);
-  int rc = ensure_work(ctx, need);
-  if (rc) return rc;
-  double* Linv = ctx->d_work;
-  double* Ysym = ctx->d_work + (size_t)nblk * NB * NB;
+  // inverses of the diagonal blocks, kept with the factor for the solves
+  const size_t need_linv = (size_t)nblk * NB * NB;
+  if (ctx->linv_cap < need_linv) {
+    cudaFree(ctx->d_linv);
+    ctx->d_linv = nullptr;
+    ctx->linv_cap = 0;
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_linv, need_linv * sizeof(double)));
+    ctx->linv_cap = need_linv;
+  }
+  double* Linv = ctx->d_linv;
   if (ctx->diag_cap < n) {
     if (ctx->d_diag) cudaFree(ctx->d_diag);
     GBEM_CUDA(ctx, cudaMalloc(&ctx->d_diag, sizeof(double) * n));
@@ -677,11 +681,34 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
     return ctx->fail(GBEM_ENUMERIC,
                      "matrix not positive definite (pivot at row " + std::to_string(*ctx->h_info) + ")");
   }
-  if (nrhs == 0) return GBEM_OK;
+  if (stats) {
+    float a = 0;
+    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    stats->ms_factor = a;
+  }
+  return GBEM_OK;
+}
+
+// Triangular solves L L^T X = B with the stored factor (gbem_internal_factor),
+// residual ||A x - b|| / ||b|| from the preserved upper triangle when d_resid.
+int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
+                                 gbem_solve_stats* stats) {
+  const int n = (int)ctx->n;
+  const long long lda = ctx->lda;
+  if (nrhs < 0 || nrhs > 64) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, 64]");
+  if (!ctx->factored) return ctx->fail(GBEM_EINVAL, "no factored matrix in the context");
+  if (stats) stats->nrhs = nrhs;
+  if (n == 0 || nrhs == 0) return GBEM_OK;
+  cudaStream_t s = ctx->stream;
   // forward + backward substitution in one cooperative kernel (a grid barrier
   // per block step instead of four launches per block step)
   const int R = (int)nrhs;
+  int rc = ensure_work(ctx, 2 * (size_t)n * (size_t)R);
+  if (rc) return rc;
+  double* Ysym = ctx->d_work;
   double* scratch = Ysym + (size_t)n * R;
+  const double* Linv = ctx->d_linv;
+  cudaEventRecord(ctx->ev[1], s);
   {
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSolveSmem));
     const double* cA = ctx->d_A;
@@ -722,10 +749,9 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
   if (stats) {
     GBEM_CUDA(ctx, cudaEventSynchronize(ctx->ev[3]));
     float a = 0, b2 = 0, c = 0;
-    cudaEventElapsedTime(&a, ctx->ev[0], ctx->ev[1]);
+    (void)a;
     cudaEventElapsedTime(&b2, ctx->ev[1], ctx->ev[2]);
     cudaEventElapsedTime(&c, ctx->ev[2], ctx->ev[3]);
-    stats->ms_factor = a;
     stats->ms_solve = b2;
     stats->ms_residual = c;
     if (d_resid) {
@@ -737,4 +763,13 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
     }
   }
   return GBEM_OK;
+}
+
+int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
+                        gbem_solve_stats* stats) {
+  if (nrhs < 0 || nrhs > 64) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, 64]");
+  int rc = gbem_internal_factor(ctx, stats);
+  if (rc) return rc;
+  if (stats) stats->nrhs = nrhs;
+  return gbem_internal_solve_factored(ctx, d_B, nrhs, d_X, d_resid, stats);
 }

@@ -18,5 +18,6 @@ def ctx():
     """One GPU context for the session; the CUDA path must load (no fallback)."""
     from paper_2203_11733_b200._native import Context
     c = Context(0)
+    c.set_stream(0)  # torch's (legacy) default stream: device tensors made by the tests are ordered with our work
     yield c
     c.close()
