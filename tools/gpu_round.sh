@@ -17,8 +17,9 @@ if [ $rc -eq 0 ]; then
   echo "launch list rc=$?"
   python tools/launch_summary.py gpurun_out/launches_$TAG.csv > gpurun_out/launch_summary_$TAG.txt 2>&1
   head -30 gpurun_out/launch_summary_$TAG.txt
-  for K in k_gemm_nt k_far k_potrf_diag k_solve_coop; do
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 40 -c 1 \
+  for KS in k_gemm_nt:40 k_far:40 k_potrf_diag:200 k_solve_coop:2 k_near_gl:4 k_classify:4; do
+    K=${KS%%:*}; S=${KS##*:}
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
       -o gpurun_out/prof_${TAG}_$K -f python bench.py --steps 1 --warmup 3 > gpurun_out/ncu_${TAG}_$K.log 2>&1
     echo "ncu $K rc=$?"
   done
