@@ -15,6 +15,7 @@
 //   k_gemm_nt<STORE,128>: L21 = A21 * inv(L11)^T (trsm as a DMMA GEMM, in place);
 //   k_gemm_nt<SUB,64>   : A22 -= L21 * L21^T on lower 128x64 tiles (the O(n^3) part).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -51,11 +52,8 @@ __device__ long long g_potrf_clk[128];
 #endif
 constexpr int kPotrfThreads = 512;
 constexpr int kPotrfWarps = kPotrfThreads / 32;
-constexpr int kRowSlots = NB / kPotrfWarps;          // rows per warp in a pivot phase
-constexpr int kXSlots = 32 / kPotrfWarps;            // in-panel X rows per warp
-constexpr int kFinSlots = (NB + kPotrfThreads - 1) / kPotrfThreads;
 constexpr int kPanel = 32;
-constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + 2 * NB + 3 * kPanel * kPanel) * sizeof(double);
+constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + NB + 3 * kPanel * kPanel) * sizeof(double);
 
 __global__ void __launch_bounds__(kPotrfThreads)
     k_potrf_diag(double* A, long long lda, int kb, int row0, double* Linv, int* info) {
@@ -63,9 +61,12 @@ __global__ void __launch_bounds__(kPotrfThreads)
   constexpr int LD = NB + 1;
   double* a = sm;              // [NB][LD] column-major: a[c*LD + r]
   double* xd = a + NB * LD;    // diag of X (= 1 / diag of L)
-  double* sqd = xd + NB;       // diag of L
-  double* tmp = sqd + NB;      // [3][32*32] products of the X assembly
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* tmp = xd + NB;       // [3][32*32] products of the X assembly
+  const int tid = threadIdx.x, lane = tid & 31;
+  // warp index through a shuffle: ptxas then knows it is warp-uniform, and the
+  // shuffles inside `if (warp == 0)` compile without divergence handling
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  POTRF_TICK(23);
   // load the block: 8 independent global loads in flight per thread per batch
   for (int idx0 = tid; idx0 < NB * NB; idx0 += 8 * kPotrfThreads) {
     double v[8];
@@ -87,94 +88,89 @@ __global__ void __launch_bounds__(kPotrfThreads)
   __syncthreads();
   POTRF_TICK(0);
   const int npan = (kb + kPanel - 1) / kPanel;
-  bool bad = false;
   for (int p = 0; p < npan; ++p) {
     const int c0 = p * kPanel;
-    // ---- 1. panel factorisation, one barrier per pivot: phase j applies the
-    // pivot to the panel columns (j, c0+32) on every row below (unscaled column
-    // j, scaled by 1/a_jj on the fly), runs the in-panel forward substitution
-    // of X = inv(L_pp) (S = X diag(L), stored transposed in the upper half), and
-    // finalises column j-1 / X row j-1, which phase j never reads.
-    for (int j = c0; j < c0 + kPanel; ++j) {
-      // (a) every shared load of the phase first (none depends on the pivot) ...
-      double d = a[j * LD + j];
-      const int cc = c0 + lane;  // panel column of this lane
-      const bool colv = cc > j;
-      const double acj = colv ? a[j * LD + cc] : 0.0;
-      double tv[kRowSlots], arj[kRowSlots];
+    // ---- 1. warp 0: factor the 32 x 32 diagonal sub-block and invert it in
+    // registers (lane i owns row i; columns move by shuffles, no block barrier)
+    if (warp == 0) {
+      // factor: lane i owns row i; column j of L goes straight to shared memory
+      // and is read back by every lane as broadcasts (no shuffles but the pivot)
+      double v[kPanel];
 #pragma unroll
-      for (int k = 0; k < kRowSlots; ++k) {
-        const int r = j + 1 + warp + kPotrfWarps * k;
-        const bool ok = colv && r < NB && r >= cc;
-        tv[k] = ok ? a[cc * LD + r] : 0.0;
-        arj[k] = ok ? a[j * LD + r] : 0.0;
-      }
-      const int kx = c0 + lane;  // in-panel X column of this lane
-      const double sjk = kx < j ? a[j * LD + kx] : 0.0;
-      double sv[kXSlots], lij[kXSlots];
+      for (int k = 0; k < kPanel; ++k) v[k] = a[(c0 + k) * LD + c0 + lane];  // k > lane: unused
+      double myrs = 0.0;
+      int firstbad = kPanel;
 #pragma unroll
-      for (int h = 0; h < kXSlots; ++h) {
-        const int ix = j + 1 + warp + kPotrfWarps * h;
-        const bool ok = kx <= j && ix < c0 + kPanel;
-        sv[h] = ok && kx < j ? a[ix * LD + kx] : 0.0;
-        lij[h] = ok ? a[j * LD + ix] : 0.0;
-      }
-      const int q = j - 1;  // column / X row finalised in this phase
-      const bool fin = j > c0;
-      const double iq = fin ? xd[q] : 0.0;
-      double fl[kFinSlots];
+      for (int j = 0; j < kPanel; ++j) {
+        double d = __shfl_sync(0xffffffffu, v[j], j);
+        const bool bad = !(d > 0.0);
+        firstbad = (bad && firstbad == kPanel) ? j : firstbad;
+        d = bad ? 1.0 : d;  // continue (the launch sequence stays fixed); the factor is void
+        const double rs = gbem_gpu::rsq64(d);
+        const double lij = v[j] * rs;  // lane j: sqrt(d); lane i > j: L(i, j)
+        myrs = lane == j ? rs : myrs;
+        if (lane >= j) a[(c0 + j) * LD + c0 + lane] = lij;
+        __syncwarp();
 #pragma unroll
-      for (int k = 0; k < kFinSlots; ++k) {
-        const int r = q + 1 + tid + kPotrfThreads * k;
-        fl[k] = fin && r < NB ? a[q * LD + r] : 0.0;
+        for (int k = j + 1; k < kPanel; ++k) v[k] = fma(-lij, a[(c0 + j) * LD + c0 + k], v[k]);
       }
-      const double fx = fin && tid < q - c0 ? a[q * LD + c0 + tid] : 0.0;
-      // (b) ... then the pivot ...
-      if (!(d > 0.0)) {
-        if (tid == 0 && !bad && j < kb) atomicMin(info, row0 + j);
-        bad = true;
-        d = 1.0;
-      }
-      const double is = gbem_gpu::rsq64(d), isd = is * is;
-      // (c) ... then every store.  Phase j never writes column j, and each
-      // element it writes is read only by the thread writing it: one barrier.
-      if (tid == 0) {
-        xd[j] = is;
-        sqd[j] = d * is;
-      }
-      const double acjs = acj * isd;
+      if (lane == 0 && firstbad < kPanel && c0 + firstbad < kb) atomicMin(info, row0 + c0 + firstbad);
+      xd[c0 + lane] = myrs;
+      __syncwarp();
+      // X = inv(L_pp): lane k owns column k (forward substitution, L broadcast
+      // from shared memory): x_t = s_t / L_tt, then s_i -= L(i, t) x_t for i > t
+      double x[kPanel];
 #pragma unroll
-      for (int k = 0; k < kRowSlots; ++k) {
-        const int r = j + 1 + warp + kPotrfWarps * k;
-        if (colv && r < NB && r >= cc) a[cc * LD + r] = fma(-arj[k], acjs, tv[k]);   // A(r,c) -= L(r,j) L(c,j)
-      }
-      const double xjk = kx == j ? is : sjk * is;  // X(j, kx)
+      for (int i = 0; i < kPanel; ++i) x[i] = i == lane ? 1.0 : 0.0;
 #pragma unroll
-      for (int h = 0; h < kXSlots; ++h) {
-        const int ix = j + 1 + warp + kPotrfWarps * h;
-        if (kx <= j && ix < c0 + kPanel) a[ix * LD + kx] = fma(-lij[h] * is, xjk, sv[h]);  // S(i,k) -= L(i,j) X(j,k)
-      }
-      if (fin) {
+      for (int t = 0; t < kPanel; ++t) {
+        x[t] *= xd[c0 + t];
 #pragma unroll
-        for (int k = 0; k < kFinSlots; ++k) {
-          const int r = q + 1 + tid + kPotrfThreads * k;
-          if (r < NB) a[q * LD + r] = fl[k] * iq;  // L(r, q)
-        }
-        if (tid < q - c0) a[q * LD + c0 + tid] = fx * iq;  // X(q, c0+tid)
+        for (int i = t + 1; i < kPanel; ++i) x[i] = fma(-a[(c0 + t) * LD + c0 + i], x[t], x[i]);
       }
-      __syncthreads();
-    }
-    {  // finalise the last panel column and X row
-      const int q = c0 + kPanel - 1;
-      const double iq = xd[q];
-      for (int r = q + 1 + tid; r < NB; r += kPotrfThreads) a[q * LD + r] *= iq;
-      if (tid < q - c0) a[q * LD + c0 + tid] *= iq;
-      if (tid < kPanel) a[(c0 + tid) * LD + c0 + tid] = sqd[c0 + tid];
+#pragma unroll
+      for (int i = 0; i < kPanel; ++i)
+        if (i > lane) a[(c0 + i) * LD + c0 + lane] = x[i];  // X(i, lane) in the strict upper half
     }
     __syncthreads();
     POTRF_TICK(1 + 3 * p);
     const int r0 = c0 + kPanel, mrest = NB - r0;  // padded rows below the panel
     if (mrest <= 0) break;
+    // ---- 2. panel rows below: L_rp = A_rp * inv(L_pp)^T, 4 x 4 register tiles
+    {
+      const int ntile = (mrest / 4) * (kPanel / 4);
+      double acc[4][4] = {};
+      int rb = 0, jb = 0;
+      if (tid < ntile) {
+        rb = r0 + 4 * (tid / (kPanel / 4));
+        jb = 4 * (tid % (kPanel / 4));
+#pragma unroll 4
+        for (int k = 0; k < kPanel; ++k) {  // X(j, k) = 0 for k > j: fixed trip count, no branches
+          double ar[4], xv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ar[u] = a[(c0 + k) * LD + rb + u];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int j = jb + v;
+            const double up = a[(c0 + j) * LD + c0 + k], dg = xd[c0 + k];
+            xv[v] = k < j ? up : 0.0;
+            xv[v] = k == j ? dg : xv[v];  // X(j, k)
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(ar[u], xv[v], acc[u][v]);
+        }
+      }
+      __syncthreads();
+      if (tid < ntile) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) a[(c0 + jb + v) * LD + rb + u] = acc[u][v];
+      }
+    }
+    __syncthreads();
     POTRF_TICK(2 + 3 * p);
     // ---- 3. rank-32 update of the trailing lower part, 4 x 4 register tiles
     {
@@ -220,6 +216,7 @@ __global__ void __launch_bounds__(kPotrfThreads)
       const int pb = t / 64, ti = (t % 64) % 8, tk = (t % 64) / 8;
       const int col0 = pb * kPanel + 4 * tk;
       double acc[4][4] = {};
+#pragma unroll 4
       for (int m = col0; m < R0; ++m) {
         double lr[4], xc[4];
 #pragma unroll
@@ -227,7 +224,10 @@ __global__ void __launch_bounds__(kPotrfThreads)
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const int c = col0 + v;
-          xc[v] = m == c ? xd[m] : (m > c ? a[m * LD + c] : 0.0);  // X(m, c)
+          // unconditional loads + selects: no branches around the shared loads
+          const double up = a[m * LD + c], dg = xd[m];
+          xc[v] = m > c ? up : 0.0;
+          xc[v] = m == c ? dg : xc[v];  // X(m, c)
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -244,12 +244,15 @@ __global__ void __launch_bounds__(kPotrfThreads)
       const int pb = t / 64, ti = (t % 64) % 8, tk = (t % 64) / 8;
       const int col0 = pb * kPanel + 4 * tk;
       double acc[4][4] = {};
+#pragma unroll 4
       for (int m = 0; m < 4 * ti + 4; ++m) {
         double xr[4], tv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int i = 4 * ti + u;
-          xr[u] = m == i ? xd[R0 + i] : (m < i ? a[(R0 + i) * LD + R0 + m] : 0.0);  // X(R0+i, R0+m)
+          const double up = a[(R0 + i) * LD + R0 + m], dg = xd[R0 + i];
+          xr[u] = m < i ? up : 0.0;
+          xr[u] = m == i ? dg : xr[u];  // X(R0+i, R0+m)
         }
 #pragma unroll
         for (int v = 0; v < 4; ++v) tv[v] = tmp[pb * kPanel * kPanel + (4 * tk + v) * kPanel + m];
@@ -266,9 +269,9 @@ __global__ void __launch_bounds__(kPotrfThreads)
     __syncthreads();
   }
   POTRF_TICK(21);
-  for (int idx = tid; idx < kb * kb; idx += kPotrfThreads) {
-    int c = idx / kb, r = idx % kb;
-    if (r >= c) A[(long long)c * lda + r] = a[c * LD + r];
+  for (int idx = tid; idx < NB * NB; idx += kPotrfThreads) {
+    const int c = idx / NB, r = idx % NB;  // constant divisor: shifts, not a division
+    if (r >= c && r < kb && c < kb) A[(long long)c * lda + r] = a[c * LD + r];
   }
   for (int idx = tid; idx < NB * NB; idx += kPotrfThreads) {
     int c = idx / NB, r = idx % NB;
@@ -279,6 +282,7 @@ __global__ void __launch_bounds__(kPotrfThreads)
     }
     Linv[c * NB + r] = v;
   }
+  POTRF_TICK(22);
 }
 
 __global__ void k_save_diag(const double* A, long long lda, int n, double* d) {
@@ -387,15 +391,24 @@ __global__ void k_resid_norm(const double* Y, const double* B, int n, double* re
 // Forward (L Y = B) and backward (L^T X = Y) block substitution for up to
 // kSolveR right-hand sides in one cooperative launch (one CTA per SM).
 // Step k: the 128 x 128 diagonal-block inverse inv(L_kk) sits in shared memory
-// (cp.async prefetch of the next block overlaps the current step's updates);
-// every CTA forms y = inv(L_kk) w_k (or inv(L_kk)^T) redundantly, CTA 0
-// publishes it, and all CTAs update the remaining rows (right-looking); one
-// grid barrier per step.  Buffers: W = B copy that receives the forward updates
-// and finally the solution X; Out = forward results Y that receive the
-// backward updates.
+// (cp.async prefetch of the next block overlaps the current step); every CTA
+// forms y = inv(L_kk) w_k (or inv(L_kk)^T) redundantly, CTA 0 publishes it, and
+// each CTA updates the rows it owns (a fixed range of 32-row strips) below
+// (forward) or above (backward) the block; one grid barrier per step.
+// The factor entries a step needs do not depend on the solution, so each CTA
+// issues the loads of its first kSolvePF strips of the NEXT step's panel before
+// the grid barrier: the DRAM latency of the panel overlaps the barrier and the
+// diagonal solve, and a step costs ~ barrier + diagonal solve.
+// Buffers: W = B copy that receives the forward updates and finally the
+// solution X; Out = forward results Y that receive the backward updates.
 constexpr int kSolveThreads = 256;
+constexpr int kSolveWarps = kSolveThreads / 32;
 constexpr int kSolveR = 16;
-constexpr size_t kSolveSmem = (size_t)(NB * NB + 3 * kSolveR * NB) * sizeof(double);
+constexpr int kSolvePF = 3;                      // register-prefetched strips per CTA and step
+constexpr int kSolveCols = NB / kSolveWarps;     // forward: block columns per warp (16)
+static_assert(kSolveCols == 16 && NB / 32 == 4, "strip tiling assumes NB = 128, 8 warps");
+constexpr size_t kSolveSmem =
+    (size_t)(NB * NB + 3 * kSolveR * NB + kSolveWarps * kSolveR * 32 + kSolvePF * kSolveR * 32) * sizeof(double);
 
 __device__ __forceinline__ void solve_prefetch_block(double* Ls, const double* Li, int tid) {
   for (int c = tid; c < NB * NB / 2; c += kSolveThreads) {
@@ -418,6 +431,7 @@ __device__ __forceinline__ void solve_diag(const double* Ls, const double* ws, d
     const int lo = transpose ? i : 0, hi = transpose ? kb : i + 1;
     const int mid = (lo + hi) >> 1;
     const int b0 = half ? mid : lo, b1 = half ? hi : mid;
+#pragma unroll 4
     for (int kk = b0; kk < b1; ++kk) {
       const double m = transpose ? Ls[i * NB + kk] : Ls[kk * NB + i];
 #pragma unroll
@@ -437,19 +451,73 @@ __device__ __forceinline__ void solve_diag(const double* Ls, const double* ws, d
   __syncthreads();
 }
 
+// Forward panel loads of strip s for block (k0, kb): lane = row 32 s + lane,
+// warp w = block columns [16 w, 16 w + 16) (coalesced 256 B per instruction).
+__device__ __forceinline__ void fwd_load(const double* __restrict__ A, long long lda, int n, int k0, int kb, int s,
+                                         int warp, int lane, double (&l)[kSolveCols]) {
+  const long long r = 32LL * s + lane;
+#pragma unroll
+  for (int u = 0; u < kSolveCols; ++u) {
+    const int c = warp * kSolveCols + u;
+    l[u] = (r < n && c < kb) ? __ldcs(A + (long long)(k0 + c) * lda + r) : 0.0;
+  }
+}
+// Backward panel loads of strip s: warp w = rows 32 s + 4 w + {0..3}, lane =
+// block columns lane + 32 j (row r of L^T is column r of L: contiguous in c).
+__device__ __forceinline__ void bwd_load(const double* __restrict__ A, long long lda, int k0, int kb, int s,
+                                         int warp, int lane, double (&l)[kSolveCols]) {
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const long long r = 32LL * s + 4 * warp + rr;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = lane + 32 * j;
+      l[rr * 4 + j] = c < kb ? __ldcs(A + r * lda + k0 + c) : 0.0;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kSolveThreads, 1)
     k_solve_coop(const double* __restrict__ A, long long lda, const double* __restrict__ Linv, int n, int R,
-                 const double* __restrict__ B, double* W, double* Out) {
+                 const double* __restrict__ B, double* W, double* Out, int dbg) {
+  // dbg (phase-breakdown timing only, GBEM_SOLVE_DBG): 1 skip diagonal solves,
+  // 2 skip panel updates, 4 skip grid barriers (results wrong for 1/2/4)
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   double* Ls = sm;                    // [NB][NB] current diagonal-block inverse
   double* ws = Ls + NB * NB;          // [kSolveR][NB] right-hand side block
   double* ys = ws + kSolveR * NB;     // [kSolveR][NB] solved block
   double* part = ys + kSolveR * NB;   // [kSolveR][NB] partial sums
+  double* red = part + kSolveR * NB;  // [warps][kSolveR][32] forward cross-warp sums
+  double* vb = red + kSolveWarps * kSolveR * 32;  // [kSolvePF][kSolveR][32] reduced strip updates
   const int nblk = (n + NB - 1) / NB;
+  const int nstrips = (n + 31) / 32;
+  const int s_lo = (int)((long long)blockIdx.x * nstrips / gridDim.x);
+  const int s_hi = (int)((long long)(blockIdx.x + 1) * nstrips / gridDim.x);
   const long long nR = (long long)n * R;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double pf[kSolvePF][kSolveCols];
+
+  // first owned strip strictly below block b (k0 + kb is a multiple of 32 or n)
+  auto fwd_first = [&](int b) {
+    const int k0 = b * NB, kb = min(NB, n - k0);
+    return max(s_lo, (k0 + kb + 31) / 32);
+  };
+  auto fwd_prefetch = [&](int b) {
+    const int k0 = b * NB, kb = min(NB, n - k0), s0 = fwd_first(b);
+#pragma unroll
+    for (int k = 0; k < kSolvePF; ++k)
+      if (s0 + k < s_hi) fwd_load(A, lda, n, k0, kb, s0 + k, warp, lane, pf[k]);
+  };
+  auto bwd_prefetch = [&](int b) {
+    const int k0 = b * NB, kb = min(NB, n - k0), s1 = min(s_hi, k0 / 32);
+#pragma unroll
+    for (int k = 0; k < kSolvePF; ++k)
+      if (s_lo + k < s1) bwd_load(A, lda, k0, kb, s_lo + k, warp, lane, pf[k]);
+  };
+
   solve_prefetch_block(Ls, Linv, tid);
+  fwd_prefetch(0);
   for (long long i = grid.thread_rank(); i < nR; i += grid.size()) W[i] = B[i];
   grid.sync();
   // ---- forward: W holds b - sum_{j<k} L_kj y_j, Out receives y
@@ -461,51 +529,72 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
     }
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
-    solve_diag(Ls, ws, ys, part, kb, R, 0, tid);
-    if (b + 1 < nblk)
-      solve_prefetch_block(Ls, Linv + (size_t)(b + 1) * NB * NB, tid);
-    else
-      solve_prefetch_block(Ls, Linv + (size_t)b * NB * NB, tid);  // backward starts from the last block
+    const int s0 = fwd_first(b);
+    const bool active = s0 < s_hi;
+    if ((active || blockIdx.x == 0) && !(dbg & 1)) solve_diag(Ls, ws, ys, part, kb, R, 0, tid);
+    solve_prefetch_block(Ls, Linv + (size_t)min(b + 1, nblk - 1) * NB * NB, tid);  // backward starts at the last
     if (blockIdx.x == 0)
       for (int idx = tid; idx < kb * R; idx += blockDim.x) {
         const int i = idx % kb, q = idx / kb;
         Out[(long long)q * n + k0 + i] = ys[q * NB + i];
       }
-    // rows below the block: 32-row strips, a warp per strip, strips dealt across
-    // CTAs first so every SM streams; 16-deep unroll keeps 16 loads in flight
-    const int nstrips = (n - k0 - kb + 31) / 32;
-    for (int st = blockIdx.x + gridDim.x * (tid >> 5); st < nstrips; st += gridDim.x * (blockDim.x >> 5)) {
-      const long long r = (long long)k0 + kb + 32LL * st + lane;
-      if (r >= n) continue;
-      double acc[kSolveR];
+    for (int c0 = s0; c0 < ((dbg & 2) ? s0 : s_hi); c0 += kSolvePF) {
+      if (c0 != s0) {
 #pragma unroll
-      for (int q = 0; q < kSolveR; ++q) acc[q] = 0.0;
-      const double* col = A + (long long)k0 * lda + r;
-      int c = 0;
-      for (; c + 16 <= kb; c += 16) {
-        double l[16];
+        for (int k = 0; k < kSolvePF; ++k)
+          if (c0 + k < s_hi) fwd_load(A, lda, n, k0, kb, c0 + k, warp, lane, pf[k]);
+      }
+      const int nk = min(kSolvePF, s_hi - c0);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) l[u] = col[(long long)(c + u) * lda];
+      for (int k = 0; k < kSolvePF; ++k) {
+        if (k >= nk) break;
+        double acc[kSolveR];
 #pragma unroll
-        for (int u = 0; u < 16; ++u)
+        for (int q = 0; q < kSolveR; ++q) acc[q] = 0.0;
+#pragma unroll
+        for (int u = 0; u < kSolveCols; ++u) {
+          const int c = warp * kSolveCols + u;
 #pragma unroll
           for (int q = 0; q < kSolveR; ++q)
-            if (q < R) acc[q] = fma(l[u], ys[q * NB + c + u], acc[q]);
-      }
-      for (; c < kb; ++c) {
-        const double l = col[(long long)c * lda];
+            if (q < R) acc[q] = fma(pf[k][u], ys[q * NB + c], acc[q]);
+        }
 #pragma unroll
         for (int q = 0; q < kSolveR; ++q)
-          if (q < R) acc[q] = fma(l, ys[q * NB + c], acc[q]);
-      }
+          if (q < R) red[(warp * kSolveR + q) * 32 + lane] = acc[q];
+        __syncthreads();
+        for (int idx = tid; idx < 32 * R; idx += blockDim.x) {
+          double v = 0.0;
 #pragma unroll
-      for (int q = 0; q < kSolveR; ++q)
-        if (q < R) W[(long long)q * n + r] -= acc[q];
+          for (int w = 0; w < kSolveWarps; ++w) v += red[w * kSolveR * 32 + idx];
+          vb[k * kSolveR * 32 + idx] = v;
+        }
+        __syncthreads();
+      }
+      // one read-modify-write pass over the chunk's rows: every load issued
+      // before any store (one L2 round trip per chunk, not per element)
+      {
+        constexpr int kIt = (kSolvePF * kSolveR * 32 + kSolveThreads - 1) / kSolveThreads;
+        double old[kIt];
+        long long addr[kIt];
+#pragma unroll
+        for (int t = 0; t < kIt; ++t) {
+          const int idx = tid + t * kSolveThreads, k = idx / (32 * kSolveR), q = (idx / 32) % kSolveR, ln = idx % 32;
+          const long long r = 32LL * (c0 + k) + ln;
+          addr[t] = (k < nk && q < R && r < n) ? (long long)q * n + r : -1;
+          old[t] = addr[t] >= 0 ? W[addr[t]] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < kIt; ++t) {
+          const int idx = tid + t * kSolveThreads, k = idx / (32 * kSolveR), q = (idx / 32) % kSolveR, ln = idx % 32;
+          if (addr[t] >= 0) W[addr[t]] = old[t] - vb[(k * kSolveR + q) * 32 + ln];
+        }
+      }
     }
-    grid.sync();
+    if (b + 1 < nblk) fwd_prefetch(b + 1);
+    else bwd_prefetch(nblk - 1);
+    if (!(dbg & 4)) grid.sync();
   }
   // ---- backward: Out holds y - sum_{j>k} L_jk^T x_j, W receives x
-  const long long gwarp = blockIdx.x + (long long)gridDim.x * (tid >> 5), nwarps = grid.size() >> 5;
   for (int b = nblk - 1; b >= 0; --b) {
     const int k0 = b * NB, kb = min(NB, n - k0);
     for (int idx = tid; idx < kb * R; idx += blockDim.x) {
@@ -514,54 +603,61 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
     }
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
-    solve_diag(Ls, ws, ys, part, kb, R, 1, tid);
+    const int s1 = min(s_hi, k0 / 32);
+    const bool active = s_lo < s1;
+    if ((active || blockIdx.x == 0) && !(dbg & 1)) solve_diag(Ls, ws, ys, part, kb, R, 1, tid);
     if (b > 0) solve_prefetch_block(Ls, Linv + (size_t)(b - 1) * NB * NB, tid);
     if (blockIdx.x == 0)
       for (int idx = tid; idx < kb * R; idx += blockDim.x) {
         const int i = idx % kb, q = idx / kb;
         W[(long long)q * n + k0 + i] = ys[q * NB + i];
       }
-    // rows r < k0: Out[r] -= sum_{c in block} L(k0+c, r) x_c; L(c,r) sits at A[r*lda + c]
-    // (contiguous in c): a warp per row, 4 rows per pass (16 loads in flight per lane)
-    for (long long r0 = gwarp * 4; r0 < k0; r0 += nwarps * 4) {
-      double acc[4][kSolveR];
-      double l[4][4];
+    // rows r < k0: Out[r] -= sum_{c in block} L(k0+c, r) x_c
+    for (int c0 = s_lo; c0 < ((dbg & 2) ? s_lo : s1); c0 += kSolvePF) {
+      if (c0 != s_lo) {
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-#pragma unroll
-        for (int q = 0; q < kSolveR; ++q) acc[rr][q] = 0.0;
-        const long long r = r0 + rr;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int c = lane + 32 * j;
-          l[rr][j] = (r < k0 && c < kb) ? A[r * lda + k0 + c] : 0.0;
-        }
+        for (int k = 0; k < kSolvePF; ++k)
+          if (c0 + k < s1) bwd_load(A, lda, k0, kb, c0 + k, warp, lane, pf[k]);
       }
+      const int nk = min(kSolvePF, s1 - c0);
+      double* vw = vb + warp * (kSolvePF * 4 * kSolveR);  // this warp's [k][rr][q] sums
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr)
+      for (int k = 0; k < kSolvePF; ++k) {
+        if (k >= nk) break;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int c = lane + 32 * j;
-          if (c < kb) {
+        for (int rr = 0; rr < 4; ++rr) {
 #pragma unroll
-            for (int q = 0; q < kSolveR; ++q)
-              if (q < R) acc[rr][q] = fma(l[rr][j], ys[q * NB + c], acc[rr][q]);
+          for (int q = 0; q < kSolveR; ++q) {
+            if (q >= R) continue;
+            double v = 0.0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v = fma(pf[k][rr * 4 + j], ys[q * NB + lane + 32 * j], v);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0) vw[(k * 4 + rr) * kSolveR + q] = v;
           }
         }
-#pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
-        const long long r = r0 + rr;
-#pragma unroll
-        for (int q = 0; q < kSolveR; ++q) {
-          if (q >= R) continue;
-          double v = acc[rr][q];
-#pragma unroll
-          for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-          if (lane == 0 && r < k0) Out[(long long)q * n + r] -= v;
-        }
       }
+      __syncwarp();
+      {
+        constexpr int kIt = (kSolvePF * 4 * kSolveR + 31) / 32;
+        double old[kIt];
+        long long addr[kIt];
+#pragma unroll
+        for (int t = 0; t < kIt; ++t) {
+          const int idx = lane + 32 * t, k = idx / (4 * kSolveR), rr = (idx / kSolveR) % 4, q = idx % kSolveR;
+          const long long r = 32LL * (c0 + k) + 4 * warp + rr;
+          addr[t] = (k < nk && q < R) ? (long long)q * n + r : -1;
+          old[t] = addr[t] >= 0 ? Out[addr[t]] : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < kIt; ++t)
+          if (addr[t] >= 0) Out[addr[t]] = old[t] - vw[lane + 32 * t];
+      }
+      __syncwarp();
     }
-    grid.sync();
+    if (b > 0) bwd_prefetch(b - 1);
+    if (!(dbg & 4)) grid.sync();
   }
 }
 
@@ -719,7 +815,10 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
       const double* Bq = d_B + (size_t)q0 * n;
       double* Xq = d_X + (size_t)q0 * n;
       double* Sq = scratch;  // scratch holds n * R >= n * RR
-      void* args[] = {(void*)&cA, (void*)&lda, (void*)&cL, (void*)&nn, (void*)&RR, (void*)&Bq, (void*)&Xq, (void*)&Sq};
+      static const int dbg = getenv("GBEM_SOLVE_DBG") ? atoi(getenv("GBEM_SOLVE_DBG")) : 0;
+      int dd = dbg;
+      void* args[] = {(void*)&cA, (void*)&lda, (void*)&cL, (void*)&nn, (void*)&RR, (void*)&Bq, (void*)&Xq, (void*)&Sq,
+                      (void*)&dd};
       GBEM_CUDA(ctx, cudaLaunchCooperativeKernel((void*)k_solve_coop, dim3(ctx->num_sms), dim3(kSolveThreads), args,
                                                  kSolveSmem, s));
       GBEM_LAUNCH_CHECK(ctx);

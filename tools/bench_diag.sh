@@ -1,0 +1,3 @@
+python bench.py 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['e2e']['seconds_per_extraction'], d['clocks'])"
+GBEM_NO_CLOCKS=1 python bench.py 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['e2e']['seconds_per_extraction'], d['clocks'])"
+python bench.py --steps 10 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['e2e']['seconds_per_extraction'], d['clocks'])"
