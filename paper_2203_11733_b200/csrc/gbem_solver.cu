@@ -420,13 +420,14 @@ __device__ __forceinline__ void solve_prefetch_block(double* Ls, const double* L
 
 // ys[q][i] = sum_kk M(i,kk) ws[q][kk] with M = inv(L) (transpose = 0, kk <= i) or
 // inv(L)^T (transpose = 1, kk >= i); two threads per row i, partial sums folded in smem.
+template <int RT>
 __device__ __forceinline__ void solve_diag(const double* Ls, const double* ws, double* ys, double* part, int kb,
                                           int R, int transpose, int tid) {
   static_assert(2 * NB == kSolveThreads, "two threads per diagonal-block row");
   const int i = tid % NB, half = tid / NB;
-  double acc[kSolveR];
+  double acc[RT];
 #pragma unroll
-  for (int q = 0; q < kSolveR; ++q) acc[q] = 0.0;
+  for (int q = 0; q < RT; ++q) acc[q] = 0.0;
   if (i < kb) {
     const int lo = transpose ? i : 0, hi = transpose ? kb : i + 1;
     const int mid = (lo + hi) >> 1;
@@ -435,18 +436,18 @@ __device__ __forceinline__ void solve_diag(const double* Ls, const double* ws, d
     for (int kk = b0; kk < b1; ++kk) {
       const double m = transpose ? Ls[i * NB + kk] : Ls[kk * NB + i];
 #pragma unroll
-      for (int q = 0; q < kSolveR; ++q)
+      for (int q = 0; q < RT; ++q)
         if (q < R) acc[q] = fma(m, ws[q * NB + kk], acc[q]);
     }
   }
   if (half)
 #pragma unroll
-    for (int q = 0; q < kSolveR; ++q)
+    for (int q = 0; q < RT; ++q)
       if (q < R) part[q * NB + i] = acc[q];
   __syncthreads();
   if (!half && i < kb)
 #pragma unroll
-    for (int q = 0; q < kSolveR; ++q)
+    for (int q = 0; q < RT; ++q)
       if (q < R) ys[q * NB + i] = acc[q] + part[q * NB + i];
   __syncthreads();
 }
@@ -462,21 +463,82 @@ __device__ __forceinline__ void fwd_load(const double* __restrict__ A, long long
     l[u] = (r < n && c < kb) ? __ldcs(A + (long long)(k0 + c) * lda + r) : 0.0;
   }
 }
-// Backward panel loads of strip s: warp w = rows 32 s + 4 w + {0..3}, lane =
-// block columns lane + 32 j (row r of L^T is column r of L: contiguous in c).
+// Backward panel loads of strip s: lane = row r = 32 s + lane of L^T, i.e.
+// column r of L, whose block entries L(k0 + c, r) = A[r * lda + k0 + c] are
+// contiguous in c: warp w reads c in [16 w, 16 w + 16) as eight 16-byte loads
+// (one 128-byte line per lane; k0 + 16 w is a multiple of 16, lda of 8).
 __device__ __forceinline__ void bwd_load(const double* __restrict__ A, long long lda, int k0, int kb, int s,
                                          int warp, int lane, double (&l)[kSolveCols]) {
+  const long long r = 32LL * s + lane;
+  const double2* src = reinterpret_cast<const double2*>(A + r * lda + k0 + warp * kSolveCols);
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
-    const long long r = 32LL * s + 4 * warp + rr;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = lane + 32 * j;
-      l[rr * 4 + j] = c < kb ? __ldcs(A + r * lda + k0 + c) : 0.0;
-    }
+  for (int u = 0; u < kSolveCols / 2; ++u) {
+    const int c = warp * kSolveCols + 2 * u;
+    const double2 v = c < kb ? __ldcs(src + u) : make_double2(0.0, 0.0);
+    l[2 * u] = v.x;
+    l[2 * u + 1] = c + 1 < kb ? v.y : 0.0;
   }
 }
 
+// T[q][r] -= sum_c P(r, c) y[q][c] for the nk strips c0.. of this CTA: lane = row,
+// warp = 16 block columns (pf), cross-warp sums through `red`, then one
+// read-modify-write pass over the chunk with every load issued before any store.
+template <int RT>
+__device__ __forceinline__ void strip_update(const double (&pf)[kSolvePF][kSolveCols], const double* ys, double* red,
+                                             double* vb, double* T, int n, int R, int c0, int nk, int tid, int warp,
+                                             int lane) {
+#pragma unroll
+  for (int k = 0; k < kSolvePF; ++k) {
+    if (k >= nk) break;
+    double acc[RT];
+#pragma unroll
+    for (int q = 0; q < RT; ++q) acc[q] = 0.0;
+#pragma unroll
+    for (int u = 0; u < kSolveCols; ++u) {
+      const int c = warp * kSolveCols + u;
+#pragma unroll
+      for (int q = 0; q < RT; ++q) acc[q] = fma(pf[k][u], ys[q * NB + c], acc[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < RT; ++q) red[(warp * RT + q) * 32 + lane] = acc[q];
+    __syncthreads();
+    for (int idx = tid; idx < 32 * R; idx += kSolveThreads) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < kSolveWarps; ++w) v += red[w * RT * 32 + idx];
+      vb[k * RT * 32 + idx] = v;
+    }
+    __syncthreads();
+  }
+  constexpr int kIt = (kSolvePF * RT * 32 + kSolveThreads - 1) / kSolveThreads;
+  double old[kIt];
+  long long addr[kIt];
+#pragma unroll
+  for (int t = 0; t < kIt; ++t) {
+    const int idx = tid + t * kSolveThreads, k = idx / (32 * RT), q = (idx / 32) % RT, ln = idx % 32;
+    const long long r = 32LL * (c0 + k) + ln;
+    addr[t] = (k < nk && q < R && r < n) ? (long long)q * n + r : -1;
+    old[t] = addr[t] >= 0 ? T[addr[t]] : 0.0;
+  }
+#pragma unroll
+  for (int t = 0; t < kIt; ++t) {
+    const int idx = tid + t * kSolveThreads, k = idx / (32 * RT), q = (idx / 32) % RT, ln = idx % 32;
+    if (addr[t] >= 0) T[addr[t]] = old[t] - vb[(k * RT + q) * 32 + ln];
+  }
+}
+
+#ifdef GBEM_SOLVE_TIMING
+__device__ long long g_solve_clk[2][8];
+#define SOLVE_TICK(slot)                                                          \
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2)) {    \
+    long long t_ = clock64();                                                     \
+    g_solve_clk[blockIdx.x == 0 ? 0 : 1][slot] += t_ - t_prev;                    \
+    t_prev = t_;                                                                  \
+  }
+#else
+#define SOLVE_TICK(slot)
+#endif
+template <int RT>
 __global__ void __launch_bounds__(kSolveThreads, 1)
     k_solve_coop(const double* __restrict__ A, long long lda, const double* __restrict__ Linv, int n, int R,
                  const double* __restrict__ B, double* W, double* Out, int dbg) {
@@ -485,11 +547,11 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   double* Ls = sm;                    // [NB][NB] current diagonal-block inverse
-  double* ws = Ls + NB * NB;          // [kSolveR][NB] right-hand side block
-  double* ys = ws + kSolveR * NB;     // [kSolveR][NB] solved block
-  double* part = ys + kSolveR * NB;   // [kSolveR][NB] partial sums
-  double* red = part + kSolveR * NB;  // [warps][kSolveR][32] forward cross-warp sums
-  double* vb = red + kSolveWarps * kSolveR * 32;  // [kSolvePF][kSolveR][32] reduced strip updates
+  double* ws = Ls + NB * NB;          // [RT][NB] right-hand side block
+  double* ys = ws + RT * NB;     // [RT][NB] solved block
+  double* part = ys + RT * NB;   // [RT][NB] partial sums
+  double* red = part + RT * NB;  // [warps][RT][32] forward cross-warp sums
+  double* vb = red + kSolveWarps * RT * 32;  // [kSolvePF][RT][32] reduced strip updates
   const int nblk = (n + NB - 1) / NB;
   const int nstrips = (n + 31) / 32;
   const int s_lo = (int)((long long)blockIdx.x * nstrips / gridDim.x);
@@ -516,6 +578,9 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
       if (s_lo + k < s1) bwd_load(A, lda, k0, kb, s_lo + k, warp, lane, pf[k]);
   };
 
+#ifdef GBEM_SOLVE_TIMING
+  long long t_prev = clock64();
+#endif
   solve_prefetch_block(Ls, Linv, tid);
   fwd_prefetch(0);
   for (long long i = grid.thread_rank(); i < nR; i += grid.size()) W[i] = B[i];
@@ -527,11 +592,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
       const int i = idx % kb, q = idx / kb;
       ws[q * NB + i] = W[(long long)q * n + k0 + i];
     }
+    SOLVE_TICK(0);
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
+    SOLVE_TICK(1);
     const int s0 = fwd_first(b);
     const bool active = s0 < s_hi;
-    if ((active || blockIdx.x == 0) && !(dbg & 1)) solve_diag(Ls, ws, ys, part, kb, R, 0, tid);
+    if ((active || blockIdx.x == 0) && !(dbg & 1)) solve_diag<RT>(Ls, ws, ys, part, kb, R, 0, tid);
+    SOLVE_TICK(2);
     solve_prefetch_block(Ls, Linv + (size_t)min(b + 1, nblk - 1) * NB * NB, tid);  // backward starts at the last
     if (blockIdx.x == 0)
       for (int idx = tid; idx < kb * R; idx += blockDim.x) {
@@ -544,55 +612,14 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
         for (int k = 0; k < kSolvePF; ++k)
           if (c0 + k < s_hi) fwd_load(A, lda, n, k0, kb, c0 + k, warp, lane, pf[k]);
       }
-      const int nk = min(kSolvePF, s_hi - c0);
-#pragma unroll
-      for (int k = 0; k < kSolvePF; ++k) {
-        if (k >= nk) break;
-        double acc[kSolveR];
-#pragma unroll
-        for (int q = 0; q < kSolveR; ++q) acc[q] = 0.0;
-#pragma unroll
-        for (int u = 0; u < kSolveCols; ++u) {
-          const int c = warp * kSolveCols + u;
-#pragma unroll
-          for (int q = 0; q < kSolveR; ++q)
-            if (q < R) acc[q] = fma(pf[k][u], ys[q * NB + c], acc[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < kSolveR; ++q)
-          if (q < R) red[(warp * kSolveR + q) * 32 + lane] = acc[q];
-        __syncthreads();
-        for (int idx = tid; idx < 32 * R; idx += blockDim.x) {
-          double v = 0.0;
-#pragma unroll
-          for (int w = 0; w < kSolveWarps; ++w) v += red[w * kSolveR * 32 + idx];
-          vb[k * kSolveR * 32 + idx] = v;
-        }
-        __syncthreads();
-      }
-      // one read-modify-write pass over the chunk's rows: every load issued
-      // before any store (one L2 round trip per chunk, not per element)
-      {
-        constexpr int kIt = (kSolvePF * kSolveR * 32 + kSolveThreads - 1) / kSolveThreads;
-        double old[kIt];
-        long long addr[kIt];
-#pragma unroll
-        for (int t = 0; t < kIt; ++t) {
-          const int idx = tid + t * kSolveThreads, k = idx / (32 * kSolveR), q = (idx / 32) % kSolveR, ln = idx % 32;
-          const long long r = 32LL * (c0 + k) + ln;
-          addr[t] = (k < nk && q < R && r < n) ? (long long)q * n + r : -1;
-          old[t] = addr[t] >= 0 ? W[addr[t]] : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < kIt; ++t) {
-          const int idx = tid + t * kSolveThreads, k = idx / (32 * kSolveR), q = (idx / 32) % kSolveR, ln = idx % 32;
-          if (addr[t] >= 0) W[addr[t]] = old[t] - vb[(k * kSolveR + q) * 32 + ln];
-        }
-      }
+      strip_update<RT>(pf, ys, red, vb, W, n, R, c0, min(kSolvePF, s_hi - c0), tid, warp, lane);
     }
+    SOLVE_TICK(3);
     if (b + 1 < nblk) fwd_prefetch(b + 1);
     else bwd_prefetch(nblk - 1);
+    SOLVE_TICK(4);
     if (!(dbg & 4)) grid.sync();
+    SOLVE_TICK(5);
   }
   // ---- backward: Out holds y - sum_{j>k} L_jk^T x_j, W receives x
   for (int b = nblk - 1; b >= 0; --b) {
@@ -605,7 +632,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
     __syncthreads();
     const int s1 = min(s_hi, k0 / 32);
     const bool active = s_lo < s1;
-    if ((active || blockIdx.x == 0) && !(dbg & 1)) solve_diag(Ls, ws, ys, part, kb, R, 1, tid);
+    if ((active || blockIdx.x == 0) && !(dbg & 1)) solve_diag<RT>(Ls, ws, ys, part, kb, R, 1, tid);
     if (b > 0) solve_prefetch_block(Ls, Linv + (size_t)(b - 1) * NB * NB, tid);
     if (blockIdx.x == 0)
       for (int idx = tid; idx < kb * R; idx += blockDim.x) {
@@ -619,42 +646,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
         for (int k = 0; k < kSolvePF; ++k)
           if (c0 + k < s1) bwd_load(A, lda, k0, kb, c0 + k, warp, lane, pf[k]);
       }
-      const int nk = min(kSolvePF, s1 - c0);
-      double* vw = vb + warp * (kSolvePF * 4 * kSolveR);  // this warp's [k][rr][q] sums
-#pragma unroll
-      for (int k = 0; k < kSolvePF; ++k) {
-        if (k >= nk) break;
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-#pragma unroll
-          for (int q = 0; q < kSolveR; ++q) {
-            if (q >= R) continue;
-            double v = 0.0;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) v = fma(pf[k][rr * 4 + j], ys[q * NB + lane + 32 * j], v);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-            if (lane == 0) vw[(k * 4 + rr) * kSolveR + q] = v;
-          }
-        }
-      }
-      __syncwarp();
-      {
-        constexpr int kIt = (kSolvePF * 4 * kSolveR + 31) / 32;
-        double old[kIt];
-        long long addr[kIt];
-#pragma unroll
-        for (int t = 0; t < kIt; ++t) {
-          const int idx = lane + 32 * t, k = idx / (4 * kSolveR), rr = (idx / kSolveR) % 4, q = idx % kSolveR;
-          const long long r = 32LL * (c0 + k) + 4 * warp + rr;
-          addr[t] = (k < nk && q < R) ? (long long)q * n + r : -1;
-          old[t] = addr[t] >= 0 ? Out[addr[t]] : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < kIt; ++t)
-          if (addr[t] >= 0) Out[addr[t]] = old[t] - vw[lane + 32 * t];
-      }
-      __syncwarp();
+      strip_update<RT>(pf, ys, red, vb, Out, n, R, c0, min(kSolvePF, s1 - c0), tid, warp, lane);
     }
     if (b > 0) bwd_prefetch(b - 1);
     if (!(dbg & 4)) grid.sync();
@@ -806,21 +798,23 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
   const double* Linv = ctx->d_linv;
   cudaEventRecord(ctx->ev[1], s);
   {
-    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_solve_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSolveSmem));
     const double* cA = ctx->d_A;
     const double* cL = Linv;
     int nn = n;
+    static const int dbg = getenv("GBEM_SOLVE_DBG") ? atoi(getenv("GBEM_SOLVE_DBG")) : 0;
     for (int q0 = 0; q0 < R; q0 += kSolveR) {
       int RR = std::min(kSolveR, R - q0);
       const double* Bq = d_B + (size_t)q0 * n;
       double* Xq = d_X + (size_t)q0 * n;
       double* Sq = scratch;  // scratch holds n * R >= n * RR
-      static const int dbg = getenv("GBEM_SOLVE_DBG") ? atoi(getenv("GBEM_SOLVE_DBG")) : 0;
       int dd = dbg;
       void* args[] = {(void*)&cA, (void*)&lda, (void*)&cL, (void*)&nn, (void*)&RR, (void*)&Bq, (void*)&Xq, (void*)&Sq,
                       (void*)&dd};
-      GBEM_CUDA(ctx, cudaLaunchCooperativeKernel((void*)k_solve_coop, dim3(ctx->num_sms), dim3(kSolveThreads), args,
-                                                 kSolveSmem, s));
+      // register blocking over the right-hand sides: the smallest instantiated width >= RR
+      void* fn = RR <= 1 ? (void*)k_solve_coop<1> : RR <= 2 ? (void*)k_solve_coop<2> : RR <= 4 ? (void*)k_solve_coop<4>
+               : RR <= 6 ? (void*)k_solve_coop<6> : RR <= 8 ? (void*)k_solve_coop<8> : (void*)k_solve_coop<16>;
+      GBEM_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSolveSmem));
+      GBEM_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3(ctx->num_sms), dim3(kSolveThreads), args, kSolveSmem, s));
       GBEM_LAUNCH_CHECK(ctx);
     }
   }
