@@ -29,6 +29,10 @@ namespace {
 
 using namespace gbem_gemm;
 constexpr int NB = 128;       // Cholesky block size (diagonal blocks, trailing-update K)
+// trailing update: 64 x 64 tiles, 2 x 2 warps, double-buffered slabs, 4 CTAs per
+// SM (tools/gemm_bench.cu: 28.0 TFLOP/s at K = 128 vs 25.6 for 128 x 64 tiles)
+using UpdShape = GenShape<64, 64, 2, 2, 2>;
+#define kUpdate k_syrk_gen<64, 64, 2, 2, 2, 4>
 // Factor the kb x kb (kb <= NB = 128) diagonal block and invert its factor, in
 // shared memory, by 32-column panels:
 //   1. warp 0 factors the 32 x 32 diagonal sub-block in registers (lane i owns
@@ -702,8 +706,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   }
   static bool attr_done = false;
   if (!attr_done) {
-    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kSub, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)Shape<64>::SMEM));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(kUpdate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UpdShape::SMEM));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kStore, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)Shape<NB>::SMEM));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -745,18 +748,18 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_panel, s1));
     GBEM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_panel, 0));
     if (m <= 0) break;
-    // A22 -= L21 L21^T: first the next block column (tile column 0), then the rest
-    int nt = (m + BM - 1) / BM;
+    // A22 -= L21 L21^T on 64 x 64 lower tiles: first the next block column
+    // (kBand tile columns), then the rest
+    const int nt = (m + 63) / 64;
     double* A22 = ctx->d_A + (long long)(k0 + kb) * lda + (k0 + kb);
-    constexpr int kSplit = NB / 64;  // block column k+1 = kSplit tile columns of 64
-    k_gemm_nt<kSub, 64><<<dim3(nt, kSplit), GEMM_THREADS, Shape<64>::SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m,
-                                                                               kb, 2, kSplit);
+    constexpr int kBand = NB / 64;
+    const int band = std::min(kBand, nt);
+    kUpdate<<<dim3(nt, band), UpdShape::THREADS, UpdShape::SMEM, s>>>(A22, lda, A21, lda, m, kb, 0, band);
     GBEM_LAUNCH_CHECK(ctx);
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_col, s));
-    if (nt > 1) {
-      long long rest = lower_tiles_before<64>(nt) - (long long)kSplit * nt;
-      k_gemm_nt<kSub, 64><<<(unsigned)rest, GEMM_THREADS, Shape<64>::SMEM, s>>>(A22, lda, A21, lda, A21, lda, m, m,
-                                                                              kb, 3, kSplit);
+    if (nt > kBand) {
+      const long long rest = (long long)(nt - kBand) * (nt - kBand + 1) / 2;
+      kUpdate<<<(unsigned)rest, UpdShape::THREADS, UpdShape::SMEM, s>>>(A22, lda, A21, lda, m, kb, kBand, 0);
       GBEM_LAUNCH_CHECK(ctx);
     }
   }
