@@ -15,6 +15,7 @@
 //   k_gemm_nt<STORE,128>: L21 = A21 * inv(L11)^T (trsm as a DMMA GEMM, in place);
 //   k_gemm_nt<SUB,64>   : A22 -= L21 * L21^T on lower 128x64 tiles (the O(n^3) part).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <vector>
@@ -57,7 +58,7 @@ __device__ long long g_potrf_clk[128];
 constexpr int kPotrfThreads = 512;
 constexpr int kPotrfWarps = kPotrfThreads / 32;
 constexpr int kPanel = 32;
-constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + NB + 3 * kPanel * kPanel) * sizeof(double);
+constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + NB + 3 * kPanel * (kPanel + 1)) * sizeof(double);
 
 __global__ void __launch_bounds__(kPotrfThreads)
     k_potrf_diag(double* A, long long lda, int kb, int row0, double* Linv, int* info) {
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(kPotrfThreads)
   constexpr int LD = NB + 1;
   double* a = sm;              // [NB][LD] column-major: a[c*LD + r]
   double* xd = a + NB * LD;    // diag of X (= 1 / diag of L)
-  double* tmp = xd + NB;       // [3][32*32] products of the X assembly
+  double* tmp = xd + NB;       // [3][32][33] products of the X assembly
   const int tid = threadIdx.x, lane = tid & 31;
   // warp index through a shuffle: ptxas then knows it is warp-uniform, and the
   // shuffles inside `if (warp == 0)` compile without divergence handling
@@ -140,23 +141,26 @@ __global__ void __launch_bounds__(kPotrfThreads)
     POTRF_TICK(1 + 3 * p);
     const int r0 = c0 + kPanel, mrest = NB - r0;  // padded rows below the panel
     if (mrest <= 0) break;
-    // ---- 2. panel rows below: L_rp = A_rp * inv(L_pp)^T, 4 x 4 register tiles
+    // Register tiles below are 4 x 4 with stride 8 inside 32 x 32 super-tiles of
+    // 64 threads (tx, ty in 0..7: rows ty + 8u, columns tx + 8v), so that the
+    // shared loads of a warp hit consecutive addresses or broadcast.
+    const int grp = tid >> 6, tx = tid & 7, ty = (tid >> 3) & 7;
+    // ---- 2. panel rows below: L_rp = A_rp * inv(L_pp)^T
     {
-      const int ntile = (mrest / 4) * (kPanel / 4);
+      const int G = mrest / kPanel;
       double acc[4][4] = {};
-      int rb = 0, jb = 0;
-      if (tid < ntile) {
-        rb = r0 + 4 * (tid / (kPanel / 4));
-        jb = 4 * (tid % (kPanel / 4));
+      const int rowb = r0 + kPanel * grp + ty;
+      if (grp < G) {
 #pragma unroll 4
         for (int k = 0; k < kPanel; ++k) {  // X(j, k) = 0 for k > j: fixed trip count, no branches
           double ar[4], xv[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) ar[u] = a[(c0 + k) * LD + rb + u];
+          for (int u = 0; u < 4; ++u) ar[u] = a[(c0 + k) * LD + rowb + 8 * u];
+          const double dg = xd[c0 + k];
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
-            const int j = jb + v;
-            const double up = a[(c0 + j) * LD + c0 + k], dg = xd[c0 + k];
+            const int j = tx + 8 * v;
+            const double up = a[(c0 + j) * LD + c0 + k];
             xv[v] = k < j ? up : 0.0;
             xv[v] = k == j ? dg : xv[v];  // X(j, k)
           }
@@ -167,33 +171,31 @@ __global__ void __launch_bounds__(kPotrfThreads)
         }
       }
       __syncthreads();
-      if (tid < ntile) {
+      if (grp < G) {
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) a[(c0 + jb + v) * LD + rb + u] = acc[u][v];
+          for (int v = 0; v < 4; ++v) a[(c0 + tx + 8 * v) * LD + rowb + 8 * u] = acc[u][v];
       }
     }
     __syncthreads();
     POTRF_TICK(2 + 3 * p);
-    // ---- 3. rank-32 update of the trailing lower part, 4 x 4 register tiles
+    // ---- 3. rank-32 update of the trailing lower part (32 x 32 super-tiles I >= J)
     {
-      const int nb4 = mrest / 4;
-      const int ntile = nb4 * (nb4 + 1) / 2;
-      for (int t = tid; t < ntile; t += kPotrfThreads) {
-        int tr = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
-        while ((tr + 1) * (tr + 2) / 2 <= t) ++tr;
-        while (tr * (tr + 1) / 2 > t) --tr;
-        const int tc = t - tr * (tr + 1) / 2;
-        const int rb = r0 + 4 * tr, cb = r0 + 4 * tc;
+      const int G = mrest / kPanel;
+      if (grp < G * (G + 1) / 2) {
+        int I = 0;
+        while ((I + 1) * (I + 2) / 2 <= grp) ++I;
+        const int J = grp - I * (I + 1) / 2;
+        const int rowb = r0 + kPanel * I + ty, colb = r0 + kPanel * J + tx;
         double acc[4][4] = {};
 #pragma unroll 4
         for (int k = 0; k < kPanel; ++k) {
           double lr[4], lc[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            lr[u] = a[(c0 + k) * LD + rb + u];
-            lc[u] = a[(c0 + k) * LD + cb + u];
+            lr[u] = a[(c0 + k) * LD + rowb + 8 * u];
+            lc[u] = a[(c0 + k) * LD + colb + 8 * u];
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u)
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(kPotrfThreads)
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int v = 0; v < 4; ++v)
-            if (cb + v <= rb + u) a[(cb + v) * LD + rb + u] -= acc[u][v];
+            if (colb + 8 * v <= rowb + 8 * u) a[(colb + 8 * v) * LD + rowb + 8 * u] -= acc[u][v];
       }
     }
     __syncthreads();
@@ -212,65 +214,67 @@ __global__ void __launch_bounds__(kPotrfThreads)
   }
   POTRF_TICK(20);
   // ---- off-diagonal blocks of X = inv(L): X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp,
-  // 4 x 4 register tiles (8 shared loads per 16 FMAs).
-  for (int rbk = 1; rbk < npan; ++rbk) {
-    const int R0 = rbk * kPanel;
-    const int ntask = rbk * 64;  // 64 tiles of 4 x 4 per 32 x 32 block
-    for (int t = tid; t < ntask; t += kPotrfThreads) {
-      const int pb = t / 64, ti = (t % 64) % 8, tk = (t % 64) / 8;
-      const int col0 = pb * kPanel + 4 * tk;
-      double acc[4][4] = {};
+  // same strided 4 x 4 tiles; T_p = sum_q L_rq X_qp staged in tmp[p][32][33].
+  {
+    const int grp = tid >> 6, tx = tid & 7, ty = (tid >> 3) & 7;
+    constexpr int TLD = kPanel + 1;
+    for (int rbk = 1; rbk < npan; ++rbk) {
+      const int R0 = rbk * kPanel;
+      if (grp < rbk) {
+        const int pb = grp;
+        double acc[4][4] = {};
 #pragma unroll 4
-      for (int m = col0; m < R0; ++m) {
-        double lr[4], xc[4];
+        for (int m = pb * kPanel; m < R0; ++m) {
+          double lr[4], xc[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) lr[u] = a[m * LD + R0 + 4 * ti + u];  // L(R0+i, m)
+          for (int u = 0; u < 4; ++u) lr[u] = a[m * LD + R0 + ty + 8 * u];  // L(R0+i, m)
+          const double dg = xd[m];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int c = col0 + v;
-          // unconditional loads + selects: no branches around the shared loads
-          const double up = a[m * LD + c], dg = xd[m];
-          xc[v] = m > c ? up : 0.0;
-          xc[v] = m == c ? dg : xc[v];  // X(m, c)
+          for (int v = 0; v < 4; ++v) {
+            const int c = pb * kPanel + tx + 8 * v;
+            const double up = a[m * LD + c];
+            xc[v] = m > c ? up : 0.0;
+            xc[v] = m == c ? dg : xc[v];  // X(m, c)
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(lr[u], xc[v], acc[u][v]);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = fma(lr[u], xc[v], acc[u][v]);
+          for (int v = 0; v < 4; ++v) tmp[pb * kPanel * TLD + (ty + 8 * u) * TLD + tx + 8 * v] = acc[u][v];
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) tmp[pb * kPanel * kPanel + (4 * tk + v) * kPanel + 4 * ti + u] = acc[u][v];
-    }
-    __syncthreads();
-    for (int t = tid; t < ntask; t += kPotrfThreads) {
-      const int pb = t / 64, ti = (t % 64) % 8, tk = (t % 64) / 8;
-      const int col0 = pb * kPanel + 4 * tk;
-      double acc[4][4] = {};
+      __syncthreads();
+      if (grp < rbk) {
+        const int pb = grp;
+        double acc[4][4] = {};
 #pragma unroll 4
-      for (int m = 0; m < 4 * ti + 4; ++m) {
-        double xr[4], tv[4];
+        for (int m = 0; m < kPanel; ++m) {
+          double xr[4], tv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = 4 * ti + u;
-          const double up = a[(R0 + i) * LD + R0 + m], dg = xd[R0 + i];
-          xr[u] = m < i ? up : 0.0;
-          xr[u] = m == i ? dg : xr[u];  // X(R0+i, R0+m)
+          for (int u = 0; u < 4; ++u) {
+            const int i = ty + 8 * u;
+            const double up = a[(R0 + i) * LD + R0 + m], dg = xd[R0 + i];
+            xr[u] = m < i ? up : 0.0;
+            xr[u] = m == i ? dg : xr[u];  // X(R0+i, R0+m)
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) tv[v] = tmp[pb * kPanel * TLD + m * TLD + tx + 8 * v];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(xr[u], tv[v], acc[u][v]);
         }
-#pragma unroll
-        for (int v = 0; v < 4; ++v) tv[v] = tmp[pb * kPanel * kPanel + (4 * tk + v) * kPanel + m];
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = fma(xr[u], tv[v], acc[u][v]);
+          for (int v = 0; v < 4; ++v)
+            a[(R0 + ty + 8 * u) * LD + pb * kPanel + tx + 8 * v] = -acc[u][v];  // X(R0+i, col)
       }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) a[(R0 + 4 * ti + u) * LD + col0 + v] = -acc[u][v];  // X(R0+i, col)
+      __syncthreads();
     }
-    __syncthreads();
   }
   POTRF_TICK(21);
   for (int idx = tid; idx < NB * NB; idx += kPotrfThreads) {
@@ -731,12 +735,21 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   }
   cudaStream_t s1 = ctx->side_stream;
   GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_col, s));
+  // GBEM_FACTOR_PROFILE=1: per-block side-stream (diagonal factor + panel trsm)
+  // and main-stream timings on stderr (diagnostics only)
+  static const bool prof = getenv("GBEM_FACTOR_PROFILE") != nullptr;
+  std::vector<cudaEvent_t> pe;
+  if (prof) {
+    pe.resize(4 * (size_t)nblk);
+    for (auto& e : pe) cudaEventCreate(&e);
+  }
   for (int b = 0; b < nblk; ++b) {
     int k0 = b * NB, kb = std::min(NB, n - k0);
     int m = n - k0 - kb;
     double* Akk = ctx->d_A + (long long)k0 * lda + k0;
     double* A21 = Akk + kb;  // rows k0+kb.., cols k0..
     GBEM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ev_col, 0));
+    if (prof) cudaEventRecord(pe[4 * b], s1);
     k_potrf_diag<<<1, kPotrfThreads, kPotrfSmem, s1>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
     GBEM_LAUNCH_CHECK(ctx);
     if (m > 0) {
@@ -745,8 +758,10 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
           A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb, 0, 0);
       GBEM_LAUNCH_CHECK(ctx);
     }
+    if (prof) cudaEventRecord(pe[4 * b + 1], s1);
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_panel, s1));
     GBEM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_panel, 0));
+    if (prof) cudaEventRecord(pe[4 * b + 2], s);
     if (m <= 0) break;
     // A22 -= L21 L21^T on 64 x 64 lower tiles: first the next block column
     // (kBand tile columns), then the rest
@@ -757,6 +772,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     kUpdate<<<dim3(nt, band), UpdShape::THREADS, UpdShape::SMEM, s>>>(A22, lda, A21, lda, m, kb, 0, band);
     GBEM_LAUNCH_CHECK(ctx);
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_col, s));
+    if (prof) cudaEventRecord(pe[4 * b + 3], s);
     if (nt > kBand) {
       const long long rest = (long long)(nt - kBand) * (nt - kBand + 1) / 2;
       kUpdate<<<(unsigned)rest, UpdShape::THREADS, UpdShape::SMEM, s>>>(A22, lda, A21, lda, m, kb, kBand, 0);
@@ -766,6 +782,18 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   cudaEventRecord(ctx->ev[1], s);
   GBEM_CUDA(ctx, cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(int), cudaMemcpyDeviceToHost, s));
   GBEM_CUDA(ctx, cudaStreamSynchronize(s));
+  if (prof) {
+    double side = 0, band = 0, gap = 0;
+    for (int b = 0; b < nblk; ++b) {
+      float x = 0;
+      if (cudaEventElapsedTime(&x, pe[4 * b], pe[4 * b + 1]) == cudaSuccess) side += x;
+      if (b + 1 < nblk && cudaEventElapsedTime(&x, pe[4 * b + 2], pe[4 * b + 3]) == cudaSuccess) band += x;
+      if (b > 0 && cudaEventElapsedTime(&x, pe[4 * (b - 1) + 3], pe[4 * b]) == cudaSuccess) gap += x;
+    }
+    fprintf(stderr, "[factor profile] n=%d blocks=%d side(potrf+trsm)=%.3f ms band-update=%.3f ms "
+            "band->next-potrf gap=%.3f ms\n", n, nblk, side, band, gap);
+    for (auto& e : pe) cudaEventDestroy(e);
+  }
   ctx->factored = true;
   if (*ctx->h_info != big) {
     if (stats) stats->bad_pivot = *ctx->h_info;
