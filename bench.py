@@ -219,14 +219,27 @@ def run_ours(args):
               "residual_ms": sst.ms_residual}
     dmma_peak = peaks.get("fp64_dmma_tflops", 37.09)
     dfma_peak = peaks.get("fp64_dfma_tflops", 36.75)
-    roof_chol = {"bound": "tensor", "kernel": "potrf(k_potrf_diag+k_gemm_nt DMMA)",
+    traffic = _ncu_traffic()
+    roof_chol = {"bound": "tensor", "kernel": "Cholesky factor (k_potrf_diag + k_gemm_nt trsm + k_syrk_gen DMMA update)",
                  "achieved": chol_flops / (sst.ms_factor * 1e-3) / 1e12, "peak": dmma_peak, "unit": "TFLOP/s",
-                 "traffic": None, "peak_source": "tools/fp64_peaks.cu DMMA m8n8k4 loop (no FP64 in MEASURED_PEAKS.json)"}
+                 "traffic": traffic.get("k_syrk_gen"),
+                 "algorithmic": f"n^3/3 = {chol_flops:.3e} flop per factorisation (n = {n}) / device time of the factor",
+                 "peak_source": "tools/fp64_peaks.cu DMMA m8n8k4 loop (no FP64 in MEASURED_PEAKS.json)"}
     roof_chol["frac"] = roof_chol["achieved"] / roof_chol["peak"]
     roof_far = {"bound": "fp64_pipe", "kernel": "k_far", "achieved": ast.far_flops / (ast.ms_far * 1e-3) / 1e12,
-                "peak": dfma_peak, "unit": "TFLOP/s", "traffic": None,
+                "peak": dfma_peak, "unit": "TFLOP/s", "traffic": traffic.get("k_far"),
+                "algorithmic": "counted FP64 flops of the Gauss evaluations (dadd, dmul = 1, dfma = 2) / device time",
                 "peak_source": "tools/fp64_peaks.cu DFMA loop (no FP64 in MEASURED_PEAKS.json)"}
     roof_far["frac"] = roof_far["achieved"] / roof_far["peak"]
+    # each Gauss evaluation issues one MUFU.RSQ64H; its measured rate bounds k_far before the FP64 pipe does
+    rsq_rate = peaks.get("rsqrt_f64_custom_per_s", 2.2e12)
+    roof_far["mufu_rsq64_bound_frac"] = (ast.far_evals / rsq_rate) / (ast.ms_far * 1e-3)
+    # DFMA and DMMA share one FP64 datapath on B200 (tools/pipe_overlap.cu), so the
+    # step as a whole is bounded by its total FP64 work at the FP64 peak
+    step_flops = chol_flops + ast.far_flops + 2.0 * n * n * K
+    fp64_step = {"flops_per_step": step_flops, "achieved_tflops": step_flops / (ms * 1e-3) / 1e12,
+                 "peak_tflops": dmma_peak, "frac": step_flops / (ms * 1e-3) / 1e12 / dmma_peak,
+                 "note": "Cholesky n^3/3 + far-field Gauss flops + 2 n^2 K triangular solves per step"}
     dominant, secondary = (roof_chol, roof_far) if sst.ms_factor >= ast.ms_far else (roof_far, roof_chol)
 
     line = {
@@ -239,7 +252,7 @@ def run_ours(args):
                    "parallelism": f"replicas{world}" if world > 1 else "single"},
         "e2e": {"value": world * entries / e2e_s, "unit": UNIT, "seconds_per_extraction": e2e_s,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "roofline": dominant, "roofline_secondary": secondary, "phases_ms": phases,
+        "roofline": dominant, "roofline_secondary": secondary, "fp64_step": fp64_step, "phases_ms": phases,
         "assembly": {"pairs_far": ast.pairs_far, "pairs_coplanar": ast.pairs_coplanar,
                      "pairs_parallel": ast.pairs_parallel, "pairs_orthogonal": ast.pairs_orthogonal,
                      "far_evals": ast.far_evals, "near_evals": ast.near_evals, "not_converged": ast.not_converged,
@@ -254,6 +267,16 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
+
+
+def _ncu_traffic() -> dict:
+    """Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    dominant kernels from the committed ncu --set full captures (profiles/)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return {k: v for k, v in json.load(open(p)).get("bytes_per_launch", {}).items()}
+    except (OSError, ValueError):
+        return {}
 
 
 def m_name(cfg: int) -> str:

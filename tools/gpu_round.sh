@@ -1,26 +1,28 @@
 #!/bin/bash
 # Measured pipeline for one round (run under gpurun from the repo root):
 #   1. GPU tests, 2. bench (ours, then reference arm), 3. ncu launch list of the
-#   same bench command, 4. one ncu --set full capture each of the top kernels.
+#   same bench command, 4. one ncu --set full capture of each top kernel.
 # Each ncu step runs only after the same command exited 0 without ncu.
 TAG=${1:-r01}
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/tests_$TAG.log 2>&1; echo "tests rc=$?"
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/tests_$TAG.log 2>&1; echo "tests rc=$?"
 tail -2 gpurun_out/tests_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; rc=$?; echo "bench rc=$rc"
 cat gpurun_out/bench_$TAG.json
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
 if [ $rc -eq 0 ]; then
-  timeout 1200 python bench.py --steps 1 --warmup 3 > gpurun_out/plain_$TAG.log 2>&1 && \
-  timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
-    --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 3 > gpurun_out/ncu_list_$TAG.log 2>&1
+  timeout 1200 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/plain_$TAG.log 2>&1 && \
+  timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv \
+    --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_list_$TAG.log 2>&1
   echo "launch list rc=$?"
   python tools/launch_summary.py gpurun_out/launches_$TAG.csv > gpurun_out/launch_summary_$TAG.txt 2>&1
   head -30 gpurun_out/launch_summary_$TAG.txt
-  for KS in k_gemm_nt:40 k_far:40 k_potrf_diag:200 k_solve_coop:2 k_near_gl:4 k_classify:4; do
+  for KS in "k_syrk_gen:300" "k_far<\(int\)4, \(int\)3>:1" "k_potrf_diag:200" "k_solve_coop:2" "k_near_gl:2" "k_classify:2" "k_gemm_nt:200"; do
     K=${KS%%:*}; S=${KS##*:}
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
-      -o gpurun_out/prof_${TAG}_$K -f python bench.py --steps 1 --warmup 3 > gpurun_out/ncu_${TAG}_$K.log 2>&1
+    NAME=$(echo "$K" | tr -cd 'a-z_0-9')
+    timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      --kernel-name "regex:$K" -s $S -c 1 -o gpurun_out/prof_${TAG}_$NAME -f \
+      python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_${TAG}_$NAME.log 2>&1
     echo "ncu $K rc=$?"
   done
 fi
