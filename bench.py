@@ -49,63 +49,76 @@ def _peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons, sampled every 100 ms by a background
-    nvidia-smi started BEFORE the warm-up (its start-up is not inside the timed
-    region); summary() keeps the samples taken inside [mark_start, mark_end]."""
-
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled through NVML (in-process, a few
+    microseconds per query) every 250 ms from a background thread started
+    BEFORE the warm-up; summary() keeps the samples inside [mark_start,
+    mark_end].  (A polling nvidia-smi child process measurably stalled the
+    GPU at its start-up and during sampling, so it is not used.)"""
 
     def __init__(self, device: int):
         self.device = device
-        self.rows: list[tuple[float, list[str]]] = []
-        self.proc = None
+        self.rows: list[tuple[float, dict]] = []
         self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self.h = None
 
     def start(self):
         if os.environ.get("GBEM_NO_CLOCKS"):
             return self
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except (FileNotFoundError, OSError):
-            self.proc = None
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_sm = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self.h = None
+            return self
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append((time.perf_counter(), [c.strip() for c in line.split(",")]))
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        return {"sm": sm, "reasons": r}
+
+    def _run(self):
+        while not self._stop.wait(0.25):
+            try:
+                self.rows.append((time.perf_counter(), self._sample()))
+            except Exception:
+                return
 
     def mark_start(self):
         self.t0 = time.perf_counter()
 
     def mark_end(self):
         self.t1 = time.perf_counter()
+        if self.h is not None:  # at least one sample at the end of the timed region
+            try:
+                self.rows.append((self.t1, self._sample()))
+            except Exception:
+                pass
 
     def stop(self):
-        if self.proc:
-            time.sleep(0.25)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
 
     def summary(self) -> dict:
-        inside = [r for t, r in self.rows if self.t0 is not None and self.t0 <= t <= (self.t1 or t) + 0.15]
-        rows = inside or [r for _, r in self.rows[-3:]]
-        if not rows:
+        if self.h is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows), "samples_in_timed_region": len(inside)}
+        nv = self.nv
+        inside = [r for t, r in self.rows if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
+        rows = inside or [r for _, r in self.rows[-3:]]
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        reasons = sorted({name for r in rows for name, b in bits.items() if r["reasons"] & b})
+        sm = [r["sm"] for r in rows]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(rows), "samples_in_timed_region": len(inside), "source": "NVML"}
 
 
 def dist_env():
@@ -175,13 +188,22 @@ def run_ours(args):
     torch.cuda.synchronize()
     l0 = ctx.launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # stream-ordered mode for the timed steps: no host synchronisation inside a
+    # step (the SPD / non-finite checks are read back once by gbem_ctx_sync)
+    ctx.check(lib.gbem_ctx_set_async(ctx.h, 1))
     clk.mark_start()
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     ev0.record(stream)
-    for _ in range(args.steps):
+    step_ev[0].record(stream)
+    for k in range(args.steps):
         step()
+        step_ev[k + 1].record(stream)
     ev1.record(stream)
+    ctx.check(lib.gbem_ctx_sync(ctx.h))
     torch.cuda.synchronize()
     clk.mark_end()
+    ctx.check(lib.gbem_ctx_set_async(ctx.h, 0))
+    step_ms = [step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(args.steps)]
     clk.stop()
     launches = ctx.launches - l0
     ms = ev0.elapsed_time(ev1) / args.steps
@@ -257,7 +279,7 @@ def run_ours(args):
                      "pairs_parallel": ast.pairs_parallel, "pairs_orthogonal": ast.pairs_orthogonal,
                      "far_evals": ast.far_evals, "near_evals": ast.near_evals, "not_converged": ast.not_converged,
                      "far_flops": ast.far_flops},
-        "max_residual": sst.max_residual, "gpu_launches": launches, "clocks": clk.summary(),
+        "step_ms": step_ms, "max_residual": sst.max_residual, "gpu_launches": launches, "clocks": clk.summary(),
         "c_matrix_diag_F": [float(Cdev[k, k]) for k in range(K)],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -369,8 +391,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--seed", type=int, default=1)

@@ -92,6 +92,13 @@ const char* gbem_last_error(const gbem_ctx* ctx);
  * non-blocking stream; pass cudaStreamLegacy, (void*)1, for the legacy default
  * stream, which is what a framework's "stream 0" handle means). */
 int gbem_ctx_set_stream(gbem_ctx* ctx, void* cuda_stream);
+/* Stream-ordered mode (on != 0): the device-pointer (_dev) calls enqueue their
+ * work and return without blocking; the non-SPD pivot check of a factorisation
+ * is latched and reported (GBEM_ENUMERIC, same message) by gbem_ctx_sync, which
+ * synchronises the context's stream.  Off (default): every call is blocking and
+ * reports its own errors, like the reference's exceptions. */
+int gbem_ctx_set_async(gbem_ctx* ctx, int on);
+int gbem_ctx_sync(gbem_ctx* ctx);
 /* Number of this library's kernels launched on the context so far. */
 int64_t gbem_ctx_launch_count(const gbem_ctx* ctx);
 

@@ -55,6 +55,8 @@ GPU_SYMBOLS = [
     ("gbem_ctx_destroy", None, [_P]),
     ("gbem_last_error", C.c_char_p, [_P]),
     ("gbem_ctx_set_stream", C.c_int, [_P, _P]),
+    ("gbem_ctx_set_async", C.c_int, [_P, C.c_int]),
+    ("gbem_ctx_sync", C.c_int, [_P]),
     ("gbem_ctx_launch_count", C.c_int64, [_P]),
     ("gbem_u_pair_integrals", C.c_int, [_P, C.POINTER(GbemPanels), C.POINTER(GbemPanels), C.c_int64,
                                         C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats)]),

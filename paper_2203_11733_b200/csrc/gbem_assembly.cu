@@ -33,6 +33,9 @@ __constant__ double c_gw[kQMax + 1][kQMax];
 // calibrated in tools/calib_far.c (far pairs have gap >= diam, so q <= 8 at
 // far_tol = 1e-12).
 __constant__ double c_delta[kQMax + 1];
+// the same thresholds squared, in FP32, for the classifier: order q suffices when
+// gap^2 / h^2 >= c_cd2f[q]
+__constant__ float c_cd2f[kQMax + 1];
 // Gauss-Legendre nodes / weights of the graded near-field rule (near_nodes(band) entries per band)
 __constant__ double c_nx[kNearBands][48];
 __constant__ double c_nw[kNearBands][48];
@@ -142,40 +145,167 @@ void legendre_table(double gx[kQMax + 1][kQMax], double gw[kQMax + 1][kQMax]) {
 
 // ---------------------------------------------------------------- classify
 
-__device__ __forceinline__ int far_order(double gap, double h) {
-#pragma unroll 1
-  for (int q = 1; q < kQMax; ++q)
-    if (gap >= c_delta[q] * h) return q;
-  return kQMax;
+// Per-panel classification record, computed once per assembly (k_panel_cinfo):
+// world extents (geometry.hpp:62-66), squared diameter (73), and 1 / h^2 of the
+// two in-plane half-lengths for the far-field orders.  Every per-pair test is
+// then done on squared distances (no sqrt / hypot per pair) and the orders in FP32.
+struct __align__(16) CPanel {
+  double lo[3], hi[3];
+  double dm2;
+  float iha2, ihb2;
+  int axis, pad;
+};
+
+__global__ void k_panel_cinfo(const DPanel* __restrict__ P, int n, CPanel* __restrict__ out) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const DPanel p = P[k];
+  CPanel c;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) panel_extent(p, d, c.lo[d], c.hi[d]);
+  const double la = p.a1 - p.a0, lb = p.b1 - p.b0;
+  c.dm2 = la * la + lb * lb;
+  c.iha2 = (float)(4.0 / (la * la));
+  c.ihb2 = (float)(4.0 / (lb * lb));
+  c.axis = p.axis;
+  c.pad = 0;
+  out[k] = c;
 }
 
-__device__ __forceinline__ uint32_t classify_pair(const DPanel& A, const DPanel& B, bool same,
-                                                  double near_ratio) {
+// far-field order along a direction from r2 = gap^2 / h^2: the smallest q with
+// r2 >= c_cd2f[q] (thresholds decrease with q), i.e. 1 + #{k < kQMax : r2 < c_cd2f[k]}
+__device__ __forceinline__ int far_order_r2(float r2) {
+  int q = 1;
+#pragma unroll
+  for (int k = 1; k < kQMax; ++k) q += r2 < c_cd2f[k] ? 1 : 0;
+  return q;
+}
+
+__device__ __forceinline__ uint32_t classify_pair(const CPanel& A, const CPanel& B, bool same, double near_ratio) {
   if (same) return kClsCoplanar;
-  double gap = panel_gap(A, B);
-  double la = A.a1 - A.a0, lb = A.b1 - A.b0, lc = B.a1 - B.a0, ld = B.b1 - B.b0;
-  double dm = fmax(hypot(la, lb), hypot(lc, ld));
-  bool same_axis = A.axis == B.axis;
-  if (gap < near_ratio * dm) {
-    if (same_axis && A.level == B.level) return kClsCoplanar;
+  double gap2 = 0.0;
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double g = fmax(fmax(B.lo[d] - A.hi[d], A.lo[d] - B.hi[d]), 0.0);
+    gap2 = fma(g, g, gap2);
+  }
+  const double dm2 = fmax(A.dm2, B.dm2);
+  const bool same_axis = A.axis == B.axis;
+  if (gap2 < near_ratio * near_ratio * dm2) {
+    if (same_axis && A.lo[A.axis] == B.lo[B.axis]) return kClsCoplanar;
     int band;
-    if (gap == 0.0 || gap >= 0.1 * dm)
+    if (gap2 == 0.0 || gap2 >= 1e-2 * dm2)  // gap >= 0.1 diam
       band = 0;
-    else if (gap >= 0.02 * dm)
+    else if (gap2 >= 4e-4 * dm2)  // 0.02
       band = 1;
-    else if (gap >= 0.005 * dm)
+    else if (gap2 >= 2.5e-5 * dm2)  // 0.005
       band = 2;
-    else if (gap >= 1e-3 * dm)
+    else if (gap2 >= 1e-6 * dm2)  // 1e-3
       band = 3;
     else
       return same_axis ? kClsParallel : kClsOrthogonal;  // near contact: adaptive Romberg
     return (same_axis ? kClsParallelGL : kClsOrthogonalGL) + band;
   }
-  return far_key(far_order(gap, 0.5 * la), far_order(gap, 0.5 * lb), far_order(gap, 0.5 * lc),
-                 far_order(gap, 0.5 * ld));
+  const float g2 = (float)gap2;
+  return far_key(far_order_r2(g2 * A.iha2), far_order_r2(g2 * A.ihb2), far_order_r2(g2 * B.iha2),
+                 far_order_r2(g2 * B.ihb2));
 }
 
-// Warp-aggregated append of `key` (one atomic per distinct key in the warp).
+// Per-CTA key aggregation: warp groups of equal keys (__match_any_sync) add
+// their sizes into a shared open-addressing table; one global atomic per
+// distinct key per CTA then counts (pass 1) or reserves the CTA's queue range
+// (pass 2), and each warp group writes at range base + its offset.
+constexpr int kHash = 1024;  // >= pairs per CTA: the table never fills
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+
+__device__ __forceinline__ int hash_slot(uint32_t* hkey, uint32_t key) {
+  int s = (int)((key * 2654435761u) >> 22);  // 10 bits
+  while (true) {
+    const uint32_t prev = atomicCAS(&hkey[s], kEmpty, key);
+    if (prev == kEmpty || prev == key) return s;
+    s = (s + 1) & (kHash - 1);
+  }
+}
+
+// One CTA per 32x32 tile of the upper triangle restricted to rows [rb, re)
+// (full != 0: complete rows).  tile_row_off[r] = tiles in tile rows before r.
+template <bool FILL>
+__global__ void __launch_bounds__(kClassifyThreads)
+    k_classify(const CPanel* __restrict__ P, int n, int rb, int re, int bi0, int nbt,
+               const long long* __restrict__ tile_row_off, int nrows_t, long long tile_begin,
+               double near_ratio, uint32_t* counts, uint32_t* cursors, uint64_t* queue, int full) {
+  constexpr int kIter = kTile / (kClassifyThreads / 32);
+  __shared__ CPanel si[kTile], sj[kTile];
+  __shared__ uint32_t hkey[kHash], hcnt[kHash];
+  long long t = tile_begin + blockIdx.x;
+  int lo = 0, hi = nrows_t - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (tile_row_off[mid] <= t)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  const int bi = bi0 + lo;
+  const int bj = (full ? 0 : bi) + (int)(t - tile_row_off[lo]);  // full: whole rows (mirrored entries too)
+  const int tid = threadIdx.x;
+  if (tid < kTile) {
+    int i = bi * kTile + tid;
+    if (i < n) si[tid] = P[i];
+  } else if (tid < 2 * kTile) {
+    int j = bj * kTile + (tid - kTile);
+    if (j < n) sj[tid - kTile] = P[j];
+  }
+  for (int s = tid; s < kHash; s += kClassifyThreads) {
+    hkey[s] = kEmpty;
+    hcnt[s] = 0;
+  }
+  __syncthreads();
+  const int lane = tid & 31, warp = tid >> 5;
+  const int j = bj * kTile + lane;
+  uint32_t key[kIter], leader_off[kIter];
+  unsigned peers[kIter];
+  int slot[kIter];
+#pragma unroll
+  for (int it = 0; it < kIter; ++it) {
+    const int r = warp + it * (kClassifyThreads / 32);
+    const int i = bi * kTile + r;
+    const bool valid = i >= rb && i < re && j < n && (full || j >= i);
+    key[it] = valid ? classify_pair(si[r], sj[lane], i == j, near_ratio) : kEmpty;
+    peers[it] = __match_any_sync(0xffffffffu, key[it]);
+    slot[it] = -1;
+    leader_off[it] = 0;
+    if (valid && lane == __ffs(peers[it]) - 1) {
+      slot[it] = hash_slot(hkey, key[it]);
+      leader_off[it] = atomicAdd(&hcnt[slot[it]], (uint32_t)__popc(peers[it]));
+    }
+  }
+  __syncthreads();
+  // one global atomic per distinct key of the tile; hcnt becomes the range base (FILL)
+  for (int s = tid; s < kHash; s += kClassifyThreads) {
+    const uint32_t k = hkey[s];
+    if (k == kEmpty) continue;
+    if (FILL)
+      hcnt[s] = atomicAdd(&cursors[k], hcnt[s]);
+    else
+      atomicAdd(&counts[k], hcnt[s]);
+  }
+  if (!FILL) return;
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kIter; ++it) {
+    if (key[it] == kEmpty) continue;
+    const int leader = __ffs(peers[it]) - 1;
+    uint32_t base = slot[it] >= 0 ? hcnt[slot[it]] + leader_off[it] : 0;
+    base = __shfl_sync(peers[it], base, leader);
+    const int r = warp + it * (kClassifyThreads / 32);
+    const uint32_t rank = __popc(peers[it] & ((1u << lane) - 1u));
+    queue[base + rank] = pack_entry((uint32_t)(bi * kTile + r), (uint32_t)j, key[it]);
+  }
+}
+
+// Warp-aggregated append of `key` (one atomic per distinct key in the warp),
+// used by the pair-list mode.
 template <bool FILL>
 __device__ __forceinline__ void warp_append(bool valid, uint32_t key, uint32_t i, uint32_t j,
                                             uint32_t* counts, uint32_t* cursors, uint64_t* queue) {
@@ -198,51 +328,10 @@ __device__ __forceinline__ void warp_append(bool valid, uint32_t key, uint32_t i
   }
 }
 
-// One CTA per 32x32 tile of the upper triangle restricted to rows [rb, re).
-// tile_row_off[r] = number of tiles in tile rows before r (relative to bi0).
-template <bool FILL>
-__global__ void __launch_bounds__(kClassifyThreads)
-    k_classify(const DPanel* __restrict__ P, int n, int rb, int re, int bi0, int nbt,
-               const long long* __restrict__ tile_row_off, int nrows_t, long long tile_begin,
-               double near_ratio, uint32_t* counts, uint32_t* cursors, uint64_t* queue, int full) {
-  __shared__ DPanel si[kTile], sj[kTile];
-  long long t = tile_begin + blockIdx.x;
-  // binary search the tile row
-  int lo = 0, hi = nrows_t - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (tile_row_off[mid] <= t)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  int bi = bi0 + lo;
-  int bj = (full ? 0 : bi) + (int)(t - tile_row_off[lo]);  // full: whole rows (mirrored entries too)
-  int tid = threadIdx.x;
-  if (tid < kTile) {
-    int i = bi * kTile + tid;
-    if (i < n) si[tid] = P[i];
-  } else if (tid < 2 * kTile) {
-    int j = bj * kTile + (tid - kTile);
-    if (j < n) sj[tid - kTile] = P[j];
-  }
-  __syncthreads();
-  int lane = tid & 31, warp = tid >> 5;
-  int j = bj * kTile + lane;
-#pragma unroll 1
-  for (int r = warp; r < kTile; r += kClassifyThreads / 32) {
-    int i = bi * kTile + r;
-    bool valid = i >= rb && i < re && j < n && (full || j >= i);
-    uint32_t key = 0;
-    if (valid) key = classify_pair(si[r], sj[lane], i == j, near_ratio);
-    warp_append<FILL>(valid, key, (uint32_t)i, (uint32_t)j, counts, cursors, queue);
-  }
-}
-
 // Pair-list mode: pair k is (panel k, panel npairs + k).
 template <bool FILL>
 __global__ void __launch_bounds__(256)
-    k_classify_list(const DPanel* __restrict__ P, int npairs, double near_ratio, uint32_t* counts,
+    k_classify_list(const CPanel* __restrict__ P, int npairs, double near_ratio, uint32_t* counts,
                     uint32_t* cursors, uint64_t* queue) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = k < npairs;
@@ -569,6 +658,16 @@ int grow(gbem_ctx* ctx, void** p, size_t bytes_needed, int64_t* cap_elems, size_
   return GBEM_OK;
 }
 
+// Classification records of the n resident panels (k_panel_cinfo).
+int prepare_cinfo(gbem_ctx* ctx, int64_t n) {
+  int rc = grow(ctx, &ctx->d_cinfo, sizeof(CPanel) * (size_t)n, &ctx->cinfo_cap, sizeof(CPanel));
+  if (rc) return rc;
+  k_panel_cinfo<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->d_panels, (int)n,
+                                                                     (CPanel*)ctx->d_cinfo);
+  GBEM_LAUNCH_CHECK(ctx);
+  return GBEM_OK;
+}
+
 int prepare_work(gbem_ctx* ctx, const gbem_quad_config* cfg_in, gbem_quad_config* cfg) {
   gbem_quad_config c{};
   if (cfg_in) c = *cfg_in;
@@ -595,6 +694,10 @@ int prepare_work(gbem_ctx* ctx, const gbem_quad_config* cfg_in, gbem_quad_config
   }
   GBEM_CUDA(ctx, cudaMemcpyToSymbolAsync(c_delta, delta, sizeof(delta), 0, cudaMemcpyHostToDevice,
                                          ctx->stream));
+  float cd2f[kQMax + 1];
+  cd2f[0] = 3.0e38f;
+  for (int q = 1; q <= kQMax; ++q) cd2f[q] = (float)(delta[q] * delta[q]);
+  GBEM_CUDA(ctx, cudaMemcpyToSymbolAsync(c_cd2f, cd2f, sizeof(cd2f), 0, cudaMemcpyHostToDevice, ctx->stream));
   GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_stats, 0, sizeof(unsigned long long) * ST_COUNT, ctx->stream));
   // ST_FIRST_BAD starts at ~0 (atomicMin target)
   GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_stats + ST_FIRST_BAD, 0xFF, sizeof(unsigned long long), ctx->stream));
@@ -734,6 +837,8 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
   long long need = std::min<long long>(total_tiles * kTile * kTile, 1ll << 27);
   rc = grow(ctx, (void**)&ctx->d_queue, sizeof(uint64_t) * (size_t)need, &ctx->queue_cap, sizeof(uint64_t));
   if (rc) return rc;
+  rc = prepare_cinfo(ctx, n);
+  if (rc) return rc;
   long long* d_rowoff = nullptr;
   GBEM_CUDA(ctx, cudaMallocAsync(&d_rowoff, sizeof(long long) * rowoff.size(), ctx->stream));
   GBEM_CUDA(ctx, cudaMemcpyAsync(d_rowoff, rowoff.data(), sizeof(long long) * rowoff.size(),
@@ -754,13 +859,13 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
     cudaEventRecord(ctx->ev[5], ctx->stream);
     GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, ctx->stream));
     k_classify<false><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
-        ctx->d_panels, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
+        (const CPanel*)ctx->d_cinfo, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
         cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
     k_scan<<<1, 1024, 0, ctx->stream>>>(ctx->d_counts, ctx->d_offsets, ctx->d_cursors, ctx->d_stats);
     GBEM_LAUNCH_CHECK(ctx);
     k_classify<true><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
-        ctx->d_panels, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
+        (const CPanel*)ctx->d_cinfo, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
         cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
     cudaEventRecord(ctx->ev[6], ctx->stream);
@@ -792,6 +897,24 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
     stats->ms_total = tot;
     return rc;
   }
+  if (ctx->async) {  // non-finite check deferred to gbem_ctx_sync
+    GBEM_CUDA(ctx, cudaMemcpyAsync(ctx->h_stats, ctx->d_stats, sizeof(unsigned long long) * ST_COUNT,
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+    ctx->stats_pending = true;
+    return GBEM_OK;
+  }
+  return finish_stats(ctx, nullptr, pairs);
+}
+
+int gbem_internal_check_pending_stats(gbem_ctx* ctx) {
+  if (!ctx->stats_pending) return GBEM_OK;
+  ctx->stats_pending = false;
+  const unsigned long long* h = ctx->h_stats;
+  if (h[ST_NONFINITE]) {
+    unsigned long long b = h[ST_FIRST_BAD];
+    return ctx->fail(GBEM_ENUMERIC, "non-finite integrand sample (pair " + std::to_string(b >> 32) + "," +
+                                        std::to_string(b & 0xffffffffull) + ")");
+  }
   return GBEM_OK;
 }
 
@@ -804,14 +927,16 @@ int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_confi
   if (npairs > (1 << 23)) return ctx->fail(GBEM_EINVAL, "at most 2^23 pairs per call");
   rc = grow(ctx, (void**)&ctx->d_queue, sizeof(uint64_t) * (size_t)npairs, &ctx->queue_cap, sizeof(uint64_t));
   if (rc) return rc;
+  rc = prepare_cinfo(ctx, 2 * npairs);
+  if (rc) return rc;
   GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, ctx->stream));
   int blocks = (int)((npairs + 255) / 256);
-  k_classify_list<false><<<blocks, 256, 0, ctx->stream>>>(ctx->d_panels, (int)npairs, cfg.near_ratio,
+  k_classify_list<false><<<blocks, 256, 0, ctx->stream>>>((const CPanel*)ctx->d_cinfo, (int)npairs, cfg.near_ratio,
                                                           ctx->d_counts, ctx->d_cursors, ctx->d_queue);
   GBEM_LAUNCH_CHECK(ctx);
   k_scan<<<1, 1024, 0, ctx->stream>>>(ctx->d_counts, ctx->d_offsets, ctx->d_cursors, ctx->d_stats);
   GBEM_LAUNCH_CHECK(ctx);
-  k_classify_list<true><<<blocks, 256, 0, ctx->stream>>>(ctx->d_panels, (int)npairs, cfg.near_ratio,
+  k_classify_list<true><<<blocks, 256, 0, ctx->stream>>>((const CPanel*)ctx->d_cinfo, (int)npairs, cfg.near_ratio,
                                                          ctx->d_counts, ctx->d_cursors, ctx->d_queue);
   GBEM_LAUNCH_CHECK(ctx);
   OutSpec o{nullptr, 0, d_out, d_conv};

@@ -128,6 +128,7 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   if (ctx->stream && ctx->stream != ctx->own_stream) cudaStreamSynchronize(ctx->stream);
   cudaFree(ctx->d_panels);
+  cudaFree(ctx->d_cinfo);
   cudaFree(ctx->d_A);
   cudaFree(ctx->d_diag);
   cudaFree(ctx->d_queue);
@@ -159,6 +160,27 @@ int gbem_ctx_set_stream(gbem_ctx* ctx, void* stream) {
 }
 
 int64_t gbem_ctx_launch_count(const gbem_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int gbem_ctx_set_async(gbem_ctx* ctx, int on) {
+  if (!ctx) return GBEM_EINVAL;
+  ctx->async = on != 0;
+  return GBEM_OK;
+}
+
+int gbem_ctx_sync(gbem_ctx* ctx) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  int rc = gbem_internal_check_pending_stats(ctx);
+  if (rc) return rc;
+  if (ctx->info_pending) {
+    ctx->info_pending = false;
+    if (*ctx->h_info != 0x7fffffff)
+      return ctx->fail(GBEM_ENUMERIC,
+                       "matrix not positive definite (pivot at row " + std::to_string(*ctx->h_info) + ")");
+  }
+  return GBEM_OK;
+}
 
 int gbem_u_pair_integrals(gbem_ctx* ctx, const gbem_panels* I, const gbem_panels* J, int64_t npairs,
                           const gbem_quad_config* cfg, double* out, int32_t* converged,

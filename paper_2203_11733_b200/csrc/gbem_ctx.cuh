@@ -19,6 +19,8 @@ struct gbem_ctx {
   // panels (device, 48-byte records)
   gbem_gpu::DPanel* d_panels = nullptr;
   int64_t panel_cap = 0;
+  void* d_cinfo = nullptr;  // per-panel classification records (gbem_assembly.cu CPanel)
+  int64_t cinfo_cap = 0;
 
   // matrix: column-major n x n with leading dimension lda (symmetric after
   // assembly; lower triangle overwritten by the Cholesky factor)
@@ -28,6 +30,11 @@ struct gbem_ctx {
   double* d_diag = nullptr;  // original diagonal (kept for residuals after factoring)
   int64_t diag_cap = 0;
   bool factored = false;
+  // stream-ordered mode (gbem_ctx_set_async): the factorisation's pivot check is
+  // read back at gbem_ctx_sync instead of blocking inside the call
+  bool async = false;
+  bool info_pending = false;
+  bool stats_pending = false;
 
   // assembly work buffers
   uint64_t* d_queue = nullptr;
@@ -77,6 +84,7 @@ struct gbem_ctx {
 // Internal entry points implemented across the units.
 int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n);
 int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, bool device_ptrs);
+int gbem_internal_check_pending_stats(gbem_ctx* ctx);
 int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,
                            const gbem_quad_config* cfg, gbem_assembly_stats* stats, bool symmetrize,
                            double* out = nullptr, int64_t ld_out = 0, bool full_rows = false);

@@ -781,6 +781,12 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   }
   cudaEventRecord(ctx->ev[1], s);
   GBEM_CUDA(ctx, cudaMemcpyAsync(ctx->h_info, ctx->d_info, sizeof(int), cudaMemcpyDeviceToHost, s));
+  if (ctx->async && !stats && !prof) {
+    // stream-ordered mode: the pivot check is deferred to gbem_ctx_sync
+    ctx->factored = true;
+    ctx->info_pending = true;
+    return GBEM_OK;
+  }
   GBEM_CUDA(ctx, cudaStreamSynchronize(s));
   if (prof) {
     double side = 0, band = 0, gap = 0;

@@ -96,3 +96,21 @@ def test_pcg_cmatrix_matches_direct(ctx, sub_blocks):
     else:
         assert res.iterations > 2
     assert np.abs(Cp - Cd).max() <= 1e-9 * np.abs(Cd).max(), np.abs(Cp - Cd).max() / np.abs(Cd).max()
+
+
+def test_async_mode_defers_pivot_check(ctx):
+    """gbem_ctx_set_async: the factor returns immediately and the non-SPD pivot is
+    reported by gbem_ctx_sync with the synchronous call's message."""
+    m = 130
+    M = torch.eye(m, dtype=torch.float64, device="cuda")
+    M[129, 129] = -1.0
+    ctx.set_stream(0)
+    ctx.check(ctx.lib.gbem_ctx_set_async(ctx.h, 1))
+    try:
+        assert ctx.lib.gbem_spd_factor_dev(ctx.h, C.c_void_p(M.data_ptr()), m, m, None) == 0
+        rc = ctx.lib.gbem_ctx_sync(ctx.h)
+        assert rc == 2
+        assert "pivot at row 129" in ctx.lib.gbem_last_error(ctx.h).decode()
+        assert ctx.lib.gbem_ctx_sync(ctx.h) == 0  # reported once
+    finally:
+        ctx.check(ctx.lib.gbem_ctx_set_async(ctx.h, 0))
