@@ -25,4 +25,11 @@ if [ $rc -eq 0 ]; then
       python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_${TAG}_$NAME.log 2>&1
     echo "ncu $K rc=$?"
   done
+  python tools/ncu_collect.py $TAG gpurun_out > gpurun_out/ncu_collect_$TAG.log 2>&1; echo "collect rc=$?"
+  # keep the two dominant captures; the rest are summarised in gpurun_out/${TAG}_ncu_summary.txt
+  for f in gpurun_out/prof_${TAG}_*.ncu-rep; do
+    case "$f" in *k_syrk_gen*|*k_far*) ;; *) rm -f "$f" ;; esac
+  done
+  gzip -f gpurun_out/launches_$TAG.csv
+  du -sh gpurun_out
 fi

@@ -1,7 +1,7 @@
 """Collect the round's ncu --set full captures into profiles/: a text summary
 (tools/ncu_summary.py + top stall lines) and profiles/ncu_traffic.json with the
 per-launch DRAM traffic that bench.py reports as roofline.traffic.
-Usage: python tools/ncu_collect.py TAG"""
+Usage: python tools/ncu_collect.py TAG [OUTDIR (default profiles/)]"""
 import glob
 import json
 import subprocess
@@ -13,6 +13,7 @@ sys.path.insert(0, str(ROOT / "tools"))
 from ncu_summary import summarise  # noqa: E402
 
 tag = sys.argv[1]
+outdir = Path(sys.argv[2]) if len(sys.argv) > 2 else ROOT / "profiles"
 reps = sorted(glob.glob(str(ROOT / "gpurun_out" / f"prof_{tag}_*.ncu-rep")))
 text = []
 traffic = {}
@@ -33,8 +34,8 @@ for rep in reps:
     rd = float(d["dram__bytes_read.sum"].replace(",", "")) * scale.get(u["dram__bytes_read.sum"], 1)
     wr = float(d["dram__bytes_write.sum"].replace(",", "")) * scale.get(u["dram__bytes_write.sum"], 1)
     traffic[name] = rd + wr
-(ROOT / "profiles" / f"{tag}_ncu_summary.txt").write_text("\n".join(text))
+(outdir / f"{tag}_ncu_summary.txt").write_text("\n".join(text))
 json.dump({"how": f"ncu --set full --clock-control none captures of one launch each (gpurun_out/prof_{tag}_*), "
                   "dram__bytes_read.sum + dram__bytes_write.sum", "tag": tag, "bytes_per_launch": traffic},
-          open(ROOT / "profiles" / "ncu_traffic.json", "w"), indent=1)
+          open(outdir / "ncu_traffic.json", "w"), indent=1)
 print(json.dumps(traffic, indent=1))
