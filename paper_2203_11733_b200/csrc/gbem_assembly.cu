@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "gbem_ctx.cuh"
+#include "gbem_dmma_gemm.cuh"
 #include "gbem_near.cuh"
 
 using namespace gbem_gpu;
@@ -1000,12 +1001,109 @@ __global__ void __launch_bounds__(256, 2)
 }
 }  // namespace
 
+namespace {
+// Wide right-hand sides (K > 8): the same product on the FP64 tensor cores.
+// CTA = 64 rows x FN*8 columns of Q, 4 warps of 16 rows (2 x FN DMMA m8n8k4
+// fragments each), n consumed in 16-wide slabs through a 2-stage cp.async
+// pipeline (A rows 128 B contiguous, P slab rows K*8 B contiguous).
+template <int FN>
+__global__ void __launch_bounds__(128)
+    k_rowblock_mm(const double* __restrict__ Ab, long long ld, int rows, int n, const double* __restrict__ P,
+                  long long ldp, int K, int q0, double* __restrict__ Q, long long ldq) {
+  constexpr int TM = 64, KS = 16, NW = FN * 8;
+  constexpr int LA = KS + 4, LP = NW + 4;  // padded smem strides (doubles)
+  __shared__ __align__(16) double As[2][TM * LA];
+  __shared__ __align__(16) double Ps[2][KS * LP];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int r0 = blockIdx.x * TM;
+  const int ncols = min(NW, K - q0);
+  auto load = [&](int s, int buf) {
+    const int k0 = s * KS;
+    for (int c = tid; c < TM * KS / 2; c += 128) {  // A: 64 rows x KS/2 double2
+      const int r = c / (KS / 2), kk = (c % (KS / 2)) * 2;
+      const int gr = r0 + r, gk = k0 + kk;
+      int bytes = 0;
+      const double* src = Ab;
+      if (gr < rows && gk < n) {
+        bytes = gk + 1 < n ? 16 : 8;
+        src = Ab + (long long)gr * ld + gk;
+      }
+      gbem_gemm::cp_async16(&As[buf][r * LA + kk], src, bytes);
+    }
+    for (int c = tid; c < KS * NW / 2; c += 128) {  // P: KS rows x NW/2 double2
+      const int kk = c / (NW / 2), q = (c % (NW / 2)) * 2;
+      const int gk = k0 + kk;
+      int bytes = 0;
+      const double* src = P;
+      if (gk < n && q < ncols) {
+        bytes = q + 1 < ncols ? 16 : 8;
+        src = P + (long long)gk * ldp + q0 + q;
+      }
+      gbem_gemm::cp_async16(&Ps[buf][kk * LP + q], src, bytes);
+    }
+  };
+  double acc[2][FN][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int S = (n + KS - 1) / KS;
+  load(0, 0);
+  gbem_gemm::cp_async_commit();
+  for (int s = 0; s < S; ++s) {
+    if (s + 1 < S) load(s + 1, (s + 1) & 1);
+    gbem_gemm::cp_async_commit();
+    gbem_gemm::cp_async_wait<1>();
+    __syncthreads();
+    const double* as = &As[s & 1][(warp * 16 + g) * LA + t4];
+    const double* ps = &Ps[s & 1][t4 * LP + g];
+#pragma unroll
+    for (int kk = 0; kk < KS; kk += 4) {
+      const double a0 = as[kk], a1 = as[8 * LA + kk];
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+        const double b = ps[kk * LP + j * 8];
+        gbem_gemm::dmma(acc[0][j][0], acc[0][j][1], a0, b);
+        gbem_gemm::dmma(acc[1][j][0], acc[1][j][1], a1, b);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + warp * 16 + i * 8 + g;
+    if (r >= rows) continue;
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int q = j * 8 + 2 * t4 + e;
+        if (q < ncols) Q[(long long)r * ldq + q0 + q] = acc[i][j][e];
+      }
+  }
+}
+}  // namespace
+
 int gbem_internal_rowblock_matvec(gbem_ctx* ctx, const double* Ab, int64_t ld, int64_t rows, int64_t n,
                                   const double* P, int64_t ldp, int64_t K, double* Q, int64_t ldq) {
   if (rows <= 0 || K <= 0) return GBEM_OK;
-  for (int q0 = 0; q0 < K; q0 += 8) {
+  if (K <= 8) {  // HBM-bound: one pass of the FP64-pipe kernel
     k_rowblock_matvec<8, 4><<<(unsigned)((rows + 31) / 32), 256, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P,
-                                                                                 ldp, (int)K, q0, Q, ldq);
+                                                                                 ldp, (int)K, 0, Q, ldq);
+    GBEM_LAUNCH_CHECK(ctx);
+    return GBEM_OK;
+  }
+  // DMMA: up to 64 right-hand sides per pass (intensity K/4 flop/B: tensor-bound above K ~ 20)
+  for (int q0 = 0; q0 < K; q0 += 64) {
+    const int w = (int)std::min<int64_t>(64, K - q0);
+    const unsigned grid = (unsigned)((rows + 63) / 64);
+    if (w <= 16)
+      k_rowblock_mm<2><<<grid, 128, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P, ldp, (int)K, q0, Q, ldq);
+    else if (w <= 32)
+      k_rowblock_mm<4><<<grid, 128, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P, ldp, (int)K, q0, Q, ldq);
+    else
+      k_rowblock_mm<8><<<grid, 128, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P, ldp, (int)K, q0, Q, ldq);
     GBEM_LAUNCH_CHECK(ctx);
   }
   return GBEM_OK;

@@ -207,138 +207,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, BN == 64 ? 2 : 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Large-tile variant for the trailing update: CTA tile 128 x 128, 8 warps as
-// 2 (M) x 4 (N), warp tile 64 x 32 = 8 x 4 DMMA fragments (32 independent
-// accumulators per k-step, 12 fragment loads per 32 DMMA), fragments of the
-// next k-step loaded while the current k-step's DMMAs issue, BK = 16 slabs
-// through a 4-stage cp.async pipeline (139 KB shared memory, one CTA per SM).
-// kSub only: accumulators start at C, the main loop accumulates -A B^T.
-namespace big {
-constexpr int TM = 128, TN = 128, KS = 16, NST = 4;
-constexpr int LDS_ = TM + 8;  // slab row stride (doubles), conflict-free fragment loads
-constexpr size_t SMEM = (size_t)NST * KS * 2 * LDS_ * sizeof(double);
-// lower-triangle 128 x 128 tiles: tile row tm has tm + 1 tiles
-__host__ __device__ inline long long tiles_before(long long tm) { return tm * (tm + 1) / 2; }
-}  // namespace big
-
 __device__ __forceinline__ double neg_hi(double x) {
   return __hiloint2double(__double2hiint(x) ^ (int)0x80000000, __double2loint(x));
-}
-
-// tile_mode 1: every lower tile (blockIdx.x enumerates them); 3: lower tiles
-// with tile column >= 1 (block column 0 was updated first by the look-ahead).
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_syrk_big(double* C, long long ldc, const double* A, long long lda, int M, int K, int tile_mode) {
-  using namespace big;
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;                    // [NST][KS][LDS_]
-  double* Bs = smem + NST * KS * LDS_;  // [NST][KS][LDS_]
-  long long t = blockIdx.x;
-  if (tile_mode == 3) t += 0;  // mapped below
-  // tile (tm, tn), tn <= tm
-  int tm, tn;
-  if (tile_mode == 1) {
-    int x = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-    while (tiles_before(x + 1) <= t) ++x;
-    while (tiles_before(x) > t) --x;
-    tm = x;
-    tn = (int)(t - tiles_before(x));
-  } else {  // columns >= 1: row tm (>= 1) has tm tiles
-    int x = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);  // t = x(x+1)/2 + (tn - 1), tm = x + 1
-    while (tiles_before(x + 1) <= t) ++x;
-    while (tiles_before(x) > t) --x;
-    tm = x + 1;
-    tn = 1 + (int)(t - tiles_before(x));
-  }
-  const int m0 = tm * TM, n0 = tn * TN;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;  // 2 x 4 warps
-  const int g = lane >> 2, t4 = lane & 3;
-
-  double acc[8][4][2];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = m0 + wm * 64 + i * 8 + g;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = n0 + wn * 32 + j * 8 + 2 * t4 + e;
-        acc[i][j][e] = (row < M && col <= row) ? C[(long long)col * ldc + row] : 0.0;
-      }
-  }
-  const int KT = (K + KS - 1) / KS;
-  auto load_stage = [&](int kt, int st) {
-    const int k0 = kt * KS;
-    double* as = As + st * KS * LDS_;
-    double* bs = Bs + st * KS * LDS_;
-#pragma unroll
-    for (int c = tid; c < KS * TM / 2; c += GEMM_THREADS) {
-      const int kk = c / (TM / 2), mm = (c % (TM / 2)) * 2;
-      const int gk = k0 + kk;
-      int gm = m0 + mm, bytes = 0;
-      const double* src = A;
-      if (gk < K && gm < M) {
-        bytes = gm + 1 < M ? 16 : 8;
-        src = A + (long long)gk * lda + gm;
-      }
-      cp_async16(as + kk * LDS_ + mm, src, bytes);
-      gm = n0 + mm;
-      bytes = 0;
-      src = A;
-      if (gk < K && gm < M) {
-        bytes = gm + 1 < M ? 16 : 8;
-        src = A + (long long)gk * lda + gm;
-      }
-      cp_async16(bs + kk * LDS_ + mm, src, bytes);
-    }
-  };
-#pragma unroll
-  for (int st = 0; st < NST - 1; ++st) {
-    if (st < KT) load_stage(st, st);
-    cp_async_commit();
-  }
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_async_wait<NST - 2>();
-    __syncthreads();
-    const int nxt = kt + NST - 1;
-    if (nxt < KT) load_stage(nxt, nxt % NST);
-    cp_async_commit();
-    const double* as = As + (kt % NST) * KS * LDS_ + wm * 64 + g;
-    const double* bs = Bs + (kt % NST) * KS * LDS_ + wn * 32 + g;
-    double af[2][8], bf[2][4];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) af[0][i] = neg_hi(as[t4 * LDS_ + i * 8]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) bf[0][j] = bs[t4 * LDS_ + j * 8];
-#pragma unroll
-    for (int ks = 0; ks < KS / 4; ++ks) {
-      const int cur = ks & 1;
-      if (ks + 1 < KS / 4) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) af[cur ^ 1][i] = neg_hi(as[((ks + 1) * 4 + t4) * LDS_ + i * 8]);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bf[cur ^ 1][j] = bs[((ks + 1) * 4 + t4) * LDS_ + j * 8];
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
-    }
-  }
-  cp_async_wait<0>();
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int row = m0 + wm * 64 + i * 8 + g;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = n0 + wn * 32 + j * 8 + 2 * t4 + e;
-        if (row < M && col <= row) C[(long long)col * ldc + row] = acc[i][j][e];
-      }
-  }
 }
 
 // ---------------------------------------------------------------------------

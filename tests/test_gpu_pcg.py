@@ -16,7 +16,8 @@ from test_gpu_assembly import two_boxes
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("rows,n,K,ldp", [(1, 1, 1, 1), (37, 300, 5, 5), (128, 1000, 8, 8), (250, 777, 13, 16)])
+@pytest.mark.parametrize("rows,n,K,ldp", [(1, 1, 1, 1), (37, 300, 5, 5), (128, 1000, 8, 8), (250, 777, 13, 16),
+                                           (129, 515, 40, 40), (300, 1000, 64, 64), (70, 333, 70, 72), (5, 17, 9, 9)])
 def test_rowblock_matvec(ctx, rows, n, K, ldp):
     gen = torch.Generator(device="cpu").manual_seed(rows + n)
     ld = ((n + 7) // 8) * 8

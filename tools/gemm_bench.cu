@@ -60,21 +60,6 @@ int main(int argc, char** argv) {
     printf("{\"kernel\": \"k_gemm_nt<kSub> lower\", \"m\": %d, \"k\": %d, \"ms\": %.4f, \"tflops\": %.2f}\n", m, k,
            ms / 10, flops / (ms / 10 * 1e-3) / 1e12);
   }
-  {
-    CK(cudaFuncSetAttribute(k_syrk_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big::SMEM));
-    int ntb = (m + 127) / 128;
-    long long nb = big::tiles_before(ntb);
-    for (int rep = 0; rep < 3; ++rep) {
-      cudaEventRecord(e0);
-      for (int it = 0; it < 10; ++it)
-        k_syrk_big<<<(unsigned)nb, GEMM_THREADS, big::SMEM>>>(C, ldc, A, m, m, k, 1);
-      cudaEventRecord(e1);
-      CK(cudaEventSynchronize(e1));
-      cudaEventElapsedTime(&ms, e0, e1);
-      printf("{\"kernel\": \"k_syrk_big lower\", \"m\": %d, \"k\": %d, \"ms\": %.4f, \"tflops\": %.2f}\n", m, k,
-             ms / 10, flops / (ms / 10 * 1e-3) / 1e12);
-    }
-  }
   auto run_gen = [&](auto kern, int TBM, int TBN, int threads, size_t smem, const char* name) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     long long ntr = (m + TBM - 1) / TBM;
@@ -109,7 +94,8 @@ int main(int argc, char** argv) {
   // correctness: one application each from the same start
   fill<<<(unsigned)((ldc * m + 255) / 256), 256>>>(C, ldc * m, 1);
   fill<<<(unsigned)((ldc * m + 255) / 256), 256>>>(C2, ldc * m, 1);
-  k_syrk_big<<<(unsigned)big::tiles_before((m + 127) / 128), GEMM_THREADS, big::SMEM>>>(C, ldc, A, m, m, k, 1);
+  k_syrk_gen<64, 64, 2, 2, 2, 4><<<(unsigned)((long long)((m + 63) / 64) * ((m + 63) / 64 + 1) / 2), 128,
+                                   GenShape<64, 64, 2, 2, 2>::SMEM>>>(C, ldc, A, m, m, k, 0, 0);
   cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, m, k, &alpha, A, m, &beta, C2, ldc);
   CK(cudaDeviceSynchronize());
   std::vector<double> h1((size_t)ldc * m), h2((size_t)ldc * m);
