@@ -1009,7 +1009,7 @@ namespace {
 template <int FN>
 __global__ void __launch_bounds__(128)
     k_rowblock_mm(const double* __restrict__ Ab, long long ld, int rows, int n, const double* __restrict__ P,
-                  long long ldp, int K, int q0, double* __restrict__ Q, long long ldq) {
+                  long long ldp, int K, int q0, double* __restrict__ Q, long long ldq, int vec16) {
   constexpr int TM = 64, KS = 16, NW = FN * 8;
   constexpr int LA = KS + 4, LP = NW + 4;  // padded smem strides (doubles)
   __shared__ __align__(16) double As[2][TM * LA];
@@ -1023,24 +1023,40 @@ __global__ void __launch_bounds__(128)
     for (int c = tid; c < TM * KS / 2; c += 128) {  // A: 64 rows x KS/2 double2
       const int r = c / (KS / 2), kk = (c % (KS / 2)) * 2;
       const int gr = r0 + r, gk = k0 + kk;
-      int bytes = 0;
-      const double* src = Ab;
-      if (gr < rows && gk < n) {
-        bytes = gk + 1 < n ? 16 : 8;
-        src = Ab + (long long)gr * ld + gk;
+      if (vec16) {
+        int bytes = 0;
+        const double* src = Ab;
+        if (gr < rows && gk < n) {
+          bytes = gk + 1 < n ? 16 : 8;
+          src = Ab + (long long)gr * ld + gk;
+        }
+        gbem_gemm::cp_async16(&As[buf][r * LA + kk], src, bytes);
+      } else {  // unaligned leading dimensions: element-wise 8-byte copies
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = gr < rows && gk + e < n;
+          gbem_gemm::cp_async8(&As[buf][r * LA + kk + e], ok ? Ab + (long long)gr * ld + gk + e : Ab, ok ? 8 : 0);
+        }
       }
-      gbem_gemm::cp_async16(&As[buf][r * LA + kk], src, bytes);
     }
     for (int c = tid; c < KS * NW / 2; c += 128) {  // P: KS rows x NW/2 double2
       const int kk = c / (NW / 2), q = (c % (NW / 2)) * 2;
       const int gk = k0 + kk;
-      int bytes = 0;
-      const double* src = P;
-      if (gk < n && q < ncols) {
-        bytes = q + 1 < ncols ? 16 : 8;
-        src = P + (long long)gk * ldp + q0 + q;
+      if (vec16) {
+        int bytes = 0;
+        const double* src = P;
+        if (gk < n && q < ncols) {
+          bytes = q + 1 < ncols ? 16 : 8;
+          src = P + (long long)gk * ldp + q0 + q;
+        }
+        gbem_gemm::cp_async16(&Ps[buf][kk * LP + q], src, bytes);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = gk < n && q + e < ncols;
+          gbem_gemm::cp_async8(&Ps[buf][kk * LP + q + e], ok ? P + (long long)gk * ldp + q0 + q + e : P, ok ? 8 : 0);
+        }
       }
-      gbem_gemm::cp_async16(&Ps[buf][kk * LP + q], src, bytes);
     }
   };
   double acc[2][FN][2];
@@ -1095,15 +1111,19 @@ int gbem_internal_rowblock_matvec(gbem_ctx* ctx, const double* Ab, int64_t ld, i
     return GBEM_OK;
   }
   // DMMA: up to 64 right-hand sides per pass (intensity K/4 flop/B: tensor-bound above K ~ 20)
+  const int vec16 = ((ld | ldp) % 2 == 0 && ((uintptr_t)Ab % 16) == 0 && ((uintptr_t)P % 16) == 0) ? 1 : 0;
   for (int q0 = 0; q0 < K; q0 += 64) {
     const int w = (int)std::min<int64_t>(64, K - q0);
     const unsigned grid = (unsigned)((rows + 63) / 64);
     if (w <= 16)
-      k_rowblock_mm<2><<<grid, 128, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P, ldp, (int)K, q0, Q, ldq);
+      k_rowblock_mm<2><<<grid, 128, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P, ldp, (int)K, q0, Q, ldq,
+                                                         vec16);
     else if (w <= 32)
-      k_rowblock_mm<4><<<grid, 128, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P, ldp, (int)K, q0, Q, ldq);
+      k_rowblock_mm<4><<<grid, 128, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P, ldp, (int)K, q0, Q, ldq,
+                                                         vec16);
     else
-      k_rowblock_mm<8><<<grid, 128, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P, ldp, (int)K, q0, Q, ldq);
+      k_rowblock_mm<8><<<grid, 128, 0, ctx->stream>>>(Ab, ld, (int)rows, (int)n, P, ldp, (int)K, q0, Q, ldq,
+                                                         vec16);
     GBEM_LAUNCH_CHECK(ctx);
   }
   return GBEM_OK;
