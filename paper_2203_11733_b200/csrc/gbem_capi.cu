@@ -140,6 +140,7 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   cudaFree(ctx->d_info);
   cudaFree(ctx->d_rhs);
   cudaFree(ctx->d_linv);
+  cudaFree(ctx->d_sw);
   if (ctx->h_stats) cudaFreeHost(ctx->h_stats);
   if (ctx->h_info) cudaFreeHost(ctx->h_info);
   for (auto& ev : ctx->ev)

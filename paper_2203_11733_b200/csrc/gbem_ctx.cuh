@@ -50,6 +50,8 @@ struct gbem_ctx {
   size_t work_cap = 0;  // elements
   int* d_info = nullptr;
   int* h_info = nullptr;  // pinned
+  double* d_sw = nullptr;  // blocked multi-RHS solve: W, Y, X (3 n R)
+  size_t sw_cap = 0;
   double* d_linv = nullptr;  // inverses of the 128 x 128 diagonal blocks of the factor
   size_t linv_cap = 0;
   double* d_rhs = nullptr;  // B and X of the K-RHS extraction (2 * rhs_cap)

@@ -350,4 +350,135 @@ __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// General dense DMMA GEMM on 64 x 64 tiles (2 x 2 warps of 32 x 32, 4 CTAs/SM,
+// double-buffered BK = 16 slabs), for the blocked multi-right-hand-side solves:
+//   C (M x N) op= A (M x K) * op(B),  A column-major (lda),
+//   BT = 0: op(B) = B^T with B N x K column-major (ldb)   ("NT")
+//   BT = 1: op(B) = B   with B K x N column-major (ldb)   ("NN")
+//   MODE kSub: C -= A op(B) (products summed, subtracted once); kStore: C = A op(B).
+// 16-byte cp.async when the leading dimensions and base pointers allow it
+// (vec16), else element-wise 8-byte copies.
+constexpr int kGT = 64;             // tile edge
+constexpr int kGThreads = 128;
+constexpr int kGLA = kGT + 8;       // A slab [BK][64 + 8]
+constexpr int kGLBt = kGT + 8;      // NT: B slab [BK][64 + 8]
+constexpr int kGLBn = BK + 4;       // NN: B slab [64][BK + 4] (k contiguous)
+constexpr size_t kGSmem = (size_t)2 * (BK * kGLA + (kGT * kGLBn > BK * kGLBt ? kGT * kGLBn : BK * kGLBt)) * sizeof(double);
+
+template <int MODE, int BT>
+__global__ void __launch_bounds__(kGThreads, 4)
+    k_gemm_g(double* __restrict__ C, long long ldc, const double* __restrict__ A, long long lda,
+             const double* __restrict__ B, long long ldb, int M, int N, int K, int vec16) {
+  constexpr int SA = BK * kGLA;
+  constexpr int SB = (kGT * kGLBn > BK * kGLBt ? kGT * kGLBn : BK * kGLBt);
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;           // [2][SA]
+  double* Bs = smem + 2 * SA;  // [2][SB]
+  const int m0 = blockIdx.x * kGT, n0 = blockIdx.y * kGT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int g = lane >> 2, t4 = lane & 3;
+  auto load = [&](int kt, int buf) {
+    const int k0 = kt * BK;
+    double* as = As + buf * SA;
+    double* bs = Bs + buf * SB;
+    for (int c = tid; c < BK * kGT / 2; c += kGThreads) {  // A: BK rows (k) x 64 (m)
+      const int kk = c / (kGT / 2), mm = (c % (kGT / 2)) * 2;
+      const int gk = k0 + kk, gm = m0 + mm;
+      if (vec16) {
+        const bool ok = gk < K && gm < M;
+        cp_async16(as + kk * kGLA + mm, ok ? A + (long long)gk * lda + gm : A, ok ? (gm + 1 < M ? 16 : 8) : 0);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const bool ok = gk < K && gm + e < M;
+          cp_async8(as + kk * kGLA + mm + e, ok ? A + (long long)gk * lda + gm + e : A, ok ? 8 : 0);
+        }
+      }
+    }
+    if (BT == 0) {
+      for (int c = tid; c < BK * kGT / 2; c += kGThreads) {  // B (N x K): BK rows (k) x 64 (n)
+        const int kk = c / (kGT / 2), nn = (c % (kGT / 2)) * 2;
+        const int gk = k0 + kk, gn = n0 + nn;
+        if (vec16) {
+          const bool ok = gk < K && gn < N;
+          cp_async16(bs + kk * kGLBt + nn, ok ? B + (long long)gk * ldb + gn : B, ok ? (gn + 1 < N ? 16 : 8) : 0);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool ok = gk < K && gn + e < N;
+            cp_async8(bs + kk * kGLBt + nn + e, ok ? B + (long long)gk * ldb + gn + e : B, ok ? 8 : 0);
+          }
+        }
+      }
+    } else {
+      for (int c = tid; c < kGT * BK / 2; c += kGThreads) {  // B (K x N): 64 rows (n) x BK (k)
+        const int nn = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+        const int gk = k0 + kk, gn = n0 + nn;
+        if (vec16) {
+          const bool ok = gn < N && gk < K;
+          cp_async16(bs + nn * kGLBn + kk, ok ? B + (long long)gn * ldb + gk : B, ok ? (gk + 1 < K ? 16 : 8) : 0);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const bool ok = gn < N && gk + e < K;
+            cp_async8(bs + nn * kGLBn + kk + e, ok ? B + (long long)gn * ldb + gk + e : B, ok ? 8 : 0);
+          }
+        }
+      }
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int KT = (K + BK - 1) / BK;
+  if (KT > 0) load(0, 0);
+  cp_async_commit();
+  for (int kt = 0; kt < KT; ++kt) {
+    if (kt + 1 < KT) load(kt + 1, (kt + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* as = As + (kt & 1) * SA + wm * 32 + g;
+    const double* bs = Bs + (kt & 1) * SB;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[(kk + t4) * kGLA + i * 8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        bf[j] = BT == 0 ? bs[(kk + t4) * kGLBt + wn * 32 + j * 8 + g] : bs[(wn * 32 + j * 8 + g) * kGLBn + kk + t4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + wm * 32 + i * 8 + g;
+    if (row >= M) continue;
+    double cur[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = n0 + wn * 32 + j * 8 + 2 * t4 + e;
+        cur[j][e] = (MODE == kSub && col < N) ? C[(long long)col * ldc + row] : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = n0 + wn * 32 + j * 8 + 2 * t4 + e;
+        if (col < N) C[(long long)col * ldc + row] = MODE == kSub ? cur[j][e] - acc[i][j][e] : acc[i][j][e];
+      }
+  }
+}
+
 }  // namespace gbem_gemm

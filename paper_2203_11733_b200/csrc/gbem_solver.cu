@@ -661,6 +661,105 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
   }
 }
 
+// Column-major (R x n, ld n: one right-hand side per column of the caller's
+// layout) <-> row-major (n x R: the R values of a panel contiguous).
+__global__ void k_rhs_transpose(const double* __restrict__ in, int n, int R, double* __restrict__ out, int to_rows) {
+  __shared__ double t[32][33];
+  const int i0 = blockIdx.x * 32, q0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    const int i = i0 + tx, q = q0 + k;  // read coalesced along i (column-major source)
+    if (to_rows) t[k][tx] = (i < n && q < R) ? in[(long long)q * n + i] : 0.0;
+    else {
+      const int ii = i0 + k, qq = q0 + tx;  // row-major source: coalesced along q
+      t[k][tx] = (ii < n && qq < R) ? in[(long long)ii * R + qq] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    if (to_rows) {
+      const int i = i0 + k, q = q0 + tx;
+      if (i < n && q < R) out[(long long)i * R + q] = t[tx][k];
+    } else {
+      const int q = q0 + k, i = i0 + tx;
+      if (i < n && q < R) out[(long long)q * n + i] = t[tx][k];
+    }
+  }
+}
+
+}  // namespace
+
+// Blocked forward/backward substitution on the FP64 tensor cores for wide
+// right-hand-side blocks (R >= 17): the right-hand sides in row-major n x R
+// form W, then per 128-block b
+//   forward   Y_b^T = W_b^T inv(L_bb)^T             (k_gemm_g<kStore, NT>)
+//             W_below^T -= Y_b^T L_below,b^T         (k_gemm_g<kSub, NT>)
+//   backward  X_b^T = Y_b^T inv(L_bb)                (k_gemm_g<kStore, NN>)
+//             Y_above^T -= X_b^T L_b,above           (k_gemm_g<kSub, NN>)
+// 2 n^2 R flops per solve on DMMA instead of the latency-bound cooperative
+// kernel (whose per-step cost grows with R).
+static int solve_blocked(gbem_ctx* ctx, const double* d_B, int R, double* d_X) {
+  const int n = (int)ctx->n;
+  const long long lda = ctx->lda;
+  cudaStream_t s = ctx->stream;
+  const size_t nr = (size_t)n * R;
+  if (ctx->sw_cap < 3 * nr) {
+    cudaFree(ctx->d_sw);
+    ctx->d_sw = nullptr;
+    ctx->sw_cap = 0;
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_sw, 3 * nr * sizeof(double)));
+    ctx->sw_cap = 3 * nr;
+  }
+  double* W = ctx->d_sw;
+  double* Y = W + nr;
+  double* X = Y + nr;
+  static bool attr = false;
+  if (!attr) {
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_g<kStore, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_g<kSub, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_g<kStore, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_g<kSub, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
+    attr = true;
+  }
+  const dim3 tb(32, 8), tg((n + 31) / 32, (R + 31) / 32);
+  k_rhs_transpose<<<tg, tb, 0, s>>>(d_B, n, R, W, 1);
+  GBEM_LAUNCH_CHECK(ctx);
+  const double* L = ctx->d_A;
+  const double* Linv = ctx->d_linv;
+  const int vec = (R % 2 == 0 && lda % 2 == 0) ? 1 : 0;
+  const int nblk = (n + NB - 1) / NB;
+  const unsigned gm = (unsigned)((R + kGT - 1) / kGT);
+  for (int b = 0; b < nblk; ++b) {
+    const int k0 = b * NB, kb = std::min(NB, n - k0), m = n - k0 - kb;
+    const double* Lbb = Linv + (size_t)b * NB * NB;
+    k_gemm_g<kStore, 0><<<dim3(gm, (kb + kGT - 1) / kGT), kGThreads, kGSmem, s>>>(
+        Y + (size_t)k0 * R, R, W + (size_t)k0 * R, R, Lbb, NB, R, kb, kb, vec);
+    GBEM_LAUNCH_CHECK(ctx);
+    if (m > 0) {
+      k_gemm_g<kSub, 0><<<dim3(gm, (m + kGT - 1) / kGT), kGThreads, kGSmem, s>>>(
+          W + (size_t)(k0 + kb) * R, R, Y + (size_t)k0 * R, R, L + (long long)k0 * lda + k0 + kb, lda, R, m, kb, vec);
+      GBEM_LAUNCH_CHECK(ctx);
+    }
+  }
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int k0 = b * NB, kb = std::min(NB, n - k0);
+    const double* Lbb = Linv + (size_t)b * NB * NB;
+    k_gemm_g<kStore, 1><<<dim3(gm, (kb + kGT - 1) / kGT), kGThreads, kGSmem, s>>>(
+        X + (size_t)k0 * R, R, Y + (size_t)k0 * R, R, Lbb, NB, R, kb, kb, vec);
+    GBEM_LAUNCH_CHECK(ctx);
+    if (k0 > 0) {
+      k_gemm_g<kSub, 1><<<dim3(gm, (k0 + kGT - 1) / kGT), kGThreads, kGSmem, s>>>(
+          Y, R, X + (size_t)k0 * R, R, L + k0, lda, R, k0, kb, vec);
+      GBEM_LAUNCH_CHECK(ctx);
+    }
+  }
+  k_rhs_transpose<<<tg, tb, 0, s>>>(X, n, R, d_X, 0);
+  GBEM_LAUNCH_CHECK(ctx);
+  return GBEM_OK;
+}
+
+namespace {
+
 int ensure_work(gbem_ctx* ctx, size_t elems) {
   if (ctx->work_cap >= elems && ctx->d_work) return GBEM_OK;
   if (ctx->d_work) cudaFree(ctx->d_work);
@@ -834,7 +933,11 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
   double* scratch = Ysym + (size_t)n * R;
   const double* Linv = ctx->d_linv;
   cudaEventRecord(ctx->ev[1], s);
-  {
+  static const int blocked_min = getenv("GBEM_SOLVE_BLOCKED_MIN") ? atoi(getenv("GBEM_SOLVE_BLOCKED_MIN")) : 17;
+  if (R >= blocked_min) {
+    rc = solve_blocked(ctx, d_B, R, d_X);
+    if (rc) return rc;
+  } else {
     const double* cA = ctx->d_A;
     const double* cL = Linv;
     int nn = n;
