@@ -495,7 +495,7 @@ __device__ __forceinline__ double warp_reduce_d(double x) {
 // unrolling follow the orders, so the common small-order pairs run fully
 // unrolled at high occupancy.
 template <int QV, int QU>
-__global__ void __launch_bounds__(256, QV <= 4 ? 3 : 2)
+__global__ void __launch_bounds__(256, 2)
     k_far(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
           const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats) {
   const uint32_t begin = offsets[far_key_first(QV, QU > 0 ? QU : 1)];
@@ -715,8 +715,8 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
   GBEM_LAUNCH_CHECK(ctx);
   GBEM_FAR(1, 1, 1)
   GBEM_FAR(2, 1, 1) GBEM_FAR(2, 2, 1)
-  GBEM_FAR(3, 1, 2) GBEM_FAR(3, 2, 2) GBEM_FAR(3, 3, 3)
-  GBEM_FAR(4, 1, 2) GBEM_FAR(4, 2, 3) GBEM_FAR(4, 3, 3) GBEM_FAR(4, 4, 3)
+  GBEM_FAR(3, 1, 2) GBEM_FAR(3, 2, 2) GBEM_FAR(3, 3, 2)
+  GBEM_FAR(4, 1, 2) GBEM_FAR(4, 2, 2) GBEM_FAR(4, 3, 2) GBEM_FAR(4, 4, 2)
   GBEM_FAR(5, 0, 2) GBEM_FAR(6, 0, 2) GBEM_FAR(7, 0, 2) GBEM_FAR(8, 0, 2)
 #undef GBEM_FAR
   cudaEventRecord(ctx->ev[3], ctx->stream);
