@@ -832,7 +832,8 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     GBEM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_panel, cudaEventDisableTiming));
     GBEM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_col, cudaEventDisableTiming));
   }
-  cudaStream_t s1 = ctx->side_stream;
+  cudaStream_t s_side = ctx->side_stream;
+  static const int tail_rows = getenv("GBEM_FACTOR_TAIL") ? atoi(getenv("GBEM_FACTOR_TAIL")) : 1024;
   GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_col, s));
   // GBEM_FACTOR_PROFILE=1: per-block side-stream (diagonal factor + panel trsm)
   // and main-stream timings on stderr (diagnostics only)
@@ -847,7 +848,11 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     int m = n - k0 - kb;
     double* Akk = ctx->d_A + (long long)k0 * lda + k0;
     double* A21 = Akk + kb;  // rows k0+kb.., cols k0..
-    GBEM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ev_col, 0));
+    // tail: once the trailing matrix is small the look-ahead has nothing to
+    // overlap, and the cross-stream event hops only add latency to the chain
+    const bool tail = n - k0 < tail_rows;
+    cudaStream_t s1 = tail ? s : s_side;
+    if (!tail) GBEM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ev_col, 0));
     if (prof) cudaEventRecord(pe[4 * b], s1);
     k_potrf_diag<<<1, kPotrfThreads, kPotrfSmem, s1>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
     GBEM_LAUNCH_CHECK(ctx);
@@ -858,8 +863,10 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       GBEM_LAUNCH_CHECK(ctx);
     }
     if (prof) cudaEventRecord(pe[4 * b + 1], s1);
-    GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_panel, s1));
-    GBEM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_panel, 0));
+    if (!tail) {
+      GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_panel, s1));
+      GBEM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_panel, 0));
+    }
     if (prof) cudaEventRecord(pe[4 * b + 2], s);
     if (m <= 0) break;
     // A22 -= L21 L21^T on 64 x 64 lower tiles: first the next block column
