@@ -84,6 +84,23 @@ typedef struct {
   double ms_factor, ms_solve, ms_residual;
 } gbem_solve_stats;
 
+/* Block (mixed-unknown) system panels (Panel, partition.hpp:34-46), class-
+ * contiguous [conductor, dirichlet outer, neumann outer, interface]; host arrays. */
+typedef struct {
+  gbem_panels geom;
+  const int8_t* nsign;   /* Rect::normalSign, +1 / -1 */
+  const int32_t* kind;   /* 0 conductor, 1 dirichlet outer, 2 neumann outer, 3 interface */
+  const int32_t* net;    /* net id (conductor panels) */
+  const int32_t* reg_a;  /* regionA */
+  const int32_t* reg_b;  /* regionB (interface panels) */
+} gbem_block_panels;
+
+/* DielectricRegion id and relative permittivity. */
+typedef struct {
+  int32_t id;
+  double eps;
+} gbem_region;
+
 /* Context on CUDA device `device` (one process per GPU; ranks pick their own). */
 int gbem_ctx_create(int device, gbem_ctx** out);
 void gbem_ctx_destroy(gbem_ctx* ctx);
@@ -146,6 +163,27 @@ int gbem_rowblock_matvec_dev(gbem_ctx* ctx, const double* Ablk, int64_t ld, int6
 int gbem_spd_factor_dev(gbem_ctx* ctx, const double* M, int64_t m, int64_t ldm, gbem_solve_stats* stats);
 int gbem_spd_solve_factored_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
                                 gbem_solve_stats* stats);
+
+/* assemble_collocation (assembly.hpp:179-227): the point-collocation block
+ * system of the scene for main net `main_net` (rows per region and boundary
+ * panel, unknown map of assembly.hpp:51-75, closed-form u/q point kernels
+ * kernels.hpp:319-355).  The m x m matrix stays in the context (gbem_lu_solve);
+ * A_host (row-major, lda >= m) and b_host (m) receive copies when non-NULL.
+ * *m_out = m.  GBEM_EINVAL for an unconstrained scene ("no Dirichlet
+ * constraint anywhere in the scene (singular problem)"). */
+int gbem_assemble_collocation(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n,
+                              const gbem_region* regions, int32_t nregions, int32_t main_net,
+                              double* A_host, int64_t lda, double* b_host, int64_t* m_out);
+/* lu_solve (solver.hpp:53-88) of the context matrix: LU with partial pivoting
+ * (whole rows swapped), right-hand side b_host (m; NULL: the b of the last
+ * gbem_assemble_collocation), solution x_host, relative residual
+ * ||A x - b|| / ||b|| recomputed from the unfactored matrix.  A pivot below
+ * 1e-14 max|A| -> GBEM_ENUMERIC "matrix numerically singular (smallest pivot
+ * at row k)". */
+int gbem_lu_solve(gbem_ctx* ctx, const double* b_host, double* x_host, double* resid, gbem_solve_stats* stats);
+/* Upload a general (non-symmetric) matrix, row-major host with lda >= n, for
+ * gbem_lu_solve. */
+int gbem_matrix_upload_general(gbem_ctx* ctx, const double* A_host, int64_t n, int64_t lda);
 
 /* Copy the assembled (or factored) matrix to the host: row-major, lda >= n. */
 int gbem_matrix_download(gbem_ctx* ctx, double* A_host, int64_t lda);

@@ -26,6 +26,8 @@ int gbem_model_config(int config, uint64_t seed, double scale, gbem_model** out,
 void gbem_model_free(gbem_model* m);
 /* dump_model (model_io.hpp:207-228); returns the text length (copies when cap suffices). */
 int64_t gbem_model_dump(const gbem_model* m, char* buf, int64_t cap);
+/* Dielectric regions (ascending id) with their relative permittivity; returns the count. */
+int gbem_model_regions(const gbem_model* m, int32_t* ids, double* eps, int cap);
 /* Net ids ascending; returns the count. */
 int gbem_model_nets(const gbem_model* m, int32_t* ids, int cap);
 int gbem_model_info(const gbem_model* m, int32_t* nregions, int32_t* nfaces, double* eps_r, int32_t* freespace);
@@ -57,6 +59,7 @@ typedef struct {
   const char* dump_matrix; /* NULL or path prefix */
   double* cap_out;         /* NULL or rows x nets, full precision (farads), rows in solve order */
   double* outer_out;       /* NULL or per-row induced charge on the outer boundary */
+  int32_t collocation;     /* 1: the collocation baseline (--baseline collocation, cli.hpp:37-38) */
 } gbem_extract_opts;
 
 int gbem_model_extract(const gbem_model* m, const gbem_extract_opts* o, char* csv, int64_t csv_cap,

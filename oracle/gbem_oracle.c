@@ -768,6 +768,208 @@ int orc_cholesky_solve(int64_t n, const double* A, int64_t nrhs, const double* B
   return 0;
 }
 
+/* ---------------- point kernels (kernels.hpp:319-355) ---------------- */
+
+static void inplane_axes(int axis, int* i0, int* i1) {
+  *i0 = axis == 0 ? 1 : 0;
+  *i1 = axis == 2 ? 1 : 2;
+}
+
+static double pt_F(double u, double v, double h, double h2, double guard) {
+  double t = mul_log(v, u, v * v + h2, guard) + mul_log(u, v, u * u + h2, guard);
+  if (h != 0.0) {
+    double r = sqrt(u * u + v * v + h2);
+    t -= h * atan(u * v / (h * r));
+  }
+  return t;
+}
+
+double orc_u_point_rect(const double x[3], const orc_rect* R) {
+  int i0, i1;
+  inplane_axes(R->axis, &i0, &i1);
+  double h = x[R->axis] - R->level;
+  double u1 = R->a0 - x[i0], u2 = R->a1 - x[i0];
+  double v1 = R->b0 - x[i1], v2 = R->b1 - x[i1];
+  double scale = fmax(fmax(fmax(fabs(u1), fabs(u2)), fmax(fabs(v1), fabs(v2))), fmax(fabs(h), 1e-30));
+  double guard = 1e-14 * scale, h2 = h * h;
+  return (pt_F(u2, v2, h, h2, guard) - pt_F(u1, v2, h, h2, guard) - pt_F(u2, v1, h, h2, guard) +
+          pt_F(u1, v1, h, h2, guard)) /
+         kFourPi;
+}
+
+static double pt_G(double u, double v, double h, double h2) {
+  double r = sqrt(u * u + v * v + h2);
+  return atan(u * v / (h * r));
+}
+
+double orc_q_point_rect(const double x[3], const orc_rect* R, int nsign) {
+  double h = x[R->axis] - R->level;
+  if (h == 0.0) return 0.0;
+  int i0, i1;
+  inplane_axes(R->axis, &i0, &i1);
+  double u1 = R->a0 - x[i0], u2 = R->a1 - x[i0];
+  double v1 = R->b0 - x[i1], v2 = R->b1 - x[i1];
+  double h2 = h * h;
+  double sum = pt_G(u2, v2, h, h2) - pt_G(u1, v2, h, h2) - pt_G(u2, v1, h, h2) + pt_G(u1, v1, h, h2);
+  return (double)nsign * sum / kFourPi;
+}
+
+/* ---------------- collocation block system (assembly.hpp:37-75,179-227) ---------------- */
+
+int orc_assemble_collocation(int64_t n, const orc_rect* p, const int* nsign, const int* kind, const int* net,
+                             const int* reg_a, const int* reg_b, int nreg, const int* reg_id,
+                             const double* reg_eps, int main_net, double* A, double* b, int64_t* m_out) {
+  int64_t off[5] = {0, 0, 0, 0, 0};
+  for (int64_t k = 0; k < n; ++k) off[kind[k] + 1]++;
+  for (int k = 1; k < 5; ++k) off[k] += off[k - 1];
+  if (off[2] == 0) return 1; /* no conductor / Dirichlet panel */
+  int64_t o3 = off[3];
+  int64_t* qcol = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t* ucol = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  for (int64_t q = 0; q < n; ++q) { /* buildUnknownMap */
+    qcol[q] = ucol[q] = -1;
+    if (kind[q] == 0 || kind[q] == 1) qcol[q] = q;
+    else if (kind[q] == 2) ucol[q] = q;
+    else {
+      ucol[q] = o3 + 2 * (q - o3);
+      qcol[q] = o3 + 2 * (q - o3) + 1;
+    }
+  }
+  int64_t cols = o3 + 2 * (off[4] - o3);
+  /* regions in ascending id (std::map order) */
+  int* order = (int*)malloc(sizeof(int) * (size_t)nreg);
+  for (int k = 0; k < nreg; ++k) order[k] = k;
+  for (int a = 0; a < nreg; ++a)
+    for (int c = a + 1; c < nreg; ++c)
+      if (reg_id[order[c]] < reg_id[order[a]]) {
+        int t = order[a];
+        order[a] = order[c];
+        order[c] = t;
+      }
+  for (int64_t q = 0; q < n; ++q) {
+    int found = 0;
+    for (int k = 0; k < nreg; ++k) found |= reg_a[q] == reg_id[k];
+    if (!found) {
+      free(qcol); free(ucol); free(order);
+      return 1;
+    }
+  }
+  /* rows: per region (ascending), panels with regionA == id or interface with regionB == id */
+  int64_t rows = 0;
+  for (int k = 0; k < nreg; ++k) {
+    int rid = reg_id[order[k]];
+    for (int64_t q = 0; q < n; ++q)
+      if (reg_a[q] == rid || (kind[q] == 3 && reg_b[q] == rid)) rows++;
+  }
+  if (rows != cols) {
+    free(qcol); free(ucol); free(order);
+    return 2;
+  }
+  int64_t m = rows;
+  for (int64_t i = 0; i < m * m; ++i) A[i] = 0.0;
+  for (int64_t i = 0; i < m; ++i) b[i] = 0.0;
+  int64_t row = 0;
+  for (int k = 0; k < nreg; ++k) {
+    int rid = reg_id[order[k]];
+    double eps_r = reg_eps[order[k]];
+    for (int64_t a = 0; a < n; ++a) {
+      if (!(reg_a[a] == rid || (kind[a] == 3 && reg_b[a] == rid))) continue;
+      double x[3];
+      for (int d = 0; d < 3; ++d) {
+        span_t e = rect_extent(&p[a], d);
+        x[d] = 0.5 * (e.lo + e.hi); /* Rect::center */
+      }
+      for (int64_t c = 0; c < n; ++c) {
+        if (!(reg_a[c] == rid || (kind[c] == 3 && reg_b[c] == rid))) continue;
+        double side = kind[c] == 3 ? (reg_a[c] == rid ? 1.0 : -1.0) : -1.0; /* sideSign */
+        double coefU = orc_q_point_rect(x, &p[c], nsign[c]) * side + (a == c ? 0.5 : 0.0);
+        double known = (kind[c] == 0 && net[c] == main_net) ? 1.0 : 0.0; /* knownPotential */
+        if (ucol[c] >= 0)
+          A[row * m + ucol[c]] += coefU;
+        else
+          b[row] -= coefU * known;
+        if (kind[c] == 2) continue;
+        double area = (p[c].a1 - p[c].a0) * (p[c].b1 - p[c].b0);
+        double coefX = -orc_u_point_rect(x, &p[c]) / area;
+        if (kind[c] == 3 && reg_b[c] == rid) {
+          double eps_a = 1.0;
+          for (int t = 0; t < nreg; ++t)
+            if (reg_id[t] == reg_a[c]) eps_a = reg_eps[t];
+          coefX *= -(eps_a / eps_r);
+        }
+        A[row * m + qcol[c]] += coefX;
+      }
+      row++;
+    }
+  }
+  free(qcol);
+  free(ucol);
+  free(order);
+  if (m_out) *m_out = m;
+  return 0;
+}
+
+/* ---------------- LU with partial pivoting (solver.hpp:53-88) ---------------- */
+
+int orc_lu_solve(int64_t n, const double* A0, const double* b0, double* x, double* resid, int64_t* bad_row) {
+  double* A = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n * n : 1));
+  double* b = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  memcpy(A, A0, sizeof(double) * (size_t)(n * n));
+  memcpy(b, b0, sizeof(double) * (size_t)n);
+  double scale = 0.0;
+  for (int64_t i = 0; i < n * n; ++i) scale = fmax(scale, fabs(A[i]));
+  for (int64_t k = 0; k < n; ++k) {
+    int64_t pr = k; /* first maximum, as Eigen's maxCoeff */
+    double best = fabs(A[k * n + k]);
+    for (int64_t r = k + 1; r < n; ++r)
+      if (fabs(A[r * n + k]) > best) {
+        best = fabs(A[r * n + k]);
+        pr = r;
+      }
+    if (pr != k) {
+      for (int64_t c = 0; c < n; ++c) {
+        double t = A[k * n + c];
+        A[k * n + c] = A[pr * n + c];
+        A[pr * n + c] = t;
+      }
+      double t = b[k];
+      b[k] = b[pr];
+      b[pr] = t;
+    }
+    if (fabs(A[k * n + k]) < 1e-14 * scale) {
+      if (bad_row) *bad_row = k;
+      free(A);
+      free(b);
+      return 2;
+    }
+    for (int64_t r = k + 1; r < n; ++r) {
+      double f = A[r * n + k] / A[k * n + k];
+      if (f == 0.0) continue;
+      for (int64_t c = k + 1; c < n; ++c) A[r * n + c] -= f * A[k * n + c];
+      b[r] -= f * b[k];
+    }
+  }
+  for (int64_t i = n - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int64_t t = i + 1; t < n; ++t) s += A[i * n + t] * x[t];
+    x[i] = (b[i] - s) / A[i * n + i];
+  }
+  if (resid) {
+    double rn = 0.0, bn = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+      double s = 0.0;
+      for (int64_t t = 0; t < n; ++t) s += A0[i * n + t] * x[t];
+      rn += (s - b0[i]) * (s - b0[i]);
+      bn += b0[i] * b0[i];
+    }
+    bn = sqrt(bn);
+    *resid = sqrt(rn) / (bn > 0.0 ? bn : 1.0);
+  }
+  free(A);
+  free(b);
+  return 0;
+}
+
 /* ---------------- quadrature known-answer hooks ---------------- */
 
 static double qt_f(const void* vc, double x) {

@@ -71,6 +71,27 @@ int orc_assemble_single(int64_t n, const orc_rect* p, double rel_tol, int max_le
 int orc_cholesky_solve(int64_t n, const double* A, int64_t nrhs, const double* B, double* X,
                        double* resid, int64_t* bad_pivot);
 
+/* u_point_rect / q_point_rect (kernels.hpp:319-355): closed-form single- and
+ * double-layer potentials of a unit density on R at the point x; nsign is
+ * R.normalSign. */
+double orc_u_point_rect(const double x[3], const orc_rect* R);
+double orc_q_point_rect(const double x[3], const orc_rect* R, int nsign);
+
+/* assemble_collocation (assembly.hpp:179-227) on flat class-contiguous panel
+ * arrays (kind 0 conductor, 1 dirichlet outer, 2 neumann outer, 3 interface),
+ * regions (id, eps) in any order.  A is m x m row-major (m = *m_out, caller
+ * buffer of at least (panels + interfaces)^2), b has m entries.  Returns 0, 1
+ * for invalid input (no Dirichlet constraint / unknown region), 2 for a
+ * non-square system. */
+int orc_assemble_collocation(int64_t n, const orc_rect* p, const int* nsign, const int* kind, const int* net,
+                             const int* reg_a, const int* reg_b, int nreg, const int* reg_id,
+                             const double* reg_eps, int main_net, double* A, double* b, int64_t* m_out);
+
+/* lu_solve (solver.hpp:53-88): partial pivoting with whole-row swaps on a
+ * row-major copy of A (n x n).  Returns 0, or 2 with *bad_row = k for "matrix
+ * numerically singular (smallest pivot at row k)".  *resid = ||A x - b|| / ||b||. */
+int orc_lu_solve(int64_t n, const double* A, const double* b, double* x, double* resid, int64_t* bad_row);
+
 /* Romberg / integrateSegment on test integrands (quadrature.hpp:27-113), for the
  * known-answer cases of test_quadrature.cpp. which: 0 x^2, 1 const 1, 2 log1p,
  * 3 x (empty interval), 4 sin, 5 1/x, 6 1/sqrt(x), 7 log x, 8 1/sqrt(1-x),

@@ -36,6 +36,17 @@ gbem::Rect toRect(const orc_rect& r) {
 
 extern "C" {
 
+// gbem::u_point_rect / q_point_rect (kernels.hpp:319-355).
+double ref_u_point_rect(const double x[3], const orc_rect* r) {
+  return gbem::u_point_rect(gbem::Vec3{x[0], x[1], x[2]}, toRect(*r));
+}
+double ref_q_point_rect(const double x[3], const orc_rect* r, int nsign) {
+  gbem::Rect R = toRect(*r);
+  R.normalSign = nsign;
+  return gbem::q_point_rect(gbem::Vec3{x[0], x[1], x[2]}, R);
+}
+
+
 // gbem::u_pair_integral (kernels.hpp:270) with a QuadratureConfig.
 orc_kv ref_u_pair_integral(const orc_rect* a, const orc_rect* b, double rel_tol,
                            int max_levels) {

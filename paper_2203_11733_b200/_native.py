@@ -39,6 +39,15 @@ class GbemAssemblyStats(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class GbemBlockPanels(C.Structure):
+    _fields_ = [("geom", GbemPanels), ("nsign", C.c_void_p), ("kind", C.c_void_p), ("net", C.c_void_p),
+                ("reg_a", C.c_void_p), ("reg_b", C.c_void_p)]
+
+
+class GbemRegion(C.Structure):
+    _fields_ = [("id", C.c_int32), ("eps", C.c_double)]
+
+
 class GbemSolveStats(C.Structure):
     _fields_ = [("n", C.c_int64), ("nrhs", C.c_int64), ("bad_pivot", C.c_int64),
                 ("max_residual", C.c_double), ("ms_factor", C.c_double),
@@ -72,6 +81,10 @@ GPU_SYMBOLS = [
                                            C.c_int64]),
     ("gbem_spd_factor_dev", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.POINTER(GbemSolveStats)]),
     ("gbem_spd_solve_factored_dev", C.c_int, [_P, _P, C.c_int64, _P, _P, C.POINTER(GbemSolveStats)]),
+    ("gbem_assemble_collocation", C.c_int, [_P, C.POINTER(GbemBlockPanels), C.c_int64, C.POINTER(GbemRegion),
+                                            C.c_int32, C.c_int32, _P, C.c_int64, _P, C.POINTER(C.c_int64)]),
+    ("gbem_lu_solve", C.c_int, [_P, _P, _P, _P, C.POINTER(GbemSolveStats)]),
+    ("gbem_matrix_upload_general", C.c_int, [_P, _P, C.c_int64, C.c_int64]),
     ("gbem_matrix_download", C.c_int, [_P, _P, C.c_int64]),
     ("gbem_matrix_upload", C.c_int, [_P, _P, C.c_int64, C.c_int64]),
     ("gbem_matrix_device", C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
@@ -228,6 +241,43 @@ class Context:
         A = np.empty((n, n))
         self.check(self.lib.gbem_matrix_download(self.h, ptr(A), n))
         return A
+
+    def lu_solve(self, A: np.ndarray, b: np.ndarray):
+        """lu_solve (solver.hpp:53-88) of a general matrix: (x, residual, stats)."""
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        n = len(b)
+        self.check(self.lib.gbem_matrix_upload_general(self.h, ptr(A), n, A.shape[1]))
+        x = np.zeros(n)
+        res = np.zeros(1)
+        st = GbemSolveStats()
+        self.check(self.lib.gbem_lu_solve(self.h, ptr(b), ptr(x), ptr(res), C.byref(st)))
+        return x, float(res[0]), st
+
+    def assemble_collocation(self, ps, regions, main_net: int, solve: bool = False):
+        """assemble_collocation (assembly.hpp:179-227) for an api.PanelSet and
+        regions [(id, eps), ...]: (A (m, m) row-major, b (m,)) and, with solve,
+        also the lu_solve solution and residual."""
+        P = PanelArrays(ps.axis, ps.level, ps.a0, ps.a1, ps.b0, ps.b1)
+        keep = [np.ascontiguousarray(ps.nsign, dtype=np.int8)] + [
+            np.ascontiguousarray(v, dtype=np.int32) for v in (ps.kind, ps.net, ps.regA, ps.regB)]
+        bp = GbemBlockPanels(P.struct(), *[ptr(v) for v in keep])
+        regs = (GbemRegion * len(regions))(*[GbemRegion(int(i), float(e)) for i, e in regions])
+        m = C.c_int64(0)
+        self.check(self.lib.gbem_assemble_collocation(self.h, C.byref(bp), P.n, regs, len(regions), int(main_net),
+                                                      None, 0, None, C.byref(m)))
+        mm = m.value
+        A = np.zeros((mm, mm))
+        b = np.zeros(mm)
+        self.check(self.lib.gbem_assemble_collocation(self.h, C.byref(bp), P.n, regs, len(regions), int(main_net),
+                                                      ptr(A), mm, ptr(b), C.byref(m)))
+        if not solve:
+            return A, b
+        x = np.zeros(mm)
+        res = np.zeros(1)
+        st = GbemSolveStats()
+        self.check(self.lib.gbem_lu_solve(self.h, None, ptr(x), ptr(res), C.byref(st)))
+        return A, b, x, float(res[0])
 
     def spd_solve(self, B: np.ndarray):
         """B: (n,) or (n, k) right-hand sides; returns X like B, residuals (k,), stats."""

@@ -179,6 +179,7 @@ def host_lib() -> C.CDLL:
             "gbem_model_free": (None, [P]),
             "gbem_model_dump": (C.c_int64, [P, C.c_char_p, C.c_int64]),
             "gbem_model_nets": (C.c_int, [P, P, C.c_int]),
+            "gbem_model_regions": (C.c_int, [P, P, P, C.c_int]),
             "gbem_model_info": (C.c_int, [P, P, P, P, P]),
             "gbem_model_params": (C.c_int, [P, P]),
             "gbem_model_set_params": (C.c_int, [P, P, C.c_char_p, C.c_int]),
@@ -196,6 +197,7 @@ def host_lib() -> C.CDLL:
 
 
 HOST_SYMBOLS = ["gbem_model_parse", "gbem_model_config", "gbem_model_free", "gbem_model_dump", "gbem_model_nets",
+                "gbem_model_regions",
                 "gbem_model_info", "gbem_model_params", "gbem_model_set_params", "gbem_model_partition",
                 "gbem_model_panels", "gbem_model_extract"]
 
@@ -203,7 +205,7 @@ HOST_SYMBOLS = ["gbem_model_parse", "gbem_model_config", "gbem_model_free", "gbe
 class ExtractOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("mode", C.c_int32), ("net", C.c_int32), ("rel_tol", C.c_double),
                 ("max_levels", C.c_int32), ("dump_matrix", C.c_char_p), ("cap_out", C.c_void_p),
-                ("outer_out", C.c_void_p)]
+                ("outer_out", C.c_void_p), ("collocation", C.c_int32)]
 
 
 @dataclass
@@ -265,6 +267,15 @@ class Model:
         self.L.gbem_model_nets(self.h, ids.ctypes.data, k)
         return [int(v) for v in ids[:k]]
 
+    @property
+    def regions(self) -> list[tuple[int, float]]:
+        """[(region id, relative permittivity)], ascending id."""
+        k = self.L.gbem_model_regions(self.h, None, None, 0)
+        ids = np.zeros(max(k, 1), dtype=np.int32)
+        eps = np.zeros(max(k, 1))
+        self.L.gbem_model_regions(self.h, ids.ctypes.data, eps.ctypes.data, k)
+        return [(int(ids[i]), float(eps[i])) for i in range(k)]
+
     def info(self) -> dict:
         nr, nf, fs = C.c_int32(), C.c_int32(), C.c_int32()
         eps = C.c_double()
@@ -303,15 +314,17 @@ class Model:
         return PanelSet(**arrs, main_net=main_net)
 
     def extract(self, net: int = -1, mode: int = 0, device: int = 0, dump_matrix: str | None = None,
-                rel_tol: float = 1e-8, max_levels: int = 16) -> tuple[str, dict]:
+                rel_tol: float = 1e-8, max_levels: int = 16, baseline: str | None = None) -> tuple[str, dict]:
         """Run capacitance_matrix (net=-1) or capacitance_row; returns (csv, json dict).
         Full-precision values are left in self.last_cap (rows x nets) / self.last_outer."""
         ids = self.net_ids
         rows = 1 if net >= 0 else len(ids)
         self.last_cap = np.zeros((rows, len(ids)))
         self.last_outer = np.zeros(rows)
+        if baseline not in (None, "collocation"):
+            raise ValidationError("baseline must be 'collocation'")
         o = ExtractOpts(device, mode, net, rel_tol, max_levels, dump_matrix.encode() if dump_matrix else None,
-                        self.last_cap.ctypes.data, self.last_outer.ctypes.data)
+                        self.last_cap.ctypes.data, self.last_outer.ctypes.data, 1 if baseline else 0)
         cap = 1 << 20
         csv, js = C.create_string_buffer(cap), C.create_string_buffer(cap)
         cl, jl = C.c_int64(), C.c_int64()

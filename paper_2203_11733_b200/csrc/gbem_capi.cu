@@ -308,6 +308,71 @@ int gbem_spd_solve_factored_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, do
   return gbem_internal_solve_factored(ctx, B, nrhs, X, resid, stats);
 }
 
+int gbem_assemble_collocation(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n, const gbem_region* regions,
+                              int32_t nregions, int32_t main_net, double* A_host, int64_t lda, double* b_host,
+                              int64_t* m_out) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int64_t m = 0;
+  int rc = gbem_internal_assemble_collocation(ctx, P, n, regions, nregions, main_net, &m);
+  if (rc) return rc;
+  ctx->block_m = m;
+  if (m_out) *m_out = m;
+  if (A_host) {  // row-major copy of the column-major device matrix
+    if (lda < m) return ctx->fail(GBEM_EINVAL, "lda < m");
+    std::vector<double> t((size_t)ctx->lda * m);
+    GBEM_CUDA(ctx, cudaMemcpy(t.data(), ctx->d_A, sizeof(double) * t.size(), cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < m; ++r)
+      for (int64_t c = 0; c < m; ++c) A_host[r * lda + c] = t[(size_t)c * ctx->lda + r];
+  }
+  if (b_host) GBEM_CUDA(ctx, cudaMemcpy(b_host, ctx->d_rhs, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  return GBEM_OK;
+}
+
+int gbem_matrix_upload_general(gbem_ctx* ctx, const double* A_host, int64_t n, int64_t lda) {
+  if (!ctx || (!A_host && n > 0)) return GBEM_EINVAL;
+  if (n < 0 || lda < n) return ctx->fail(GBEM_EINVAL, "bad matrix dimensions");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int rc = ensure_matrix(ctx, n);
+  if (rc) return rc;
+  if (n == 0) return GBEM_OK;
+  std::vector<double> t((size_t)n * ctx->lda, 0.0);  // column-major image of the row-major input
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t c = 0; c < n; ++c) t[(size_t)c * ctx->lda + r] = A_host[r * lda + c];
+  GBEM_CUDA(ctx, cudaMemcpy(ctx->d_A, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice));
+  ctx->block_m = -1;
+  return GBEM_OK;
+}
+
+int gbem_lu_solve(gbem_ctx* ctx, const double* b_host, double* x_host, double* resid, gbem_solve_stats* stats) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int64_t m = ctx->n;
+  if (ctx->factored) return ctx->fail(GBEM_EINVAL, "matrix already factored; re-assemble or re-upload");
+  if (!b_host && ctx->block_m != m) return ctx->fail(GBEM_EINVAL, "no assembled right-hand side; pass b");
+  if (m > 0 && !x_host) return ctx->fail(GBEM_EINVAL, "null solution buffer");
+  if (ctx->rhs_cap < (size_t)m || !ctx->d_rhs) {
+    cudaFree(ctx->d_rhs);
+    ctx->d_rhs = nullptr;
+    ctx->rhs_cap = 0;
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_rhs, 2 * (size_t)(m > 0 ? m : 1) * sizeof(double)));
+    ctx->rhs_cap = m;
+  }
+  double* d_b = ctx->d_rhs;
+  double* d_x = ctx->d_rhs + m;
+  if (b_host) GBEM_CUDA(ctx, cudaMemcpy(d_b, b_host, sizeof(double) * m, cudaMemcpyHostToDevice));
+  double* d_r = nullptr;
+  GBEM_CUDA(ctx, cudaMalloc(&d_r, sizeof(double)));
+  int rc = gbem_internal_lu_solve(ctx, d_b, d_x, d_r, stats);
+  ctx->block_m = -1;
+  if (rc == GBEM_OK) {
+    if (m > 0) GBEM_CUDA(ctx, cudaMemcpy(x_host, d_x, sizeof(double) * m, cudaMemcpyDeviceToHost));
+    if (resid) GBEM_CUDA(ctx, cudaMemcpy(resid, d_r, sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  cudaFree(d_r);
+  return rc;
+}
+
 int gbem_matrix_download(gbem_ctx* ctx, double* A_host, int64_t lda) {
   if (!ctx || !A_host) return GBEM_EINVAL;
   if (lda < ctx->n) return ctx->fail(GBEM_EINVAL, "lda < n");

@@ -30,6 +30,7 @@ struct gbem_ctx {
   double* d_diag = nullptr;  // original diagonal (kept for residuals after factoring)
   int64_t diag_cap = 0;
   bool factored = false;
+  int64_t block_m = -1;  // size of the assembled block system whose b sits in d_rhs (-1: none)
   // stream-ordered mode (gbem_ctx_set_async): the factorisation's pivot check is
   // read back at gbem_ctx_sync instead of blocking inside the call
   bool async = false;
@@ -85,6 +86,9 @@ struct gbem_ctx {
 
 // Internal entry points implemented across the units.
 int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n);
+int gbem_internal_assemble_collocation(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n,
+                                       const gbem_region* regions, int32_t nreg, int32_t main_net, int64_t* m_out);
+int gbem_internal_lu_solve(gbem_ctx* ctx, double* d_b, double* d_x, double* d_resid, gbem_solve_stats* stats);
 int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, bool device_ptrs);
 int gbem_internal_check_pending_stats(gbem_ctx* ctx);
 int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,

@@ -415,12 +415,17 @@ constexpr int kSolveR = 16;
 constexpr int kSolvePF = 3;                      // register-prefetched strips per CTA and step
 constexpr int kSolveCols = NB / kSolveWarps;     // forward: block columns per warp (16)
 static_assert(kSolveCols == 16 && NB / 32 == 4, "strip tiling assumes NB = 128, 8 warps");
+// The diagonal-block inverse sits in shared memory with column stride NB + 2
+// (16-byte aligned columns; column reads (forward) and row reads (backward,
+// the transposed product) are both at most 2-way bank conflicted).
+constexpr int kLsLd = NB + 2;
 constexpr size_t kSolveSmem =
-    (size_t)(NB * NB + 3 * kSolveR * NB + kSolveWarps * kSolveR * 32 + kSolvePF * kSolveR * 32) * sizeof(double);
+    (size_t)(NB * kLsLd + 3 * kSolveR * NB + kSolveWarps * kSolveR * 32 + kSolvePF * kSolveR * 32) * sizeof(double);
 
 __device__ __forceinline__ void solve_prefetch_block(double* Ls, const double* Li, int tid) {
   for (int c = tid; c < NB * NB / 2; c += kSolveThreads) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(Ls + 2 * c);
+    const int col = (2 * c) / NB, row = (2 * c) % NB;
+    unsigned s = (unsigned)__cvta_generic_to_shared(Ls + col * kLsLd + row);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(Li + 2 * c));
   }
   asm volatile("cp.async.commit_group;\n" ::);
@@ -442,7 +447,7 @@ __device__ __forceinline__ void solve_diag(const double* Ls, const double* ws, d
     const int b0 = half ? mid : lo, b1 = half ? hi : mid;
 #pragma unroll 4
     for (int kk = b0; kk < b1; ++kk) {
-      const double m = transpose ? Ls[i * NB + kk] : Ls[kk * NB + i];
+      const double m = transpose ? Ls[i * kLsLd + kk] : Ls[kk * kLsLd + i];
 #pragma unroll
       for (int q = 0; q < RT; ++q)
         if (q < R) acc[q] = fma(m, ws[q * NB + kk], acc[q]);
@@ -555,7 +560,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double sm[];
   double* Ls = sm;                    // [NB][NB] current diagonal-block inverse
-  double* ws = Ls + NB * NB;          // [RT][NB] right-hand side block
+  double* ws = Ls + NB * kLsLd;       // [RT][NB] right-hand side block
   double* ys = ws + RT * NB;     // [RT][NB] solved block
   double* part = ys + RT * NB;   // [RT][NB] partial sums
   double* red = part + RT * NB;  // [warps][RT][32] forward cross-warp sums

@@ -5,6 +5,7 @@
 //   gbem extract --input F [--net N | --all] [--p1 X] [--p2 X] [--p3 X] [--p5 X]
 //                [--format csv|json] [--output P] [--dump-matrix P]
 //                [--mode per-net|shared] [--uniform H | --graded H0,R,HMAX] [--device D]
+//                [--baseline collocation]
 //   gbem validate --input F
 //   gbem config --id N [--seed S] [--scale X]      (prints the config scene + panel count)
 #include <cstdio>
@@ -90,7 +91,7 @@ int main(int argc, char** argv) {
     return 0;
   }
   if (cmd != "extract") return usage(("unknown subcommand " + cmd).c_str());
-  std::string in, out, format = "csv", dump, mode = "per-net", v;
+  std::string in, out, format = "csv", dump, mode = "per-net", v, baseline;
   double p[4] = {-1, -1, -1, -1}, netd = -1, dev = 0, uni = -1;
   double graded[3] = {-1, -1, -1};
   bool all = false, have_net = false;
@@ -101,6 +102,7 @@ int main(int argc, char** argv) {
     if (k == "--format" && value(i, format) && (format == "csv" || format == "json")) continue;
     if (k == "--dump-matrix" && value(i, dump)) continue;
     if (k == "--mode" && value(i, mode) && (mode == "per-net" || mode == "shared")) continue;
+    if (k == "--baseline" && value(i, baseline) && baseline == "collocation") continue;  // cli.hpp:37-38
     if (k == "--all") {
       all = true;
       continue;
@@ -154,6 +156,12 @@ int main(int argc, char** argv) {
   o.mode = mode == "shared" ? 1 : 0;
   o.net = have_net ? (int32_t)netd : -1;
   o.dump_matrix = dump.empty() ? nullptr : dump.c_str();
+  o.collocation = baseline == "collocation" ? 1 : 0;
+  if (o.collocation && o.mode == 1) {
+    std::cerr << "input error: --baseline collocation runs per net (--mode per-net)\n";
+    gbem_model_free(m);
+    return 1;
+  }
   if (o.mode == 1) {
     int64_t n = -1;
     if (uni > 0)

@@ -61,11 +61,85 @@ gbem_quad_config quad(const Options& o) {
 
 }  // namespace
 
+// The block (mixed-unknown) path of capacitance_row (extraction.hpp:132-143)
+// for the collocation baseline: GPU assemble_collocation + GPU lu_solve, then
+// net_charges through the flux-unknown columns (extraction.hpp:55-79).
+static Row block_row(gbem_ctx* ctx, const Scene& s, const PanelSet& ps, int main_net, const Options& o) {
+  const size_t n = ps.panels.size();
+  Row row;
+  row.main_net = main_net;
+  row.diag.panels = n;
+  row.diag.method = "collocation";
+  SoA soa(ps);
+  std::vector<int8_t> nsign(n);
+  std::vector<int32_t> kind(n), net(n), ra(n), rb(n);
+  for (size_t k = 0; k < n; ++k) {
+    const Panel& pn = ps.panels[k];
+    nsign[k] = (int8_t)pn.r.nsign;
+    kind[k] = (int32_t)pn.kind;
+    net[k] = pn.net;
+    ra[k] = pn.regA;
+    rb[k] = pn.regB;
+  }
+  gbem_block_panels bp{soa.view(), nsign.data(), kind.data(), net.data(), ra.data(), rb.data()};
+  std::vector<gbem_region> regs;
+  for (const Region& r : s.regions) regs.push_back(gbem_region{r.id, r.eps});
+  auto t0 = std::chrono::steady_clock::now();
+  int64_t m = 0;
+  raise(ctx, gbem_assemble_collocation(ctx, &bp, (int64_t)n, regs.data(), (int32_t)regs.size(), main_net, nullptr,
+                                       0, nullptr, &m));
+  if (!o.dump_matrix.empty()) {  // dump_system_matrix (extraction.hpp:83-99): row-major m x m
+    std::vector<double> A((size_t)m * m);
+    raise(ctx, gbem_assemble_collocation(ctx, &bp, (int64_t)n, regs.data(), (int32_t)regs.size(), main_net,
+                                         A.data(), m, nullptr, &m));
+    dump_matrix_file(o.dump_matrix, A, (size_t)m);
+  }
+  std::vector<double> x((size_t)m, 0.0);
+  double resid = 0;
+  gbem_solve_stats sst{};
+  raise(ctx, gbem_lu_solve(ctx, nullptr, x.data(), &resid, &sst));
+  auto t1 = std::chrono::steady_clock::now();
+  row.diag.seconds = std::chrono::duration<double>(t1 - t0).count();
+  row.diag.residual = resid;
+  // qCol of buildUnknownMap (assembly.hpp:51-75)
+  const size_t o3 = ps.offset[3];
+  for (const Net& nn : s.nets) row.cap[nn.id] = 0.0;
+  double outer = 0;
+  for (size_t k = 0; k < n; ++k) {
+    const Panel& pn = ps.panels[k];
+    if (pn.kind == kInterface || pn.kind == kNeumann) continue;
+    const size_t col = k;  // conductor / Dirichlet panels precede o3: qCol = index
+    (void)o3;
+    const Region* reg = s.region(pn.regA);
+    if (!reg) throw ValidationError("missing permittivity for region " + std::to_string(pn.regA));
+    const double qv = reg->eps * kEps0 * x[col] * kUnitScale;
+    if (pn.kind == kConductor)
+      row.cap[pn.net] += qv;
+    else
+      outer += qv;
+  }
+  row.outer = outer;
+  bool all_dirichlet = s.freespace;
+  if (!s.freespace) {
+    all_dirichlet = true;
+    for (int b : s.bc)
+      if (b != 0) all_dirichlet = false;
+  }
+  if (all_dirichlet) {  // neutrality only for all-Dirichlet scenes (extraction.hpp:153-158)
+    double total = outer;
+    for (const auto& kv : row.cap) total += kv.second;
+    row.diag.neutrality = std::abs(total) / std::max(std::abs(row.cap.at(main_net)), 1e-300);
+  }
+  return row;
+}
+
 Row capacitance_row(gbem_ctx* ctx, const Scene& s, int main_net, const Params& p, const Options& o) {
   PanelSet ps = partition_for_net(s, main_net, p);
+  if (o.collocation) return block_row(ctx, s, ps, main_net, o);
   if (!single_dielectric(s))
     throw ValidationError(
-        "the GPU path solves the single-dielectric all-Dirichlet system (multi-dielectric block system is out of scope)");
+        "multi-region / mixed-boundary scenes need the Galerkin block system, which the GPU path does not "
+        "implement yet; --baseline collocation solves them with the collocation block system");
   if (ps.count(kNeumann) || ps.count(kInterface))
     throw ValidationError("single-dielectric assembly requires one region with an all-Dirichlet boundary");
   const size_t n = ps.panels.size();

@@ -179,6 +179,7 @@ struct Options {
   std::string dump_matrix;  // matrix dump path (extraction.hpp:83-99 format)
   double rel_tol = 1e-8;
   int max_levels = 16;
+  bool collocation = false;  // ExtractionOptions::baselineCollocation (extraction.hpp:110-114)
 };
 
 struct RowDiag {
@@ -214,6 +215,7 @@ struct Report {
   std::vector<int> ids;
   std::vector<Row> rows;
   double reciprocity = -1;
+  std::string baseline;  // "" or "collocation" (model_io.hpp:236,274)
 };
 std::string to_csv(const Report& r);   // model_io.hpp:242-263
 std::string to_json(const Report& r);  // model_io.hpp:266-299

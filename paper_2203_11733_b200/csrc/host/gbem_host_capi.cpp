@@ -106,6 +106,16 @@ int gbem_model_info(const gbem_model* m, int32_t* nregions, int32_t* nfaces, dou
   return 0;
 }
 
+int gbem_model_regions(const gbem_model* m, int32_t* ids, double* eps, int cap) {
+  if (!m) return -1;
+  const int k = (int)m->scene.regions.size();
+  for (int i = 0; i < k && i < cap; ++i) {
+    if (ids) ids[i] = m->scene.regions[(size_t)i].id;
+    if (eps) eps[i] = m->scene.regions[(size_t)i].eps;
+  }
+  return k;
+}
+
 int gbem_model_params(const gbem_model* m, double p[4]) {
   if (!m || !p) return 1;
   p[0] = m->params.p1;
@@ -199,7 +209,9 @@ int gbem_model_extract(const gbem_model* m, const gbem_extract_opts* o, char* cs
     if (o->rel_tol > 0) opt.rel_tol = o->rel_tol;
     if (o->max_levels > 0) opt.max_levels = o->max_levels;
     if (o->dump_matrix) opt.dump_matrix = o->dump_matrix;
+    opt.collocation = o->collocation != 0;
     gbh::Report rep;
+    if (opt.collocation) rep.baseline = "collocation";
     rep.params = m->params;
     for (const gbh::Net& n : m->scene.nets) rep.ids.push_back(n.id);
     if (o->mode == 1) {

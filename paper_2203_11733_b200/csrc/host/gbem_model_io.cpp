@@ -218,6 +218,7 @@ std::string to_json(const Report& r) {
   o << "{\n  \"tool\": \"gbem\",\n  \"version\": \"" << r.version << "\",\n";
   o << "  \"params\": {\"p1\": " << g9(r.params.p1) << ", \"p2\": " << g9(r.params.p2) << ", \"p3\": "
     << g9(r.params.p3) << ", \"p5\": " << g9(r.params.p5) << "},\n";
+  if (!r.baseline.empty()) o << "  \"baseline\": \"" << r.baseline << "\",\n";
   o << "  \"netIds\": [";
   for (size_t i = 0; i < r.ids.size(); ++i) o << (i ? ", " : "") << r.ids[i];
   o << "],\n  \"rows\": [\n";

@@ -47,6 +47,12 @@ def _bind(lib, prefix):
     f = getattr(lib, prefix + "_oracle_pair_integral")
     f.restype = C.c_double
     f.argtypes = [RP, RP, C.c_int]
+    f = getattr(lib, prefix + "_u_point_rect")
+    f.restype = C.c_double
+    f.argtypes = [C.POINTER(C.c_double), RP]
+    f = getattr(lib, prefix + "_q_point_rect")
+    f.restype = C.c_double
+    f.argtypes = [C.POINTER(C.c_double), RP, C.c_int]
 
 
 _orc = _ref = None
@@ -67,6 +73,12 @@ def orc():
         _orc.orc_cholesky_solve.restype = C.c_int
         _orc.orc_cholesky_solve.argtypes = [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                             C.c_void_p, C.POINTER(C.c_int64)]
+        _orc.orc_assemble_collocation.restype = C.c_int
+        _orc.orc_assemble_collocation.argtypes = [C.c_int64, C.c_void_p] + [C.c_void_p] * 5 + [
+            C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
+        _orc.orc_lu_solve.restype = C.c_int
+        _orc.orc_lu_solve.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.POINTER(C.c_int64)]
         _orc.orc_quad_test.restype = C.c_double
         _orc.orc_quad_test.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
                                        C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_long)]
@@ -141,3 +153,42 @@ def assemble(lib_name: str, P: np.ndarray, nthreads=8, rel_tol=1e-8, max_levels=
     f = lib.orc_assemble_single if lib_name == "orc" else lib.ref_assemble_single
     st = f(n, rp, rel_tol, max_levels, A.ctypes.data, C.byref(conv), nthreads)
     return A, bool(conv.value), st
+
+
+def point_kernels(lib_name: str, X: np.ndarray, R: np.ndarray, nsign: np.ndarray):
+    """u_point_rect / q_point_rect at points X (k, 3) for rect rows R (k, 6)."""
+    lib = orc() if lib_name == "orc" else ref()
+    rr = rects_from_matrix(R)
+    fu = getattr(lib, lib_name + "_u_point_rect")
+    fq = getattr(lib, lib_name + "_q_point_rect")
+    u = np.empty(len(X)); q = np.empty(len(X))
+    for k in range(len(X)):
+        x = (C.c_double * 3)(*map(float, X[k]))
+        u[k] = fu(x, C.byref(rr[k]))
+        q[k] = fq(x, C.byref(rr[k]), int(nsign[k]))
+    return u, q
+
+
+def lu_solve(A: np.ndarray, b: np.ndarray):
+    """orc_lu_solve (solver.hpp:53-88): (x, resid, status, bad_row)."""
+    A = np.ascontiguousarray(A, dtype=np.float64); b = np.ascontiguousarray(b, dtype=np.float64)
+    n = len(b)
+    x = np.zeros(n); res = np.zeros(1); bad = C.c_int64(-1)
+    st = orc().orc_lu_solve(n, A.ctypes.data, b.ctypes.data, x.ctypes.data, res.ctypes.data, C.byref(bad))
+    return x, float(res[0]), st, bad.value
+
+
+def assemble_collocation(P: np.ndarray, nsign, kind, net, reg_a, reg_b, regions, main_net: int):
+    """orc_assemble_collocation: (A (m, m), b (m,), status).  regions: [(id, eps), ...]."""
+    n = len(P)
+    rp = rects_from_matrix(P)
+    ints = [np.ascontiguousarray(v, dtype=np.int32) for v in (nsign, kind, net, reg_a, reg_b)]
+    rid = np.array([r[0] for r in regions], dtype=np.int32)
+    reps = np.array([r[1] for r in regions], dtype=np.float64)
+    mmax = n + int(np.sum(ints[1] == 3))
+    A = np.zeros(mmax * mmax); b = np.zeros(mmax); m = C.c_int64(0)
+    st = orc().orc_assemble_collocation(n, C.cast(rp, C.c_void_p), *[v.ctypes.data for v in ints], len(rid),
+                                        rid.ctypes.data, reps.ctypes.data, int(main_net), A.ctypes.data,
+                                        b.ctypes.data, C.byref(m))
+    mm = m.value
+    return A[:mm * mm].reshape(mm, mm), b[:mm], st

@@ -1,0 +1,120 @@
+"""The block (mixed-unknown) system on the GPU: lu_solve (solver.hpp:53-88) and
+the collocation baseline assemble_collocation (assembly.hpp:179-227), against
+the CPU oracle restatement (oracle/gbem_oracle.c, its point kernels pinned
+bit-for-bit to the compiled reference in test_oracle_golden.py)."""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import paper_2203_11733_b200 as g
+from paper_2203_11733_b200._native import GbemError
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+TWO = ROOT / "tests" / "golden" / "bench_two_layer.gbem"
+SINGLE = ROOT / "tests" / "golden" / "bench_single.gbem"
+EPS0 = 8.854187817e-12
+
+
+@pytest.mark.parametrize("n", [1, 5, 63, 64, 65, 130, 500, 1100])
+def test_lu_matches_oracle_and_numpy(ctx, n):
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n)) + 0.5 * np.eye(n)
+    b = rng.standard_normal(n)
+    x, res, st = ctx.lu_solve(A, b)
+    xr = np.linalg.solve(A, b)
+    assert np.abs(x - xr).max() <= 1e-9 * np.abs(xr).max()
+    if n <= 500:
+        xo, ro, sto, _ = O.lu_solve(A, b)
+        assert sto == 0
+        assert np.abs(x - xo).max() <= 1e-10 * np.abs(xo).max()
+        # backward error of the same order as the reference algorithm's (both
+        # grow with cond(A); seed 130 gives cond 5e4)
+        assert res <= 4 * max(ro, 1e-14), (res, ro)
+    else:
+        assert res <= 1e-11
+
+
+def test_lu_pivots_zero_diagonal(ctx):
+    # needs a row exchange at every step
+    A = np.array([[0.0, 2.0, 1.0], [1.0, 0.0, 3.0], [4.0, 1.0, 0.0]])
+    b = np.array([1.0, 2.0, 3.0])
+    x, res, _ = ctx.lu_solve(A, b)
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=1e-14)
+
+
+def test_lu_singular_reports_row(ctx):
+    A = np.array([[1.0, 2.0, 3.0], [2.0, 4.0, 6.0], [1.0, 0.0, 1.0]])
+    _, _, st, bad = O.lu_solve(A, np.ones(3))
+    with pytest.raises(GbemError) as e:
+        ctx.lu_solve(A, np.ones(3))
+    assert e.value.code == 2 and f"smallest pivot at row {bad}" in str(e.value)
+
+
+def _oracle_system(ps, regions, main_net):
+    return O.assemble_collocation(ps.matrix(), ps.nsign, ps.kind, ps.net, ps.regA, ps.regB, regions, main_net)
+
+
+@pytest.mark.parametrize("scene,net", [(TWO, 1), (TWO, 2), (SINGLE, 1)])
+def test_collocation_system_matches_oracle(ctx, scene, net):
+    m = g.parse_model(scene.read_text())
+    ps = m.partition(0, net)
+    A, b, x, res = ctx.assemble_collocation(ps, m.regions, net, solve=True)
+    Ao, bo, st = _oracle_system(ps, m.regions, net)
+    assert st == 0 and A.shape == Ao.shape
+    scale = np.abs(Ao).max()
+    assert np.abs(A - Ao).max() <= 1e-13 * scale
+    assert np.abs(b - bo).max() <= 1e-13 * max(np.abs(bo).max(), 1.0)
+    xo, ro, sto, _ = O.lu_solve(Ao, bo)
+    assert sto == 0
+    assert np.abs(x - xo).max() <= 1e-9 * np.abs(xo).max()
+    assert res <= 1e-12
+
+
+def _oracle_cmatrix(m):
+    """capacitance_matrix with the collocation baseline, all on the CPU oracle."""
+    ids = m.net_ids
+    eps = dict(m.regions)
+    C = np.zeros((len(ids), len(ids)))
+    for r, net in enumerate(ids):
+        ps = m.partition(0, net)
+        A, b, st = _oracle_system(ps, m.regions, net)
+        x, _, _, _ = O.lu_solve(A, b)
+        for k in range(len(ps)):
+            if ps.kind[k] == 0:  # conductor: qCol = k (extraction.hpp:55-79)
+                C[r, ids.index(int(ps.net[k]))] += eps[int(ps.regA[k])] * EPS0 * x[k] * 1e-6
+    return C
+
+
+def test_two_layer_cmatrix_collocation_end_to_end(ctx):
+    m = g.parse_model(TWO.read_text())
+    csv, js = m.extract(net=-1, mode=0, baseline="collocation")
+    assert js["baseline"] == "collocation"
+    assert [r["method"] for r in js["rows"]] == ["collocation", "collocation"]
+    Cg = m.last_cap
+    Co = _oracle_cmatrix(m)
+    assert np.abs(Cg - Co).max() <= 1e-9 * np.abs(Co).max(), (Cg, Co)
+    assert Cg[0, 0] > 0 and Cg[1, 1] > 0 and Cg[0, 1] < 0 and Cg[1, 0] < 0
+    assert "# method net1=collocation net2=collocation" in csv
+
+
+def test_multi_region_needs_block_formulation(ctx):
+    m = g.parse_model(TWO.read_text())
+    with pytest.raises(g.api.ValidationError if hasattr(g, "api") else ValueError) as e:
+        m.extract(net=1)
+    assert "collocation" in str(e.value)
+
+
+def test_collocation_single_region_agrees_with_galerkin(ctx):
+    """Cross-method check (SPEC.md:522 in SURVEY §8f): on the single-dielectric
+    benchmark the collocation C-matrix agrees with the Galerkin one to the
+    discretisation level."""
+    m = g.parse_model(SINGLE.read_text())
+    m.extract(net=-1)
+    Cg = m.last_cap.copy()
+    m.extract(net=-1, baseline="collocation")
+    Cc = m.last_cap
+    assert np.abs(Cc - Cg).max() <= 0.1 * np.abs(Cg).max()

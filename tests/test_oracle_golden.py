@@ -161,3 +161,60 @@ def test_cholesky_restatement():
     assert res[0] <= 1e-10
     rc, _, _, piv = _chol(np.array([[1.0, 2.0], [2.0, 1.0]]), np.ones((2, 1)))
     assert rc == 2 and piv == 1
+
+
+# --- block-system pieces (kernels.hpp:319-355, solver.hpp:53-88) -------------------
+
+def _random_point_cases(rng, k):
+    R = np.zeros((k, 6)); X = np.zeros((k, 3))
+    for t in range(k):
+        ax = int(rng.integers(3)); lvl = rng.uniform(-1, 1)
+        a0 = rng.uniform(-1, 1); b0 = rng.uniform(-1, 1)
+        R[t] = [ax, lvl, a0, a0 + rng.uniform(0.01, 1.5), b0, b0 + rng.uniform(0.01, 1.5)]
+        X[t] = rng.uniform(-2, 2, size=3)
+        if t % 5 == 0:
+            X[t, ax] = lvl  # in the panel plane: q vanishes, u keeps its log terms
+        if t % 7 == 0:  # on an edge / corner line
+            i0 = 1 if ax == 0 else 0
+            X[t, i0] = R[t, 2]
+    return X, R
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference headers not compiled here")
+def test_point_kernels_bit_identical_to_reference():
+    rng = np.random.default_rng(11)
+    X, R = _random_point_cases(rng, 2000)
+    ns = np.where(rng.random(len(R)) < 0.5, 1, -1)
+    u1, q1 = O.point_kernels("orc", X, R, ns)
+    u2, q2 = O.point_kernels("ref", X, R, ns)
+    assert np.array_equal(u1, u2) and np.array_equal(q1, q2)
+    assert np.all(np.isfinite(u1)) and np.all(q1[::5] == 0.0)
+
+
+def test_point_kernels_known_answers():
+    """Unit square seen from its own centre plane and from far away."""
+    R = np.array([[2, 0.0, -0.5, 0.5, -0.5, 0.5]] * 3)
+    X = np.array([[0, 0, 1e-12], [0, 0, 50.0], [0, 0, -50.0]])
+    u, q = O.point_kernels("orc", X, R, np.array([1, 1, 1]))
+    # solid angle of the square seen from just above its centre -> 1/2 of the sphere
+    assert abs(q[0] - 0.5) < 1e-9
+    # far field: u -> area / (4 pi r), q -> area / (4 pi r^2) (signed by the side)
+    assert abs(u[1] - 1.0 / (4 * np.pi * 50.0)) < 1e-3 * u[1]  # finite-size correction O((a/r)^2)
+    assert abs(q[1] - 1.0 / (4 * np.pi * 2500.0)) < 1e-3 * q[1] and abs(q[2] + q[1]) < 1e-15
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 40])
+def test_lu_oracle_matches_numpy(n):
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n)) + 0.1 * np.eye(n)
+    b = rng.standard_normal(n)
+    x, res, st, _ = O.lu_solve(A, b)
+    assert st == 0
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=1e-9, atol=1e-12)
+    assert res < 1e-13
+
+
+def test_lu_oracle_singular_row():
+    A = np.array([[1.0, 2.0, 3.0], [2.0, 4.0, 6.0], [1.0, 0.0, 1.0]])
+    _, _, st, bad = O.lu_solve(A, np.ones(3))
+    assert st == 2 and bad == 2

@@ -1,1 +1,3 @@
-for rep in 1 2 3; do for t in 0 1024 1536; do GBEM_FACTOR_TAIL=$t python tools/solve_bench.py 11340 6 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($t, round(d['factor_ms'],3))"; done; done
+./tools/solve_phase_bench 11340 6 | tail -3
+for R in 1 6 16; do python tools/solve_bench.py 11340 $R 2>&1 | tail -1; done
+timeout 600 python -m pytest tests/test_gpu_pcg.py tests/test_gpu_extract.py -x -q 2>&1 | tail -2
