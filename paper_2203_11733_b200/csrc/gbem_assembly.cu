@@ -238,17 +238,27 @@ __global__ void __launch_bounds__(kClassifyThreads)
   constexpr int kIter = kTile / (kClassifyThreads / 32);
   __shared__ CPanel si[kTile], sj[kTile];
   __shared__ uint32_t hkey[kHash], hcnt[kHash];
-  long long t = tile_begin + blockIdx.x;
-  int lo = 0, hi = nrows_t - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (tile_row_off[mid] <= t)
-      lo = mid;
-    else
-      hi = mid - 1;
+  const long long t = tile_begin + blockIdx.x;
+  // tile row of t: full rows hold nbt tiles each; upper-triangle rows hold
+  // nbt - bi tiles, so tile_row_off[r] = r c - r (r - 1) / 2 with c = nbt - bi0,
+  // inverted in closed form (a per-thread binary search over tile_row_off was
+  // ~40% of the classifier's issue slots).  The fix-up loops only absorb the
+  // rounding of the square root.
+  int lo;
+  if (full) {
+    lo = (int)(t / nbt);
+  } else {
+    const double c2 = 2.0 * (nbt - bi0) + 1.0;
+    lo = (int)((c2 - sqrt(fmax(c2 * c2 - 8.0 * (double)t, 0.0))) * 0.5);
+    lo = min(max(lo, 0), nrows_t - 1);
+    const long long c = nbt - bi0;
+    auto off = [&](long long r) { return r * c - r * (r - 1) / 2; };
+    while (lo > 0 && off(lo) > t) --lo;
+    while (lo + 1 < nrows_t && off(lo + 1) <= t) ++lo;
   }
+  const long long row_off = full ? (long long)lo * nbt : (long long)lo * (nbt - bi0) - (long long)lo * (lo - 1) / 2;
   const int bi = bi0 + lo;
-  const int bj = (full ? 0 : bi) + (int)(t - tile_row_off[lo]);  // full: whole rows (mirrored entries too)
+  const int bj = (full ? 0 : bi) + (int)(t - row_off);  // full: whole rows (mirrored entries too)
   const int tid = threadIdx.x;
   if (tid < kTile) {
     int i = bi * kTile + tid;

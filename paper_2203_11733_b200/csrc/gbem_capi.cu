@@ -7,10 +7,10 @@
 
 namespace {
 
-int ensure_matrix(gbem_ctx* ctx, int64_t n) {
-  int64_t lda = ((n + 7) / 8) * 8;  // 64-byte columns (cp.async alignment)
+int ensure_matrix(gbem_ctx* ctx, int64_t n, int64_t border = 0) {
+  int64_t lda = ((n + border + 7) / 8) * 8;  // 64-byte columns (cp.async alignment)
   if (lda == 0) lda = 8;
-  size_t need = (size_t)lda * (size_t)(n > 0 ? n : 1);
+  size_t need = (size_t)lda * (size_t)(n + border > 0 ? n + border : 1);
   if (ctx->A_cap < need || !ctx->d_A) {
     if (ctx->d_A) cudaFree(ctx->d_A);
     ctx->d_A = nullptr;
@@ -20,6 +20,7 @@ int ensure_matrix(gbem_ctx* ctx, int64_t n) {
   }
   ctx->n = n;
   ctx->lda = lda;
+  ctx->border = border;
   ctx->factored = false;
   return GBEM_OK;
 }
@@ -55,13 +56,35 @@ __global__ void k_build_rhs(const int32_t* net, int n, int K, double* B) {
   B[i] = net[p] == r ? 1.0 : 0.0;
 }
 
+// Border of the bordered factorisation: row n + q of column c is B(c, q) =
+// [net(c) == q]; the K x K corner (columns n..n+K-1, rows n..n+K-1) starts at 0.
+__global__ void k_build_border(const int32_t* net, int n, int K, double* A, long long lda) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long cols = (long long)n + K;
+  if (i >= cols * K) return;
+  const long long c = i / K;
+  const int q = (int)(i % K);
+  A[c * lda + n + q] = c < n ? (net[c] == q ? 1.0 : 0.0) : 0.0;
+}
+
+// C = scale * B^T A^-1 B = -scale * corner (the corner holds -Y^T Y after the
+// bordered factorisation; lower triangle, mirrored).  C[r * K + k]: charge of
+// net k for unit potential on net r.
+__global__ void k_corner_charges(const double* A, long long lda, int n, int K, double scale, double* C) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= K * K) return;
+  const int r = i / K, k = i % K;
+  const int hi = r > k ? r : k, lo = r > k ? k : r;
+  C[i] = -scale * A[(long long)(n + lo) * lda + n + hi];
+}
+
 int extract_impl(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* d_net, int32_t K, double eps_r,
                  const gbem_quad_config* cfg, double* d_C, double* d_resid, gbem_assembly_stats* as,
                  gbem_solve_stats* ss, bool device_panels) {
   if (K < 1 || K > 64) return ctx->fail(GBEM_EINVAL, "K must be in [1, 64]");
   int rc = gbem_internal_upload_panels(ctx, P, n, device_panels);
   if (rc) return rc;
-  rc = ensure_matrix(ctx, n);
+  rc = ensure_matrix(ctx, n, K);
   if (rc) return rc;
   rc = gbem_internal_assemble(ctx, n, 0, n, cfg, as, true);
   if (rc) return rc;
@@ -77,14 +100,26 @@ int extract_impl(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* 
   double* dX = ctx->d_rhs + cnt;
   k_build_rhs<<<(unsigned)((cnt + 255) / 256), 256, 0, ctx->stream>>>(d_net, (int)n, K, dB);
   GBEM_LAUNCH_CHECK(ctx);
-  rc = gbem_internal_solve(ctx, dB, K, dX, d_resid, ss);
+  const long long bcnt = ((long long)n + K) * K;
+  k_build_border<<<(unsigned)((bcnt + 255) / 256), 256, 0, ctx->stream>>>(d_net, (int)n, K, ctx->d_A, ctx->lda);
+  GBEM_LAUNCH_CHECK(ctx);
+  // bordered Cholesky: the forward substitution and C = B^T A^-1 B come out of
+  // the factorisation; the backward substitution gives X for the residual
+  // ||A X - B|| / ||B|| recomputed from the unfactored A (solver.hpp:47)
+  rc = gbem_internal_factor(ctx, ss);
   if (rc) return rc;
-  return gbem_net_charges_dev(ctx, d_net, n, dX, K, K, eps_r * 8.854187817e-12 * 1e-6, d_C, nullptr);
+  if (ss) ss->nrhs = K;
+  rc = gbem_internal_solve_factored(ctx, dB, K, dX, d_resid, ss, true);
+  if (rc) return rc;
+  k_corner_charges<<<(unsigned)((K * K + 255) / 256), 256, 0, ctx->stream>>>(
+      ctx->d_A, ctx->lda, (int)n, K, eps_r * 8.854187817e-12 * 1e-6, d_C);
+  GBEM_LAUNCH_CHECK(ctx);
+  return GBEM_OK;
 }
 
 }  // namespace
 
-int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n) { return ensure_matrix(ctx, n); }
+int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n, int64_t border) { return ensure_matrix(ctx, n, border); }
 
 extern "C" {
 

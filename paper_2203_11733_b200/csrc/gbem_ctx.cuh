@@ -26,6 +26,12 @@ struct gbem_ctx {
   // assembly; lower triangle overwritten by the Cholesky factor)
   double* d_A = nullptr;
   int64_t n = 0, lda = 0;
+  // bordered factorisation (K-RHS extraction): `border` rows below the matrix
+  // hold B^T (the net incidence) and a border x border corner block starts at
+  // zero; the Cholesky then carries them along, leaving Y^T = (L^-1 B)^T in the
+  // border rows and -Y^T Y = -B^T A^-1 B in the corner (the forward
+  // substitution and the charge reduction fused into the factorisation)
+  int64_t border = 0;
   size_t A_cap = 0;  // elements
   double* d_diag = nullptr;  // original diagonal (kept for residuals after factoring)
   int64_t diag_cap = 0;
@@ -85,7 +91,7 @@ struct gbem_ctx {
   } while (0)
 
 // Internal entry points implemented across the units.
-int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n);
+int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n, int64_t border = 0);
 int gbem_internal_assemble_collocation(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n,
                                        const gbem_region* regions, int32_t nreg, int32_t main_net, int64_t* m_out);
 int gbem_internal_lu_solve(gbem_ctx* ctx, double* d_b, double* d_x, double* d_resid, gbem_solve_stats* stats);
@@ -103,4 +109,4 @@ int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* 
                         double* d_resid, gbem_solve_stats* stats);
 int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats);
 int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
-                                 gbem_solve_stats* stats);
+                                 gbem_solve_stats* stats, bool y_from_border = false);

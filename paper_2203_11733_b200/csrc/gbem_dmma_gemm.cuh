@@ -351,6 +351,105 @@ __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
 }
 
 // ---------------------------------------------------------------------------
+// Panel trsm of the Cholesky as a GEMM on 32-row strips: C = A B^T with A the
+// M x K strip (column-major, lda), B the N x K inverse of the diagonal factor
+// (column-major, ldb), N, K <= 128; C may alias A (a CTA reads its whole strip
+// before it writes).  One CTA of 4 warps per 32 rows, warp w owns columns
+// [32 w, 32 w + 32): a strip is 1 MFLOP, so the m / 32 CTAs finish in a few
+// microseconds (128-row strips are 4.2 MFLOP each, ~17 us at one SM's DMMA
+// peak, on the factorisation's critical path).
+constexpr int kTrsmRows = 32, kTrsmThreads = 128, kTrsmStages = 3;
+constexpr int kTrsmLA = kTrsmRows + 8, kTrsmLB = 128 + 8;
+constexpr size_t kTrsmSmem = (size_t)kTrsmStages * BK * (kTrsmLA + kTrsmLB) * sizeof(double);
+
+static __global__ void __launch_bounds__(kTrsmThreads, 3)
+    k_trsm_rows(double* C, long long ldc, const double* A, long long lda, const double* __restrict__ B,
+                long long ldb, int M, int N, int K) {
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                                 // [stages][BK][kTrsmLA]
+  double* Bs = smem + kTrsmStages * BK * kTrsmLA;    // [stages][BK][kTrsmLB]
+  const int m0 = blockIdx.x * kTrsmRows;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int KT = (K + BK - 1) / BK;
+  auto load_stage = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    double* as = As + st * BK * kTrsmLA;
+    double* bs = Bs + st * BK * kTrsmLB;
+    {  // A: 16 x 32 doubles = 256 16-byte chunks, 2 per thread
+#pragma unroll
+      for (int c = tid; c < BK * kTrsmRows / 2; c += kTrsmThreads) {
+        const int kk = c / (kTrsmRows / 2), mm = (c % (kTrsmRows / 2)) * 2;
+        const int gk = k0 + kk, gm = m0 + mm;
+        int bytes = 0;
+        const double* src = A;
+        if (gk < K && gm < M) {
+          bytes = gm + 1 < M ? 16 : 8;
+          src = A + (long long)gk * lda + gm;
+        }
+        cp_async16(as + kk * kTrsmLA + mm, src, bytes);
+      }
+    }
+#pragma unroll
+    for (int c = tid; c < BK * 128 / 2; c += kTrsmThreads) {  // B: 16 x 128, 8 per thread
+      const int kk = c / 64, nn = (c % 64) * 2;
+      const int gk = k0 + kk;
+      int bytes = 0;
+      const double* src = B;
+      if (gk < K && nn < N) {
+        bytes = nn + 1 < N ? 16 : 8;
+        src = B + (long long)gk * ldb + nn;
+      }
+      cp_async16(bs + kk * kTrsmLB + nn, src, bytes);
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < kTrsmStages - 1; ++st) {
+    if (st < KT) load_stage(st, st);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_async_wait<kTrsmStages - 2>();
+    __syncthreads();
+    const int nxt = kt + kTrsmStages - 1;
+    if (nxt < KT) load_stage(nxt, nxt % kTrsmStages);
+    cp_async_commit();
+    const double* as = As + (kt % kTrsmStages) * BK * kTrsmLA + g;
+    const double* bs = Bs + (kt % kTrsmStages) * BK * kTrsmLB + warp * 32 + g;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[(kk + t4) * kTrsmLA + i * 8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bs[(kk + t4) * kTrsmLB + j * 8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // every warp's reads of the strip precede any write (C may alias A)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = m0 + i * 8 + g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = warp * 32 + j * 8 + 2 * t4 + e;
+        if (row < M && col < N) C[(long long)col * ldc + row] = acc[i][j][e];
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // General dense DMMA GEMM on 64 x 64 tiles (2 x 2 warps of 32 x 32, 4 CTAs/SM,
 // double-buffered BK = 16 slabs), for the blocked multi-right-hand-side solves:
 //   C (M x N) op= A (M x K) * op(B),  A column-major (lda),

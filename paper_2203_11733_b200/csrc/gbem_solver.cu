@@ -12,8 +12,11 @@
 // residual uses the original A.  Block size NB = 128:
 //   k_potrf_diag  : one CTA factors the NB x NB diagonal block in shared memory
 //                   and forms inv(L11) (kept for the solves);
-//   k_gemm_nt<STORE,128>: L21 = A21 * inv(L11)^T (trsm as a DMMA GEMM, in place);
-//   k_gemm_nt<SUB,64>   : A22 -= L21 * L21^T on lower 128x64 tiles (the O(n^3) part).
+//   k_trsm_rows   : L21 = A21 * inv(L11)^T (trsm as a DMMA GEMM on 32-row strips, in place);
+//   k_syrk_gen    : A22 -= L21 * L21^T on lower 64x64 tiles (the O(n^3) part).
+// Bordered mode (ctx->border > 0, the K-RHS extraction): the K rows below the
+// matrix hold B^T and ride along as extra rows of every trsm and update, so the
+// factorisation also leaves Y = inv(L) B (forward substitution) and -B^T A^-1 B.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -59,6 +62,77 @@ constexpr int kPotrfThreads = 512;
 constexpr int kPotrfWarps = kPotrfThreads / 32;
 constexpr int kPanel = 32;
 constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + NB + 3 * kPanel * (kPanel + 1)) * sizeof(double);
+
+// Off-diagonal 32 x 32 blocks of X = inv(L) for a factored block in shared
+// memory (L in the lower half of a, the diagonal blocks' inverses X_pp in the
+// strict upper half (transposed) and xd): X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp,
+// strided 4 x 4 register tiles, T_p = sum_q L_rq X_qp staged in tmp[p][32][33].
+__device__ __forceinline__ void potrf_inverse_offdiag(double* a, const double* xd, double* tmp, int npan, int tid) {
+  constexpr int LD = NB + 1;
+  // off-diagonal blocks of X = inv(L): X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp,
+  // same strided 4 x 4 tiles; T_p = sum_q L_rq X_qp staged in tmp[p][32][33].
+  {
+    const int grp = tid >> 6, tx = tid & 7, ty = (tid >> 3) & 7;
+    constexpr int TLD = kPanel + 1;
+    for (int rbk = 1; rbk < npan; ++rbk) {
+      const int R0 = rbk * kPanel;
+      if (grp < rbk) {
+        const int pb = grp;
+        double acc[4][4] = {};
+#pragma unroll 4
+        for (int m = pb * kPanel; m < R0; ++m) {
+          double lr[4], xc[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) lr[u] = a[m * LD + R0 + ty + 8 * u];  // L(R0+i, m)
+          const double dg = xd[m];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const int c = pb * kPanel + tx + 8 * v;
+            const double up = a[m * LD + c];
+            xc[v] = m > c ? up : 0.0;
+            xc[v] = m == c ? dg : xc[v];  // X(m, c)
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(lr[u], xc[v], acc[u][v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) tmp[pb * kPanel * TLD + (ty + 8 * u) * TLD + tx + 8 * v] = acc[u][v];
+      }
+      __syncthreads();
+      if (grp < rbk) {
+        const int pb = grp;
+        double acc[4][4] = {};
+#pragma unroll 4
+        for (int m = 0; m < kPanel; ++m) {
+          double xr[4], tv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int i = ty + 8 * u;
+            const double up = a[(R0 + i) * LD + R0 + m], dg = xd[R0 + i];
+            xr[u] = m < i ? up : 0.0;
+            xr[u] = m == i ? dg : xr[u];  // X(R0+i, R0+m)
+          }
+#pragma unroll
+          for (int v = 0; v < 4; ++v) tv[v] = tmp[pb * kPanel * TLD + m * TLD + tx + 8 * v];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(xr[u], tv[v], acc[u][v]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v)
+            a[(R0 + ty + 8 * u) * LD + pb * kPanel + tx + 8 * v] = -acc[u][v];  // X(R0+i, col)
+      }
+      __syncthreads();
+    }
+  }
+}
 
 __global__ void __launch_bounds__(kPotrfThreads)
     k_potrf_diag(double* A, long long lda, int kb, int row0, double* Linv, int* info) {
@@ -213,69 +287,7 @@ __global__ void __launch_bounds__(kPotrfThreads)
     POTRF_TICK(3 + 3 * p);
   }
   POTRF_TICK(20);
-  // ---- off-diagonal blocks of X = inv(L): X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp,
-  // same strided 4 x 4 tiles; T_p = sum_q L_rq X_qp staged in tmp[p][32][33].
-  {
-    const int grp = tid >> 6, tx = tid & 7, ty = (tid >> 3) & 7;
-    constexpr int TLD = kPanel + 1;
-    for (int rbk = 1; rbk < npan; ++rbk) {
-      const int R0 = rbk * kPanel;
-      if (grp < rbk) {
-        const int pb = grp;
-        double acc[4][4] = {};
-#pragma unroll 4
-        for (int m = pb * kPanel; m < R0; ++m) {
-          double lr[4], xc[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) lr[u] = a[m * LD + R0 + ty + 8 * u];  // L(R0+i, m)
-          const double dg = xd[m];
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int c = pb * kPanel + tx + 8 * v;
-            const double up = a[m * LD + c];
-            xc[v] = m > c ? up : 0.0;
-            xc[v] = m == c ? dg : xc[v];  // X(m, c)
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = fma(lr[u], xc[v], acc[u][v]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) tmp[pb * kPanel * TLD + (ty + 8 * u) * TLD + tx + 8 * v] = acc[u][v];
-      }
-      __syncthreads();
-      if (grp < rbk) {
-        const int pb = grp;
-        double acc[4][4] = {};
-#pragma unroll 4
-        for (int m = 0; m < kPanel; ++m) {
-          double xr[4], tv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = ty + 8 * u;
-            const double up = a[(R0 + i) * LD + R0 + m], dg = xd[R0 + i];
-            xr[u] = m < i ? up : 0.0;
-            xr[u] = m == i ? dg : xr[u];  // X(R0+i, R0+m)
-          }
-#pragma unroll
-          for (int v = 0; v < 4; ++v) tv[v] = tmp[pb * kPanel * TLD + m * TLD + tx + 8 * v];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = fma(xr[u], tv[v], acc[u][v]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            a[(R0 + ty + 8 * u) * LD + pb * kPanel + tx + 8 * v] = -acc[u][v];  // X(R0+i, col)
-      }
-      __syncthreads();
-    }
-  }
+  potrf_inverse_offdiag(a, xd, tmp, npan, tid);
   POTRF_TICK(21);
   for (int idx = tid; idx < NB * NB; idx += kPotrfThreads) {
     const int c = idx / NB, r = idx % NB;  // constant divisor: shifts, not a division
@@ -299,71 +311,102 @@ __global__ void k_save_diag(const double* A, long long lda, int n, double* d) {
 }
 
 // y = A x with A given by its strict upper triangle (col-major, A[c*lda + r],
-// r < c) and the saved diagonal; 64 x 64 tiles (I <= J), atomics into y.
+// r < c) and the saved diagonal.  One CTA per (64-row block, column chunk):
+// it walks the 64 x 64 tiles of its rows, reading A(r, c) = A[c*lda + r] right
+// of the diagonal and A(r, c) = A(c, r) = A[r*lda + c] left of it (both
+// coalesced, staged into shared memory as [c][r]), and keeps y in registers;
+// one atomic per (row, right-hand side, chunk).  Reads n^2 * 8 B (twice the
+// stored triangle) but needs no per-tile atomics, which bound the symmetric
+// one-pass form (~12M FP64 atomics at n = 11,340).
+constexpr int kSymvChunks = 4;
 template <int MAXR>
-__global__ void k_symv_upper(const double* A, long long lda, const double* diag, int n,
-                             const double* X, long long ldx, int nrhs, double* Y) {
-  constexpr int T = 64;
-  long long t = blockIdx.x;
-  int nbt = (n + T - 1) / T;
-  // upper tile (bi <= bj) from linear index, row-major over bi
-  int bi = 0;
-  long long off = 0;
-  while (off + (nbt - bi) <= t) {
-    off += nbt - bi;
-    ++bi;
-  }
-  int bj = bi + (int)(t - off);
-  __shared__ double xi[T * MAXR], xj[T * MAXR];
-  for (int idx = threadIdx.x; idx < T * nrhs; idx += blockDim.x) {
-    int r = idx % T, q = idx / T;
-    int gi = bi * T + r, gj = bj * T + r;
-    xi[r * MAXR + q] = gi < n ? X[(long long)q * ldx + gi] : 0.0;
-    xj[r * MAXR + q] = gj < n ? X[(long long)q * ldx + gj] : 0.0;
-  }
-  __syncthreads();
-  // thread per column c of the tile (T threads): y_j[c] += sum_r A(r,c) x_i[r];
-  // and per row r: y_i[r] += sum_c A(r,c) x_j[c] (second pass)
-  int tid = threadIdx.x;
-  if (tid < T) {
-    int c = bj * T + tid;
-    if (c < n) {
-      double acc[MAXR];
+__global__ void __launch_bounds__(256) k_symv_upper(const double* __restrict__ A, long long lda,
+                                                    const double* __restrict__ diag, int n, const double* X,
+                                                    long long ldx, int nrhs, double* Y) {
+  constexpr int T = 64, LD = T + 1;
+  __shared__ double sa[T * LD];
+  __shared__ double xs[T * MAXR];
+  double* red = sa;  // [3][T][MAXR] quarter partials, after the tile loop
+  static_assert(3 * T * MAXR <= T * LD, "partials fit in the tile buffer");
+  const int nbt = (n + T - 1) / T;
+  const int rb = blockIdx.x, r0 = rb * T;
+  const int cb0 = (int)((long long)blockIdx.y * nbt / gridDim.y), cb1 = (int)((long long)(blockIdx.y + 1) * nbt / gridDim.y);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int row = tid & (T - 1), quarter = tid >> 6;
+  double acc[MAXR];
 #pragma unroll
-      for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
-      for (int rr = 0; rr < T; ++rr) {
-        int r = bi * T + rr;
-        if (r >= n || r >= c) break;
-        double a = A[(long long)c * lda + r];
+  for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
+  for (int cb = cb0; cb < cb1; ++cb) {
+    const int c0 = cb * T;
+    double v[T / 8][2];
+    if (cb >= rb) {
+      // right of (or on) the diagonal: column c of the tile is contiguous in r
 #pragma unroll
-        for (int q = 0; q < MAXR; ++q) acc[q] = fma(a, xi[rr * MAXR + q], acc[q]);
+      for (int u = 0; u < T / 8; ++u) {
+        const int c = c0 + warp + 8 * u;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + h * 32 + lane;
+          v[u][h] = (c < n && r < c) ? __ldcs(A + (long long)c * lda + r) : 0.0;
+        }
       }
-      if (bi == bj) {
+    } else {
+      // left of the diagonal: A(r, c) = A[r*lda + c], contiguous in c
 #pragma unroll
-        for (int q = 0; q < MAXR; ++q) acc[q] = fma(diag[c], xj[tid * MAXR + q], acc[q]);
+      for (int u = 0; u < T / 8; ++u) {
+        const int r = r0 + warp + 8 * u;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = c0 + h * 32 + lane;
+          v[u][h] = (r < n) ? __ldcs(A + (long long)r * lda + c) : 0.0;
+        }
       }
-#pragma unroll
-      for (int q = 0; q < MAXR; ++q)
-        if (q < nrhs) atomicAdd(&Y[(long long)q * n + c], acc[q]);
     }
-  } else if (tid < 2 * T) {
-    int rr = tid - T;
-    int r = bi * T + rr;
-    if (r < n) {
-      double acc[MAXR];
+    __syncthreads();  // the previous tile's reads of sa / xs are done
+    if (cb >= rb) {
 #pragma unroll
-      for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
-      for (int cc = 0; cc < T; ++cc) {
-        int c = bj * T + cc;
-        if (c >= n) break;
-        if (c <= r) continue;
-        double a = A[(long long)c * lda + r];
+      for (int u = 0; u < T / 8; ++u)
 #pragma unroll
-        for (int q = 0; q < MAXR; ++q) acc[q] = fma(a, xj[cc * MAXR + q], acc[q]);
+        for (int h = 0; h < 2; ++h) sa[(warp + 8 * u) * LD + h * 32 + lane] = v[u][h];
+    } else {
+#pragma unroll
+      for (int u = 0; u < T / 8; ++u)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) sa[(h * 32 + lane) * LD + warp + 8 * u] = v[u][h];
+    }
+    for (int idx = tid; idx < T * MAXR; idx += 256) {
+      const int c = idx % T, q = idx / T;
+      xs[c * MAXR + q] = (q < nrhs && c0 + c < n) ? X[(long long)q * ldx + c0 + c] : 0.0;
+    }
+    __syncthreads();
+    if (cb == rb) {
+      // diagonal tile: mirror the strict upper half into the lower, add the diagonal
+      for (int idx = tid; idx < T * T; idx += 256) {
+        const int c = idx / T, r = idx % T;
+        if (r > c) sa[c * LD + r] = sa[r * LD + c];
+        else if (r == c) sa[c * LD + r] = (r0 + r < n) ? diag[r0 + r] : 0.0;
       }
+      __syncthreads();
+    }
+#pragma unroll 4
+    for (int k = 0; k < T / 4; ++k) {
+      const int c = quarter * (T / 4) + k;
+      const double a = sa[c * LD + row];
 #pragma unroll
-      for (int q = 0; q < MAXR; ++q)
-        if (q < nrhs) atomicAdd(&Y[(long long)q * n + r], acc[q]);
+      for (int q = 0; q < MAXR; ++q) acc[q] = fma(a, xs[c * MAXR + q], acc[q]);
+    }
+  }
+  __syncthreads();  // last tile's reads of sa are done
+  if (quarter > 0)
+#pragma unroll
+    for (int q = 0; q < MAXR; ++q) red[((quarter - 1) * T + row) * MAXR + q] = acc[q];
+  __syncthreads();
+  if (quarter == 0 && r0 + row < n) {
+#pragma unroll
+    for (int q = 0; q < MAXR; ++q) {
+      const double y = acc[q] + red[(0 * T + row) * MAXR + q] + red[(1 * T + row) * MAXR + q] +
+                       red[(2 * T + row) * MAXR + q];
+      if (q < nrhs) atomicAdd(&Y[(long long)q * n + r0 + row], y);
     }
   }
 }
@@ -554,7 +597,7 @@ __device__ long long g_solve_clk[2][8];
 template <int RT>
 __global__ void __launch_bounds__(kSolveThreads, 1)
     k_solve_coop(const double* __restrict__ A, long long lda, const double* __restrict__ Linv, int n, int R,
-                 const double* __restrict__ B, double* W, double* Out, int dbg) {
+                 const double* __restrict__ B, double* W, double* Out, int dbg, int skip_fwd) {
   // dbg (phase-breakdown timing only, GBEM_SOLVE_DBG): 1 skip diagonal solves,
   // 2 skip panel updates, 4 skip grid barriers (results wrong for 1/2/4)
   cg::grid_group grid = cg::this_grid();
@@ -594,12 +637,18 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
 #ifdef GBEM_SOLVE_TIMING
   long long t_prev = clock64();
 #endif
-  solve_prefetch_block(Ls, Linv, tid);
-  fwd_prefetch(0);
-  for (long long i = grid.thread_rank(); i < nR; i += grid.size()) W[i] = B[i];
-  grid.sync();
+  if (skip_fwd) {
+    // bordered factorisation: Out already holds y = inv(L) b
+    solve_prefetch_block(Ls, Linv + (size_t)(nblk - 1) * NB * NB, tid);
+    bwd_prefetch(nblk - 1);
+  } else {
+    solve_prefetch_block(Ls, Linv, tid);
+    fwd_prefetch(0);
+    for (long long i = grid.thread_rank(); i < nR; i += grid.size()) W[i] = B[i];
+    grid.sync();
+  }
   // ---- forward: W holds b - sum_{j<k} L_kj y_j, Out receives y
-  for (int b = 0; b < nblk; ++b) {
+  for (int b = 0; b < (skip_fwd ? 0 : nblk); ++b) {
     const int k0 = b * NB, kb = min(NB, n - k0);
     for (int idx = tid; idx < kb * R; idx += blockDim.x) {
       const int i = idx % kb, q = idx / kb;
@@ -694,6 +743,21 @@ __global__ void k_rhs_transpose(const double* __restrict__ in, int n, int R, dou
 
 }  // namespace
 
+// y of the bordered factorisation: border row n + q of column c holds Y(c, q).
+// rowmajor: Y[c * R + q] (blocked solve), else Y[q * n + c] (cooperative solve).
+__global__ void k_border_to_y(const double* __restrict__ A, long long lda, int n, int R, double* __restrict__ Y,
+                              int rowmajor) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)n * R) return;
+  const long long c = i / R;
+  const int q = (int)(i % R);
+  const double v = A[c * lda + n + q];
+  if (rowmajor)
+    Y[i] = v;
+  else
+    Y[(long long)q * n + c] = v;
+}
+
 // Blocked forward/backward substitution on the FP64 tensor cores for wide
 // right-hand-side blocks (R >= 17): the right-hand sides in row-major n x R
 // form W, then per 128-block b
@@ -703,7 +767,7 @@ __global__ void k_rhs_transpose(const double* __restrict__ in, int n, int R, dou
 //             Y_above^T -= X_b^T L_b,above           (k_gemm_g<kSub, NN>)
 // 2 n^2 R flops per solve on DMMA instead of the latency-bound cooperative
 // kernel (whose per-step cost grows with R).
-static int solve_blocked(gbem_ctx* ctx, const double* d_B, int R, double* d_X) {
+static int solve_blocked(gbem_ctx* ctx, const double* d_B, int R, double* d_X, bool y_from_border) {
   const int n = (int)ctx->n;
   const long long lda = ctx->lda;
   cudaStream_t s = ctx->stream;
@@ -727,14 +791,19 @@ static int solve_blocked(gbem_ctx* ctx, const double* d_B, int R, double* d_X) {
     attr = true;
   }
   const dim3 tb(32, 8), tg((n + 31) / 32, (R + 31) / 32);
-  k_rhs_transpose<<<tg, tb, 0, s>>>(d_B, n, R, W, 1);
+  if (y_from_border) {
+    const long long cnt = (long long)n * R;
+    k_border_to_y<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(ctx->d_A, lda, n, R, Y, 1);
+  } else {
+    k_rhs_transpose<<<tg, tb, 0, s>>>(d_B, n, R, W, 1);
+  }
   GBEM_LAUNCH_CHECK(ctx);
   const double* L = ctx->d_A;
   const double* Linv = ctx->d_linv;
   const int vec = (R % 2 == 0 && lda % 2 == 0) ? 1 : 0;
   const int nblk = (n + NB - 1) / NB;
   const unsigned gm = (unsigned)((R + kGT - 1) / kGT);
-  for (int b = 0; b < nblk; ++b) {
+  for (int b = 0; b < (y_from_border ? 0 : nblk); ++b) {
     const int k0 = b * NB, kb = std::min(NB, n - k0), m = n - k0 - kb;
     const double* Lbb = Linv + (size_t)b * NB * NB;
     k_gemm_g<kStore, 0><<<dim3(gm, (kb + kGT - 1) / kGT), kGThreads, kGSmem, s>>>(
@@ -815,8 +884,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   static bool attr_done = false;
   if (!attr_done) {
     GBEM_CUDA(ctx, cudaFuncSetAttribute(kUpdate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UpdShape::SMEM));
-    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt<kStore, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)Shape<NB>::SMEM));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kPotrfSmem));
     attr_done = true;
@@ -850,7 +918,9 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   }
   for (int b = 0; b < nblk; ++b) {
     int k0 = b * NB, kb = std::min(NB, n - k0);
-    int m = n - k0 - kb;
+    // rows below the diagonal block: the remaining matrix rows plus the border
+    // rows of a bordered factorisation (ctx->border, gbem_ctx.cuh)
+    int m = n - k0 - kb + (int)ctx->border;
     double* Akk = ctx->d_A + (long long)k0 * lda + k0;
     double* A21 = Akk + kb;  // rows k0+kb.., cols k0..
     // tail: once the trailing matrix is small the look-ahead has nothing to
@@ -862,9 +932,9 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     k_potrf_diag<<<1, kPotrfThreads, kPotrfSmem, s1>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
     GBEM_LAUNCH_CHECK(ctx);
     if (m > 0) {
-      // L21 = A21 * inv(L11)^T  (in place, one CTA per 128-row strip)
-      k_gemm_nt<kStore, NB><<<dim3((m + BM - 1) / BM, 1), GEMM_THREADS, Shape<NB>::SMEM, s1>>>(
-          A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb, 0, 0);
+      // L21 = A21 * inv(L11)^T  (in place, one CTA per 32-row strip)
+      k_trsm_rows<<<(unsigned)((m + kTrsmRows - 1) / kTrsmRows), kTrsmThreads, kTrsmSmem, s1>>>(
+          A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb);
       GBEM_LAUNCH_CHECK(ctx);
     }
     if (prof) cudaEventRecord(pe[4 * b + 1], s1);
@@ -928,13 +998,15 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
 // Triangular solves L L^T X = B with the stored factor (gbem_internal_factor),
 // residual ||A x - b|| / ||b|| from the preserved upper triangle when d_resid.
 int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
-                                 gbem_solve_stats* stats) {
+                                 gbem_solve_stats* stats, bool y_from_border) {
   const int n = (int)ctx->n;
   const long long lda = ctx->lda;
   if (nrhs < 0 || nrhs > 64) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, 64]");
   if (!ctx->factored) return ctx->fail(GBEM_EINVAL, "no factored matrix in the context");
   if (stats) stats->nrhs = nrhs;
   if (n == 0 || nrhs == 0) return GBEM_OK;
+  if (y_from_border && ctx->border != nrhs)
+    return ctx->fail(GBEM_EINVAL, "bordered solve: the border does not hold nrhs right-hand sides");
   cudaStream_t s = ctx->stream;
   // forward + backward substitution in one cooperative kernel (a grid barrier
   // per block step instead of four launches per block step)
@@ -947,7 +1019,7 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
   cudaEventRecord(ctx->ev[1], s);
   static const int blocked_min = getenv("GBEM_SOLVE_BLOCKED_MIN") ? atoi(getenv("GBEM_SOLVE_BLOCKED_MIN")) : 17;
   if (R >= blocked_min) {
-    rc = solve_blocked(ctx, d_B, R, d_X);
+    rc = solve_blocked(ctx, d_B, R, d_X, y_from_border);
     if (rc) return rc;
   } else {
     const double* cA = ctx->d_A;
@@ -960,8 +1032,15 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
       double* Xq = d_X + (size_t)q0 * n;
       double* Sq = scratch;  // scratch holds n * R >= n * RR
       int dd = dbg;
+      int skip = y_from_border ? 1 : 0;
+      if (y_from_border) {
+        // Sq (the kernel's Out) receives y of columns q0.. from the border rows
+        const long long cnt = (long long)n * RR;
+        k_border_to_y<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(ctx->d_A + q0, lda, n, RR, Sq, 0);
+        GBEM_LAUNCH_CHECK(ctx);
+      }
       void* args[] = {(void*)&cA, (void*)&lda, (void*)&cL, (void*)&nn, (void*)&RR, (void*)&Bq, (void*)&Xq, (void*)&Sq,
-                      (void*)&dd};
+                      (void*)&dd, (void*)&skip};
       // register blocking over the right-hand sides: the smallest instantiated width >= RR
       void* fn = RR <= 1 ? (void*)k_solve_coop<1> : RR <= 2 ? (void*)k_solve_coop<2> : RR <= 4 ? (void*)k_solve_coop<4>
                : RR <= 6 ? (void*)k_solve_coop<6> : RR <= 8 ? (void*)k_solve_coop<8> : (void*)k_solve_coop<16>;
@@ -974,17 +1053,12 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
   if (d_resid) {
     GBEM_CUDA(ctx, cudaMemsetAsync(Ysym, 0, sizeof(double) * (size_t)n * R, s));
     int nbt = (n + 63) / 64;
-    long long ntiles = (long long)nbt * (nbt + 1) / 2;
-    for (int q0 = 0; q0 < R; q0 += 32) {
-      int rq = std::min(32, R - q0);
+    const dim3 sgrid((unsigned)nbt, (unsigned)std::min(kSymvChunks, nbt));
+    for (int q0 = 0; q0 < R; q0 += 8) {
+      int rq = std::min(8, R - q0);
       const double* Xq = d_X + (long long)q0 * n;
       double* Yq = Ysym + (long long)q0 * n;
-      if (rq <= 8)
-        k_symv_upper<8><<<(unsigned)ntiles, 128, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-      else if (rq <= 16)
-        k_symv_upper<16><<<(unsigned)ntiles, 128, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-      else
-        k_symv_upper<32><<<(unsigned)ntiles, 128, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      k_symv_upper<8><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
       GBEM_LAUNCH_CHECK(ctx);
     }
     k_resid_norm<<<R, 256, 0, s>>>(Ysym, d_B, n, d_resid);
