@@ -3,6 +3,9 @@
 #include <new>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "gbem_ctx.cuh"
 
 namespace {
@@ -151,6 +154,14 @@ int gbem_ctx_create(int device, gbem_ctx** out) {
   GBEM_CUDA(ctx, cudaDeviceSetLimit(cudaLimitStackSize, 8192));
   GBEM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
   ctx->stream = ctx->own_stream;
+  // the stream-ordered allocations of a call (work arrays of the host-buffer
+  // entry points) stay cached in the pool instead of going back to the driver
+  // at every synchronisation
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    cuuint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
   for (auto& ev : ctx->ev) GBEM_CUDA(ctx, cudaEventCreate(&ev));
   int rc = gbem_internal_init_tables(ctx);
   *out = ctx;
@@ -183,6 +194,19 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   if (ctx->ev_panel) cudaEventDestroy(ctx->ev_panel);
   if (ctx->ev_col) cudaEventDestroy(ctx->ev_col);
+  if (ctx->g_side) cudaStreamDestroy(ctx->g_side);
+  if (ctx->g_main) cudaStreamDestroy(ctx->g_main);
+  if (ctx->g_main_hi) cudaStreamDestroy(ctx->g_main_hi);
+  for (cudaEvent_t e : {ctx->ev_gs, ctx->ev_ge, ctx->ev_gt, ctx->ev_gra})
+    if (e) cudaEventDestroy(e);
+  if (ctx->green_ctx[0] || ctx->green_ctx[1]) {
+    PFN_cuGreenCtxDestroy p_destroy = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuGreenCtxDestroy", (void**)&p_destroy, cudaEnableDefault, &q) == cudaSuccess &&
+        p_destroy)
+      for (void* g : ctx->green_ctx)
+        if (g) p_destroy((CUgreenCtx)g);
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }

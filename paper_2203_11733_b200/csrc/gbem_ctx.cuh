@@ -67,6 +67,16 @@ struct gbem_ctx {
   cudaEvent_t ev[8] = {};
   cudaStream_t side_stream = nullptr;  // high-priority look-ahead stream of the factorisation
   cudaEvent_t ev_panel = nullptr, ev_col = nullptr;
+  // SM-partitioned factorisation (green contexts): the diagonal-block factor
+  // runs on a reserved SM pair (g_side) while the trailing updates run on the
+  // other SMs (g_main); otherwise the update CTAs fill every SM and the
+  // full-SM factor kernel waits for an SM to drain.  green_state: 0 untried,
+  // 1 available, -1 unavailable (fall back to side_stream in the primary context).
+  int green_state = 0;
+  int green_side_sms = 0;
+  cudaStream_t g_main = nullptr, g_main_hi = nullptr, g_side = nullptr;
+  cudaEvent_t ev_gs = nullptr, ev_ge = nullptr, ev_gt = nullptr, ev_gra = nullptr;
+  void* green_ctx[2] = {nullptr, nullptr};  // CUgreenCtx (side, main)
 
   int fail(int code, const std::string& msg) {
     err = msg;

@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
   int tm, tn;
   if (band > 0) {
     tm = blockIdx.x;
-    tn = blockIdx.y;
+    tn = split + blockIdx.y;
     if (tn > tm) return;
   } else {
     const long long t = blockIdx.x;
@@ -355,19 +355,20 @@ __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
 // M x K strip (column-major, lda), B the N x K inverse of the diagonal factor
 // (column-major, ldb), N, K <= 128; C may alias A (a CTA reads its whole strip
 // before it writes).  One CTA of 4 warps per 32 rows, warp w owns columns
-// [32 w, 32 w + 32): a strip is 1 MFLOP, so the m / 32 CTAs finish in a few
-// microseconds (128-row strips are 4.2 MFLOP each, ~17 us at one SM's DMMA
-// peak, on the factorisation's critical path).
-constexpr int kTrsmRows = 32, kTrsmThreads = 128, kTrsmStages = 3;
+// [32 w, 32 w + 32).  The footprint (<= 128 registers x 128 threads, 34 KB of
+// shared memory in BK = 8 slabs) is at most one trailing-update CTA's, so on a
+// high-priority stream a strip takes the first update slot that frees up
+// instead of waiting for an SM to drain.
+constexpr int kTrsmRows = 32, kTrsmThreads = 128, kTrsmStages = 3, kTrsmBK = 8;
 constexpr int kTrsmLA = kTrsmRows + 8, kTrsmLB = 128 + 8;
-constexpr size_t kTrsmSmem = (size_t)kTrsmStages * BK * (kTrsmLA + kTrsmLB) * sizeof(double);
+constexpr size_t kTrsmSmem = (size_t)kTrsmStages * kTrsmBK * (kTrsmLA + kTrsmLB) * sizeof(double);
 
-static __global__ void __launch_bounds__(kTrsmThreads, 3)
+static __global__ void __launch_bounds__(kTrsmThreads, 4)
     k_trsm_rows(double* C, long long ldc, const double* A, long long lda, const double* __restrict__ B,
                 long long ldb, int M, int N, int K) {
   extern __shared__ __align__(16) double smem[];
-  double* As = smem;                                 // [stages][BK][kTrsmLA]
-  double* Bs = smem + kTrsmStages * BK * kTrsmLA;    // [stages][BK][kTrsmLB]
+  double* As = smem;                                      // [stages][BK][kTrsmLA]
+  double* Bs = smem + kTrsmStages * kTrsmBK * kTrsmLA;    // [stages][BK][kTrsmLB]
   const int m0 = blockIdx.x * kTrsmRows;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
@@ -376,27 +377,24 @@ static __global__ void __launch_bounds__(kTrsmThreads, 3)
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const int KT = (K + BK - 1) / BK;
+  const int KT = (K + kTrsmBK - 1) / kTrsmBK;
   auto load_stage = [&](int kt, int st) {
-    const int k0 = kt * BK;
-    double* as = As + st * BK * kTrsmLA;
-    double* bs = Bs + st * BK * kTrsmLB;
-    {  // A: 16 x 32 doubles = 256 16-byte chunks, 2 per thread
-#pragma unroll
-      for (int c = tid; c < BK * kTrsmRows / 2; c += kTrsmThreads) {
-        const int kk = c / (kTrsmRows / 2), mm = (c % (kTrsmRows / 2)) * 2;
-        const int gk = k0 + kk, gm = m0 + mm;
-        int bytes = 0;
-        const double* src = A;
-        if (gk < K && gm < M) {
-          bytes = gm + 1 < M ? 16 : 8;
-          src = A + (long long)gk * lda + gm;
-        }
-        cp_async16(as + kk * kTrsmLA + mm, src, bytes);
+    const int k0 = kt * kTrsmBK;
+    double* as = As + st * kTrsmBK * kTrsmLA;
+    double* bs = Bs + st * kTrsmBK * kTrsmLB;
+    {  // A: 8 x 32 doubles = 128 16-byte chunks, 1 per thread
+      const int kk = tid / (kTrsmRows / 2), mm = (tid % (kTrsmRows / 2)) * 2;
+      const int gk = k0 + kk, gm = m0 + mm;
+      int bytes = 0;
+      const double* src = A;
+      if (gk < K && gm < M) {
+        bytes = gm + 1 < M ? 16 : 8;
+        src = A + (long long)gk * lda + gm;
       }
+      cp_async16(as + kk * kTrsmLA + mm, src, bytes);
     }
 #pragma unroll
-    for (int c = tid; c < BK * 128 / 2; c += kTrsmThreads) {  // B: 16 x 128, 8 per thread
+    for (int c = tid; c < kTrsmBK * 128 / 2; c += kTrsmThreads) {  // B: 8 x 128, 4 per thread
       const int kk = c / 64, nn = (c % 64) * 2;
       const int gk = k0 + kk;
       int bytes = 0;
@@ -419,10 +417,10 @@ static __global__ void __launch_bounds__(kTrsmThreads, 3)
     const int nxt = kt + kTrsmStages - 1;
     if (nxt < KT) load_stage(nxt, nxt % kTrsmStages);
     cp_async_commit();
-    const double* as = As + (kt % kTrsmStages) * BK * kTrsmLA + g;
-    const double* bs = Bs + (kt % kTrsmStages) * BK * kTrsmLB + warp * 32 + g;
+    const double* as = As + (kt % kTrsmStages) * kTrsmBK * kTrsmLA + g;
+    const double* bs = Bs + (kt % kTrsmStages) * kTrsmBK * kTrsmLB + warp * 32 + g;
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
+    for (int kk = 0; kk < kTrsmBK; kk += 4) {
       double af[4], bf[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = as[(kk + t4) * kTrsmLA + i * 8];

@@ -23,6 +23,9 @@
 #include <cmath>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "gbem_ctx.cuh"
 #include "gbem_common.cuh"
 #include "gbem_dmma_gemm.cuh"
@@ -846,6 +849,65 @@ int ensure_work(gbem_ctx* ctx, size_t elems) {
 
 }  // namespace
 
+// SM partition for the factorisation (green contexts, driver API reached
+// through the runtime's entry-point query: no link-time libcuda dependency).
+// GBEM_GREEN_SIDE = SMs reserved for the diagonal-block factor (default 2).
+static int init_green(gbem_ctx* ctx) {
+  if (ctx->green_state) return ctx->green_state;
+  ctx->green_state = -1;
+  PFN_cuDeviceGet p_get = nullptr;
+  PFN_cuDeviceGetDevResource p_res = nullptr;
+  PFN_cuDevSmResourceSplitByCount p_split = nullptr;
+  PFN_cuDevResourceGenerateDesc p_desc = nullptr;
+  PFN_cuGreenCtxCreate p_create = nullptr;
+  PFN_cuGreenCtxStreamCreate p_stream = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuDeviceGet", (void**)&p_get, cudaEnableDefault, &q) != cudaSuccess || !p_get ||
+      cudaGetDriverEntryPoint("cuDeviceGetDevResource", (void**)&p_res, cudaEnableDefault, &q) != cudaSuccess || !p_res ||
+      cudaGetDriverEntryPoint("cuDevSmResourceSplitByCount", (void**)&p_split, cudaEnableDefault, &q) != cudaSuccess ||
+      !p_split ||
+      cudaGetDriverEntryPoint("cuDevResourceGenerateDesc", (void**)&p_desc, cudaEnableDefault, &q) != cudaSuccess ||
+      !p_desc || cudaGetDriverEntryPoint("cuGreenCtxCreate", (void**)&p_create, cudaEnableDefault, &q) != cudaSuccess ||
+      !p_create ||
+      cudaGetDriverEntryPoint("cuGreenCtxStreamCreate", (void**)&p_stream, cudaEnableDefault, &q) != cudaSuccess ||
+      !p_stream) {
+    cudaGetLastError();
+    return ctx->green_state;
+  }
+  CUdevice dev;
+  if (p_get(&dev, ctx->device) != CUDA_SUCCESS) return ctx->green_state;
+  CUdevResource all, side, rest;
+  if (p_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return ctx->green_state;
+  const int want = getenv("GBEM_GREEN_SIDE") ? atoi(getenv("GBEM_GREEN_SIDE")) : 2;
+  unsigned ng = 1;
+  if (p_split(&side, &ng, &all, &rest, 0, (unsigned)want) != CUDA_SUCCESS || ng != 1) return ctx->green_state;
+  CUdevResourceDesc d_side, d_rest;
+  if (p_desc(&d_side, &side, 1) != CUDA_SUCCESS || p_desc(&d_rest, &rest, 1) != CUDA_SUCCESS) return ctx->green_state;
+  CUgreenCtx g_side, g_main;
+  if (p_create(&g_side, d_side, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return ctx->green_state;
+  if (p_create(&g_main, d_rest, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return ctx->green_state;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  CUstream ss, sm;
+  if (p_stream(&ss, g_side, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS) return ctx->green_state;
+  if (p_stream(&sm, g_main, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return ctx->green_state;
+  CUstream sh;
+  if (p_stream(&sh, g_main, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS) return ctx->green_state;
+  ctx->g_side = (cudaStream_t)ss;
+  ctx->g_main = (cudaStream_t)sm;
+  ctx->g_main_hi = (cudaStream_t)sh;
+  ctx->green_ctx[0] = (void*)g_side;
+  ctx->green_ctx[1] = (void*)g_main;
+  ctx->green_side_sms = (int)side.sm.smCount;
+  if (cudaEventCreateWithFlags(&ctx->ev_gs, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_ge, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_gt, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_gra, cudaEventDisableTiming) != cudaSuccess)
+    return ctx->green_state;
+  ctx->green_state = 1;
+  return ctx->green_state;
+}
+
 // Blocked Cholesky of ctx->d_A (n x n) + solves for nrhs columns of d_B (ld n)
 // into d_X; d_resid[nrhs] optional.
 // Blocked Cholesky of ctx->d_A in place (lower triangle <- L, diagonal saved,
@@ -913,10 +975,136 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   static const bool prof = getenv("GBEM_FACTOR_PROFILE") != nullptr;
   std::vector<cudaEvent_t> pe;
   if (prof) {
-    pe.resize(4 * (size_t)nblk);
+    pe.resize(6 * (size_t)nblk);
     for (auto& e : pe) cudaEventCreate(&e);
   }
-  for (int b = 0; b < nblk; ++b) {
+  static const bool no_green = getenv("GBEM_NO_GREEN") != nullptr;
+  const bool green = !no_green && n >= 2 * tail_rows && init_green(ctx) == 1;
+  if (green) {
+    // Look-ahead on an SM partition.  U(b, c) = update of block column c by
+    // L21 of block b.  Three streams:
+    //   p  (reserved SMs)           potrf(b+1)
+    //   hi (main SMs, high prio.)   trsm(b+1), band(b+1) = U(b+1, b+2)
+    //   lo (main SMs)               rest_a(b) = U(b, b+2), rest_b(b) = U(b, >= b+3)
+    // so the latency-bound chain potrf -> trsm -> band of the next blocks runs
+    // under the bulk trailing update; rest_a splits off the column that the
+    // next band update writes (no two updates of one column run concurrently).
+    // Events: P (potrf done), T (trsm done), B (band done), RA (rest_a done).
+    cudaStream_t lo = ctx->g_main, hi = ctx->g_main_hi, p = ctx->g_side;
+    cudaEvent_t evP = ctx->ev_panel, evB = ctx->ev_col, evT = ctx->ev_gt, evRA = ctx->ev_gra;
+    GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_gs, s));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, ctx->ev_gs, 0));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, ctx->ev_gs, 0));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(p, ctx->ev_gs, 0));
+    constexpr int kBand = NB / 64;  // tile columns per block column
+    auto trailing = [&](int b, int& m, int& nt, double*& A21, double*& A22) {
+      const int k0 = b * NB, kb = std::min(NB, n - k0);
+      m = n - k0 - kb + (int)ctx->border;
+      nt = (m + 63) / 64;
+      A21 = ctx->d_A + (long long)k0 * lda + k0 + kb;
+      A22 = ctx->d_A + (long long)(k0 + kb) * lda + (k0 + kb);
+    };
+    auto potrf = [&](int b, cudaStream_t st) {
+      const int k0 = b * NB, kb = std::min(NB, n - k0);
+      k_potrf_diag<<<1, kPotrfThreads, kPotrfSmem, st>>>(ctx->d_A + (long long)k0 * lda + k0, lda, kb, k0,
+                                                         Linv + (size_t)b * NB * NB, ctx->d_info);
+    };
+    auto trsm = [&](int b, cudaStream_t st) {
+      int m, nt;
+      double *A21, *A22;
+      trailing(b, m, nt, A21, A22);
+      const int kb = std::min(NB, n - b * NB);
+      if (m > 0)
+        k_trsm_rows<<<(unsigned)((m + kTrsmRows - 1) / kTrsmRows), kTrsmThreads, kTrsmSmem, st>>>(
+            A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb);
+    };
+    // U(b, b+1+j) for j = j0 (one block column; tile columns [kBand j0, kBand j0 + kBand))
+    auto update_col = [&](int b, int j0, cudaStream_t st) {
+      int m, nt;
+      double *A21, *A22;
+      trailing(b, m, nt, A21, A22);
+      const int t0 = kBand * j0;
+      if (t0 >= nt) return;
+      kUpdate<<<dim3(nt, std::min(kBand, nt - t0)), UpdShape::THREADS, UpdShape::SMEM, st>>>(
+          A22, lda, A21, lda, m, std::min(NB, n - b * NB), t0, std::min(kBand, nt - t0));
+    };
+    // U(b, >= b+1+j0)
+    auto update_from = [&](int b, int j0, cudaStream_t st) {
+      int m, nt;
+      double *A21, *A22;
+      trailing(b, m, nt, A21, A22);
+      const int t0 = kBand * j0;
+      if (t0 >= nt) return;
+      const long long tiles = (long long)(nt - t0) * (nt - t0 + 1) / 2;
+      kUpdate<<<(unsigned)tiles, UpdShape::THREADS, UpdShape::SMEM, st>>>(A22, lda, A21, lda, m,
+                                                                           std::min(NB, n - b * NB), t0, 0);
+    };
+    int b = 0;
+    // block 0
+    if (prof) cudaEventRecord(pe[0], p);
+    potrf(0, p);
+    GBEM_LAUNCH_CHECK(ctx);
+    if (prof) cudaEventRecord(pe[1], p);
+    GBEM_CUDA(ctx, cudaEventRecord(evP, p));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, evP, 0));
+    trsm(0, hi);
+    GBEM_LAUNCH_CHECK(ctx);
+    GBEM_CUDA(ctx, cudaEventRecord(evT, hi));
+    update_col(0, 0, hi);  // band(0) = U(0, 1)
+    GBEM_LAUNCH_CHECK(ctx);
+    GBEM_CUDA(ctx, cudaEventRecord(evB, hi));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, evT, 0));
+    update_col(0, 1, lo);  // rest_a(0) = U(0, 2)
+    GBEM_LAUNCH_CHECK(ctx);
+    GBEM_CUDA(ctx, cudaEventRecord(evRA, lo));
+    update_from(0, 2, lo);  // rest_b(0) = U(0, >= 3)
+    GBEM_LAUNCH_CHECK(ctx);
+    for (b = 1; b < nblk; ++b) {
+      const int k0 = b * NB;
+      if (n - k0 < tail_rows) break;
+      // potrf(b): block column b is complete once band(b-1) is (band(b-1) waited for rest_a(b-2))
+      GBEM_CUDA(ctx, cudaStreamWaitEvent(p, evB, 0));
+      if (prof) cudaEventRecord(pe[6 * b], p);
+      potrf(b, p);
+      GBEM_LAUNCH_CHECK(ctx);
+      if (prof) cudaEventRecord(pe[6 * b + 1], p);
+      GBEM_CUDA(ctx, cudaEventRecord(evP, p));
+      // trsm(b), band(b) = U(b, b+1) after rest_a(b-1) = U(b-1, b+1)
+      GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, evP, 0));
+      trsm(b, hi);
+      GBEM_LAUNCH_CHECK(ctx);
+      if (prof) cudaEventRecord(pe[6 * b + 2], hi);
+      GBEM_CUDA(ctx, cudaEventRecord(evT, hi));
+      GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, evRA, 0));
+      update_col(b, 0, hi);
+      GBEM_LAUNCH_CHECK(ctx);
+      if (prof) cudaEventRecord(pe[6 * b + 3], hi);
+      GBEM_CUDA(ctx, cudaEventRecord(evB, hi));
+      // rest_a(b), rest_b(b) behind rest_b(b-1) on the low-priority stream
+      GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, evT, 0));
+      if (prof) cudaEventRecord(pe[6 * b + 5], lo);
+      update_col(b, 1, lo);
+      GBEM_LAUNCH_CHECK(ctx);
+      GBEM_CUDA(ctx, cudaEventRecord(evRA, lo));
+      update_from(b, 2, lo);
+      GBEM_LAUNCH_CHECK(ctx);
+      if (prof) cudaEventRecord(pe[6 * b + 4], lo);
+    }
+    // tail: one stream, in order (the band update of the last pipelined block
+    // and everything on hi are joined first)
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, evB, 0));
+    for (; b < nblk; ++b) {
+      potrf(b, lo);
+      GBEM_LAUNCH_CHECK(ctx);
+      trsm(b, lo);
+      GBEM_LAUNCH_CHECK(ctx);
+      update_from(b, 0, lo);
+      GBEM_LAUNCH_CHECK(ctx);
+    }
+    GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_ge, lo));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_ge, 0));
+  }
+  for (int b = 0; b < (green ? 0 : nblk); ++b) {
     int k0 = b * NB, kb = std::min(NB, n - k0);
     // rows below the diagonal block: the remaining matrix rows plus the border
     // rows of a bordered factorisation (ctx->border, gbem_ctx.cuh)
@@ -928,7 +1116,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     const bool tail = n - k0 < tail_rows;
     cudaStream_t s1 = tail ? s : s_side;
     if (!tail) GBEM_CUDA(ctx, cudaStreamWaitEvent(s1, ctx->ev_col, 0));
-    if (prof) cudaEventRecord(pe[4 * b], s1);
+    if (prof) cudaEventRecord(pe[6 * b], s1);
     k_potrf_diag<<<1, kPotrfThreads, kPotrfSmem, s1>>>(Akk, lda, kb, k0, Linv + (size_t)b * NB * NB, ctx->d_info);
     GBEM_LAUNCH_CHECK(ctx);
     if (m > 0) {
@@ -937,12 +1125,12 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
           A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb);
       GBEM_LAUNCH_CHECK(ctx);
     }
-    if (prof) cudaEventRecord(pe[4 * b + 1], s1);
+    if (prof) cudaEventRecord(pe[6 * b + 1], s1);
     if (!tail) {
       GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_panel, s1));
       GBEM_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_panel, 0));
     }
-    if (prof) cudaEventRecord(pe[4 * b + 2], s);
+    if (prof) cudaEventRecord(pe[6 * b + 2], s);
     if (m <= 0) break;
     // A22 -= L21 L21^T on 64 x 64 lower tiles: first the next block column
     // (kBand tile columns), then the rest
@@ -953,7 +1141,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     kUpdate<<<dim3(nt, band), UpdShape::THREADS, UpdShape::SMEM, s>>>(A22, lda, A21, lda, m, kb, 0, band);
     GBEM_LAUNCH_CHECK(ctx);
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_col, s));
-    if (prof) cudaEventRecord(pe[4 * b + 3], s);
+    if (prof) cudaEventRecord(pe[6 * b + 3], s);
     if (nt > kBand) {
       const long long rest = (long long)(nt - kBand) * (nt - kBand + 1) / 2;
       kUpdate<<<(unsigned)rest, UpdShape::THREADS, UpdShape::SMEM, s>>>(A22, lda, A21, lda, m, kb, kBand, 0);
@@ -973,12 +1161,30 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     double side = 0, band = 0, gap = 0;
     for (int b = 0; b < nblk; ++b) {
       float x = 0;
-      if (cudaEventElapsedTime(&x, pe[4 * b], pe[4 * b + 1]) == cudaSuccess) side += x;
-      if (b + 1 < nblk && cudaEventElapsedTime(&x, pe[4 * b + 2], pe[4 * b + 3]) == cudaSuccess) band += x;
-      if (b > 0 && cudaEventElapsedTime(&x, pe[4 * (b - 1) + 3], pe[4 * b]) == cudaSuccess) gap += x;
+      if (cudaEventElapsedTime(&x, pe[6 * b], pe[6 * b + 1]) == cudaSuccess) side += x;
+      if (b + 1 < nblk && cudaEventElapsedTime(&x, pe[6 * b + 2], pe[6 * b + 3]) == cudaSuccess) band += x;
+      if (b > 0 && cudaEventElapsedTime(&x, pe[6 * (b - 1) + 3], pe[6 * b]) == cudaSuccess) gap += x;
     }
-    fprintf(stderr, "[factor profile] n=%d blocks=%d side(potrf+trsm)=%.3f ms band-update=%.3f ms "
-            "band->next-potrf gap=%.3f ms\n", n, nblk, side, band, gap);
+    cudaGetLastError();
+    fprintf(stderr, "[factor profile] n=%d blocks=%d mode=%s side=%.3f ms band-update=%.3f ms "
+            "band->next-potrf gap=%.3f ms\n", n, nblk, green ? "green" : "streams", side, band, gap);
+    if (green) {
+      // per pipelined block (us): potrf, trsm (after potrf), band, rest (rest_a + rest_b on lo)
+      double tp = 0, tt = 0, tb = 0, tr = 0;
+      for (int b = 1; b < nblk && n - b * NB >= tail_rows; ++b) {
+        float pf = 0, t = 0, bd = 0, r = 0;
+        cudaEventElapsedTime(&pf, pe[6 * b], pe[6 * b + 1]);
+        cudaEventElapsedTime(&t, pe[6 * b + 1], pe[6 * b + 2]);
+        cudaEventElapsedTime(&bd, pe[6 * b + 2], pe[6 * b + 3]);
+        cudaEventElapsedTime(&r, pe[6 * b + 5], pe[6 * b + 4]);
+        tp += pf; tt += t; tb += bd; tr += r;
+        if (b % 8 == 1)
+          fprintf(stderr, "  blk %3d potrf %6.1f trsm %6.1f band %6.1f rest(lo) %7.1f\n", b, 1e3 * pf, 1e3 * t, 1e3 * bd,
+                  1e3 * r);
+        cudaGetLastError();
+      }
+      fprintf(stderr, "  totals: potrf %.3f trsm %.3f band %.3f rest(lo) %.3f ms\n", tp, tt, tb, tr);
+    }
     for (auto& e : pe) cudaEventDestroy(e);
   }
   ctx->factored = true;
