@@ -556,14 +556,24 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-// Graded Gauss-Legendre near field (keys 2..9), one thread per pair.
+// Graded Gauss-Legendre near field (keys 2..9): a team of kNearTeam lanes
+// per pair shares its quadrature nodes (gl_graded), partial sums folded by
+// shuffles in a fixed order; the queue is sorted by band, so a warp's teams
+// mostly run the same node counts.
 __global__ void __launch_bounds__(128)
     k_near_gl(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
               const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats) {
   const uint32_t begin = offsets[kClsParallelGL], end = offsets[kClsOrthogonalGL + kNearBands];
+  const int tl = threadIdx.x % kNearTeam;
   long long evals = 0, nonfinite = 0;
-  for (uint32_t idx = begin + blockIdx.x * blockDim.x + threadIdx.x; idx < end; idx += gridDim.x * blockDim.x) {
-    uint64_t e = queue[idx];
+  const uint32_t team = (blockIdx.x * blockDim.x + threadIdx.x) / kNearTeam;
+  const uint32_t nteams = gridDim.x * blockDim.x / kNearTeam;
+  // trip count uniform across the warp (inactive teams run with a dummy pair)
+  const uint32_t warp_team0 = team - (threadIdx.x % 32) / kNearTeam;
+  for (uint32_t base = begin + warp_team0; base < end; base += nteams) {
+    const uint32_t idx = base + (threadIdx.x % 32) / kNearTeam;
+    const bool active = idx < end;
+    uint64_t e = queue[active ? idx : base];
     uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e);
     DPanel Pi = load_panel(P, i), Pj = load_panel(P, j);
     bool swap = d_rect_less(Pj, Pi);
@@ -572,17 +582,27 @@ __global__ void __launch_bounds__(128)
     bool bad = false;
     const bool par = key < (uint32_t)kClsOrthogonalGL;
     const int band = (int)key - (par ? kClsParallelGL : kClsOrthogonalGL);
-    double U = par ? gl_u_parallel(a, b, band, c_nx, c_nw, bad) : gl_u_orthogonal(a, b, band, c_nx, c_nw, bad);
-    evals += 2 * near_nodes(band);
-    store_value(o, i, j, Pi, Pj, U);
-    if (!o.A && o.conv) o.conv[i] = 1;
-    if (bad) {
-      ++nonfinite;
-      atomicMin(&stats[ST_FIRST_BAD], ((unsigned long long)i << 32) | j);
+    double U = par ? gl_u_parallel(a, b, band, c_nx, c_nw, bad, tl)
+                   : gl_u_orthogonal(a, b, band, c_nx, c_nw, bad, tl);
+    int bb = bad ? 1 : 0;
+#pragma unroll
+    for (int off = 1; off < kNearTeam; off <<= 1) {
+      U += __shfl_xor_sync(0xffffffffu, U, off);
+      bb |= __shfl_xor_sync(0xffffffffu, bb, off);
+    }
+    bad = bb != 0;
+    if (active && tl == 0) {
+      evals += 2 * near_nodes(band);
+      store_value(o, i, j, Pi, Pj, U);
+      if (!o.A && o.conv) o.conv[i] = 1;
+      if (bad) {
+        ++nonfinite;
+        atomicMin(&stats[ST_FIRST_BAD], ((unsigned long long)i << 32) | j);
+      }
     }
   }
   if (nonfinite) atomicAdd(&stats[ST_NONFINITE], (unsigned long long)nonfinite);
-  atomicAdd(&stats[ST_NEAR_EVALS], (unsigned long long)evals);
+  if (evals) atomicAdd(&stats[ST_NEAR_EVALS], (unsigned long long)evals);
 }
 
 __global__ void __launch_bounds__(128)
@@ -732,7 +752,7 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
   cudaEventRecord(ctx->ev[3], ctx->stream);
   k_coplanar<<<sms * 4, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o);
   GBEM_LAUNCH_CHECK(ctx);
-  k_near_gl<<<sms * 4, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, ctx->d_stats);
+  k_near_gl<<<sms * 8, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, ctx->d_stats);
   GBEM_LAUNCH_CHECK(ctx);
   k_near_warp<<<sms * 8, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o,
                                                 cfg.rel_tol, cfg.max_levels, ctx->d_stats);

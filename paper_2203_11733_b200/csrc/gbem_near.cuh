@@ -483,9 +483,15 @@ __host__ __device__ constexpr int near_nodes(int band) {
   return band == 0 ? 20 : band == 1 ? 24 : band == 2 ? 32 : 48;
 }
 
+// A pair's nodes are shared by a team of kNearTeam consecutive lanes: lane tl
+// of the team evaluates nodes tl, tl + kNearTeam, ...; the functions below
+// return that lane's partial sum (linear in the nodes) and the kernel sums
+// the team's partials (k_near_gl).
+constexpr int kNearTeam = 4;
+
 template <class F>
 __device__ double gl_graded(const F& f, double a, double b, int band, const double (*nx)[48],
-                            const double (*nw)[48], bool& bad) {
+                            const double (*nw)[48], bool& bad, int tl) {
   if (a == b) return 0.0;
   const int n = near_nodes(band);
   const double m = 0.5 * (a + b);
@@ -497,7 +503,7 @@ __device__ double gl_graded(const F& f, double a, double b, int band, const doub
     const double h = 0.5 * sqrt(len);
     double part = 0.0;
 #pragma unroll 1
-    for (int i = 0; i < n; ++i) {
+    for (int i = tl; i < n; i += kNearTeam) {
       const double t = fma(h, nx[band][i], h);
       const double x = side ? base - t * t : base + t * t;
       const double v = f(x);
@@ -511,7 +517,7 @@ __device__ double gl_graded(const F& f, double a, double b, int band, const doub
 
 // uParallelOffset (kernels.hpp:138-153) with the graded Gauss rule.
 __device__ inline double gl_u_parallel(const DPanel& A, const DPanel& B, int band, const double (*nx)[48],
-                                       const double (*nw)[48], bool& bad) {
+                                       const double (*nw)[48], bool& bad, int tl) {
   double off = A.level - B.level;
   ParIntegrandFast f;
   Corners c(A.a0, A.a1, B.a0, B.a1);
@@ -531,20 +537,21 @@ __device__ inline double gl_u_parallel(const DPanel& A, const DPanel& B, int ban
   for (int i = 0; i < n; ++i)
     if (count == 0 || pts[i] > cuts[count - 1]) cuts[count++] = pts[i];
   double total = 0.0;
-  for (int i = 0; i + 1 < count; ++i) total += gl_graded(f, cuts[i], cuts[i + 1], band, nx, nw, bad);
+  for (int i = 0; i + 1 < count; ++i) total += gl_graded(f, cuts[i], cuts[i + 1], band, nx, nw, bad, tl);
   return total / kFourPi;
 }
 
 template <class F>
 __device__ double gl_split0(const F& f, double a, double b, int band, const double (*nx)[48],
-                            const double (*nw)[48], bool& bad) {
-  if (a < 0.0 && 0.0 < b) return gl_graded(f, a, 0.0, band, nx, nw, bad) + gl_graded(f, 0.0, b, band, nx, nw, bad);
-  return gl_graded(f, a, b, band, nx, nw, bad);
+                            const double (*nw)[48], bool& bad, int tl) {
+  if (a < 0.0 && 0.0 < b)
+    return gl_graded(f, a, 0.0, band, nx, nw, bad, tl) + gl_graded(f, 0.0, b, band, nx, nw, bad, tl);
+  return gl_graded(f, a, b, band, nx, nw, bad, tl);
 }
 
 // orthFrame + uOrthogonal (kernels.hpp:175-214, 245-255) with the graded Gauss rule.
 __device__ inline double gl_u_orthogonal(const DPanel& A, const DPanel& B, int band, const double (*nx)[48],
-                                         const double (*nw)[48], bool& bad) {
+                                         const double (*nw)[48], bool& bad, int tl) {
   int shared = 3 - A.axis - B.axis;
   double s1lo, s1hi, t1lo, t1hi, i3lo, i3hi, j2lo, j2hi;
   panel_extent(A, shared, s1lo, s1hi);
@@ -568,8 +575,8 @@ __device__ inline double gl_u_orthogonal(const DPanel& A, const DPanel& B, int b
   fy.x3d = s3lo;
   fy.x3u = s3hi;
   fy.guard = fx.guard;
-  double tx = gl_split0(fx, s3lo, s3hi, band, nx, nw, bad);
-  double ty = gl_split0(fy, t2lo, t2hi, band, nx, nw, bad);
+  double tx = gl_split0(fx, s3lo, s3hi, band, nx, nw, bad, tl);
+  double ty = gl_split0(fy, t2lo, t2hi, band, nx, nw, bad, tl);
   return (tx + ty) / kFourPi;
 }
 
