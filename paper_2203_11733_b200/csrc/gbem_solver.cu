@@ -1039,56 +1039,82 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       kUpdate<<<(unsigned)tiles, UpdShape::THREADS, UpdShape::SMEM, st>>>(A22, lda, A21, lda, m,
                                                                            std::min(NB, n - b * NB), t0, 0);
     };
-    int b = 0;
-    // block 0
-    if (prof) cudaEventRecord(pe[0], p);
-    potrf(0, p);
-    GBEM_LAUNCH_CHECK(ctx);
-    if (prof) cudaEventRecord(pe[1], p);
-    GBEM_CUDA(ctx, cudaEventRecord(evP, p));
-    GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, evP, 0));
-    trsm(0, hi);
-    GBEM_LAUNCH_CHECK(ctx);
-    GBEM_CUDA(ctx, cudaEventRecord(evT, hi));
-    update_col(0, 0, hi);  // band(0) = U(0, 1)
-    GBEM_LAUNCH_CHECK(ctx);
-    GBEM_CUDA(ctx, cudaEventRecord(evB, hi));
-    GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, evT, 0));
-    update_col(0, 1, lo);  // rest_a(0) = U(0, 2)
-    GBEM_LAUNCH_CHECK(ctx);
-    GBEM_CUDA(ctx, cudaEventRecord(evRA, lo));
-    update_from(0, 2, lo);  // rest_b(0) = U(0, >= 3)
-    GBEM_LAUNCH_CHECK(ctx);
-    for (b = 1; b < nblk; ++b) {
-      const int k0 = b * NB;
-      if (n - k0 < tail_rows) break;
-      // potrf(b): block column b is complete once band(b-1) is (band(b-1) waited for rest_a(b-2))
+    // Super-blocks of two 128-column blocks: the diagonal factors and panel
+    // trsms stay at 128 columns (chain on p / hi), the trailing update of a
+    // super-block is one K = 256 DMMA update (band2: the next super-block's
+    // columns, then rest2: everything right of it), which amortises each
+    // tile's C read-modify-write over twice the flops of a K = 128 update.
+    //   p/hi: stepA(s+1) = potrf, trsm, U(b, b+1), potrf, trsm   (after band2(s))
+    //   lo:   band2(s) -> rest2(s) -> [T(s+1)] band2(s+1) -> ...
+    // U(., c) for one column never runs concurrently on two streams.
+    auto stepA = [&](int b0, int nb) -> int {
       GBEM_CUDA(ctx, cudaStreamWaitEvent(p, evB, 0));
-      if (prof) cudaEventRecord(pe[6 * b], p);
-      potrf(b, p);
-      GBEM_LAUNCH_CHECK(ctx);
-      if (prof) cudaEventRecord(pe[6 * b + 1], p);
-      GBEM_CUDA(ctx, cudaEventRecord(evP, p));
-      // trsm(b), band(b) = U(b, b+1) after rest_a(b-1) = U(b-1, b+1)
-      GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, evP, 0));
-      trsm(b, hi);
-      GBEM_LAUNCH_CHECK(ctx);
-      if (prof) cudaEventRecord(pe[6 * b + 2], hi);
+      for (int k = 0; k < nb; ++k) {
+        const int bb = b0 + k;
+        if (k > 0) {
+          update_col(b0, 0, hi);  // U(b0, b0 + 1)
+          GBEM_LAUNCH_CHECK(ctx);
+          GBEM_CUDA(ctx, cudaEventRecord(evB, hi));
+          GBEM_CUDA(ctx, cudaStreamWaitEvent(p, evB, 0));
+        }
+        if (prof) cudaEventRecord(pe[6 * bb], p);
+        potrf(bb, p);
+        GBEM_LAUNCH_CHECK(ctx);
+        if (prof) cudaEventRecord(pe[6 * bb + 1], p);
+        GBEM_CUDA(ctx, cudaEventRecord(evP, p));
+        GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, evP, 0));
+        trsm(bb, hi);
+        GBEM_LAUNCH_CHECK(ctx);
+        if (prof) cudaEventRecord(pe[6 * bb + 2], hi);
+      }
       GBEM_CUDA(ctx, cudaEventRecord(evT, hi));
-      GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, evRA, 0));
-      update_col(b, 0, hi);
-      GBEM_LAUNCH_CHECK(ctx);
-      if (prof) cudaEventRecord(pe[6 * b + 3], hi);
-      GBEM_CUDA(ctx, cudaEventRecord(evB, hi));
-      // rest_a(b), rest_b(b) behind rest_b(b-1) on the low-priority stream
+      return GBEM_OK;
+    };
+    // U([b0, b0 + nb), block columns >= b0 + nb + j0): band (j0 = 0, one super-
+    // block of kBand2 tile columns) or triangular rest (j0 = 2)
+    constexpr int kBand2 = 2 * kBand;
+    auto update2 = [&](int b0, int nb, bool band_part) {
+      const int k0 = b0 * NB, kw = std::min(nb * NB, n - k0);
+      const int m = n - k0 - kw + (int)ctx->border;
+      if (m <= 0) return;
+      const int nt = (m + 63) / 64;
+      double* A21 = ctx->d_A + (long long)k0 * lda + k0 + kw;
+      double* A22 = ctx->d_A + (long long)(k0 + kw) * lda + (k0 + kw);
+      if (band_part) {
+        kUpdate<<<dim3(nt, std::min(kBand2, nt)), UpdShape::THREADS, UpdShape::SMEM, lo>>>(A22, lda, A21, lda, m, kw,
+                                                                                            0, std::min(kBand2, nt));
+      } else if (nt > kBand2) {
+        const long long tiles = (long long)(nt - kBand2) * (nt - kBand2 + 1) / 2;
+        kUpdate<<<(unsigned)tiles, UpdShape::THREADS, UpdShape::SMEM, lo>>>(A22, lda, A21, lda, m, kw, kBand2, 0);
+      }
+    };
+    GBEM_CUDA(ctx, cudaEventRecord(evB, p));  // stepA(0) waits on nothing
+    int b = 0;
+    int rc2 = stepA(0, std::min(2, nblk));
+    if (rc2) return rc2;
+    for (;;) {
+      const int nb = std::min(2, nblk - b), next = b + nb;
       GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, evT, 0));
       if (prof) cudaEventRecord(pe[6 * b + 5], lo);
-      update_col(b, 1, lo);
+      if (next >= nblk) {  // the last super-block: its trsm covered the border rows
+        update2(b, nb, true);
+        GBEM_LAUNCH_CHECK(ctx);
+        b = nblk;
+        break;
+      }
+      update2(b, nb, true);  // band2(b): block columns next, next + 1
       GBEM_LAUNCH_CHECK(ctx);
-      GBEM_CUDA(ctx, cudaEventRecord(evRA, lo));
-      update_from(b, 2, lo);
+      GBEM_CUDA(ctx, cudaEventRecord(evB, lo));
+      const bool next_tail = n - next * NB < tail_rows;
+      if (!next_tail) {
+        rc2 = stepA(next, std::min(2, nblk - next));
+        if (rc2) return rc2;
+      }
+      update2(b, nb, false);  // rest2(b)
       GBEM_LAUNCH_CHECK(ctx);
       if (prof) cudaEventRecord(pe[6 * b + 4], lo);
+      b = next;
+      if (next_tail) break;
     }
     // tail: one stream, in order (the band update of the last pipelined block
     // and everything on hi are joined first)
@@ -1169,21 +1195,19 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     fprintf(stderr, "[factor profile] n=%d blocks=%d mode=%s side=%.3f ms band-update=%.3f ms "
             "band->next-potrf gap=%.3f ms\n", n, nblk, green ? "green" : "streams", side, band, gap);
     if (green) {
-      // per pipelined block (us): potrf, trsm (after potrf), band, rest (rest_a + rest_b on lo)
-      double tp = 0, tt = 0, tb = 0, tr = 0;
-      for (int b = 1; b < nblk && n - b * NB >= tail_rows; ++b) {
-        float pf = 0, t = 0, bd = 0, r = 0;
+      // per pipelined block (us): potrf, trsm (after potrf); per super-block: band2 + rest2 on lo
+      double tp = 0, tt = 0, tr = 0;
+      for (int b = 0; b < nblk && n - b * NB >= tail_rows; ++b) {
+        float pf = 0, t = 0, r = 0;
         cudaEventElapsedTime(&pf, pe[6 * b], pe[6 * b + 1]);
         cudaEventElapsedTime(&t, pe[6 * b + 1], pe[6 * b + 2]);
-        cudaEventElapsedTime(&bd, pe[6 * b + 2], pe[6 * b + 3]);
-        cudaEventElapsedTime(&r, pe[6 * b + 5], pe[6 * b + 4]);
-        tp += pf; tt += t; tb += bd; tr += r;
-        if (b % 8 == 1)
-          fprintf(stderr, "  blk %3d potrf %6.1f trsm %6.1f band %6.1f rest(lo) %7.1f\n", b, 1e3 * pf, 1e3 * t, 1e3 * bd,
-                  1e3 * r);
+        if (b % 2 == 0) cudaEventElapsedTime(&r, pe[6 * b + 5], pe[6 * b + 4]);
+        tp += pf; tt += t; tr += r;
+        if (b % 8 == 0)
+          fprintf(stderr, "  blk %3d potrf %6.1f trsm %6.1f update2(lo) %7.1f\n", b, 1e3 * pf, 1e3 * t, 1e3 * r);
         cudaGetLastError();
       }
-      fprintf(stderr, "  totals: potrf %.3f trsm %.3f band %.3f rest(lo) %.3f ms\n", tp, tt, tb, tr);
+      fprintf(stderr, "  totals: potrf %.3f trsm %.3f update2(lo) %.3f ms\n", tp, tt, tr);
     }
     for (auto& e : pe) cudaEventDestroy(e);
   }
