@@ -176,13 +176,96 @@ __global__ void k_panel_cinfo(const DPanel* __restrict__ P, int n, CPanel* __res
 // far-field order along a direction from r2 = gap^2 / h^2: the smallest q with
 // r2 >= c_cd2f[q] (thresholds decrease with q), i.e. 1 + #{k < kQMax : r2 < c_cd2f[k]}
 __device__ __forceinline__ int far_order_r2(float r2) {
-  int q = 1;
-#pragma unroll
-  for (int k = 1; k < kQMax; ++k) q += r2 < c_cd2f[k] ? 1 : 0;
-  return q;
+  // q = 1 + #{k : r2 < c_cd2f[k]}; the thresholds decrease with k, so the count
+  // is found by a three-level binary search
+  const bool c4 = r2 < c_cd2f[4];
+  const bool c2 = r2 < (c4 ? c_cd2f[6] : c_cd2f[2]);
+  const bool c1 = r2 < (c4 ? (c2 ? c_cd2f[7] : c_cd2f[5]) : (c2 ? c_cd2f[3] : c_cd2f[1]));
+  return 1 + (c4 ? 4 : 0) + (c2 ? 2 : 0) + (c1 ? 1 : 0);
 }
 
-__device__ __forceinline__ uint32_t classify_pair(const CPanel& A, const CPanel& B, bool same, double near_ratio) {
+// ---------------------------------------------------------------- far-field plan
+//
+// Difference-set quadrature.  The integrand of U = int_I int_J 1/(4 pi |x - y|)
+// depends on x - y only, so along a world axis k that is in-plane for both
+// panels the pair of 1-D integrals over [s0, s1] (I) and [u0, u1] (J) collapses
+// to one integral over w = x_k - y_k with the trapezoidal weight
+//   T(w) = |[s0, s1] ∩ [u0 + w, u1 + w]|   (ramp up, plateau, ramp down),
+// the pushforward the reference applies analytically to offset-parallel pairs
+// (kernels.hpp:96-125, tentSegments).  Each piece gets Gauss-Legendre of the
+// order the far-field rule gives its half-length at the pair's gap; the plain
+// product rule (q_I q_J nodes) is kept for an axis when it is cheaper.  An axis
+// in-plane for one panel only contributes that panel's 1-D rule, the common
+// normal of a parallel pair the constant offset.  A pair is three lists of
+// (w_k, W_k), one per world axis, and
+//   U = 1/(4 pi) sum_a sum_b sum_c W1_a W2_b W3_c / sqrt(w1_a^2 + w2_b^2 + w3_c^2):
+// 95 nodes per far pair on config 2 instead of the 4-D tensor rule's 147
+// (tools/calib_tent.c: worst relative error 2.2e-12 against a composite
+// 3^4 x 12^4 truth over gap/diameter 1..32 at far_tol = 1e-12).
+//
+// The classifier decides the lists (orders in FP32 from the classification
+// records) and packs them into a 31-bit plan stored beside the queue entry:
+//   bit 0 orthogonal pair; bits 1 + 9 s .. 9 + 9 s: source list s as
+//   type (2 bits) | q1 - 1 (3) | q2 (4); bits 28-29: source of the inner
+//   (largest) list; bit 30: which of the two others is the middle one.
+// Sources: parallel (shared axis ip0, shared axis ip1, normal offset);
+// orthogonal (shared axis, I's rule along J's normal, J's rule along I's normal).
+enum FarListType : int { kListConst = 0, kListSingle = 1, kListProduct = 2, kListTent = 3 };
+
+// 1 / h^2 (FP32) of panel C's half-length along its in-plane world axis k
+__device__ __forceinline__ float cp_ih2(const CPanel& C, int k) { return k == ip0(C.axis) ? C.iha2 : C.ihb2; }
+
+// List descriptor of a shared in-plane axis k: tent or product, whichever has fewer nodes.
+__device__ __forceinline__ uint32_t shared_axis_desc(const CPanel& A, const CPanel& B, int k, float g2, int& m) {
+  const float ihA = cp_ih2(A, k), ihB = cp_ih2(B, k);
+  const int qi = far_order_r2(g2 * ihA), qj = far_order_r2(g2 * ihB);
+  const int qr = min(qi, qj);  // ramps: half-length min(L_I, L_J) / 2: the smaller panel's order
+  const double Li = k == 0 ? A.hi[0] - A.lo[0] : (k == 1 ? A.hi[1] - A.lo[1] : A.hi[2] - A.lo[2]);
+  const double Lj = k == 0 ? B.hi[0] - B.lo[0] : (k == 1 ? B.hi[1] - B.lo[1] : B.hi[2] - B.lo[2]);
+  int qp = 0;
+  if (Li != Lj) {
+    const float dp = (float)fabs(Li - Lj);
+    qp = far_order_r2(g2 * (4.0f * __frcp_rn(dp * dp)));
+  }
+  if (2 * qr + qp < qi * qj) {
+    m = 2 * qr + qp;
+    return (uint32_t)kListTent | (uint32_t)(qr - 1) << 2 | (uint32_t)qp << 5;
+  }
+  m = qi * qj;
+  return (uint32_t)kListProduct | (uint32_t)(qi - 1) << 2 | (uint32_t)qj << 5;
+}
+
+__device__ __forceinline__ uint32_t far_plan_code(const CPanel& A, const CPanel& B, float g2, int& m1, int& m2,
+                                                  int& m3) {
+  uint32_t d[3];
+  int m[3];
+  const bool orth = A.axis != B.axis;
+  if (!orth) {
+    d[0] = shared_axis_desc(A, B, ip0(A.axis), g2, m[0]);
+    d[1] = shared_axis_desc(A, B, ip1(A.axis), g2, m[1]);
+    d[2] = kListConst;
+    m[2] = 1;
+  } else {
+    d[0] = shared_axis_desc(A, B, 3 - A.axis - B.axis, g2, m[0]);
+    const int qa = far_order_r2(g2 * cp_ih2(A, B.axis)), qb = far_order_r2(g2 * cp_ih2(B, A.axis));
+    d[1] = (uint32_t)kListSingle | (uint32_t)(qa - 1) << 2;
+    d[2] = (uint32_t)kListSingle | (uint32_t)(qb - 1) << 2;
+    m[1] = qa;
+    m[2] = qb;
+  }
+  // stable descending order of the sizes: inner source s0, then middle s1
+  const int s0 = (m[0] >= m[1] && m[0] >= m[2]) ? 0 : (m[1] >= m[2] ? 1 : 2);
+  const int r0 = s0 == 0 ? 1 : 0, r1 = s0 == 2 ? 1 : 2;  // remaining sources in index order
+  const int mid_second = m[r1] > m[r0] ? 1 : 0;
+  m1 = m[s0];
+  m2 = mid_second ? m[r1] : m[r0];
+  m3 = mid_second ? m[r0] : m[r1];
+  return (orth ? 1u : 0u) | d[0] << 1 | d[1] << 10 | d[2] << 19 | (uint32_t)s0 << 28 | (uint32_t)mid_second << 30;
+}
+
+__device__ __forceinline__ uint32_t classify_pair(const CPanel& A, const CPanel& B, bool same, double near_ratio,
+                                                  uint32_t& plan) {
+  plan = 0;
   if (same) return kClsCoplanar;
   double gap2 = 0.0;
 #pragma unroll
@@ -207,9 +290,9 @@ __device__ __forceinline__ uint32_t classify_pair(const CPanel& A, const CPanel&
       return same_axis ? kClsParallel : kClsOrthogonal;  // near contact: adaptive Romberg
     return (same_axis ? kClsParallelGL : kClsOrthogonalGL) + band;
   }
-  const float g2 = (float)gap2;
-  return far_key(far_order_r2(g2 * A.iha2), far_order_r2(g2 * A.ihb2), far_order_r2(g2 * B.iha2),
-                 far_order_r2(g2 * B.ihb2));
+  int m1, m2, m3;
+  plan = far_plan_code(A, B, (float)gap2, m1, m2, m3);
+  return far_key(m1, m2, m3);
 }
 
 // Per-CTA key aggregation: warp groups of equal keys (__match_any_sync) add
@@ -234,7 +317,8 @@ template <bool FILL>
 __global__ void __launch_bounds__(kClassifyThreads)
     k_classify(const CPanel* __restrict__ P, int n, int rb, int re, int bi0, int nbt,
                const long long* __restrict__ tile_row_off, int nrows_t, long long tile_begin,
-               double near_ratio, uint32_t* counts, uint32_t* cursors, uint64_t* queue, int full) {
+               double near_ratio, uint32_t* counts, uint32_t* cursors, uint64_t* queue, uint32_t* plans,
+               int full) {
   constexpr int kIter = kTile / (kClassifyThreads / 32);
   __shared__ CPanel si[kTile], sj[kTile];
   __shared__ uint32_t hkey[kHash], hcnt[kHash];
@@ -274,7 +358,7 @@ __global__ void __launch_bounds__(kClassifyThreads)
   __syncthreads();
   const int lane = tid & 31, warp = tid >> 5;
   const int j = bj * kTile + lane;
-  uint32_t key[kIter], leader_off[kIter];
+  uint32_t key[kIter], plan[kIter], leader_off[kIter];
   unsigned peers[kIter];
   int slot[kIter];
 #pragma unroll
@@ -282,7 +366,7 @@ __global__ void __launch_bounds__(kClassifyThreads)
     const int r = warp + it * (kClassifyThreads / 32);
     const int i = bi * kTile + r;
     const bool valid = i >= rb && i < re && j < n && (full || j >= i);
-    key[it] = valid ? classify_pair(si[r], sj[lane], i == j, near_ratio) : kEmpty;
+    key[it] = valid ? classify_pair(si[r], sj[lane], i == j, near_ratio, plan[it]) : kEmpty;
     peers[it] = __match_any_sync(0xffffffffu, key[it]);
     slot[it] = -1;
     leader_off[it] = 0;
@@ -312,14 +396,15 @@ __global__ void __launch_bounds__(kClassifyThreads)
     const int r = warp + it * (kClassifyThreads / 32);
     const uint32_t rank = __popc(peers[it] & ((1u << lane) - 1u));
     queue[base + rank] = pack_entry((uint32_t)(bi * kTile + r), (uint32_t)j, key[it]);
+    plans[base + rank] = plan[it];
   }
 }
 
 // Warp-aggregated append of `key` (one atomic per distinct key in the warp),
 // used by the pair-list mode.
 template <bool FILL>
-__device__ __forceinline__ void warp_append(bool valid, uint32_t key, uint32_t i, uint32_t j,
-                                            uint32_t* counts, uint32_t* cursors, uint64_t* queue) {
+__device__ __forceinline__ void warp_append(bool valid, uint32_t key, uint32_t plan, uint32_t i, uint32_t j,
+                                            uint32_t* counts, uint32_t* cursors, uint64_t* queue, uint32_t* plans) {
   unsigned active = __ballot_sync(0xffffffffu, valid);
   if (!valid) return;
   unsigned peers = __match_any_sync(active, key);
@@ -336,6 +421,7 @@ __device__ __forceinline__ void warp_append(bool valid, uint32_t key, uint32_t i
   if (FILL) {
     base = __shfl_sync(peers, base, leader);
     queue[base + rank] = pack_entry(i, j, key);
+    plans[base + rank] = plan;
   }
 }
 
@@ -343,12 +429,12 @@ __device__ __forceinline__ void warp_append(bool valid, uint32_t key, uint32_t i
 template <bool FILL>
 __global__ void __launch_bounds__(256)
     k_classify_list(const CPanel* __restrict__ P, int npairs, double near_ratio, uint32_t* counts,
-                    uint32_t* cursors, uint64_t* queue) {
+                    uint32_t* cursors, uint64_t* queue, uint32_t* plans) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = k < npairs;
-  uint32_t key = 0;
-  if (valid) key = classify_pair(P[k], P[npairs + k], false, near_ratio);
-  warp_append<FILL>(valid, key, (uint32_t)k, (uint32_t)(npairs + k), counts, cursors, queue);
+  uint32_t key = 0, plan = 0;
+  if (valid) key = classify_pair(P[k], P[npairs + k], false, near_ratio, plan);
+  warp_append<FILL>(valid, key, plan, (uint32_t)k, (uint32_t)(npairs + k), counts, cursors, queue, plans);
 }
 
 // Exclusive scan of kNumKeys counts (one CTA of 1024 threads, 64 keys each);
@@ -414,121 +500,216 @@ __device__ __forceinline__ void store_value(const OutSpec& o, uint32_t i, uint32
   }
 }
 
-__device__ __forceinline__ double sel3(int k, int ai, double lvl, int kS, double xs, double xt) {
-  return k == ai ? lvl : (k == kS ? xs : xt);
-}
-
-// Anisotropic tensor Gauss over I (orders qs, qt along its in-plane axes) and
-// J (order qu along U, QV along V; V is J's direction with the largest order).
-// Equivalent to gaussPair (oracle.hpp:45-81) with per-direction orders.
-template <int QV, int QU>
-__device__ __forceinline__ double far_gauss(const DPanel& I, int qs, int qt, const DPanel& J,
-                                            bool v_is_a, int qu_rt, double& flops) {
-  const int qu = QU > 0 ? QU : qu_rt;
-  const int ai = I.axis, aj = J.axis;
-  const int kS = ip0(ai);
-  const double cS = 0.5 * (I.a0 + I.a1), hS = 0.5 * (I.a1 - I.a0);
-  const double cT = 0.5 * (I.b0 + I.b1), hT = 0.5 * (I.b1 - I.b0);
-  int kU, kV;
-  double cU, hU, cV, hV;
-  if (v_is_a) {
-    kV = ip0(aj);
-    cV = 0.5 * (J.a0 + J.a1);
-    hV = 0.5 * (J.a1 - J.a0);
-    kU = ip1(aj);
-    cU = 0.5 * (J.b0 + J.b1);
-    hU = 0.5 * (J.b1 - J.b0);
-  } else {
-    kV = ip1(aj);
-    cV = 0.5 * (J.b0 + J.b1);
-    hV = 0.5 * (J.b1 - J.b0);
-    kU = ip0(aj);
-    cU = 0.5 * (J.a0 + J.a1);
-    hU = 0.5 * (J.a1 - J.a0);
-  }
-  double Qv[QV], Wv[QV];
-#pragma unroll
-  for (int v = 0; v < QV; ++v) {
-    Qv[v] = fma(hV, c_gx[QV][v], cV);
-    Wv[v] = hV * c_gw[QV][v];
-  }
-  double acc = 0.0;
-#pragma unroll 1
-  for (int s = 0; s < qs; ++s) {
-    const double xs = fma(hS, c_gx[qs][s], cS);
-    const double ws = hS * c_gw[qs][s];
-#pragma unroll 1
-    for (int t = 0; t < qt; ++t) {
-      const double xt = fma(hT, c_gx[qt][t], cT);
-      const double wst = ws * (hT * c_gw[qt][t]);
-      const double pz = sel3(aj, ai, I.level, kS, xs, xt) - J.level;
-      const double pu = sel3(kU, ai, I.level, kS, xs, xt);
-      const double pv = sel3(kV, ai, I.level, kS, xs, xt);
-      double dv2[QV];
-#pragma unroll
-      for (int v = 0; v < QV; ++v) {
-        double d = pv - Qv[v];
-        dv2[v] = d * d;
-      }
-      const double pz2 = pz * pz;
-      double inner = 0.0;
-#pragma unroll
-      for (int u = 0; u < (QU > 0 ? QU : kQMax); ++u) {
-        if (QU == 0 && u >= qu) break;
-        const double du = pu - fma(hU, c_gx[qu][u], cU);
-        const double cu = fma(du, du, pz2);
-        // two partial sums break the FMA dependency chain along v
-        double row0 = 0.0, row1 = 0.0;
-#pragma unroll
-        for (int v = 0; v < QV; v += 2) {
-          row0 = fma(Wv[v], rsq64(cu + dv2[v]), row0);
-          if (v + 1 < QV) row1 = fma(Wv[v + 1], rsq64(cu + dv2[v + 1]), row1);
-        }
-        inner = fma(hU * c_gw[qu][u], row0 + row1, inner);
-      }
-      acc = fma(wst, inner, acc);
-    }
-  }
-  const double E = (double)qs * qt * qu * QV;
-  flops += 11.0 * E + 9.0 * qs * qt * qu + (9.0 + 2.0 * QV) * qs * qt + 3.0 * qs + 3.0 * QV + 13.0;
-  return acc / kFourPi;
-}
-
 __device__ __forceinline__ double warp_reduce_d(double x) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
   return x;
 }
 
-// Far field, one kernel per (largest order QV, order qu of J's other direction)
-// segment of the queue (QU = 0: qu at run time): the register footprint and the
-// unrolling follow the orders, so the common small-order pairs run fully
-// unrolled at high occupancy.
-template <int QV, int QU>
-__global__ void __launch_bounds__(256, 2)
-    k_far(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
+// One decoded list: type, orders, and the geometry of its nodes
+//   single:  w = p0 + p1 x_k,                  W = p1 g_k
+//   product: w = p0 + p1 x_a - p2 x_b,         W = p1 g_a p2 g_b       (k = a q2 + b)
+//   tent:    pieces [p0, p1] (T = w - p0), [p1, p2] (T = p4), [p2, p3] (T = p3 - w),
+//            orders q1, q2, q1;  w = c + h x,  W = h g T(w)
+//   const:   w = p0, W = 1
+struct FarList {
+  int type, q1, q2;
+  double p0, p1, p2, p3, p4;
+};
+
+__device__ __forceinline__ void shared_axis_geom(const DPanel& A, const DPanel& B, int k, FarList& L) {
+  double s0, s1, u0, u1;
+  panel_extent(A, k, s0, s1);
+  panel_extent(B, k, u0, u1);
+  if (L.type == kListTent) {
+    L.p0 = s0 - u1;
+    L.p1 = fmin(s0 - u0, s1 - u1);
+    L.p2 = fmax(s0 - u0, s1 - u1);
+    L.p3 = s1 - u0;
+    L.p4 = fmin(s1 - s0, u1 - u0);
+  } else {
+    L.p0 = 0.5 * (s0 + s1) - 0.5 * (u0 + u1);
+    L.p1 = 0.5 * (s1 - s0);
+    L.p2 = 0.5 * (u1 - u0);
+  }
+}
+
+// List `src` (0..2) of a pair from its plan code and the panel records.
+__device__ __forceinline__ void far_list(uint32_t code, int src, const DPanel& A, const DPanel& B, FarList& L) {
+  const uint32_t d = (code >> (1 + 9 * src)) & 511u;
+  L.type = (int)(d & 3u);
+  L.q1 = (int)((d >> 2) & 7u) + 1;
+  L.q2 = (int)(d >> 5);
+  L.p0 = L.p1 = L.p2 = L.p3 = L.p4 = 0.0;
+  const bool orth = code & 1u;
+  if (src == 0) {
+    shared_axis_geom(A, B, orth ? 3 - A.axis - B.axis : ip0(A.axis), L);
+  } else if (!orth) {
+    if (src == 1)
+      shared_axis_geom(A, B, ip1(A.axis), L);
+    else
+      L.p0 = A.level - B.level;
+  } else {
+    // I's rule along J's normal (w = x - level_J), J's rule along I's normal
+    const DPanel& C = src == 1 ? A : B;
+    const DPanel& D = src == 1 ? B : A;
+    double c0, c1;
+    panel_extent(C, D.axis, c0, c1);
+    L.p0 = 0.5 * (c0 + c1) - D.level;
+    L.p1 = 0.5 * (c1 - c0);
+  }
+}
+
+__device__ __forceinline__ void node_single(const FarList& L, int k, const double* gx, const double* gw, double& w2,
+                                            double& W) {
+  const double w = fma(L.p1, gx[L.q1 * kQMax + k], L.p0);
+  W = L.p1 * gw[L.q1 * kQMax + k];
+  w2 = w * w;
+}
+__device__ __forceinline__ void node_product(const FarList& L, int k, const double* gx, const double* gw, double& w2,
+                                             double& W) {
+  const int a = (k * ((65536 + L.q2 - 1) / L.q2)) >> 16, b = k - a * L.q2;  // k / q2 (exact for k < 64)
+  const double w = fma(L.p1, gx[L.q1 * kQMax + a], L.p0) - L.p2 * gx[L.q2 * kQMax + b];
+  W = (L.p1 * gw[L.q1 * kQMax + a]) * (L.p2 * gw[L.q2 * kQMax + b]);
+  w2 = w * w;
+}
+__device__ __forceinline__ void node_tent(const FarList& L, int k, const double* gx, const double* gw, double& w2,
+                                          double& W) {
+  const int qr = L.q1, qp = L.q2;
+  const int piece = k < qr ? 0 : (k < qr + qp ? 1 : 2);
+  const int kk = piece == 0 ? k : (piece == 1 ? k - qr : k - qr - qp);
+  const int q = piece == 1 ? qp : qr;
+  const double lo = piece == 0 ? L.p0 : (piece == 1 ? L.p1 : L.p2);
+  const double hi = piece == 0 ? L.p1 : (piece == 1 ? L.p2 : L.p3);
+  const double h = 0.5 * (hi - lo);
+  const double w = fma(h, gx[q * kQMax + kk], 0.5 * (lo + hi));
+  const double T = piece == 0 ? w - L.p0 : (piece == 1 ? L.p4 : L.p3 - w);
+  W = (h * gw[q * kQMax + kk]) * T;
+  w2 = w * w;
+}
+
+// The inner list into registers (M compile-time): one type branch per pair,
+// the node loop unrolled inside it.
+template <int M>
+__device__ __forceinline__ void build_inner(const FarList& L, const double* gx, const double* gw, double (&w2)[M],
+                                            double (&W)[M]) {
+  if (L.type == kListTent) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) node_tent(L, k, gx, gw, w2[k], W[k]);
+  } else if (L.type == kListProduct) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) node_product(L, k, gx, gw, w2[k], W[k]);
+  } else if (L.type == kListSingle) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) node_single(L, k, gx, gw, w2[k], W[k]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      w2[k] = L.p0 * L.p0;
+      W[k] = 1.0;
+    }
+  }
+}
+
+// An outer list of m nodes into this thread's shared-memory slots (stride ST).
+template <int ST>
+__device__ __forceinline__ void build_outer(const FarList& L, int m, const double* gx, const double* gw, double* w2,
+                                            double* W) {
+  if (L.type == kListTent) {
+    for (int k = 0; k < m; ++k) node_tent(L, k, gx, gw, w2[k * ST], W[k * ST]);
+  } else if (L.type == kListProduct) {
+    for (int k = 0; k < m; ++k) node_product(L, k, gx, gw, w2[k * ST], W[k * ST]);
+  } else if (L.type == kListSingle) {
+    for (int k = 0; k < m; ++k) node_single(L, k, gx, gw, w2[k * ST], W[k * ST]);
+  } else {
+    w2[0] = L.p0 * L.p0;
+    W[0] = 1.0;
+  }
+}
+
+// Far field, one kernel per inner-list size M (the queue segment of keys with
+// m1 = M).  Per pair: the plan written by the classifier names the three
+// lists; the inner one (M nodes) goes to registers, the other two to
+// per-thread shared-memory slots, then
+//   for c < m3, b < m2:  acc += W3_c W2_b sum_a W1_a rsq64(w1_a^2 + w2_b^2 + w3_c^2)
+// with (m2, m3) uniform across a warp (equal keys are contiguous).  Per node:
+// DADD, MUFU.RSQ64H + Householder step (rsq64), DFMA.  OUT2 slots for the
+// middle list (m2 <= m1 = M) and the smallest (m3 <= 8); CTAs of 128 threads
+// (64 for M > 14, whose slots would not fit 48 KB).
+__host__ __device__ constexpr int far_threads(int M) { return M <= 14 ? 128 : 64; }
+template <int M>
+__global__ void __launch_bounds__(far_threads(M), M <= 12 ? 4 : 2)
+    k_far(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue, const uint32_t* __restrict__ plans,
           const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats) {
-  const uint32_t begin = offsets[far_key_first(QV, QU > 0 ? QU : 1)];
-  const uint32_t end = offsets[QU > 0 && QU < QV ? far_key_first(QV, QU + 1)
-                                                 : (QV < kQMax ? far_key_first(QV + 1) : kNumKeys)];
+  constexpr int kFarThreads = far_threads(M);
+  constexpr int OUT2 = M, OUT3 = M < 8 ? M : 8;
+  __shared__ double sgx[(kQMax + 1) * kQMax], sgw[(kQMax + 1) * kQMax];
+  __shared__ double ow2[(OUT2 + OUT3) * kFarThreads], oW[(OUT2 + OUT3) * kFarThreads];
+  for (int t = threadIdx.x; t < (kQMax + 1) * kQMax; t += blockDim.x) {
+    sgx[t] = (&c_gx[0][0])[t];
+    sgw[t] = (&c_gw[0][0])[t];
+  }
+  __syncthreads();
+  double* w2s = ow2 + threadIdx.x;
+  double* W2s = oW + threadIdx.x;
+  double* w3s = ow2 + OUT2 * kFarThreads + threadIdx.x;
+  double* W3s = oW + OUT2 * kFarThreads + threadIdx.x;
+  const uint32_t begin = offsets[far_key_first(M)];
+  const uint32_t end = offsets[M < kFarListMax ? far_key_first(M + 1) : kNumKeys];
   double flops = 0.0, evals = 0.0;
   const uint32_t stride = gridDim.x * blockDim.x;
-  // Warps walk the queue in 32-entry runs so a warp shares one key.
-  for (uint32_t base = begin + (blockIdx.x * blockDim.x + (threadIdx.x & ~31u)); base < end;
-       base += stride) {
-    uint32_t idx = base + (threadIdx.x & 31u);
-    if (idx < end) {
-      uint64_t e = queue[idx];
-      uint32_t i = entry_i(e), j = entry_j(e), k = entry_key(e) - 16u;
-      DPanel Pi = load_panel(P, i), Pj = load_panel(P, j);
-      const bool swap = (k >> 7) & 1u, v_is_a = (k >> 6) & 1u;
-      const int qu = (int)((k >> 8) & 7u) + 1, qs = (int)((k >> 3) & 7u) + 1, qt = (int)(k & 7u) + 1;
-      double U = swap ? far_gauss<QV, QU>(Pj, qs, qt, Pi, v_is_a, qu, flops)
-                      : far_gauss<QV, QU>(Pi, qs, qt, Pj, v_is_a, qu, flops);
-      evals += (double)(qs * qt * qu * QV);
-      store_value(o, i, j, Pi, Pj, U);
-      if (!o.A && o.conv) o.conv[i] = 1;
+  uint32_t base = begin + (blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
+  uint32_t nidx = base + (threadIdx.x & 31u);
+  uint64_t ne = nidx < end ? queue[nidx] : 0;
+  uint32_t ncode = nidx < end ? plans[nidx] : 0;
+  for (; base < end; base += stride) {
+    // the next run's queue entry and plan are in flight while this pair runs
+    const uint32_t idx = nidx;
+    const uint64_t e = ne;
+    const uint32_t code = ncode;
+    nidx += stride;
+    if (nidx < end) {
+      ne = queue[nidx];
+      ncode = plans[nidx];
     }
+    if (idx >= end) continue;
+    const uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e) - 16u;
+    const int m2 = (int)((key >> 3) & 31u) + 1, m3 = (int)(key & 7u) + 1;
+    const DPanel A = load_panel(P, i), B = load_panel(P, j);
+    const int s0 = (int)((code >> 28) & 3u);
+    const int r0 = s0 == 0 ? 1 : 0, r1 = s0 == 2 ? 1 : 2;
+    const bool mid_second = (code >> 30) & 1u;
+    double w1[M], W1[M];
+    {
+      FarList L;
+      far_list(code, s0, A, B, L);
+      build_inner<M>(L, sgx, sgw, w1, W1);
+      far_list(code, mid_second ? r1 : r0, A, B, L);
+      build_outer<kFarThreads>(L, m2, sgx, sgw, w2s, W2s);
+      far_list(code, mid_second ? r0 : r1, A, B, L);
+      build_outer<kFarThreads>(L, m3, sgx, sgw, w3s, W3s);
+    }
+    double acc = 0.0;
+    for (int c = 0; c < m3; ++c) {
+      const double w3 = w3s[c * kFarThreads], W3 = W3s[c * kFarThreads];
+      for (int b = 0; b < m2; ++b) {
+        const double r2 = w3 + w2s[b * kFarThreads];
+        // two partial sums break the FMA dependency chain
+        double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+        for (int a = 0; a < M; a += 2) {
+          t0 = fma(W1[a], rsq64(r2 + w1[a]), t0);
+          if (a + 1 < M) t1 = fma(W1[a + 1], rsq64(r2 + w1[a + 1]), t1);
+        }
+        acc = fma(W3 * W2s[b * kFarThreads], t0 + t1, acc);
+      }
+    }
+    const double U = acc / kFourPi;
+    const double nodes = (double)M * m2 * m3;
+    evals += nodes;
+    flops += 11.0 * nodes + 4.0 * m2 * m3 + 6.0 * (M + m2 + m3) + 30.0;
+    store_value(o, i, j, A, B, U);
+    if (!o.A && o.conv) o.conv[i] = 1;
   }
   flops = warp_reduce_d(flops);
   evals = warp_reduce_d(evals);
@@ -740,14 +921,13 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
              float* ms_near) {
   int sms = ctx->num_sms;
   cudaEventRecord(ctx->ev[2], ctx->stream);
-#define GBEM_FAR(QV, QU, B) \
-  k_far<QV, QU><<<sms * (B), 256, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, ctx->d_stats); \
+#define GBEM_FAR(M) \
+  k_far<M><<<sms * 4, far_threads(M), 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan, \
+                                                                     ctx->d_offsets, o, ctx->d_stats); \
   GBEM_LAUNCH_CHECK(ctx);
-  GBEM_FAR(1, 1, 1)
-  GBEM_FAR(2, 1, 1) GBEM_FAR(2, 2, 1)
-  GBEM_FAR(3, 1, 2) GBEM_FAR(3, 2, 2) GBEM_FAR(3, 3, 2)
-  GBEM_FAR(4, 1, 2) GBEM_FAR(4, 2, 2) GBEM_FAR(4, 3, 2) GBEM_FAR(4, 4, 2)
-  GBEM_FAR(5, 0, 2) GBEM_FAR(6, 0, 2) GBEM_FAR(7, 0, 2) GBEM_FAR(8, 0, 2)
+  GBEM_FAR(1) GBEM_FAR(2) GBEM_FAR(3) GBEM_FAR(4) GBEM_FAR(5) GBEM_FAR(6) GBEM_FAR(7) GBEM_FAR(8)
+  GBEM_FAR(9) GBEM_FAR(10) GBEM_FAR(11) GBEM_FAR(12) GBEM_FAR(13) GBEM_FAR(14) GBEM_FAR(15) GBEM_FAR(16)
+  GBEM_FAR(17) GBEM_FAR(18) GBEM_FAR(19) GBEM_FAR(20) GBEM_FAR(21) GBEM_FAR(22) GBEM_FAR(23) GBEM_FAR(24)
 #undef GBEM_FAR
   cudaEventRecord(ctx->ev[3], ctx->stream);
   k_coplanar<<<sms * 4, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o);
@@ -868,6 +1048,8 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
   long long need = std::min<long long>(total_tiles * kTile * kTile, 1ll << 27);
   rc = grow(ctx, (void**)&ctx->d_queue, sizeof(uint64_t) * (size_t)need, &ctx->queue_cap, sizeof(uint64_t));
   if (rc) return rc;
+  rc = grow(ctx, (void**)&ctx->d_plan, sizeof(uint32_t) * (size_t)ctx->queue_cap, &ctx->plan_cap, sizeof(uint32_t));
+  if (rc) return rc;
   rc = prepare_cinfo(ctx, n);
   if (rc) return rc;
   long long* d_rowoff = nullptr;
@@ -891,13 +1073,13 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
     GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, ctx->stream));
     k_classify<false><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
         (const CPanel*)ctx->d_cinfo, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
-        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, full_rows ? 1 : 0);
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, ctx->d_plan, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
     k_scan<<<1, 1024, 0, ctx->stream>>>(ctx->d_counts, ctx->d_offsets, ctx->d_cursors, ctx->d_stats);
     GBEM_LAUNCH_CHECK(ctx);
     k_classify<true><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
         (const CPanel*)ctx->d_cinfo, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
-        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, full_rows ? 1 : 0);
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, ctx->d_plan, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
     cudaEventRecord(ctx->ev[6], ctx->stream);
     if (timing) {
@@ -958,17 +1140,21 @@ int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_confi
   if (npairs > (1 << 23)) return ctx->fail(GBEM_EINVAL, "at most 2^23 pairs per call");
   rc = grow(ctx, (void**)&ctx->d_queue, sizeof(uint64_t) * (size_t)npairs, &ctx->queue_cap, sizeof(uint64_t));
   if (rc) return rc;
+  rc = grow(ctx, (void**)&ctx->d_plan, sizeof(uint32_t) * (size_t)ctx->queue_cap, &ctx->plan_cap, sizeof(uint32_t));
+  if (rc) return rc;
   rc = prepare_cinfo(ctx, 2 * npairs);
   if (rc) return rc;
   GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, ctx->stream));
   int blocks = (int)((npairs + 255) / 256);
   k_classify_list<false><<<blocks, 256, 0, ctx->stream>>>((const CPanel*)ctx->d_cinfo, (int)npairs, cfg.near_ratio,
-                                                          ctx->d_counts, ctx->d_cursors, ctx->d_queue);
+                                                          ctx->d_counts, ctx->d_cursors, ctx->d_queue,
+                                                          ctx->d_plan);
   GBEM_LAUNCH_CHECK(ctx);
   k_scan<<<1, 1024, 0, ctx->stream>>>(ctx->d_counts, ctx->d_offsets, ctx->d_cursors, ctx->d_stats);
   GBEM_LAUNCH_CHECK(ctx);
   k_classify_list<true><<<blocks, 256, 0, ctx->stream>>>((const CPanel*)ctx->d_cinfo, (int)npairs, cfg.near_ratio,
-                                                         ctx->d_counts, ctx->d_cursors, ctx->d_queue);
+                                                         ctx->d_counts, ctx->d_cursors, ctx->d_queue,
+                                                         ctx->d_plan);
   GBEM_LAUNCH_CHECK(ctx);
   OutSpec o{nullptr, 0, d_out, d_conv};
   rc = run_eval(ctx, o, cfg, nullptr, nullptr);

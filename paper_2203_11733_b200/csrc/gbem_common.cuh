@@ -20,7 +20,7 @@ struct __align__(16) DPanel {
 constexpr double kFourPi = 4.0 * 3.14159265358979323846;  // oracle.hpp:11
 constexpr int kQMax = 8;                                   // max far-field Gauss order per direction
 
-// Pair classes (queue key < kFarKeyBase).  Far keys pack four 4-bit orders.
+// Pair classes (queue key < kFarKeyBase); far keys above (far_key).
 enum PairClass : uint32_t {
   kClsCoplanar = 1,   // coplanar closed form (self, touching, near coplanar): kernels.hpp:86-94
   // offset-parallel / orthogonal near pairs on the reference's reduced 1-D
@@ -36,25 +36,17 @@ enum PairClass : uint32_t {
 };
 constexpr int kNumKeys = 1 << 16;
 
-// Far keys are canonical: the largest of the four per-direction orders (QV)
-// sits in direction V of panel J; `swap` says J is the pair's first panel,
-// `v_is_a` that V is J's first in-plane axis.  QV is the most significant field,
-// so the queue segment of one QV is contiguous and runs in its own kernel.
-//   key = kFarKeyBase + ((QV-1) << 11 | (qu-1) << 8 | swap << 7 | v_is_a << 6 | (qs-1) << 3 | (qt-1))
-// (QV, qu) segments are contiguous too: the common small-order cases run fully unrolled.
-__host__ __device__ inline uint32_t far_key(int qa_i, int qb_i, int qa_j, int qb_j) {
-  const int mi = qa_i > qb_i ? qa_i : qb_i, mj = qa_j > qb_j ? qa_j : qb_j;
-  const int swap = mi > mj ? 1 : 0;
-  const int qs = swap ? qa_j : qa_i, qt = swap ? qb_j : qb_i;
-  const int ja = swap ? qa_i : qa_j, jb = swap ? qb_i : qb_j;
-  const int v_is_a = ja > jb ? 1 : 0;
-  const int QV = v_is_a ? ja : jb, qu = v_is_a ? jb : ja;
-  return 16u + (uint32_t)(((QV - 1) << 11) | ((qu - 1) << 8) | (swap << 7) | (v_is_a << 6) | ((qs - 1) << 3) |
-                          (qt - 1));
+// Far keys hold the three per-axis node-list sizes of the difference-set rule
+// (gbem_assembly.cu, far_plan_code), sorted descending: m1 (the inner, register-
+// resident list, <= 24) is the most significant field, so the queue segment
+// of one m1 is contiguous and runs in its own kernel k_far<m1>; pairs with
+// equal (m1, m2, m3) are contiguous, so a warp's loops are uniform.
+//   key = kFarKeyBase + ((m1-1) << 8 | (m2-1) << 3 | (m3-1)),  m2 <= 24, m3 <= 8
+constexpr int kFarListMax = 24;
+__host__ __device__ inline uint32_t far_key(int m1, int m2, int m3) {
+  return 16u + (uint32_t)(((m1 - 1) << 8) | ((m2 - 1) << 3) | (m3 - 1));
 }
-__host__ __device__ inline uint32_t far_key_first(int QV, int qu = 1) {
-  return 16u + (uint32_t)(((QV - 1) << 11) | ((qu - 1) << 8));
-}
+__host__ __device__ inline uint32_t far_key_first(int m1) { return 16u + (uint32_t)((m1 - 1) << 8); }
 
 // Queue entry: i (24 bits) | j (24 bits) | key (16 bits).
 __host__ __device__ inline uint64_t pack_entry(uint32_t i, uint32_t j, uint32_t key) {

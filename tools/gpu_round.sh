@@ -11,13 +11,14 @@ timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TA
 cat gpurun_out/bench_$TAG.json
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
 if [ $rc -eq 0 ]; then
+  export GBEM_NO_GREEN=1  # ncu cannot profile kernels launched into green contexts
   timeout 1200 python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/plain_$TAG.log 2>&1 && \
   timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_list_$TAG.log 2>&1
   echo "launch list rc=$?"
   python tools/launch_summary.py gpurun_out/launches_$TAG.csv > gpurun_out/launch_summary_$TAG.txt 2>&1
   head -30 gpurun_out/launch_summary_$TAG.txt
-  for KS in "k_syrk_gen:300" "k_far<\(int\)4, \(int\)3>:1" "k_potrf_diag:200" "k_solve_coop:2" "k_near_gl:2" "k_classify:2" "k_gemm_nt:200"; do
+  for KS in "k_syrk_gen:300" "k_far<\(int\)4, \(int\)3>:1" "k_potrf_diag:200" "k_solve_coop:2" "k_near_gl:2" "k_classify:2" "k_trsm_rows:200" "k_symv_upper:1"; do
     K=${KS%%:*}; S=${KS##*:}
     NAME=$(echo "$K" | tr -cd 'a-z_0-9')
     timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
