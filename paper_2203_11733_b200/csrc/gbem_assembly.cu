@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kClassifyThreads)
     k_classify(const CPanel* __restrict__ P, int n, int rb, int re, int bi0, int nbt,
                const long long* __restrict__ tile_row_off, int nrows_t, long long tile_begin,
                double near_ratio, uint32_t* counts, uint32_t* cursors, uint64_t* queue, uint32_t* plans,
-               int full) {
+               uint64_t* kp, int full) {
   constexpr int kIter = kTile / (kClassifyThreads / 32);
   __shared__ CPanel si[kTile], sj[kTile];
   __shared__ uint32_t hkey[kHash], hcnt[kHash];
@@ -344,10 +344,10 @@ __global__ void __launch_bounds__(kClassifyThreads)
   const int bi = bi0 + lo;
   const int bj = (full ? 0 : bi) + (int)(t - row_off);  // full: whole rows (mirrored entries too)
   const int tid = threadIdx.x;
-  if (tid < kTile) {
+  if (!FILL && tid < kTile) {
     int i = bi * kTile + tid;
     if (i < n) si[tid] = P[i];
-  } else if (tid < 2 * kTile) {
+  } else if (!FILL && tid < 2 * kTile) {
     int j = bj * kTile + (tid - kTile);
     if (j < n) sj[tid - kTile] = P[j];
   }
@@ -366,7 +366,16 @@ __global__ void __launch_bounds__(kClassifyThreads)
     const int r = warp + it * (kClassifyThreads / 32);
     const int i = bi * kTile + r;
     const bool valid = i >= rb && i < re && j < n && (full || j >= i);
-    key[it] = valid ? classify_pair(si[r], sj[lane], i == j, near_ratio, plan[it]) : kEmpty;
+    // pass 1 classifies and keeps (key, plan) in tile order; pass 2 reads them back
+    uint64_t* kp_at = kp + (size_t)blockIdx.x * (kTile * kTile) + r * kTile + lane;
+    if (!FILL) {
+      key[it] = valid ? classify_pair(si[r], sj[lane], i == j, near_ratio, plan[it]) : kEmpty;
+      *kp_at = (uint64_t)key[it] << 32 | plan[it];
+    } else {
+      const uint64_t v = *kp_at;
+      key[it] = (uint32_t)(v >> 32);
+      plan[it] = (uint32_t)v;
+    }
     peers[it] = __match_any_sync(0xffffffffu, key[it]);
     slot[it] = -1;
     leader_off[it] = 0;
@@ -1050,6 +1059,8 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
   if (rc) return rc;
   rc = grow(ctx, (void**)&ctx->d_plan, sizeof(uint32_t) * (size_t)ctx->queue_cap, &ctx->plan_cap, sizeof(uint32_t));
   if (rc) return rc;
+  rc = grow(ctx, (void**)&ctx->d_kp, sizeof(uint64_t) * (size_t)ctx->queue_cap, &ctx->kp_cap, sizeof(uint64_t));
+  if (rc) return rc;
   rc = prepare_cinfo(ctx, n);
   if (rc) return rc;
   long long* d_rowoff = nullptr;
@@ -1073,13 +1084,13 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
     GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, ctx->stream));
     k_classify<false><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
         (const CPanel*)ctx->d_cinfo, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
-        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, ctx->d_plan, full_rows ? 1 : 0);
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, ctx->d_plan, ctx->d_kp, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
     k_scan<<<1, 1024, 0, ctx->stream>>>(ctx->d_counts, ctx->d_offsets, ctx->d_cursors, ctx->d_stats);
     GBEM_LAUNCH_CHECK(ctx);
     k_classify<true><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
         (const CPanel*)ctx->d_cinfo, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
-        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, ctx->d_plan, full_rows ? 1 : 0);
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, ctx->d_plan, ctx->d_kp, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
     cudaEventRecord(ctx->ev[6], ctx->stream);
     if (timing) {

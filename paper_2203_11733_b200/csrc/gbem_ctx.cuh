@@ -48,6 +48,8 @@ struct gbem_ctx {
   int64_t queue_cap = 0;
   uint32_t* d_plan = nullptr;  // far-field plan per queue entry (gbem_assembly.cu, far_plan_code)
   int64_t plan_cap = 0;
+  uint64_t* d_kp = nullptr;  // (key, plan) per pair in tile order between the two classification passes
+  int64_t kp_cap = 0;
   uint32_t* d_counts = nullptr;   // per key
   uint32_t* d_offsets = nullptr;  // exclusive scan of counts (kNumKeys + 1)
   uint32_t* d_cursors = nullptr;
