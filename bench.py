@@ -242,7 +242,7 @@ def run_ours(args):
     dmma_peak = peaks.get("fp64_dmma_tflops", 37.09)
     dfma_peak = peaks.get("fp64_dfma_tflops", 36.75)
     traffic = _ncu_traffic()
-    roof_chol = {"bound": "tensor", "kernel": "Cholesky factor (k_potrf_diag + k_gemm_nt trsm + k_syrk_gen DMMA update)",
+    roof_chol = {"bound": "tensor", "kernel": "Cholesky factor (k_potrf_diag + k_trsm_rows + k_syrk_gen DMMA update, bordered: forward substitution fused)",
                  "achieved": chol_flops / (sst.ms_factor * 1e-3) / 1e12, "peak": dmma_peak, "unit": "TFLOP/s",
                  "traffic": traffic.get("k_syrk_gen"),
                  "algorithmic": f"n^3/3 = {chol_flops:.3e} flop per factorisation (n = {n}) / device time of the factor",
