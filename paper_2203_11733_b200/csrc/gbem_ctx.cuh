@@ -65,6 +65,8 @@ struct gbem_ctx {
   size_t sw_cap = 0;
   double* d_linv = nullptr;  // inverses of the 128 x 128 diagonal blocks of the factor
   size_t linv_cap = 0;
+  int* d_flags = nullptr;  // per-block ready flags of the dataflow backward substitution
+  int flow_epoch = 0;
   double* d_rhs = nullptr;  // B and X of the K-RHS extraction (2 * rhs_cap)
   size_t rhs_cap = 0;
 

@@ -718,6 +718,109 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
   }
 }
 
+// Backward substitution L^T X = Y as a dataflow over the 128-row blocks, for
+// the bordered factorisation (Y from the border rows).  CTA b owns block b:
+//   X_b = inv(L_bb)^T (Y_b - sum_{c > b} L_cb^T X_c)
+// in the left-looking (dot-product) form, walking c = nblk-1 .. b+1.  The
+// 128 x 128 block L_cb is staged in shared memory by coalesced cp.async
+// (its load is issued before the CTA waits for the flag of X_c, so the L
+// stream, n^2/2 * 8 B over all CTAs, overlaps the dependency chain); the
+// diagonal-block inverse sits in registers from the start.  The chain per
+// block is one X_c hand-off (release / acquire flag), a 128 x 128 x R product
+// from shared memory and the diagonal solve -- no grid barrier.  Thread
+// (i, h): column i of the block, rows [64 h, 64 h + 64).  One CTA per block,
+// all co-resident (cooperative launch), nblk <= #SMs.
+constexpr int kFlowThreads = 256, kFlowLD = NB + 1;
+constexpr size_t kFlowSmem = (size_t)(NB * kFlowLD + 3 * NB * 8) * sizeof(double);
+template <int RT>
+__global__ void __launch_bounds__(kFlowThreads, 1)
+    k_bwd_flow(const double* __restrict__ A, long long lda, const double* __restrict__ Linv, int n, int R,
+               const double* __restrict__ Y, double* X, int* flags, int epoch) {
+  extern __shared__ __align__(16) double fsm[];
+  double* Lb = fsm;                       // [row r][col i] of L_cb, ld kFlowLD
+  double* xs = Lb + NB * kFlowLD;         // [r][RT]
+  double* red = xs + NB * RT;             // [i][RT] half-1 partials
+  double* ys = red + NB * RT;             // [k][RT]
+  const int b = blockIdx.x, nblk = gridDim.x;
+  const int k0 = b * NB, kb = min(NB, n - k0);
+  const int tid = threadIdx.x, i = tid & (NB - 1), h = tid >> 7;
+  // inv(L_bb)(k, i) for k in [64 h, 64 h + 64): column i of the inverse (contiguous)
+  double dinv[64];
+  {
+    const double* li = Linv + (size_t)b * NB * NB + (size_t)i * NB + 64 * h;
+#pragma unroll
+    for (int k = 0; k < 64; ++k) dinv[k] = li[k];
+  }
+  double acc[RT];
+#pragma unroll
+  for (int q = 0; q < RT; ++q) acc[q] = 0.0;
+  auto issue_block = [&](int c) {  // L(c0 + r, k0 + i) -> Lb[r][i], zero outside the matrix
+    const int c0 = c * NB, kc = min(NB, n - c0);
+    for (int idx = tid; idx < NB * NB; idx += kFlowThreads) {
+      const int r = idx & (NB - 1), col = idx >> 7;
+      const bool ok = r < kc && col < kb;
+      gbem_gemm::cp_async8(Lb + r * kFlowLD + col, ok ? A + (long long)(k0 + col) * lda + c0 + r : A, ok ? 8 : 0);
+    }
+    gbem_gemm::cp_async_commit();
+  };
+  if (b + 1 < nblk) issue_block(nblk - 1);
+  for (int c = nblk - 1; c > b; --c) {
+    const int c0 = c * NB, kc = min(NB, n - c0);
+    if (tid == 0) {
+      int f;
+      do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(flags + c) : "memory");
+      } while (f != epoch);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < NB * RT; idx += kFlowThreads) {
+      const int r = idx / RT, q = idx % RT;
+      xs[idx] = (q < R && r < kc) ? __ldcg(X + (long long)q * n + c0 + r) : 0.0;
+    }
+    gbem_gemm::cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll 8
+    for (int r = 0; r < 64; ++r) {
+      const double l = Lb[(64 * h + r) * kFlowLD + i];
+#pragma unroll
+      for (int q = 0; q < RT; ++q) acc[q] = fma(l, xs[(64 * h + r) * RT + q], acc[q]);
+    }
+    __syncthreads();  // Lb and xs are reused
+    if (c - 1 > b) issue_block(c - 1);
+  }
+  // y = Y_b - (both row halves)
+  if (h == 1)
+#pragma unroll
+    for (int q = 0; q < RT; ++q) red[i * RT + q] = acc[q];
+  __syncthreads();
+  if (h == 0)
+#pragma unroll
+    for (int q = 0; q < RT; ++q)
+      ys[i * RT + q] = (i < kb && q < R) ? Y[(long long)q * n + k0 + i] - (acc[q] + red[i * RT + q]) : 0.0;
+  __syncthreads();
+  // X_b(i) = sum_k inv(L_bb)(k, i) y_k (the inverse is zero above its diagonal)
+  double o[RT];
+#pragma unroll
+  for (int q = 0; q < RT; ++q) o[q] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 64; ++k)
+#pragma unroll
+    for (int q = 0; q < RT; ++q) o[q] = fma(dinv[k], ys[(64 * h + k) * RT + q], o[q]);
+  if (h == 1)
+#pragma unroll
+    for (int q = 0; q < RT; ++q) red[i * RT + q] = o[q];
+  __syncthreads();
+  if (h == 0 && i < kb)
+#pragma unroll
+    for (int q = 0; q < RT; ++q)
+      if (q < R) X[(long long)q * n + k0 + i] = o[q] + red[i * RT + q];
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(flags + b), "r"(epoch) : "memory");
+  }
+}
+
 // Column-major (R x n, ld n: one right-hand side per column of the caller's
 // layout) <-> row-major (n x R: the R values of a panel contiguous).
 __global__ void k_rhs_transpose(const double* __restrict__ in, int n, int R, double* __restrict__ out, int to_rows) {
@@ -1248,7 +1351,33 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
   const double* Linv = ctx->d_linv;
   cudaEventRecord(ctx->ev[1], s);
   static const int blocked_min = getenv("GBEM_SOLVE_BLOCKED_MIN") ? atoi(getenv("GBEM_SOLVE_BLOCKED_MIN")) : 17;
-  if (R >= blocked_min) {
+  const int nblk_s = (n + NB - 1) / NB;
+  if (y_from_border && R <= 8 && nblk_s <= ctx->num_sms) {
+    // bordered factorisation: y is in the border rows; dataflow backward substitution
+    if (!ctx->d_flags) {
+      GBEM_CUDA(ctx, cudaMalloc(&ctx->d_flags, sizeof(int) * 1024));
+      GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_flags, 0, sizeof(int) * 1024, s));
+    }
+    if (++ctx->flow_epoch == 0x7fffffff) {
+      ctx->flow_epoch = 1;
+      GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_flags, 0, sizeof(int) * 1024, s));
+    }
+    double* Ys = scratch;
+    const long long cnt = (long long)n * R;
+    k_border_to_y<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(ctx->d_A, lda, n, R, Ys, 0);
+    GBEM_LAUNCH_CHECK(ctx);
+    const double* cA = ctx->d_A;
+    const double* cL = Linv;
+    const double* cY = Ys;
+    int nn = n, RR = R, ep = ctx->flow_epoch;
+    int* fl = ctx->d_flags;
+    void* args[] = {(void*)&cA, (void*)&lda, (void*)&cL, (void*)&nn, (void*)&RR, (void*)&cY, (void*)&d_X, (void*)&fl,
+                    (void*)&ep};
+    void* fn = R <= 2 ? (void*)k_bwd_flow<2> : R <= 4 ? (void*)k_bwd_flow<4> : (void*)k_bwd_flow<8>;
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlowSmem));
+    GBEM_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3(nblk_s), dim3(kFlowThreads), args, kFlowSmem, s));
+    GBEM_LAUNCH_CHECK(ctx);
+  } else if (R >= blocked_min) {
     rc = solve_blocked(ctx, d_B, R, d_X, y_from_border);
     if (rc) return rc;
   } else {
