@@ -339,11 +339,12 @@ __global__ void __launch_bounds__(256) k_symv_upper(const double* __restrict__ A
   double acc[MAXR];
 #pragma unroll
   for (int q = 0; q < MAXR; ++q) acc[q] = 0.0;
-  for (int cb = cb0; cb < cb1; ++cb) {
+  // the tile of column block cb: column-wise right of (or on) the diagonal
+  // (column c contiguous in r), row-wise left of it (A(r, c) = A[r*lda + c],
+  // contiguous in c); the next tile's loads are in flight while this one is used
+  auto load_tile = [&](int cb, double (&v)[T / 8][2]) {
     const int c0 = cb * T;
-    double v[T / 8][2];
     if (cb >= rb) {
-      // right of (or on) the diagonal: column c of the tile is contiguous in r
 #pragma unroll
       for (int u = 0; u < T / 8; ++u) {
         const int c = c0 + warp + 8 * u;
@@ -354,7 +355,6 @@ __global__ void __launch_bounds__(256) k_symv_upper(const double* __restrict__ A
         }
       }
     } else {
-      // left of the diagonal: A(r, c) = A[r*lda + c], contiguous in c
 #pragma unroll
       for (int u = 0; u < T / 8; ++u) {
         const int r = r0 + warp + 8 * u;
@@ -365,6 +365,11 @@ __global__ void __launch_bounds__(256) k_symv_upper(const double* __restrict__ A
         }
       }
     }
+  };
+  double v[T / 8][2], vn[T / 8][2];
+  if (cb0 < cb1) load_tile(cb0, v);
+  for (int cb = cb0; cb < cb1; ++cb) {
+    const int c0 = cb * T;
     __syncthreads();  // the previous tile's reads of sa / xs are done
     if (cb >= rb) {
 #pragma unroll
@@ -381,6 +386,7 @@ __global__ void __launch_bounds__(256) k_symv_upper(const double* __restrict__ A
       const int c = idx % T, q = idx / T;
       xs[c * MAXR + q] = (q < nrhs && c0 + c < n) ? X[(long long)q * ldx + c0 + c] : 0.0;
     }
+    if (cb + 1 < cb1) load_tile(cb + 1, vn);
     __syncthreads();
     if (cb == rb) {
       // diagonal tile: mirror the strict upper half into the lower, add the diagonal
@@ -397,6 +403,11 @@ __global__ void __launch_bounds__(256) k_symv_upper(const double* __restrict__ A
       const double a = sa[c * LD + row];
 #pragma unroll
       for (int q = 0; q < MAXR; ++q) acc[q] = fma(a, xs[c * MAXR + q], acc[q]);
+    }
+#pragma unroll
+    for (int u = 0; u < T / 8; ++u) {
+      v[u][0] = vn[u][0];
+      v[u][1] = vn[u][1];
     }
   }
   __syncthreads();  // last tile's reads of sa are done
