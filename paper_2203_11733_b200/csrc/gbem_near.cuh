@@ -183,7 +183,7 @@ struct ParIntegrandFast {
   __device__ double operator()(double v) const {
     const double c2 = v * v + b2;
     double acc = 0.0;
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < 4; ++k) {
       const double u = val[k];
       const double r = sqrt(u * u + c2);
@@ -203,7 +203,8 @@ struct OrthFxFast {
   __device__ double operator()(double x) const {
     double acc = 0.0;
     const double x2 = x * x;
-#pragma unroll
+    // loops kept rolled: the log expansions appear once (instruction-cache footprint)
+#pragma unroll 1
     for (int k = 0; k < 4; ++k) {
       const double cv = val[k];
       const double u2 = cv * cv;
@@ -234,7 +235,7 @@ struct OrthFyFast {
   __device__ double operator()(double y) const {
     double acc = 0.0;
     const double y2 = y * y;
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < 4; ++k)
 #pragma unroll
       for (int side = 0; side < 2; ++side) {
@@ -490,7 +491,7 @@ __host__ __device__ constexpr int near_nodes(int band) {
 constexpr int kNearTeam = 4;
 
 template <class F>
-__device__ double gl_graded(const F& f, double a, double b, int band, const double (*nx)[48],
+__device__ __noinline__ double gl_graded(const F& f, double a, double b, int band, const double (*nx)[48],
                             const double (*nw)[48], bool& bad, int tl) {
   if (a == b) return 0.0;
   const int n = near_nodes(band);
