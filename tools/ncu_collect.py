@@ -29,7 +29,7 @@ for rep in reps:
         continue
     d = dict(zip(rows[0], rows[2]))
     u = dict(zip(rows[0], rows[1]))
-    name = d.get("Kernel Name", "?").split("(")[0].split("::")[-1].split("<")[0].strip()
+    name = d.get("Kernel Name", "?").split("(")[0].split("::")[-1].split("<")[0].strip().split(" ")[-1]
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     rd = float(d["dram__bytes_read.sum"].replace(",", "")) * scale.get(u["dram__bytes_read.sum"], 1)
     wr = float(d["dram__bytes_write.sum"].replace(",", "")) * scale.get(u["dram__bytes_write.sum"], 1)
