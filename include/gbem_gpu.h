@@ -164,6 +164,17 @@ int gbem_spd_factor_dev(gbem_ctx* ctx, const double* M, int64_t m, int64_t ldm, 
 int gbem_spd_solve_factored_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
                                 gbem_solve_stats* stats);
 
+/* assemble_multi (assembly.hpp:110-175, replaces gbem::assemble_multi): the
+ * Galerkin block system over all dielectric regions (double-layer
+ * q_pair_integral kernels.hpp:295-315 and single-layer u_pair_integral with the
+ * reference's reductions and Romberg rule, cfg = QuadratureConfig), same
+ * panel / region arguments and outputs as gbem_assemble_collocation; the m x m
+ * system stays in the context for gbem_lu_solve.  *all_converged ANDs the
+ * kernels' convergence flags (assembly.hpp:97,133-135). */
+int gbem_assemble_multi(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n, const gbem_region* regions,
+                        int32_t nregions, int32_t main_net, const gbem_quad_config* cfg, double* A_host, int64_t lda,
+                        double* b_host, int64_t* m_out, int32_t* all_converged);
+
 /* assemble_collocation (assembly.hpp:179-227): the point-collocation block
  * system of the scene for main net `main_net` (rows per region and boundary
  * panel, unknown map of assembly.hpp:51-75, closed-form u/q point kernels

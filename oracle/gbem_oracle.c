@@ -431,6 +431,92 @@ orc_kv orc_u_pair_integral(const orc_rect* Ii, const orc_rect* Ij, double rel_to
   return out;
 }
 
+/* ---------------- double layer (kernels.hpp:157-169, 218-237, 295-315) ---------------- */
+
+/* integrand of qParallelOffset (kernels.hpp:162-167) */
+static double qpar_f(const void* vc, double v) {
+  const par_ctx* c = (const par_ctx*)vc;
+  double c2 = v * v + c->b2;
+  double acc = 0.0;
+  for (int k = 0; k < 4; ++k) acc += c->sign[k] * sqrt(c->val[k] * c->val[k] + c2) / c2;
+  return tent_w(&c->w, v) * acc;
+}
+
+/* qParallelOffset (kernels.hpp:157-169): b = test level - source level */
+static double q_parallel_offset(span_t sx, span_t sy, span_t tx, span_t ty, double b, double rel_tol,
+                                int max_levels, qstats* st) {
+  par_ctx c;
+  c.b2 = b * b;
+  u_corners(sx.lo, sx.hi, tx.lo, tx.hi, c.sign, c.val);
+  double cuts[5];
+  int count = tent_segments(sy.lo, sy.hi, ty.lo, ty.hi, &c.w, cuts);
+  double total = 0.0;
+  for (int i = 0; i + 1 < count; ++i) {
+    total += romberg(qpar_f, &c, cuts[i], cuts[i + 1], rel_tol, max_levels, st);
+    if (st->status) return NAN;
+  }
+  return b * total / kFourPi;
+}
+
+/* fy of qOrthogonal (kernels.hpp:224-235) */
+static double qorth_fy(const void* vc, double y) {
+  const orth_ctx* c = (const orth_ctx*)vc;
+  double acc = 0.0;
+  double y2 = y * y;
+  for (int side = 0; side < 2; ++side) {
+    double s3s = side == 0 ? +1.0 : -1.0;
+    double x3 = side == 0 ? c->x3d : c->x3u;
+    double c2 = y2 + x3 * x3;
+    for (int k = 0; k < 4; ++k) {
+      double r = sqrt(c->val[k] * c->val[k] + c2);
+      acc += s3s * c->sign[k] * (mul_log(c->val[k], c->val[k], c2, c->guard) - r);
+    }
+  }
+  return acc;
+}
+
+/* qOrthogonal (kernels.hpp:218-237) */
+static double q_orthogonal(span_t s1, span_t s3, span_t t1, span_t t2, double rel_tol, int max_levels,
+                           qstats* st) {
+  orth_ctx c;
+  u_corners(s1.lo, s1.hi, t1.lo, t1.hi, c.sign, c.val);
+  c.x3d = s3.lo;
+  c.x3u = s3.hi;
+  c.y2d = t2.lo;
+  c.y2u = t2.hi;
+  double scale = max4(s1.hi - s1.lo, t1.hi - t1.lo, s3.hi - s3.lo, t2.hi - t2.lo);
+  if (scale < 1e-30) scale = 1e-30;
+  c.guard = 1e-14 * scale;
+  double ty = integrate_with_splits(qorth_fy, &c, t2.lo, t2.hi, rel_tol, max_levels, st);
+  if (st->status) return NAN;
+  return ty / kFourPi;
+}
+
+orc_kv orc_q_pair_integral(const orc_rect* Ii, const orc_rect* Ij, int nsign_j, double rel_tol, int max_levels) {
+  /* q_pair_integral (kernels.hpp:295-315): test Ii, source Ij with its normal
+   * sign; no canonical reordering; coplanar pairs vanish. */
+  qstats st = {0, 1, 0};
+  orc_kv out;
+  if (max_levels > ROMB_MAX) max_levels = ROMB_MAX;
+  double ns = (double)nsign_j;
+  span_t iA = {Ii->a0, Ii->a1}, iB = {Ii->b0, Ii->b1}, jA = {Ij->a0, Ij->a1}, jB = {Ij->b0, Ij->b1};
+  if (Ii->axis == Ij->axis) {
+    double off = Ii->level - Ij->level;
+    out.value = off == 0.0 ? 0.0 : ns * q_parallel_offset(iA, iB, jA, jB, off, rel_tol, max_levels, &st);
+  } else {
+    int shared = 3 - Ii->axis - Ij->axis;
+    span_t s1 = rect_extent(Ii, shared), t1 = rect_extent(Ij, shared);
+    span_t i3 = rect_extent(Ii, Ij->axis), j2 = rect_extent(Ij, Ii->axis);
+    span_t s3 = {i3.lo - Ij->level, i3.hi - Ij->level};
+    span_t t2 = {j2.lo - Ii->level, j2.hi - Ii->level};
+    out.value = ns * q_orthogonal(s1, s3, t1, t2, rel_tol, max_levels, &st);
+  }
+  out.converged = st.converged;
+  out.evals = st.evals;
+  out.status = st.status;
+  return out;
+}
+
 /* ---------------- brute-force oracle (oracle.hpp:44-131,191-205) ---------------- */
 
 static void gauss_nodes(double lo, double hi, double* x, double* w) {
@@ -906,6 +992,105 @@ int orc_assemble_collocation(int64_t n, const orc_rect* p, const int* nsign, con
   free(ucol);
   free(order);
   if (m_out) *m_out = m;
+  return 0;
+}
+
+/* ---------------- Galerkin block system (assembly.hpp:37-75, 110-175) ---------------- */
+
+int orc_assemble_multi(int64_t n, const orc_rect* p, const int* nsign, const int* kind, const int* net,
+                       const int* reg_a, const int* reg_b, int nreg, const int* reg_id, const double* reg_eps,
+                       int main_net, double rel_tol, int max_levels, double* A, double* b, int64_t* m_out,
+                       int* all_converged) {
+  int64_t off[5] = {0, 0, 0, 0, 0};
+  for (int64_t k = 0; k < n; ++k) off[kind[k] + 1]++;
+  for (int k = 1; k < 5; ++k) off[k] += off[k - 1];
+  if (off[2] == 0) return 1;
+  int64_t o3 = off[3];
+  int64_t* qcol = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t* ucol = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  for (int64_t q = 0; q < n; ++q) { /* buildUnknownMap (assembly.hpp:51-75) */
+    qcol[q] = ucol[q] = -1;
+    if (kind[q] == 0 || kind[q] == 1) qcol[q] = q;
+    else if (kind[q] == 2) ucol[q] = q;
+    else {
+      ucol[q] = o3 + 2 * (q - o3);
+      qcol[q] = o3 + 2 * (q - o3) + 1;
+    }
+  }
+  int64_t cols = o3 + 2 * (off[4] - o3);
+  int* order = (int*)malloc(sizeof(int) * (size_t)nreg);
+  for (int k = 0; k < nreg; ++k) order[k] = k;
+  for (int a = 0; a < nreg; ++a)
+    for (int c = a + 1; c < nreg; ++c)
+      if (reg_id[order[c]] < reg_id[order[a]]) {
+        int t = order[a];
+        order[a] = order[c];
+        order[c] = t;
+      }
+  for (int64_t q = 0; q < n; ++q) {
+    int found = 0;
+    for (int k = 0; k < nreg; ++k) found |= reg_a[q] == reg_id[k];
+    if (!found) {
+      free(qcol); free(ucol); free(order);
+      return 1;
+    }
+  }
+  int64_t rows = 0;
+  for (int k = 0; k < nreg; ++k) {
+    int rid = reg_id[order[k]];
+    for (int64_t q = 0; q < n; ++q)
+      if (reg_a[q] == rid || (kind[q] == 3 && reg_b[q] == rid)) rows++;
+  }
+  if (rows != cols) {
+    free(qcol); free(ucol); free(order);
+    return 2;
+  }
+  int64_t m = rows;
+  for (int64_t i = 0; i < m * m; ++i) A[i] = 0.0;
+  for (int64_t i = 0; i < m; ++i) b[i] = 0.0;
+  int conv = 1;
+  int64_t row = 0;
+  for (int k = 0; k < nreg; ++k) {
+    int rid = reg_id[order[k]];
+    double eps_r = reg_eps[order[k]];
+    for (int64_t a = 0; a < n; ++a) {
+      if (!(reg_a[a] == rid || (kind[a] == 3 && reg_b[a] == rid))) continue;
+      double area_a = (p[a].a1 - p[a].a0) * (p[a].b1 - p[a].b0);
+      for (int64_t c = 0; c < n; ++c) {
+        if (!(reg_a[c] == rid || (kind[c] == 3 && reg_b[c] == rid))) continue;
+        /* Qloc(a, c) = q_pair_integral(P_a, P_c) * sideSign(P_c, region) */
+        orc_kv kq = orc_q_pair_integral(&p[a], &p[c], nsign[c], rel_tol, max_levels);
+        if (kq.status) { free(qcol); free(ucol); free(order); return 3; }
+        conv &= kq.converged;
+        double side = kind[c] == 3 ? (reg_a[c] == rid ? 1.0 : -1.0) : -1.0; /* sideSign (assembly.hpp:37-40) */
+        double coefU = kq.value * side / area_a + (a == c ? 0.5 : 0.0);
+        double known = (kind[c] == 0 && net[c] == main_net) ? 1.0 : 0.0; /* knownPotential */
+        if (ucol[c] >= 0)
+          A[row * m + ucol[c]] += coefU;
+        else
+          b[row] -= coefU * known;
+        if (kind[c] == 2) continue;
+        orc_kv ku = orc_u_pair_integral(&p[a], &p[c], rel_tol, max_levels);
+        if (ku.status) { free(qcol); free(ucol); free(order); return 3; }
+        conv &= ku.converged;
+        double area_c = (p[c].a1 - p[c].a0) * (p[c].b1 - p[c].b0);
+        double coefX = -ku.value / (area_a * area_c);
+        if (kind[c] == 3 && reg_b[c] == rid) {
+          double eps_a = 1.0;
+          for (int t = 0; t < nreg; ++t)
+            if (reg_id[t] == reg_a[c]) eps_a = reg_eps[t];
+          coefX *= -(eps_a / eps_r);
+        }
+        A[row * m + qcol[c]] += coefX;
+      }
+      row++;
+    }
+  }
+  free(qcol);
+  free(ucol);
+  free(order);
+  if (m_out) *m_out = m;
+  if (all_converged) *all_converged = conv;
   return 0;
 }
 

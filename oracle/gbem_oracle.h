@@ -87,6 +87,17 @@ int orc_assemble_collocation(int64_t n, const orc_rect* p, const int* nsign, con
                              const int* reg_a, const int* reg_b, int nreg, const int* reg_id,
                              const double* reg_eps, int main_net, double* A, double* b, int64_t* m_out);
 
+/* q_pair_integral (kernels.hpp:295-315): test Ii, source Ij with normal sign nsign_j. */
+orc_kv orc_q_pair_integral(const orc_rect* Ii, const orc_rect* Ij, int nsign_j, double rel_tol, int max_levels);
+
+/* assemble_multi (assembly.hpp:110-175), same arguments and layout as
+ * orc_assemble_collocation plus the QuadratureConfig; returns 3 on a non-finite
+ * integrand sample; *all_converged ANDs the kernels' flags. */
+int orc_assemble_multi(int64_t n, const orc_rect* p, const int* nsign, const int* kind, const int* net,
+                       const int* reg_a, const int* reg_b, int nreg, const int* reg_id, const double* reg_eps,
+                       int main_net, double rel_tol, int max_levels, double* A, double* b, int64_t* m_out,
+                       int* all_converged);
+
 /* lu_solve (solver.hpp:53-88): partial pivoting with whole-row swaps on a
  * row-major copy of A (n x n).  Returns 0, or 2 with *bad_row = k for "matrix
  * numerically singular (smallest pivot at row k)".  *resid = ||A x - b|| / ||b||. */

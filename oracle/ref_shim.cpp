@@ -47,6 +47,25 @@ double ref_q_point_rect(const double x[3], const orc_rect* r, int nsign) {
 }
 
 
+// gbem::q_pair_integral (kernels.hpp:295): test a, source b with normal sign nsign.
+orc_kv ref_q_pair_integral(const orc_rect* a, const orc_rect* b, int nsign, double rel_tol, int max_levels) {
+  orc_kv out{0.0, 1, 0, 0};
+  gbem::QuadratureConfig cfg;
+  cfg.relTol = rel_tol;
+  cfg.maxLevels = max_levels;
+  gbem::Rect B = toRect(*b);
+  B.normalSign = nsign;
+  try {
+    gbem::KernelValue kv = gbem::q_pair_integral(toRect(*a), B, cfg);
+    out.value = kv.value;
+    out.converged = kv.converged ? 1 : 0;
+    out.evals = kv.evals;
+  } catch (...) {
+    out.status = 2;
+  }
+  return out;
+}
+
 // gbem::u_pair_integral (kernels.hpp:270) with a QuadratureConfig.
 orc_kv ref_u_pair_integral(const orc_rect* a, const orc_rect* b, double rel_tol,
                            int max_levels) {

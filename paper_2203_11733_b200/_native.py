@@ -83,6 +83,9 @@ GPU_SYMBOLS = [
     ("gbem_spd_solve_factored_dev", C.c_int, [_P, _P, C.c_int64, _P, _P, C.POINTER(GbemSolveStats)]),
     ("gbem_assemble_collocation", C.c_int, [_P, C.POINTER(GbemBlockPanels), C.c_int64, C.POINTER(GbemRegion),
                                             C.c_int32, C.c_int32, _P, C.c_int64, _P, C.POINTER(C.c_int64)]),
+    ("gbem_assemble_multi", C.c_int, [_P, C.POINTER(GbemBlockPanels), C.c_int64, C.POINTER(GbemRegion),
+                                      C.c_int32, C.c_int32, C.POINTER(GbemQuadConfig), _P, C.c_int64, _P,
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     ("gbem_lu_solve", C.c_int, [_P, _P, _P, _P, C.POINTER(GbemSolveStats)]),
     ("gbem_matrix_upload_general", C.c_int, [_P, _P, C.c_int64, C.c_int64]),
     ("gbem_matrix_download", C.c_int, [_P, _P, C.c_int64]),
@@ -278,6 +281,35 @@ class Context:
         st = GbemSolveStats()
         self.check(self.lib.gbem_lu_solve(self.h, None, ptr(x), ptr(res), C.byref(st)))
         return A, b, x, float(res[0])
+
+    def assemble_multi(self, ps, regions, main_net: int, solve: bool = False, cfg=None):
+        """assemble_multi (assembly.hpp:110-175), the Galerkin block system, for an
+        api.PanelSet and regions [(id, eps), ...]: (A (m, m) row-major, b (m,),
+        all_converged) and, with solve, also the lu_solve solution and residual."""
+        P = PanelArrays(ps.axis, ps.level, ps.a0, ps.a1, ps.b0, ps.b1)
+        keep = [np.ascontiguousarray(ps.nsign, dtype=np.int8)] + [
+            np.ascontiguousarray(v, dtype=np.int32) for v in (ps.kind, ps.net, ps.regA, ps.regB)]
+        bp = GbemBlockPanels(P.struct(), *[ptr(v) for v in keep])
+        regs = (GbemRegion * len(regions))(*[GbemRegion(int(i), float(e)) for i, e in regions])
+        m = C.c_int64(0)
+        conv = C.c_int32(0)
+        q = cfg or self.quad()
+        mmax = P.n + int(np.sum(keep[1] == 3))  # rows: panels + interfaces (two unknowns each)
+        Abuf = np.zeros((mmax, mmax))
+        bbuf = np.zeros(mmax)
+        # the system stays in the context (for gbem_lu_solve); a row-major copy comes back
+        self.check(self.lib.gbem_assemble_multi(self.h, C.byref(bp), P.n, regs, len(regions), int(main_net),
+                                                C.byref(q), ptr(Abuf), mmax, ptr(bbuf), C.byref(m), C.byref(conv)))
+        mm = m.value
+        A = np.ascontiguousarray(Abuf[:mm, :mm])
+        b = bbuf[:mm].copy()
+        if not solve:
+            return A, b, bool(conv.value)
+        x = np.zeros(mm)
+        res = np.zeros(1)
+        st = GbemSolveStats()
+        self.check(self.lib.gbem_lu_solve(self.h, None, ptr(x), ptr(res), C.byref(st)))
+        return A, b, bool(conv.value), x, float(res[0])
 
     def spd_solve(self, B: np.ndarray):
         """B: (n,) or (n, k) right-hand sides; returns X like B, residuals (k,), stats."""

@@ -125,6 +125,72 @@ __global__ void k_collocation(const BPanel* __restrict__ P, const int32_t* __res
   if (lane == 0) b[warp] = bsum;
 }
 
+// Galerkin block system (assemble_multi, assembly.hpp:110-175): one warp per
+// (row, c) of a region's local blocks; the warp evaluates the reference's
+// double-layer q_pair_integral(P_a, P_c) and single-layer u_pair_integral with
+// the reference's own reductions and warp-cooperative Romberg (gbem_near.cuh):
+//   coefU = Qloc(a, c) / |P_a| + 1/2 [c == a],  Qloc = q * nsign_c * sideSign(P_c, region)
+//           -> A(row, uCol[c]) or b(row) -= coefU * known(c);
+//   coefX = -Uloc(a, c) / (|P_a| |P_c|) (x -(eps_A / eps_r) on the B side of an
+//           interface) -> A(row, qCol[c]), skipped for Neumann panels.
+// A's (row, column) entries are written once each; b accumulates atomically.
+// flags[0] counts non-converged Romberg runs, flags[1] non-finite samples.
+__global__ void __launch_bounds__(128)
+    k_galerkin_multi(const BPanel* __restrict__ P, const int32_t* __restrict__ row_region,
+                     const int32_t* __restrict__ row_panel, const int32_t* __restrict__ list_off,
+                     const int32_t* __restrict__ list, const int32_t* __restrict__ region_ids,
+                     const double* __restrict__ region_eps, int nreg, double* A, long long lda, double* b,
+                     double rel_tol, int max_levels, unsigned long long* flags) {
+  const int row = blockIdx.y, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int ri = row_region[row], a = row_panel[row];
+  const int lo = list_off[ri], hi = list_off[ri + 1];
+  if (lo + t >= hi) return;  // warp-uniform
+  const int c = list[lo + t];
+  const int rid = region_ids[ri];
+  const double eps_r = region_eps[ri];
+  const BPanel pa = P[a], pc = P[c];
+  WarpQuad st;
+  double q = 0.0;
+  if (pa.g.axis != pc.g.axis)
+    q = warp_q_orthogonal(pa.g, pc.g, rel_tol, max_levels, lane, st);
+  else if (pa.g.level != pc.g.level)
+    q = warp_q_parallel(pa.g, pc.g, rel_tol, max_levels, lane, st);
+  q *= (double)pc.nsign;
+  const double side = pc.kind == 3 ? (pc.rega == rid ? 1.0 : -1.0) : -1.0;  // sideSign (assembly.hpp:37-40)
+  const double coefU = q * side / pa.area + (c == a ? 0.5 : 0.0);
+  if (lane == 0) {
+    if (pc.ucol >= 0)
+      A[(long long)pc.ucol * lda + row] = coefU;
+    else if (pc.known != 0.0)
+      atomicAdd(&b[row], -coefU * pc.known);
+  }
+  if (pc.kind != 2) {  // Neumann: q known zero
+    // u_pair_integral (kernels.hpp:270-291): canonical argument order
+    const bool sw = d_rect_less(pc.g, pa.g);
+    const DPanel& x = sw ? pc.g : pa.g;
+    const DPanel& y = sw ? pa.g : pc.g;
+    double U;
+    if (x.axis == y.axis)
+      U = x.level == y.level ? d_u_coplanar(x.a0, x.a1, x.b0, x.b1, y.a0, y.a1, y.b0, y.b1)
+                             : warp_u_parallel(x, y, rel_tol, max_levels, lane, st);
+    else
+      U = warp_u_orthogonal(x, y, rel_tol, max_levels, lane, st);
+    double coefX = -U / (pa.area * pc.area);
+    if (pc.kind == 3 && pc.regb == rid) {
+      double eps_a = 1.0;
+      for (int k = 0; k < nreg; ++k)
+        if (region_ids[k] == pc.rega) eps_a = region_eps[k];
+      coefX *= -(eps_a / eps_r);
+    }
+    if (lane == 0) A[(long long)pc.qcol * lda + row] = coefX;
+  }
+  if (lane == 0) {
+    if (!st.converged) atomicAdd(&flags[0], 1ull);
+    if (st.nonfinite) atomicAdd(&flags[1], 1ull);
+  }
+}
+
 // ------------------------------------------------------------ LU
 
 constexpr int LNB = 64;          // LU block size
@@ -347,8 +413,9 @@ __global__ void k_absmax(const double* __restrict__ A, long long lda, int m, uns
 
 // Host side of the block system: unknown map (assembly.hpp:46-75), rows per
 // region (partition.hpp:238-243), device arrays, the collocation kernel.
-int gbem_internal_assemble_collocation(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n,
-                                       const gbem_region* regions, int32_t nreg, int32_t main_net, int64_t* m_out) {
+int gbem_internal_assemble_block(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n, const gbem_region* regions,
+                                 int32_t nreg, int32_t main_net, bool galerkin, const gbem_quad_config* cfg,
+                                 int64_t* m_out, int64_t* nonconv_out) {
   if (n <= 0 || nreg <= 0) return ctx->fail(GBEM_EINVAL, "empty block system");
   if (!P || !P->kind || !P->net || !P->reg_a || !P->reg_b || !P->nsign || !P->geom.axis || !P->geom.level ||
       !P->geom.a_lo || !P->geom.a_hi || !P->geom.b_lo || !P->geom.b_hi || !regions)
@@ -450,16 +517,43 @@ int gbem_internal_assemble_collocation(gbem_ctx* ctx, const gbem_block_panels* P
   GBEM_CUDA(ctx, cudaMemcpy(d_blob, blob.data(), sizeof(int32_t) * blob.size(), cudaMemcpyHostToDevice));
   GBEM_CUDA(ctx, cudaMemcpy(d_eps, eps.data(), sizeof(double) * nreg, cudaMemcpyHostToDevice));
   GBEM_CUDA(ctx, cudaMemcpy(d_bp, bp.data(), sizeof(BPanel) * n, cudaMemcpyHostToDevice));
-  k_collocation<<<(unsigned)((m * 32 + 255) / 256), 256, 0, ctx->stream>>>(
-      d_bp, d_blob + o_rr, d_blob + o_rp, d_blob + o_lo, d_blob + o_l, d_blob + o_id, d_eps, nreg, (int)m, ctx->d_A,
-      ctx->lda, ctx->d_rhs);
-  GBEM_LAUNCH_CHECK(ctx);
+  unsigned long long* d_flags = nullptr;
+  unsigned long long h_flags[2] = {0, 0};
+  if (!galerkin) {
+    k_collocation<<<(unsigned)((m * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+        d_bp, d_blob + o_rr, d_blob + o_rp, d_blob + o_lo, d_blob + o_l, d_blob + o_id, d_eps, nreg, (int)m, ctx->d_A,
+        ctx->lda, ctx->d_rhs);
+    GBEM_LAUNCH_CHECK(ctx);
+  } else {
+    if (m > 65535) return ctx->fail(GBEM_EINVAL, "Galerkin block system limited to 65535 rows");
+    double rel_tol = cfg && cfg->rel_tol > 0 ? cfg->rel_tol : 1e-8;
+    int levels = cfg && cfg->max_levels > 0 ? cfg->max_levels : 16;
+    if (levels > kRombMax) return ctx->fail(GBEM_EINVAL, "max_levels exceeds 20");
+    int lmax = 0;
+    for (int k = 0; k < nreg; ++k) lmax = std::max(lmax, list_off[k + 1] - list_off[k]);
+    GBEM_CUDA(ctx, cudaMalloc(&d_flags, sizeof(h_flags)));
+    GBEM_CUDA(ctx, cudaMemsetAsync(d_flags, 0, sizeof(h_flags), ctx->stream));
+    GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_rhs, 0, sizeof(double) * m, ctx->stream));
+    k_galerkin_multi<<<dim3((unsigned)((lmax + 3) / 4), (unsigned)m), 128, 0, ctx->stream>>>(
+        d_bp, d_blob + o_rr, d_blob + o_rp, d_blob + o_lo, d_blob + o_l, d_blob + o_id, d_eps, nreg, ctx->d_A,
+        ctx->lda, ctx->d_rhs, rel_tol, levels, d_flags);
+    GBEM_LAUNCH_CHECK(ctx);
+    GBEM_CUDA(ctx, cudaMemcpyAsync(h_flags, d_flags, sizeof(h_flags), cudaMemcpyDeviceToHost, ctx->stream));
+  }
   GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   cudaFree(d_blob);
   cudaFree(d_eps);
   cudaFree(d_bp);
+  if (d_flags) cudaFree(d_flags);
+  if (h_flags[1]) return ctx->fail(GBEM_ENUMERIC, "non-finite integrand sample in the Galerkin block system");
   if (m_out) *m_out = m;
+  if (nonconv_out) *nonconv_out = (int64_t)h_flags[0];
   return GBEM_OK;
+}
+
+int gbem_internal_assemble_collocation(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n,
+                                       const gbem_region* regions, int32_t nreg, int32_t main_net, int64_t* m_out) {
+  return gbem_internal_assemble_block(ctx, P, n, regions, nreg, main_net, false, nullptr, m_out, nullptr);
 }
 
 // lu_solve (solver.hpp:53-88) of the context matrix with right-hand side

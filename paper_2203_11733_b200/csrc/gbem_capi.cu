@@ -391,6 +391,28 @@ int gbem_assemble_collocation(gbem_ctx* ctx, const gbem_block_panels* P, int64_t
   return GBEM_OK;
 }
 
+int gbem_assemble_multi(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n, const gbem_region* regions,
+                        int32_t nregions, int32_t main_net, const gbem_quad_config* cfg, double* A_host, int64_t lda,
+                        double* b_host, int64_t* m_out, int32_t* all_converged) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int64_t m = 0, nonconv = 0;
+  int rc = gbem_internal_assemble_block(ctx, P, n, regions, nregions, main_net, true, cfg, &m, &nonconv);
+  if (rc) return rc;
+  ctx->block_m = m;
+  if (m_out) *m_out = m;
+  if (all_converged) *all_converged = nonconv == 0 ? 1 : 0;
+  if (A_host) {  // row-major copy of the column-major device matrix
+    if (lda < m) return ctx->fail(GBEM_EINVAL, "lda < m");
+    std::vector<double> t((size_t)ctx->lda * m);
+    GBEM_CUDA(ctx, cudaMemcpy(t.data(), ctx->d_A, sizeof(double) * t.size(), cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < m; ++r)
+      for (int64_t c = 0; c < m; ++c) A_host[r * lda + c] = t[(size_t)c * ctx->lda + r];
+  }
+  if (b_host) GBEM_CUDA(ctx, cudaMemcpy(b_host, ctx->d_rhs, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  return GBEM_OK;
+}
+
 int gbem_matrix_upload_general(gbem_ctx* ctx, const double* A_host, int64_t n, int64_t lda) {
   if (!ctx || (!A_host && n > 0)) return GBEM_EINVAL;
   if (n < 0 || lda < n) return ctx->fail(GBEM_EINVAL, "bad matrix dimensions");

@@ -110,6 +110,9 @@ struct gbem_ctx {
 int gbem_internal_ensure_matrix(gbem_ctx* ctx, int64_t n, int64_t border = 0);
 int gbem_internal_assemble_collocation(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n,
                                        const gbem_region* regions, int32_t nreg, int32_t main_net, int64_t* m_out);
+int gbem_internal_assemble_block(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n, const gbem_region* regions,
+                                 int32_t nreg, int32_t main_net, bool galerkin, const gbem_quad_config* cfg,
+                                 int64_t* m_out, int64_t* nonconv_out);
 int gbem_internal_lu_solve(gbem_ctx* ctx, double* d_b, double* d_x, double* d_resid, gbem_solve_stats* stats);
 int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, bool device_ptrs);
 int gbem_internal_check_pending_stats(gbem_ctx* ctx);

@@ -470,6 +470,102 @@ __device__ inline double warp_u_orthogonal(const DPanel& A, const DPanel& B, dou
   return (tx + ty) / kFourPi;
 }
 
+// ---- double layer (kernels.hpp:157-169, 218-237, 295-315), warp-cooperative
+// Romberg as the reference: test panel I, source panel J; the caller applies
+// the source normal sign.
+
+// qParallelOffset integrand (kernels.hpp:162-167): w(v) * sum_k s_k sqrt(u_k^2 + c2) / c2
+struct QParIntegrand {
+  double val[4];
+  double b2, t0, t3, plateau;
+  __device__ double operator()(double v) const {
+    const double c2 = v * v + b2;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc += Corners::sign(k) * sqrt(val[k] * val[k] + c2) / c2;
+    double m = v - t0;
+    m = plateau < m ? plateau : m;
+    m = (t3 - v) < m ? (t3 - v) : m;
+    const double w = 0.0 < m ? m : 0.0;
+    return w * acc;
+  }
+};
+
+// fy of qOrthogonal (kernels.hpp:224-235)
+struct QOrthFy {
+  double val[4];
+  double x3d, x3u, guard;
+  __device__ double operator()(double y) const {
+    double acc = 0.0;
+    const double y2 = y * y;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const double s3s = side == 0 ? 1.0 : -1.0;
+      const double x3 = side == 0 ? x3d : x3u;
+      const double c2 = y2 + x3 * x3;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double r = sqrt(val[k] * val[k] + c2);
+        acc += s3s * Corners::sign(k) * (d_mul_log(val[k], val[k], c2, guard) - r);
+      }
+    }
+    return acc;
+  }
+};
+
+// qParallelOffset for test I over source J, b = I.level - J.level != 0
+__device__ inline double warp_q_parallel(const DPanel& I, const DPanel& J, double rel_tol, int L, int lane,
+                                         WarpQuad& st) {
+  const double off = I.level - J.level;
+  QParIntegrand f;
+  Corners c(I.a0, I.a1, J.a0, J.a1);
+  for (int k = 0; k < 4; ++k) f.val[k] = c.val[k];
+  f.b2 = off * off;
+  const double xd = I.b0, xu = I.b1, yd = J.b0, yu = J.b1;
+  const double t0 = xd - yu, t3 = xu - yd;
+  const double da = xd - yd, db = xu - yu;
+  f.t0 = t0;
+  f.t3 = t3;
+  f.plateau = (yu - yd) < (xu - xd) ? (yu - yd) : (xu - xd);
+  double pts[5] = {t0, db < da ? db : da, da < db ? db : da, t3, 0.0};
+  int n = (t0 < 0.0 && 0.0 < t3) ? 5 : 4;
+  sort5(pts, n);
+  double cuts[5];
+  int count = 0;
+  for (int i = 0; i < n; ++i)
+    if (count == 0 || pts[i] > cuts[count - 1]) cuts[count++] = pts[i];
+  double total = 0.0;
+  for (int i = 0; i + 1 < count; ++i) {
+    total += warp_romberg(f, cuts[i], cuts[i + 1], rel_tol, L, lane, st);
+    if (st.nonfinite) return CUDART_NAN;
+  }
+  return off * total / kFourPi;
+}
+
+// orthFrame(I, J) + qOrthogonal (kernels.hpp:218-237, 245-255)
+__device__ inline double warp_q_orthogonal(const DPanel& I, const DPanel& J, double rel_tol, int L, int lane,
+                                           WarpQuad& st) {
+  const int shared = 3 - I.axis - J.axis;
+  double s1lo, s1hi, t1lo, t1hi, i3lo, i3hi, j2lo, j2hi;
+  panel_extent(I, shared, s1lo, s1hi);
+  panel_extent(J, shared, t1lo, t1hi);
+  panel_extent(I, J.axis, i3lo, i3hi);
+  panel_extent(J, I.axis, j2lo, j2hi);
+  const double s3lo = i3lo - J.level, s3hi = i3hi - J.level;
+  const double t2lo = j2lo - I.level, t2hi = j2hi - I.level;
+  Corners c(s1lo, s1hi, t1lo, t1hi);
+  double scale = dmax4(s1hi - s1lo, t1hi - t1lo, s3hi - s3lo, t2hi - t2lo);
+  scale = scale < 1e-30 ? 1e-30 : scale;
+  QOrthFy fy;
+  for (int k = 0; k < 4; ++k) fy.val[k] = c.val[k];
+  fy.x3d = s3lo;
+  fy.x3u = s3hi;
+  fy.guard = 1e-14 * scale;
+  const double ty = warp_with_splits(fy, t2lo, t2hi, rel_tol, L, lane, st);
+  if (st.nonfinite) return CUDART_NAN;
+  return ty / kFourPi;
+}
+
 // ---------------------------------------------------------------------------
 // Fixed-cost near field: the same reduced integrands, each reference segment
 // split at its midpoint and both halves integrated with x = end -+ t^2 grading

@@ -61,15 +61,16 @@ gbem_quad_config quad(const Options& o) {
 
 }  // namespace
 
-// The block (mixed-unknown) path of capacitance_row (extraction.hpp:132-143)
-// for the collocation baseline: GPU assemble_collocation + GPU lu_solve, then
+// The block (mixed-unknown) path of capacitance_row (extraction.hpp:132-143):
+// GPU assemble_multi (the Galerkin block system, method "galerkin-block") or,
+// for the collocation baseline, GPU assemble_collocation; then GPU lu_solve and
 // net_charges through the flux-unknown columns (extraction.hpp:55-79).
 static Row block_row(gbem_ctx* ctx, const Scene& s, const PanelSet& ps, int main_net, const Options& o) {
   const size_t n = ps.panels.size();
   Row row;
   row.main_net = main_net;
   row.diag.panels = n;
-  row.diag.method = "collocation";
+  row.diag.method = o.collocation ? "collocation" : "galerkin-block";
   SoA soa(ps);
   std::vector<int8_t> nsign(n);
   std::vector<int32_t> kind(n), net(n), ra(n), rb(n);
@@ -86,14 +87,34 @@ static Row block_row(gbem_ctx* ctx, const Scene& s, const PanelSet& ps, int main
   for (const Region& r : s.regions) regs.push_back(gbem_region{r.id, r.eps});
   auto t0 = std::chrono::steady_clock::now();
   int64_t m = 0;
-  raise(ctx, gbem_assemble_collocation(ctx, &bp, (int64_t)n, regs.data(), (int32_t)regs.size(), main_net, nullptr,
-                                       0, nullptr, &m));
-  if (!o.dump_matrix.empty()) {  // dump_system_matrix (extraction.hpp:83-99): row-major m x m
-    std::vector<double> A((size_t)m * m);
-    raise(ctx, gbem_assemble_collocation(ctx, &bp, (int64_t)n, regs.data(), (int32_t)regs.size(), main_net,
-                                         A.data(), m, nullptr, &m));
-    dump_matrix_file(o.dump_matrix, A, (size_t)m);
+  std::vector<double> A;
+  const bool dump = !o.dump_matrix.empty();
+  if (o.collocation) {
+    raise(ctx, gbem_assemble_collocation(ctx, &bp, (int64_t)n, regs.data(), (int32_t)regs.size(), main_net, nullptr,
+                                         0, nullptr, &m));
+    if (dump) {
+      A.resize((size_t)m * m);
+      raise(ctx, gbem_assemble_collocation(ctx, &bp, (int64_t)n, regs.data(), (int32_t)regs.size(), main_net,
+                                           A.data(), m, nullptr, &m));
+    }
+  } else {
+    gbem_quad_config q{};
+    q.rel_tol = o.rel_tol;
+    q.max_levels = o.max_levels;
+    int64_t mmax = (int64_t)n;
+    for (size_t k = 0; k < n; ++k) mmax += ps.panels[k].kind == kInterface ? 1 : 0;
+    if (dump) A.resize((size_t)mmax * mmax);
+    int32_t conv = 1;
+    raise(ctx, gbem_assemble_multi(ctx, &bp, (int64_t)n, regs.data(), (int32_t)regs.size(), main_net, &q,
+                                   dump ? A.data() : nullptr, mmax, nullptr, &m, &conv));
+    row.diag.converged = conv != 0;
+    if (dump) {  // compact the mmax-strided copy to m x m
+      for (int64_t r = 0; r < m; ++r)
+        for (int64_t c = 0; c < m; ++c) A[(size_t)r * m + c] = A[(size_t)r * mmax + c];
+      A.resize((size_t)m * m);
+    }
   }
+  if (dump) dump_matrix_file(o.dump_matrix, A, (size_t)m);  // dump_system_matrix (extraction.hpp:83-99)
   std::vector<double> x((size_t)m, 0.0);
   double resid = 0;
   gbem_solve_stats sst{};
@@ -135,11 +156,8 @@ static Row block_row(gbem_ctx* ctx, const Scene& s, const PanelSet& ps, int main
 
 Row capacitance_row(gbem_ctx* ctx, const Scene& s, int main_net, const Params& p, const Options& o) {
   PanelSet ps = partition_for_net(s, main_net, p);
-  if (o.collocation) return block_row(ctx, s, ps, main_net, o);
-  if (!single_dielectric(s))
-    throw ValidationError(
-        "multi-region / mixed-boundary scenes need the Galerkin block system, which the GPU path does not "
-        "implement yet; --baseline collocation solves them with the collocation block system");
+  // single path iff one region, all-Dirichlet boundary and no collocation baseline (extraction.hpp:110-114)
+  if (o.collocation || !single_dielectric(s)) return block_row(ctx, s, ps, main_net, o);
   if (ps.count(kNeumann) || ps.count(kInterface))
     throw ValidationError("single-dielectric assembly requires one region with an all-Dirichlet boundary");
   const size_t n = ps.panels.size();

@@ -53,6 +53,9 @@ def _bind(lib, prefix):
     f = getattr(lib, prefix + "_q_point_rect")
     f.restype = C.c_double
     f.argtypes = [C.POINTER(C.c_double), RP, C.c_int]
+    f = getattr(lib, prefix + "_q_pair_integral")
+    f.restype = KV
+    f.argtypes = [RP, RP, C.c_int, C.c_double, C.c_int]
 
 
 _orc = _ref = None
@@ -76,6 +79,10 @@ def orc():
         _orc.orc_assemble_collocation.restype = C.c_int
         _orc.orc_assemble_collocation.argtypes = [C.c_int64, C.c_void_p] + [C.c_void_p] * 5 + [
             C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
+        _orc.orc_assemble_multi.restype = C.c_int
+        _orc.orc_assemble_multi.argtypes = [C.c_int64, C.c_void_p] + [C.c_void_p] * 5 + [
+            C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_void_p, C.c_void_p,
+            C.POINTER(C.c_int64), C.POINTER(C.c_int)]
         _orc.orc_lu_solve.restype = C.c_int
         _orc.orc_lu_solve.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.POINTER(C.c_int64)]
@@ -192,3 +199,33 @@ def assemble_collocation(P: np.ndarray, nsign, kind, net, reg_a, reg_b, regions,
                                         b.ctypes.data, C.byref(m))
     mm = m.value
     return A[:mm * mm].reshape(mm, mm), b[:mm], st
+
+
+def q_pairs(lib_name: str, A: np.ndarray, B: np.ndarray, nsign, rel_tol=1e-8, max_levels=16):
+    """q_pair_integral (kernels.hpp:295-315) of test rects A against source rects B
+    (normal signs nsign): (values, converged, status)."""
+    lib = orc() if lib_name == "orc" else ref()
+    f = lib.orc_q_pair_integral if lib_name == "orc" else lib.ref_q_pair_integral
+    ra, rb = rects_from_matrix(A), rects_from_matrix(B)
+    out = np.zeros(len(A)); conv = np.zeros(len(A), dtype=np.int32); st = np.zeros(len(A), dtype=np.int32)
+    for k in range(len(A)):
+        kv = f(C.byref(ra[k]), C.byref(rb[k]), int(nsign[k]), rel_tol, max_levels)
+        out[k], conv[k], st[k] = kv.value, kv.converged, kv.status
+    return out, conv, st
+
+
+def assemble_multi(P: np.ndarray, nsign, kind, net, reg_a, reg_b, regions, main_net: int, rel_tol=1e-8,
+                   max_levels=16):
+    """orc_assemble_multi (assembly.hpp:110-175): (A (m, m), b (m,), status, all_converged)."""
+    n = len(P)
+    rp = rects_from_matrix(P)
+    ints = [np.ascontiguousarray(v, dtype=np.int32) for v in (nsign, kind, net, reg_a, reg_b)]
+    rid = np.array([r[0] for r in regions], dtype=np.int32)
+    reps = np.array([r[1] for r in regions], dtype=np.float64)
+    mmax = n + int(np.sum(ints[1] == 3))
+    A = np.zeros(mmax * mmax); b = np.zeros(mmax); m = C.c_int64(0); conv = C.c_int(0)
+    st = orc().orc_assemble_multi(n, C.cast(rp, C.c_void_p), *[v.ctypes.data for v in ints], len(rid),
+                                  rid.ctypes.data, reps.ctypes.data, int(main_net), rel_tol, max_levels,
+                                  A.ctypes.data, b.ctypes.data, C.byref(m), C.byref(conv))
+    mm = m.value
+    return A[:mm * mm].reshape(mm, mm), b[:mm], st, bool(conv.value)

@@ -1,6 +1,7 @@
-"""The block (mixed-unknown) system on the GPU: lu_solve (solver.hpp:53-88) and
-the collocation baseline assemble_collocation (assembly.hpp:179-227), against
-the CPU oracle restatement (oracle/gbem_oracle.c, its point kernels pinned
+"""The block (mixed-unknown) system on the GPU: lu_solve (solver.hpp:53-88), the
+Galerkin block system assemble_multi (assembly.hpp:110-175) and the collocation
+baseline assemble_collocation (assembly.hpp:179-227), against the CPU oracle
+restatement (oracle/gbem_oracle.c, its point and double-layer kernels pinned
 bit-for-bit to the compiled reference in test_oracle_golden.py)."""
 import json
 from pathlib import Path
@@ -101,11 +102,61 @@ def test_two_layer_cmatrix_collocation_end_to_end(ctx):
     assert "# method net1=collocation net2=collocation" in csv
 
 
-def test_multi_region_needs_block_formulation(ctx):
+def _oracle_multi(ps, regions, net):
+    return O.assemble_multi(ps.matrix(), ps.nsign, ps.kind, ps.net, ps.regA, ps.regB, regions, net)
+
+
+@pytest.mark.parametrize("scene,net", [(TWO, 1), (TWO, 2)])
+def test_galerkin_block_system_matches_oracle(ctx, scene, net):
+    """assemble_multi (assembly.hpp:110-175) on the GPU against the CPU restatement
+    (its q_pair_integral pinned bit-for-bit to the compiled reference): same
+    reductions and Romberg rule, warp-parallel sample sums."""
+    m = g.parse_model(scene.read_text())
+    ps = m.partition(0, net)
+    A, b, conv, x, res = ctx.assemble_multi(ps, m.regions, net, solve=True)
+    Ao, bo, st, convo = _oracle_multi(ps, m.regions, net)
+    assert st == 0 and A.shape == Ao.shape and conv == convo
+    # entries agree to the quadrature tolerance (relTol 1e-8); most bit-for-bit close
+    d = np.abs(A - Ao)
+    assert d.max() <= 1e-8 * np.abs(Ao).max(), d.max() / np.abs(Ao).max()
+    assert np.median(d[Ao != 0] / np.abs(Ao[Ao != 0])) <= 1e-13
+    assert np.abs(b - bo).max() <= 1e-8 * max(np.abs(bo).max(), 1.0)
+    xo, ro, sto, _ = O.lu_solve(Ao, bo)
+    assert sto == 0
+    assert np.abs(x - xo).max() <= 1e-6 * np.abs(xo).max()
+    assert res <= 1e-12
+
+
+def _oracle_cmatrix_multi(m):
+    """capacitance_matrix through the Galerkin block system, all on the CPU oracle."""
+    ids = m.net_ids
+    eps = dict(m.regions)
+    C = np.zeros((len(ids), len(ids)))
+    for r, net in enumerate(ids):
+        ps = m.partition(0, net)
+        A, b, st, _ = _oracle_multi(ps, m.regions, net)
+        assert st == 0
+        x, _, _, _ = O.lu_solve(A, b)
+        for k in range(len(ps)):
+            if ps.kind[k] == 0:
+                C[r, ids.index(int(ps.net[k]))] += eps[int(ps.regA[k])] * EPS0 * x[k] * 1e-6
+    return C
+
+
+def test_two_layer_cmatrix_galerkin_end_to_end(ctx):
+    """The reference's default path for a two-dielectric scene
+    (capacitance_row -> assemble_multi -> lu_solve, extraction.hpp:132-143)."""
     m = g.parse_model(TWO.read_text())
-    with pytest.raises(g.api.ValidationError if hasattr(g, "api") else ValueError) as e:
-        m.extract(net=1)
-    assert "collocation" in str(e.value)
+    csv, js = m.extract(net=-1, mode=0)
+    assert [r["method"] for r in js["rows"]] == ["galerkin-block", "galerkin-block"]
+    Cg = m.last_cap
+    Co = _oracle_cmatrix_multi(m)
+    assert np.abs(Cg - Co).max() <= 1e-6 * np.abs(Co).max(), (Cg, Co)
+    assert Cg[0, 0] > 0 and Cg[1, 1] > 0 and Cg[0, 1] < 0 and Cg[1, 0] < 0
+    assert "# method net1=galerkin-block net2=galerkin-block" in csv
+    # the Galerkin and collocation block systems agree to the discretisation level
+    m.extract(net=-1, baseline="collocation")
+    assert np.abs(m.last_cap - Cg).max() <= 0.1 * np.abs(Cg).max()
 
 
 def test_collocation_single_region_agrees_with_galerkin(ctx):

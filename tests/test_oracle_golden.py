@@ -218,3 +218,60 @@ def test_lu_oracle_singular_row():
     A = np.array([[1.0, 2.0, 3.0], [2.0, 4.0, 6.0], [1.0, 0.0, 1.0]])
     _, _, st, bad = O.lu_solve(A, np.ones(3))
     assert st == 2 and bad == 2
+
+
+# Double layer (test rect, source rect, source normal sign, frozen value):
+# proj/tests/test_kernels.cpp:217-241, checked there at 1e-6 relative.
+QGOLD = [
+    ((2, 1, (0, 1), (0, 1)), (2, 0, (-0.2, 1.3), (0.1, 0.8)), 1, 0.0554151455434669),
+    ((2, 0, (0, 1), (0, 1)), (0, 2, (0.5, 1.5), (1, 2)), -1, 0.011324772441013004),
+    ((2, 0, (0, 1), (0, 1)), (1, 0, (0, 1), (0, 1)), 1, 0.11113873320194041),
+    ((1, -0.8575535635412491, (0.34410487297464243, 0.9076144923978153), (-0.622649673169549, 0.1631672183635413)),
+     (0, 0.9076144923978153, (-1.6627438264788437, -0.8575535635412491), (-0.6769789681037953, 1.073134547946061)),
+     1, -0.0733166487590698),
+]
+
+
+def _qrows(rs):
+    return np.array([[r[0], r[1], r[2][0], r[2][1], r[3][0], r[3][1]] for r in rs], dtype=float)
+
+
+def test_double_layer_frozen_values():
+    A = _qrows([g[0] for g in QGOLD]); B = _qrows([g[1] for g in QGOLD]); ns = [g[2] for g in QGOLD]
+    v, conv, st = O.q_pairs("orc", A, B, ns)
+    assert (st == 0).all() and conv.all()
+    for k, g in enumerate(QGOLD):
+        assert abs(v[k] - g[3]) <= 1e-6 * abs(g[3]), (k, v[k], g[3])
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("seed", [424242, 5])
+def test_double_layer_bit_exact_vs_compiled_reference(seed):
+    rng = np.random.default_rng(seed)
+    A, B = G.classic_pairs(rng, 120)
+    ns = rng.choice([-1, 1], size=len(A))
+    vo, co, so = O.q_pairs("orc", A, B, ns)
+    vr, cr, sr = O.q_pairs("ref", A, B, ns)
+    assert (so == sr).all() and (co == cr).all()
+    assert np.array_equal(vo, vr)
+    Aq = _qrows([g[0] for g in QGOLD]); Bq = _qrows([g[1] for g in QGOLD]); nq = [g[2] for g in QGOLD]
+    assert np.array_equal(O.q_pairs("orc", Aq, Bq, nq)[0], O.q_pairs("ref", Aq, Bq, nq)[0])
+
+
+def test_double_layer_closed_surface_identity():
+    """test_kernels.cpp:274-295: on a closed cube (2x2 panels per face, outward
+    normals) the double-layer row sums equal -|I|/2."""
+    rows, ns = [], []
+    for axis in range(3):
+        for side in range(2):
+            for ia in range(2):
+                for ib in range(2):
+                    rows.append([axis, float(side), 0.5 * ia, 0.5 * (ia + 1), 0.5 * ib, 0.5 * (ib + 1)])
+                    ns.append(1 if side else -1)
+    P = np.array(rows)
+    n = len(P)
+    ii, jj = np.meshgrid(np.arange(n), np.arange(n), indexing="ij")
+    v, _, st = O.q_pairs("orc", P[ii.ravel()], P[jj.ravel()], np.array(ns)[jj.ravel()])
+    assert (st == 0).all()
+    s = v.reshape(n, n).sum(axis=1)
+    assert np.abs(s + 0.5 * 0.25).max() <= 1e-3 * 0.125
