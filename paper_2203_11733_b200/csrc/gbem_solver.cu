@@ -1105,7 +1105,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     // next band update writes (no two updates of one column run concurrently).
     // Events: P (potrf done), T (trsm done), B (band done), RA (rest_a done).
     cudaStream_t lo = ctx->g_main, hi = ctx->g_main_hi, p = ctx->g_side;
-    cudaEvent_t evP = ctx->ev_panel, evB = ctx->ev_col, evT = ctx->ev_gt, evRA = ctx->ev_gra;
+    cudaEvent_t evP = ctx->ev_panel, evB = ctx->ev_col, evT = ctx->ev_gt;
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_gs, s));
     GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, ctx->ev_gs, 0));
     GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, ctx->ev_gs, 0));
