@@ -611,7 +611,7 @@ __device__ long long g_solve_clk[2][8];
 template <int RT>
 __global__ void __launch_bounds__(kSolveThreads, 1)
     k_solve_coop(const double* __restrict__ A, long long lda, const double* __restrict__ Linv, int n, int R,
-                 const double* __restrict__ B, double* W, double* Out, int dbg, int skip_fwd) {
+                 const double* __restrict__ B, double* W, double* Out, int dbg) {
   // dbg (phase-breakdown timing only, GBEM_SOLVE_DBG): 1 skip diagonal solves,
   // 2 skip panel updates, 4 skip grid barriers (results wrong for 1/2/4)
   cg::grid_group grid = cg::this_grid();
@@ -651,18 +651,12 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
 #ifdef GBEM_SOLVE_TIMING
   long long t_prev = clock64();
 #endif
-  if (skip_fwd) {
-    // bordered factorisation: Out already holds y = inv(L) b
-    solve_prefetch_block(Ls, Linv + (size_t)(nblk - 1) * NB * NB, tid);
-    bwd_prefetch(nblk - 1);
-  } else {
-    solve_prefetch_block(Ls, Linv, tid);
-    fwd_prefetch(0);
-    for (long long i = grid.thread_rank(); i < nR; i += grid.size()) W[i] = B[i];
-    grid.sync();
-  }
+  solve_prefetch_block(Ls, Linv, tid);
+  fwd_prefetch(0);
+  for (long long i = grid.thread_rank(); i < nR; i += grid.size()) W[i] = B[i];
+  grid.sync();
   // ---- forward: W holds b - sum_{j<k} L_kj y_j, Out receives y
-  for (int b = 0; b < (skip_fwd ? 0 : nblk); ++b) {
+  for (int b = 0; b < nblk; ++b) {
     const int k0 = b * NB, kb = min(NB, n - k0);
     for (int idx = tid; idx < kb * R; idx += blockDim.x) {
       const int i = idx % kb, q = idx / kb;
@@ -742,7 +736,7 @@ __global__ void __launch_bounds__(kSolveThreads, 1)
 // (i, h): column i of the block, rows [64 h, 64 h + 64).  One CTA per block,
 // all co-resident (cooperative launch), nblk <= #SMs.
 constexpr int kFlowThreads = 256, kFlowLD = NB + 1;
-constexpr size_t kFlowSmem = (size_t)(NB * kFlowLD + 3 * NB * 8) * sizeof(double);
+constexpr size_t kFlowSmem = (size_t)(NB * kFlowLD + 3 * NB * 16) * sizeof(double);
 template <int RT>
 __global__ void __launch_bounds__(kFlowThreads, 1)
     k_bwd_flow(const double* __restrict__ A, long long lda, const double* __restrict__ Linv, int n, int R,
@@ -1363,7 +1357,7 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
   cudaEventRecord(ctx->ev[1], s);
   static const int blocked_min = getenv("GBEM_SOLVE_BLOCKED_MIN") ? atoi(getenv("GBEM_SOLVE_BLOCKED_MIN")) : 17;
   const int nblk_s = (n + NB - 1) / NB;
-  if (y_from_border && R <= 8 && nblk_s <= ctx->num_sms) {
+  if (y_from_border && R < blocked_min && R <= 16 && nblk_s <= ctx->num_sms) {
     // bordered factorisation: y is in the border rows; dataflow backward substitution
     if (!ctx->d_flags) {
       GBEM_CUDA(ctx, cudaMalloc(&ctx->d_flags, sizeof(int) * 1024));
@@ -1384,11 +1378,13 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
     int* fl = ctx->d_flags;
     void* args[] = {(void*)&cA, (void*)&lda, (void*)&cL, (void*)&nn, (void*)&RR, (void*)&cY, (void*)&d_X, (void*)&fl,
                     (void*)&ep};
-    void* fn = R <= 2 ? (void*)k_bwd_flow<2> : R <= 4 ? (void*)k_bwd_flow<4> : (void*)k_bwd_flow<8>;
+    void* fn = R <= 2 ? (void*)k_bwd_flow<2> : R <= 4 ? (void*)k_bwd_flow<4> : R <= 8 ? (void*)k_bwd_flow<8>
+                                                                                 : (void*)k_bwd_flow<16>;
     GBEM_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlowSmem));
     GBEM_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3(nblk_s), dim3(kFlowThreads), args, kFlowSmem, s));
     GBEM_LAUNCH_CHECK(ctx);
-  } else if (R >= blocked_min) {
+  } else if (R >= blocked_min || y_from_border) {
+    // (bordered: y sits in the border rows; the DMMA-blocked backward sweep takes it for any width)
     rc = solve_blocked(ctx, d_B, R, d_X, y_from_border);
     if (rc) return rc;
   } else {
@@ -1402,15 +1398,8 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
       double* Xq = d_X + (size_t)q0 * n;
       double* Sq = scratch;  // scratch holds n * R >= n * RR
       int dd = dbg;
-      int skip = y_from_border ? 1 : 0;
-      if (y_from_border) {
-        // Sq (the kernel's Out) receives y of columns q0.. from the border rows
-        const long long cnt = (long long)n * RR;
-        k_border_to_y<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(ctx->d_A + q0, lda, n, RR, Sq, 0);
-        GBEM_LAUNCH_CHECK(ctx);
-      }
       void* args[] = {(void*)&cA, (void*)&lda, (void*)&cL, (void*)&nn, (void*)&RR, (void*)&Bq, (void*)&Xq, (void*)&Sq,
-                      (void*)&dd, (void*)&skip};
+                      (void*)&dd};
       // register blocking over the right-hand sides: the smallest instantiated width >= RR
       void* fn = RR <= 1 ? (void*)k_solve_coop<1> : RR <= 2 ? (void*)k_solve_coop<2> : RR <= 4 ? (void*)k_solve_coop<4>
                : RR <= 6 ? (void*)k_solve_coop<6> : RR <= 8 ? (void*)k_solve_coop<8> : (void*)k_solve_coop<16>;

@@ -113,3 +113,26 @@ def test_matrix_dump_round_trip(tmp_path):
     ps = g.partition_scene(m, 1)
     sysm = g.assemble_single(ps)
     assert n == len(ps) and np.array_equal(A, sysm.A)
+
+
+@pytest.mark.parametrize("K", [1, 3, 6, 8, 9, 12, 16, 17, 24])
+def test_bordered_extraction_every_solve_path(ctx, K):
+    """gbem_extract_cmatrix's bordered factorisation (C = B^T A^-1 B from the
+    border corner, X from the backward substitution) across the right-hand-side
+    widths that select the dataflow (K <= 8), cooperative (9..16) and DMMA-
+    blocked (>= 17) backward substitutions; n = 2,688 also runs the
+    SM-partitioned look-ahead (n >= 2 * 1024).  Reference: the GPU-assembled A
+    solved densely by numpy."""
+    m = g.config_model(1, scale=1.0)
+    ps = m.partition(1)
+    n = len(ps)
+    rng = np.random.default_rng(K)
+    net = rng.integers(0, K, size=n).astype(np.int32)
+    net[:K] = np.arange(K)  # every net has a panel
+    Cm, res, ast, sst = ctx.extract_cmatrix(ps.arrays(), net, K, 3.9)
+    A, _ = ctx.assemble_single(ps.arrays())
+    B = (net[:, None] == np.arange(K)[None, :]).astype(float)
+    Cref = 3.9 * 8.854187817e-12 * 1e-6 * (B.T @ np.linalg.solve(A, B))
+    assert np.abs(Cm - Cref).max() <= 1e-9 * np.abs(Cref).max(), np.abs(Cm - Cref).max()
+    assert np.array_equal(Cm, Cm.T)  # Y^T Y: exactly symmetric
+    assert res.max() <= 1e-12, res
