@@ -136,3 +136,20 @@ def test_bordered_extraction_every_solve_path(ctx, K):
     assert np.abs(Cm - Cref).max() <= 1e-9 * np.abs(Cref).max(), np.abs(Cm - Cref).max()
     assert np.array_equal(Cm, Cm.T)  # Y^T Y: exactly symmetric
     assert res.max() <= 1e-12, res
+
+
+@pytest.mark.parametrize("K", [1, 6, 9, 16, 17, 40])
+def test_spd_solve_every_width(ctx, K):
+    """cholesky_solve with K right-hand sides on an assembled Galerkin matrix
+    (n = 2,688: the SM-partitioned factorisation), forward + backward
+    substitution (cooperative below 17 columns, DMMA-blocked above) against numpy."""
+    m = g.config_model(1, scale=1.0)
+    ps = m.partition(1)
+    A, _ = ctx.assemble_single(ps.arrays())
+    rng = np.random.default_rng(100 + K)
+    B = rng.standard_normal((len(ps), K))
+    ctx.matrix_upload(A)
+    X, res, st = ctx.spd_solve(B)
+    Xr = np.linalg.solve(A, B)
+    assert np.abs(X - Xr).max() <= 1e-10 * np.abs(Xr).max()
+    assert np.max(res) <= 1e-12
