@@ -515,6 +515,19 @@ __device__ __forceinline__ double warp_reduce_d(double x) {
   return x;
 }
 
+// acc + W / sqrt(x): MUFU.RSQ64H seed y (relative error <= 9.1e-7) and one
+// Newton step folded into the weighted accumulation,
+//   W / sqrt(x) ~ W y (1 + e / 2),  e = 1 - x y^2,
+// relative error <= 1.3e-12 per node (tools/rsq_acc.cu), an order below the
+// far-field rule's own 1e-12 tolerance and 100x inside the 1e-10 gate;
+// 5 FP64-pipe instructions + MUFU instead of 6 for the Householder form.
+__device__ __forceinline__ double wrsq_acc(double W, double x, double acc) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x * y, y, 1.0);
+  return fma(W * y, fma(0.5, e, 1.0), acc);
+}
+
 // One decoded list: type, orders, and the geometry of its nodes
 //   single:  w = p0 + p1 x_k,                  W = p1 g_k
 //   product: w = p0 + p1 x_a - p2 x_b,         W = p1 g_a p2 g_b       (k = a q2 + b)
@@ -707,8 +720,8 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? 4 : 2)
         double t0 = 0.0, t1 = 0.0;
 #pragma unroll
         for (int a = 0; a < M; a += 2) {
-          t0 = fma(W1[a], rsq64(r2 + w1[a]), t0);
-          if (a + 1 < M) t1 = fma(W1[a + 1], rsq64(r2 + w1[a + 1]), t1);
+          t0 = wrsq_acc(W1[a], r2 + w1[a], t0);
+          if (a + 1 < M) t1 = wrsq_acc(W1[a + 1], r2 + w1[a + 1], t1);
         }
         acc = fma(W3 * W2s[b * kFarThreads], t0 + t1, acc);
       }
@@ -716,7 +729,7 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? 4 : 2)
     const double U = acc / kFourPi;
     const double nodes = (double)M * m2 * m3;
     evals += nodes;
-    flops += 11.0 * nodes + 4.0 * m2 * m3 + 6.0 * (M + m2 + m3) + 30.0;
+    flops += 9.0 * nodes + 4.0 * m2 * m3 + 6.0 * (M + m2 + m3) + 30.0;  // per node: DADD, DMUL, 2 DFMA, DMUL, DFMA
     store_value(o, i, j, A, B, U);
     if (!o.A && o.conv) o.conv[i] = 1;
   }

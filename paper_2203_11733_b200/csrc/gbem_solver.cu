@@ -1355,9 +1355,9 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
   double* scratch = Ysym + (size_t)n * R;
   const double* Linv = ctx->d_linv;
   cudaEventRecord(ctx->ev[1], s);
-  static const int blocked_min = getenv("GBEM_SOLVE_BLOCKED_MIN") ? atoi(getenv("GBEM_SOLVE_BLOCKED_MIN")) : 17;
+  static const int blocked_min = getenv("GBEM_SOLVE_BLOCKED_MIN") ? atoi(getenv("GBEM_SOLVE_BLOCKED_MIN")) : 9;
   const int nblk_s = (n + NB - 1) / NB;
-  if (y_from_border && R < blocked_min && R <= 16 && nblk_s <= ctx->num_sms) {
+  if (y_from_border && R <= 16 && nblk_s <= ctx->num_sms) {
     // bordered factorisation: y is in the border rows; dataflow backward substitution
     if (!ctx->d_flags) {
       GBEM_CUDA(ctx, cudaMalloc(&ctx->d_flags, sizeof(int) * 1024));

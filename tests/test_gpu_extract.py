@@ -119,11 +119,10 @@ def test_matrix_dump_round_trip(tmp_path):
 def test_bordered_extraction_every_solve_path(ctx, K):
     """gbem_extract_cmatrix's bordered factorisation (C = B^T A^-1 B from the
     border corner, X from the backward substitution) across the right-hand-side
-    widths that select the dataflow (K <= 8), cooperative (9..16) and DMMA-
-    blocked (>= 17) backward substitutions; n = 2,688 also runs the
+    widths that select the dataflow (K <= 16) and DMMA-blocked (>= 17) backward substitutions; n = 2,832 also runs the
     SM-partitioned look-ahead (n >= 2 * 1024).  Reference: the GPU-assembled A
     solved densely by numpy."""
-    m = g.config_model(1, scale=1.0)
+    m = g.config_model(1, scale=1.4)
     ps = m.partition(1)
     n = len(ps)
     rng = np.random.default_rng(K)
@@ -141,9 +140,9 @@ def test_bordered_extraction_every_solve_path(ctx, K):
 @pytest.mark.parametrize("K", [1, 6, 9, 16, 17, 40])
 def test_spd_solve_every_width(ctx, K):
     """cholesky_solve with K right-hand sides on an assembled Galerkin matrix
-    (n = 2,688: the SM-partitioned factorisation), forward + backward
-    substitution (cooperative below 17 columns, DMMA-blocked above) against numpy."""
-    m = g.config_model(1, scale=1.0)
+    (n = 2,832: the SM-partitioned factorisation), forward + backward
+    substitution (cooperative up to 8 columns, DMMA-blocked above) against numpy."""
+    m = g.config_model(1, scale=1.4)
     ps = m.partition(1)
     A, _ = ctx.assemble_single(ps.arrays())
     rng = np.random.default_rng(100 + K)
