@@ -582,67 +582,46 @@ __device__ __forceinline__ void far_list(uint32_t code, int src, const DPanel& A
   }
 }
 
-__device__ __forceinline__ void node_single(const FarList& L, int k, const double* gx, const double* gw, double& w2,
-                                            double& W) {
-  const double w = fma(L.p1, gx[L.q1 * kQMax + k], L.p0);
-  W = L.p1 * gw[L.q1 * kQMax + k];
-  w2 = w * w;
-}
-__device__ __forceinline__ void node_product(const FarList& L, int k, const double* gx, const double* gw, double& w2,
-                                             double& W) {
-  const int a = (k * ((65536 + L.q2 - 1) / L.q2)) >> 16, b = k - a * L.q2;  // k / q2 (exact for k < 64)
-  const double w = fma(L.p1, gx[L.q1 * kQMax + a], L.p0) - L.p2 * gx[L.q2 * kQMax + b];
-  W = (L.p1 * gw[L.q1 * kQMax + a]) * (L.p2 * gw[L.q2 * kQMax + b]);
-  w2 = w * w;
-}
-__device__ __forceinline__ void node_tent(const FarList& L, int k, const double* gx, const double* gw, double& w2,
-                                          double& W) {
-  const int qr = L.q1, qp = L.q2;
-  const int piece = k < qr ? 0 : (k < qr + qp ? 1 : 2);
-  const int kk = piece == 0 ? k : (piece == 1 ? k - qr : k - qr - qp);
-  const int q = piece == 1 ? qp : qr;
-  const double lo = piece == 0 ? L.p0 : (piece == 1 ? L.p1 : L.p2);
-  const double hi = piece == 0 ? L.p1 : (piece == 1 ? L.p2 : L.p3);
-  const double h = 0.5 * (hi - lo);
-  const double w = fma(h, gx[q * kQMax + kk], 0.5 * (lo + hi));
-  const double T = piece == 0 ? w - L.p0 : (piece == 1 ? L.p4 : L.p3 - w);
-  W = (h * gw[q * kQMax + kk]) * T;
-  w2 = w * w;
-}
-
-// The inner list into registers (M compile-time): one type branch per pair,
-// the node loop unrolled inside it.
-template <int M>
-__device__ __forceinline__ void build_inner(const FarList& L, const double* gx, const double* gw, double (&w2)[M],
-                                            double (&W)[M]) {
-  if (L.type == kListTent) {
-#pragma unroll
-    for (int k = 0; k < M; ++k) node_tent(L, k, gx, gw, w2[k], W[k]);
-  } else if (L.type == kListProduct) {
-#pragma unroll
-    for (int k = 0; k < M; ++k) node_product(L, k, gx, gw, w2[k], W[k]);
-  } else if (L.type == kListSingle) {
-#pragma unroll
-    for (int k = 0; k < M; ++k) node_single(L, k, gx, gw, w2[k], W[k]);
-  } else {
-#pragma unroll
-    for (int k = 0; k < M; ++k) {
-      w2[k] = L.p0 * L.p0;
-      W[k] = 1.0;
-    }
-  }
-}
-
-// An outer list of m nodes into this thread's shared-memory slots (stride ST).
+// A list's nodes into this thread's shared-memory slots (stride ST), walked
+// piece by piece (one Gauss rule per piece: the panel rule of a single list,
+// q_I shifted copies of the q_J rule for a product, ramp / plateau / ramp for
+// a tent), so a node costs two table loads and four FP64 operations.
 template <int ST>
-__device__ __forceinline__ void build_outer(const FarList& L, int m, const double* gx, const double* gw, double* w2,
-                                            double* W) {
+__device__ __forceinline__ void emit_list(const FarList& L, const double* gx, const double* gw, double* w2,
+                                          double* W) {
   if (L.type == kListTent) {
-    for (int k = 0; k < m; ++k) node_tent(L, k, gx, gw, w2[k * ST], W[k * ST]);
+    int idx = 0;
+    for (int piece = 0; piece < 3; ++piece) {
+      const bool up = piece == 0, flat = piece == 1;
+      const int q = flat ? L.q2 : L.q1;
+      const double lo = up ? L.p0 : (flat ? L.p1 : L.p2), hi = up ? L.p1 : (flat ? L.p2 : L.p3);
+      const double c = 0.5 * (lo + hi), h = 0.5 * (hi - lo);
+      const double al = up ? -L.p0 : (flat ? L.p4 : L.p3), be = up ? 1.0 : (flat ? 0.0 : -1.0);
+      for (int k = 0; k < q; ++k, ++idx) {
+        const double w = fma(h, gx[q * kQMax + k], c);
+        w2[idx * ST] = w * w;
+        W[idx * ST] = (h * gw[q * kQMax + k]) * fma(be, w, al);
+      }
+    }
   } else if (L.type == kListProduct) {
-    for (int k = 0; k < m; ++k) node_product(L, k, gx, gw, w2[k * ST], W[k * ST]);
+    const int qi = L.q1, qj = L.q2;
+    int idx = 0;
+    for (int a = 0; a < qi; ++a) {
+      const double ca = fma(L.p1, gx[qi * kQMax + a], L.p0);
+      const double fa = (L.p1 * gw[qi * kQMax + a]) * L.p2;
+      for (int bq = 0; bq < qj; ++bq, ++idx) {
+        const double w = fma(-L.p2, gx[qj * kQMax + bq], ca);
+        w2[idx * ST] = w * w;
+        W[idx * ST] = fa * gw[qj * kQMax + bq];
+      }
+    }
   } else if (L.type == kListSingle) {
-    for (int k = 0; k < m; ++k) node_single(L, k, gx, gw, w2[k * ST], W[k * ST]);
+    const int q = L.q1;
+    for (int k = 0; k < q; ++k) {
+      const double w = fma(L.p1, gx[q * kQMax + k], L.p0);
+      w2[k * ST] = w * w;
+      W[k * ST] = L.p1 * gw[q * kQMax + k];
+    }
   } else {
     w2[0] = L.p0 * L.p0;
     W[0] = 1.0;
@@ -672,7 +651,7 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? 4 : 2)
     sgw[t] = (&c_gw[0][0])[t];
   }
   __syncthreads();
-  double* w2s = ow2 + threadIdx.x;
+  double* w2s = ow2 + threadIdx.x;  // middle list (and, first, the inner one): OUT2 = M slots
   double* W2s = oW + threadIdx.x;
   double* w3s = ow2 + OUT2 * kFarThreads + threadIdx.x;
   double* W3s = oW + OUT2 * kFarThreads + threadIdx.x;
@@ -680,19 +659,31 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? 4 : 2)
   const uint32_t end = offsets[M < kFarListMax ? far_key_first(M + 1) : kNumKeys];
   double flops = 0.0, evals = 0.0;
   const uint32_t stride = gridDim.x * blockDim.x;
+  // Software pipeline over a thread's pairs: the queue entry and plan two runs
+  // ahead are loading, and the panel records of the next run are prefetched
+  // into L1, while this pair is evaluated.
   uint32_t base = begin + (blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
   uint32_t nidx = base + (threadIdx.x & 31u);
   uint64_t ne = nidx < end ? queue[nidx] : 0;
   uint32_t ncode = nidx < end ? plans[nidx] : 0;
+  uint32_t nnidx = nidx + stride;
+  uint64_t nne = nnidx < end ? queue[nnidx] : 0;
+  uint32_t nncode = nnidx < end ? plans[nnidx] : 0;
   for (; base < end; base += stride) {
-    // the next run's queue entry and plan are in flight while this pair runs
     const uint32_t idx = nidx;
     const uint64_t e = ne;
     const uint32_t code = ncode;
-    nidx += stride;
+    nidx = nnidx;
+    ne = nne;
+    ncode = nncode;
+    nnidx += stride;
+    if (nnidx < end) {
+      nne = queue[nnidx];
+      nncode = plans[nnidx];
+    }
     if (nidx < end) {
-      ne = queue[nidx];
-      ncode = plans[nidx];
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_i(ne)));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_j(ne)));
     }
     if (idx >= end) continue;
     const uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e) - 16u;
@@ -703,13 +694,19 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? 4 : 2)
     const bool mid_second = (code >> 30) & 1u;
     double w1[M], W1[M];
     {
+      // the inner list goes through the middle list's slots into registers
       FarList L;
       far_list(code, s0, A, B, L);
-      build_inner<M>(L, sgx, sgw, w1, W1);
+      emit_list<kFarThreads>(L, sgx, sgw, w2s, W2s);
+#pragma unroll
+      for (int a = 0; a < M; ++a) {
+        w1[a] = w2s[a * kFarThreads];
+        W1[a] = W2s[a * kFarThreads];
+      }
       far_list(code, mid_second ? r1 : r0, A, B, L);
-      build_outer<kFarThreads>(L, m2, sgx, sgw, w2s, W2s);
+      emit_list<kFarThreads>(L, sgx, sgw, w2s, W2s);
       far_list(code, mid_second ? r0 : r1, A, B, L);
-      build_outer<kFarThreads>(L, m3, sgx, sgw, w3s, W3s);
+      emit_list<kFarThreads>(L, sgx, sgw, w3s, W3s);
     }
     double acc = 0.0;
     for (int c = 0; c < m3; ++c) {
