@@ -78,6 +78,10 @@ int main(int argc, char** argv) {
   run_gen(k_syrk_gen<a, b, c, d, e, f>, a, b, 32 * c * d, GenShape<a, b, c, d, e>::SMEM, "gen " #a "x" #b " w" #c "x" #d " st" #e " min" #f)
   GEN(64, 64, 2, 2, 2, 4);
   GEN(64, 64, 2, 2, 3, 3);
+  GEN(128, 128, 4, 2, 2, 1);
+  GEN(128, 128, 2, 4, 2, 1);
+  GEN(96, 96, 3, 2, 2, 2);
+  GEN(64, 64, 2, 2, 4, 3);
   cublasHandle_t h;
   cublasCreate(&h);
   double alpha = -1.0, beta = 1.0;
