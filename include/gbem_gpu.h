@@ -164,6 +164,22 @@ int gbem_spd_factor_dev(gbem_ctx* ctx, const double* M, int64_t m, int64_t ldm, 
 int gbem_spd_solve_factored_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
                                 gbem_solve_stats* stats);
 
+/* run_selftest (selftest.hpp:184-245, the CLI's `kernels selftest`): the
+ * randomised audit of the pair evaluators against the brute-force oracle
+ * (oracle.hpp:44-205), ten geometric classes x `pairs` seeded pairs, all on the
+ * GPU (production single-layer evaluators, the double-layer kernel, and the
+ * recursive oracle with Aitken extrapolation for touching classes).  Fills
+ * cases[0..9]; *ncases = 10. */
+typedef struct {
+  char name[32];
+  int32_t pairs;
+  double worst_rel;
+  double tol;
+  int32_t pass;
+} gbem_selftest_case;
+int gbem_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gbem_quad_config* cfg,
+                  gbem_selftest_case* cases, int32_t* ncases);
+
 /* assemble_multi (assembly.hpp:110-175, replaces gbem::assemble_multi): the
  * Galerkin block system over all dielectric regions (double-layer
  * q_pair_integral kernels.hpp:295-315 and single-layer u_pair_integral with the

@@ -27,6 +27,11 @@ class GbemQuadConfig(C.Structure):
                 ("near_ratio", C.c_double), ("far_tol", C.c_double)]
 
 
+class GbemSelftestCase(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("pairs", C.c_int32), ("worst_rel", C.c_double), ("tol", C.c_double),
+                ("pass_", C.c_int32)]
+
+
 class GbemAssemblyStats(C.Structure):
     _fields_ = [("pairs_total", C.c_int64), ("pairs_coplanar", C.c_int64),
                 ("pairs_parallel", C.c_int64), ("pairs_orthogonal", C.c_int64),
@@ -87,6 +92,8 @@ GPU_SYMBOLS = [
                                       C.c_int32, C.c_int32, C.POINTER(GbemQuadConfig), _P, C.c_int64, _P,
                                       C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     ("gbem_lu_solve", C.c_int, [_P, _P, _P, _P, C.POINTER(GbemSolveStats)]),
+    ("gbem_selftest", C.c_int, [_P, C.c_int32, C.c_uint64, C.POINTER(GbemQuadConfig), C.POINTER(GbemSelftestCase),
+                                C.POINTER(C.c_int32)]),
     ("gbem_matrix_upload_general", C.c_int, [_P, _P, C.c_int64, C.c_int64]),
     ("gbem_matrix_download", C.c_int, [_P, _P, C.c_int64]),
     ("gbem_matrix_upload", C.c_int, [_P, _P, C.c_int64, C.c_int64]),
@@ -310,6 +317,14 @@ class Context:
         st = GbemSolveStats()
         self.check(self.lib.gbem_lu_solve(self.h, None, ptr(x), ptr(res), C.byref(st)))
         return A, b, bool(conv.value), x, float(res[0])
+
+    def selftest(self, pairs: int = 500, seed: int = 20260817):
+        """run_selftest (selftest.hpp:184-245) on the GPU: [{name, pairs, worst_rel, tol, pass}] x 10."""
+        cases = (GbemSelftestCase * 10)()
+        nc = C.c_int32(0)
+        self.check(self.lib.gbem_selftest(self.h, int(pairs), int(seed), C.byref(self.quad()), cases, C.byref(nc)))
+        return [dict(name=c.name.decode(), pairs=c.pairs, worst_rel=c.worst_rel, tol=c.tol, passed=bool(c.pass_))
+                for c in cases[:nc.value]]
 
     def spd_solve(self, B: np.ndarray):
         """B: (n,) or (n, k) right-hand sides; returns X like B, residuals (k,), stats."""

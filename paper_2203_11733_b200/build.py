@@ -32,7 +32,7 @@ NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{
 EXTRA = {"gbem_assembly.cu": ["-fmad=false"]}
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", f"-I{INCLUDE}"]
 
-CU_SOURCES = ["gbem_assembly.cu", "gbem_solver.cu", "gbem_block.cu", "gbem_capi.cu"]
+CU_SOURCES = ["gbem_assembly.cu", "gbem_solver.cu", "gbem_block.cu", "gbem_selftest.cu", "gbem_capi.cu"]
 
 
 def _run(cmd: list[str]) -> None:

@@ -413,6 +413,13 @@ int gbem_assemble_multi(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n, co
   return GBEM_OK;
 }
 
+int gbem_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gbem_quad_config* cfg,
+                  gbem_selftest_case* cases, int32_t* ncases) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  return gbem_internal_selftest(ctx, pairs, seed, cfg, cases, ncases);
+}
+
 int gbem_matrix_upload_general(gbem_ctx* ctx, const double* A_host, int64_t n, int64_t lda) {
   if (!ctx || (!A_host && n > 0)) return GBEM_EINVAL;
   if (n < 0 || lda < n) return ctx->fail(GBEM_EINVAL, "bad matrix dimensions");

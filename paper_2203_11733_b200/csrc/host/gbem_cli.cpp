@@ -7,6 +7,7 @@
 //                [--mode per-net|shared] [--uniform H | --graded H0,R,HMAX] [--device D]
 //                [--baseline collocation]
 //   gbem validate --input F
+//   gbem kernels selftest [--pairs N] [--seed S] [--device D]   (cli.hpp:48-75, on the GPU)
 //   gbem config --id N [--seed S] [--scale X]      (prints the config scene + panel count)
 #include <cstdio>
 #include <cstdlib>
@@ -15,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "../../../include/gbem_gpu.h"
 #include "../../../include/gbem_host.h"
 #include "gbem_host.hpp"
 
@@ -24,6 +26,7 @@ int usage(const char* msg) {
   std::cerr << "input error: " << msg << "\n"
             << "usage: gbem extract --input F [--net N|--all] [--format csv|json] [--output P]\n"
             << "       gbem validate --input F\n"
+            << "       gbem kernels selftest [--pairs N] [--seed S] [--device D]\n"
             << "       gbem config --id N [--seed S] [--scale X]\n";
   return 1;
 }
@@ -66,6 +69,46 @@ int main(int argc, char** argv) {
       std::cerr << "input error: " << e.what() << "\n";
       return 1;
     }
+  }
+  if (cmd == "kernels") {
+    // run_selftest (selftest.hpp:184-245) on the GPU; exit 2 when a class fails (cli.hpp:70-75)
+    if (a.empty() || a[0] != "selftest") return usage("expected: kernels selftest");
+    double pairs = 500, seed = 20260817, dev = 0;
+    std::string v;
+    for (size_t i = 1; i < a.size(); ++i) {
+      if (a[i] == "--pairs" && value(i, v) && num(v, pairs) && pairs >= 1) continue;
+      if (a[i] == "--seed" && value(i, v) && num(v, seed)) continue;
+      if (a[i] == "--device" && value(i, v) && num(v, dev)) continue;
+      return usage(("bad option " + a[i]).c_str());
+    }
+    gbem_ctx* ctx = nullptr;
+    if (gbem_ctx_create((int)dev, &ctx) != GBEM_OK) {
+      std::cerr << "runtime error: " << gbem_last_error(ctx) << "\n";
+      gbem_ctx_destroy(ctx);
+      return 3;
+    }
+    gbem_selftest_case cases[10];
+    int32_t nc = 0;
+    int rc = gbem_selftest(ctx, (int32_t)pairs, (uint64_t)seed, nullptr, cases, &nc);
+    if (rc) {
+      std::cerr << (rc == GBEM_EINVAL ? "input error: " : "runtime error: ") << gbem_last_error(ctx) << "\n";
+      gbem_ctx_destroy(ctx);
+      return rc;
+    }
+    gbem_ctx_destroy(ctx);
+    bool pass = true;
+    for (int c = 0; c < nc; ++c) {
+      char buf[160];
+      std::snprintf(buf, sizeof(buf), "%-24s pairs=%-5d worst_rel=%.3e tol=%.0e  %s", cases[c].name, cases[c].pairs,
+                    cases[c].worst_rel, cases[c].tol, cases[c].pass ? "PASS" : "FAIL");
+      std::cout << buf << "\n";
+      pass = pass && cases[c].pass;
+    }
+    if (!pass) {
+      std::cerr << "selftest failed: kernel/oracle disagreement above threshold\n";
+      return 2;
+    }
+    return 0;
   }
   if (cmd == "config") {
     double id = 2, seed = 1, scale = 1;

@@ -169,3 +169,23 @@ def test_collocation_single_region_agrees_with_galerkin(ctx):
     m.extract(net=-1, baseline="collocation")
     Cc = m.last_cap
     assert np.abs(Cc - Cg).max() <= 0.1 * np.abs(Cg).max()
+
+
+def test_kernel_selftest_on_device(ctx):
+    """run_selftest (selftest.hpp:184-245) on the GPU: the ten geometric classes
+    against the recursive brute-force oracle, at the reference's tolerances."""
+    cases = ctx.selftest(pairs=200)
+    assert [c["name"] for c in cases][:3] == ["U coplanar disjoint", "U coplanar adjacent", "U coplanar identical"]
+    assert len(cases) == 10
+    for c in cases:
+        assert c["passed"], c
+        assert c["pairs"] == 200
+
+
+def test_kernel_selftest_cli():
+    import subprocess
+    cli = ROOT / "paper_2203_11733_b200" / "lib" / "gbem"
+    r = subprocess.run([str(cli), "kernels", "selftest", "--pairs", "64"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    lines = r.stdout.strip().splitlines()
+    assert len(lines) == 10 and all(l.endswith("PASS") for l in lines), r.stdout
