@@ -175,6 +175,14 @@ __global__ void k_panel_cinfo(const DPanel* __restrict__ P, int n, CPanel* __res
 
 // far-field order along a direction from r2 = gap^2 / h^2: the smallest q with
 // r2 >= c_cd2f[q] (thresholds decrease with q), i.e. 1 + #{k < kQMax : r2 < c_cd2f[k]}
+// The same count for r2 = num / den without the division: r2 < t  <=>  num < t den (den > 0).
+__device__ __forceinline__ int far_order_ratio(float num, float den) {
+  const bool c4 = num < c_cd2f[4] * den;
+  const bool c2 = num < (c4 ? c_cd2f[6] : c_cd2f[2]) * den;
+  const bool c1 = num < (c4 ? (c2 ? c_cd2f[7] : c_cd2f[5]) : (c2 ? c_cd2f[3] : c_cd2f[1])) * den;
+  return 1 + (c4 ? 4 : 0) + (c2 ? 2 : 0) + (c1 ? 1 : 0);
+}
+
 __device__ __forceinline__ int far_order_r2(float r2) {
   // q = 1 + #{k : r2 < c_cd2f[k]}; the thresholds decrease with k, so the count
   // is found by a three-level binary search
@@ -225,7 +233,7 @@ __device__ __forceinline__ uint32_t shared_axis_desc(const CPanel& A, const CPan
   int qp = 0;
   if (Li != Lj) {
     const float dp = (float)fabs(Li - Lj);
-    qp = far_order_r2(g2 * (4.0f * __frcp_rn(dp * dp)));
+    qp = far_order_ratio(4.0f * g2, dp * dp);  // half-length |L_I - L_J| / 2
   }
   if (2 * qr + qp < qi * qj) {
     m = 2 * qr + qp;
