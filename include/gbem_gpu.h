@@ -176,6 +176,11 @@ typedef struct {
   double worst_rel;
   double tol;
   int32_t pass;
+  /* the worst pair: test and source panels (axis, level, a0, a1, b0, b1), the
+   * source normal sign, the evaluator's and the oracle's values */
+  double worst_test[6], worst_source[6];
+  int32_t worst_nsign;
+  double worst_value, worst_oracle;
 } gbem_selftest_case;
 int gbem_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gbem_quad_config* cfg,
                   gbem_selftest_case* cases, int32_t* ncases);

@@ -157,6 +157,13 @@ double ref_oracle_pair_integral(const orc_rect* a, const orc_rect* b, int depth)
                                     depth);
 }
 
+// gbem::oracle_pair_integral(DoubleLayer) (oracle.hpp:191, the Q branch).
+double ref_q_oracle_pair_integral(const orc_rect* a, const orc_rect* b, int nsign, int depth) {
+  gbem::Rect B = toRect(*b);
+  B.normalSign = nsign;
+  return gbem::oracle_pair_integral(gbem::KernelKind::DoubleLayer, toRect(*a), B, depth);
+}
+
 // gbem::rectDistance (geometry.hpp:79).
 double ref_rect_distance(const orc_rect* a, const orc_rect* b) {
   return gbem::rectDistance(toRect(*a), toRect(*b));

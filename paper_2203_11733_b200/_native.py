@@ -29,7 +29,8 @@ class GbemQuadConfig(C.Structure):
 
 class GbemSelftestCase(C.Structure):
     _fields_ = [("name", C.c_char * 32), ("pairs", C.c_int32), ("worst_rel", C.c_double), ("tol", C.c_double),
-                ("pass_", C.c_int32)]
+                ("pass_", C.c_int32), ("worst_test", C.c_double * 6), ("worst_source", C.c_double * 6),
+                ("worst_nsign", C.c_int32), ("worst_value", C.c_double), ("worst_oracle", C.c_double)]
 
 
 class GbemAssemblyStats(C.Structure):
@@ -323,7 +324,9 @@ class Context:
         cases = (GbemSelftestCase * 10)()
         nc = C.c_int32(0)
         self.check(self.lib.gbem_selftest(self.h, int(pairs), int(seed), C.byref(self.quad()), cases, C.byref(nc)))
-        return [dict(name=c.name.decode(), pairs=c.pairs, worst_rel=c.worst_rel, tol=c.tol, passed=bool(c.pass_))
+        return [dict(name=c.name.decode(), pairs=c.pairs, worst_rel=c.worst_rel, tol=c.tol, passed=bool(c.pass_),
+                     worst_test=list(c.worst_test), worst_source=list(c.worst_source), worst_nsign=c.worst_nsign,
+                     worst_value=c.worst_value, worst_oracle=c.worst_oracle)
                 for c in cases[:nc.value]]
 
     def spd_solve(self, B: np.ndarray):

@@ -358,17 +358,20 @@ __device__ double aitken(double v0, double v1, double v2) {
 // worst error of the class: mode 0 relErr vs o2 (disjoint), 1 relErr vs
 // Aitken(o0, o1, o2) (touching), 2 |semi| + |o2| (vanishing coplanar Q)
 __global__ void k_st_worst(const double* semi, const double* o0, const double* o1, const double* o2, int npairs,
-                           int mode, unsigned long long* worst) {
+                           int mode, unsigned long long* worst, double* err, double* ref_out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   double e = 0.0;
   if (t < npairs) {
+    double ref = o2[t];
     if (mode == 2) {
       e = fabs(semi[t]) + fabs(o2[t]);
     } else {
-      const double ref = mode == 1 ? aitken(o0[t], o1[t], o2[t]) : o2[t];
+      ref = mode == 1 ? aitken(o0[t], o1[t], o2[t]) : o2[t];
       e = fabs(semi[t] - ref) / fmax(fabs(ref), 1e-9);  // relErr (selftest.hpp:57-59)
     }
     if (!(e == e)) e = 1e300;  // NaN fails the class
+    err[t] = e;
+    ref_out[t] = ref;
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) e = fmax(e, __shfl_xor_sync(0xffffffffu, e, off));
@@ -415,7 +418,7 @@ int gbem_internal_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gb
   unsigned long long* d_worst = nullptr;
   int32_t* d_conv = nullptr;
   GBEM_CUDA(ctx, cudaMalloc(&d_ns, sizeof(int) * pairs));
-  GBEM_CUDA(ctx, cudaMalloc(&d_buf, sizeof(double) * 4 * (size_t)pairs));
+  GBEM_CUDA(ctx, cudaMalloc(&d_buf, sizeof(double) * 6 * (size_t)pairs));
   GBEM_CUDA(ctx, cudaMalloc(&d_conv, sizeof(int32_t) * pairs));
   GBEM_CUDA(ctx, cudaMalloc(&d_worst, sizeof(unsigned long long) * 10));
   GBEM_CUDA(ctx, cudaMemsetAsync(d_worst, 0, sizeof(unsigned long long) * 10, ctx->stream));
@@ -446,8 +449,43 @@ int gbem_internal_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gb
                                                             cd.mode == 2 ? 3 : 6, o[2]);
       GBEM_LAUNCH_CHECK(ctx);
     }
-    k_st_worst<<<gb, 128, 0, ctx->stream>>>(semi, o[0], o[1], o[2], pairs, cd.mode, d_worst + c);
+    double* d_err = d_buf + 4 * (size_t)pairs;
+    double* d_ref = d_buf + 5 * (size_t)pairs;
+    k_st_worst<<<gb, 128, 0, ctx->stream>>>(semi, o[0], o[1], o[2], pairs, cd.mode, d_worst + c, d_err, d_ref);
     GBEM_LAUNCH_CHECK(ctx);
+    // the worst pair of the class, for the report
+    std::vector<double> herr((size_t)pairs);
+    cudaError_t ce = cudaMemcpyAsync(herr.data(), d_err, sizeof(double) * pairs, cudaMemcpyDeviceToHost, ctx->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->stream);
+    if (ce != cudaSuccess) {
+      rc = ctx->fail(GBEM_ECUDA, std::string("selftest: ") + cudaGetErrorString(ce));
+      break;
+    }
+    int64_t arg = 0;
+    for (int64_t k = 1; k < pairs; ++k)
+      if (herr[(size_t)k] > herr[(size_t)arg]) arg = k;
+    DPanel pt, ps;
+    int ns = 0;
+    double sv = 0, rv = 0;
+    cudaMemcpy(&pt, ctx->d_panels + arg, sizeof(DPanel), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&ps, ctx->d_panels + pairs + arg, sizeof(DPanel), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&ns, d_ns + arg, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&sv, semi + arg, sizeof(double), cudaMemcpyDeviceToHost);
+    cudaMemcpy(&rv, d_ref + arg, sizeof(double), cudaMemcpyDeviceToHost);
+    gbem_selftest_case& w = cases[c];
+    const DPanel* pp[2] = {&pt, &ps};
+    double* dst[2] = {w.worst_test, w.worst_source};
+    for (int q = 0; q < 2; ++q) {
+      dst[q][0] = pp[q]->axis;
+      dst[q][1] = pp[q]->level;
+      dst[q][2] = pp[q]->a0;
+      dst[q][3] = pp[q]->a1;
+      dst[q][4] = pp[q]->b0;
+      dst[q][5] = pp[q]->b1;
+    }
+    w.worst_nsign = ns;
+    w.worst_value = sv;
+    w.worst_oracle = rv;
   }
   unsigned long long hw[10] = {};
   if (rc == GBEM_OK) {
@@ -462,7 +500,7 @@ int gbem_internal_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gb
   if (rc) return rc;
   for (int c = 0; c < 10; ++c) {
     gbem_selftest_case& out = cases[c];
-    std::memset(&out, 0, sizeof(out));
+    std::memset(out.name, 0, sizeof(out.name));
     std::strncpy(out.name, kCases[c].name, sizeof(out.name) - 1);
     out.pairs = pairs;
     double wv;

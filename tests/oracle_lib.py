@@ -214,6 +214,16 @@ def q_pairs(lib_name: str, A: np.ndarray, B: np.ndarray, nsign, rel_tol=1e-8, ma
     return out, conv, st
 
 
+def q_oracle(A: np.ndarray, B: np.ndarray, nsign, depth: int):
+    """The reference's brute-force double-layer oracle (oracle.hpp:191, compiled in place)."""
+    lib = ref()
+    f = lib.ref_q_oracle_pair_integral
+    f.restype = C.c_double
+    f.argtypes = [RP, RP, C.c_int, C.c_int]
+    ra, rb = rects_from_matrix(A), rects_from_matrix(B)
+    return np.array([f(C.byref(ra[k]), C.byref(rb[k]), int(nsign[k]), depth) for k in range(len(A))])
+
+
 def assemble_multi(P: np.ndarray, nsign, kind, net, reg_a, reg_b, regions, main_net: int, rel_tol=1e-8,
                    max_levels=16):
     """orc_assemble_multi (assembly.hpp:110-175): (A (m, m), b (m,), status, all_converged)."""
