@@ -66,75 +66,68 @@ constexpr int kPotrfWarps = kPotrfThreads / 32;
 constexpr int kPanel = 32;
 constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + NB + 3 * kPanel * (kPanel + 1)) * sizeof(double);
 
-// Off-diagonal 32 x 32 blocks of X = inv(L) for a factored block in shared
-// memory (L in the lower half of a, the diagonal blocks' inverses X_pp in the
-// strict upper half (transposed) and xd): X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp,
-// strided 4 x 4 register tiles, T_p = sum_q L_rq X_qp staged in tmp[p][32][33].
-__device__ __forceinline__ void potrf_inverse_offdiag(double* a, const double* xd, double* tmp, int npan, int tid) {
-  constexpr int LD = NB + 1;
-  // off-diagonal blocks of X = inv(L): X_rp = -X_rr * sum_{q=p}^{r-1} L_rq X_qp,
-  // same strided 4 x 4 tiles; T_p = sum_q L_rq X_qp staged in tmp[p][32][33].
-  {
-    const int grp = tid >> 6, tx = tid & 7, ty = (tid >> 3) & 7;
-    constexpr int TLD = kPanel + 1;
-    for (int rbk = 1; rbk < npan; ++rbk) {
-      const int R0 = rbk * kPanel;
-      if (grp < rbk) {
-        const int pb = grp;
-        double acc[4][4] = {};
+// Off-diagonal 32 x 32 blocks of X = inv(L) of the diagonal block, one block row
+// r = rbk at a time: X_rp = -X_rr * T_p with T_p = sum_{q=p}^{r-1} L_rq X_qp, for
+// p < r, on strided 4 x 4 register tiles of one 64-thread group per p.  X(r,c),
+// r > c, lives in the strict upper half a[r*LD + c], its diagonal in xd; T_p is
+// staged in tmp[p][32][33].  Part 1 (T_p) only needs block rows < r of X and the
+// finished L_rq, so it runs while warp 0 factors panel r; part 2 runs beside the
+// panel-row step of panel r (disjoint rows of the same columns).
+__device__ __forceinline__ void potrf_inv_part1(const double* a, const double* xd, double* tmp, int rbk, int pb,
+                                                int tx, int ty) {
+  constexpr int LD = NB + 1, TLD = kPanel + 1;
+  const int R0 = rbk * kPanel;
+  double acc[4][4] = {};
 #pragma unroll 4
-        for (int m = pb * kPanel; m < R0; ++m) {
-          double lr[4], xc[4];
+  for (int m = pb * kPanel; m < R0; ++m) {
+    double lr[4], xc[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) lr[u] = a[m * LD + R0 + ty + 8 * u];  // L(R0+i, m)
-          const double dg = xd[m];
+    for (int u = 0; u < 4; ++u) lr[u] = a[m * LD + R0 + ty + 8 * u];  // L(R0+i, m)
+    const double dg = xd[m];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const int c = pb * kPanel + tx + 8 * v;
-            const double up = a[m * LD + c];
-            xc[v] = m > c ? up : 0.0;
-            xc[v] = m == c ? dg : xc[v];  // X(m, c)
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = fma(lr[u], xc[v], acc[u][v]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) tmp[pb * kPanel * TLD + (ty + 8 * u) * TLD + tx + 8 * v] = acc[u][v];
-      }
-      __syncthreads();
-      if (grp < rbk) {
-        const int pb = grp;
-        double acc[4][4] = {};
-#pragma unroll 4
-        for (int m = 0; m < kPanel; ++m) {
-          double xr[4], tv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int i = ty + 8 * u;
-            const double up = a[(R0 + i) * LD + R0 + m], dg = xd[R0 + i];
-            xr[u] = m < i ? up : 0.0;
-            xr[u] = m == i ? dg : xr[u];  // X(R0+i, R0+m)
-          }
-#pragma unroll
-          for (int v = 0; v < 4; ++v) tv[v] = tmp[pb * kPanel * TLD + m * TLD + tx + 8 * v];
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int v = 0; v < 4; ++v) acc[u][v] = fma(xr[u], tv[v], acc[u][v]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v)
-            a[(R0 + ty + 8 * u) * LD + pb * kPanel + tx + 8 * v] = -acc[u][v];  // X(R0+i, col)
-      }
-      __syncthreads();
+    for (int v = 0; v < 4; ++v) {
+      const int c = pb * kPanel + tx + 8 * v;
+      const double up = a[m * LD + c];
+      xc[v] = m > c ? up : 0.0;
+      xc[v] = m == c ? dg : xc[v];  // X(m, c)
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = fma(lr[u], xc[v], acc[u][v]);
   }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) tmp[pb * kPanel * TLD + (ty + 8 * u) * TLD + tx + 8 * v] = acc[u][v];
+}
+
+__device__ __forceinline__ void potrf_inv_part2(double* a, const double* xd, const double* tmp, int rbk, int pb,
+                                                int tx, int ty) {
+  constexpr int LD = NB + 1, TLD = kPanel + 1;
+  const int R0 = rbk * kPanel;
+  double acc[4][4] = {};
+#pragma unroll 4
+  for (int m = 0; m < kPanel; ++m) {
+    double xr[4], tv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = ty + 8 * u;
+      const double up = a[(R0 + i) * LD + R0 + m], dg = xd[R0 + i];
+      xr[u] = m < i ? up : 0.0;
+      xr[u] = m == i ? dg : xr[u];  // X(R0+i, R0+m)
+    }
+#pragma unroll
+    for (int v = 0; v < 4; ++v) tv[v] = tmp[pb * kPanel * TLD + m * TLD + tx + 8 * v];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = fma(xr[u], tv[v], acc[u][v]);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) a[(R0 + ty + 8 * u) * LD + pb * kPanel + tx + 8 * v] = -acc[u][v];  // X(R0+i, col)
 }
 
 __global__ void __launch_bounds__(kPotrfThreads)
@@ -213,11 +206,22 @@ __global__ void __launch_bounds__(kPotrfThreads)
 #pragma unroll
       for (int i = 0; i < kPanel; ++i)
         if (i > lane) a[(c0 + i) * LD + c0 + lane] = x[i];  // X(i, lane) in the strict upper half
+    } else {
+      // odd groups 1, 3, 5 (warps off warp 0's sub-partition): T_q of block row p
+      // of inv(L) (needs block rows < p only)
+      const int grp = tid >> 6, pb = (grp - 1) >> 1;
+      if ((grp & 1) && pb < p) potrf_inv_part1(a, xd, tmp, p, pb, tid & 7, (tid >> 3) & 7);
     }
     __syncthreads();
     POTRF_TICK(1 + 3 * p);
     const int r0 = c0 + kPanel, mrest = NB - r0;  // padded rows below the panel
-    if (mrest <= 0) break;
+    if (mrest <= 0) {
+      // last panel: block row p of inv(L) on groups 0..p-1
+      const int pb = tid >> 6;
+      if (pb < p) potrf_inv_part2(a, xd, tmp, p, pb, tid & 7, (tid >> 3) & 7);
+      __syncthreads();
+      break;
+    }
     // Register tiles below are 4 x 4 with stride 8 inside 32 x 32 super-tiles of
     // 64 threads (tx, ty in 0..7: rows ty + 8u, columns tx + 8v), so that the
     // shared loads of a warp hit consecutive addresses or broadcast.
@@ -227,6 +231,9 @@ __global__ void __launch_bounds__(kPotrfThreads)
       const int G = mrest / kPanel;
       double acc[4][4] = {};
       const int rowb = r0 + kPanel * grp + ty;
+      // groups 4..4+p-1: block row p of inv(L) (rows < c0 of panel p's columns;
+      // the panel rows below write rows >= r0 of the same columns)
+      if (grp >= 4 && grp - 4 < p) potrf_inv_part2(a, xd, tmp, p, grp - 4, tx, ty);
       if (grp < G) {
 #pragma unroll 4
         for (int k = 0; k < kPanel; ++k) {  // X(j, k) = 0 for k > j: fixed trip count, no branches
@@ -290,16 +297,13 @@ __global__ void __launch_bounds__(kPotrfThreads)
     POTRF_TICK(3 + 3 * p);
   }
   POTRF_TICK(20);
-  potrf_inverse_offdiag(a, xd, tmp, npan, tid);
   POTRF_TICK(21);
+  // one pass: L (lower) back to A, X = inv(L) to Linv
   for (int idx = tid; idx < NB * NB; idx += kPotrfThreads) {
     const int c = idx / NB, r = idx % NB;  // constant divisor: shifts, not a division
-    if (r >= c && r < kb && c < kb) A[(long long)c * lda + r] = a[c * LD + r];
-  }
-  for (int idx = tid; idx < NB * NB; idx += kPotrfThreads) {
-    int c = idx / NB, r = idx % NB;
     double v = 0.0;
     if (r < kb && c < kb) {
+      if (r >= c) A[(long long)c * lda + r] = a[c * LD + r];
       if (r > c) v = a[r * LD + c];
       else if (r == c) v = xd[r];
     }
