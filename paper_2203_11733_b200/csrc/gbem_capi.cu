@@ -186,6 +186,7 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   cudaFree(ctx->d_info);
   cudaFree(ctx->d_plan);
   cudaFree(ctx->d_flags);
+  cudaFree(ctx->d_band_done);
   cudaFree(ctx->d_kp);
   cudaFree(ctx->d_rhs);
   cudaFree(ctx->d_linv);

@@ -67,6 +67,7 @@ struct gbem_ctx {
   size_t linv_cap = 0;
   int* d_flags = nullptr;  // per-block ready flags of the dataflow backward substitution
   int flow_epoch = 0;
+  unsigned* d_band_done = nullptr;  // finished look-ahead band tiles of the factor (counter)
   double* d_rhs = nullptr;  // B and X of the K-RHS extraction (2 * rhs_cap)
   size_t rhs_cap = 0;
 

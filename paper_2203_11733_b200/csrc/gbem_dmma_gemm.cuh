@@ -238,21 +238,46 @@ __host__ __device__ inline long long gen_tiles_before(long long tm) {
 // with tn = y < band, tm = x (tiles above the diagonal exit) -- the look-ahead
 // block column; band == 0: the lower tiles with tile column >= split,
 // enumerated triangularly (row tm = split + x holds x + 1 of them).
+// band < 0: both in one 1-D grid -- the first nt * (-band) CTAs are the band
+// tiles of tile columns [0, -band) (nt = tile rows), dispatched first, then the
+// triangle from split = -band; each band CTA bumps *band_done when its tile is
+// stored (release), which is what the next diagonal factor waits for.
 template <int TBM, int TBN, int WMW, int WNW, int NSTG, int MINB>
 __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
-    k_syrk_gen(double* C, long long ldc, const double* A, long long lda, int M, int K, int split, int band) {
+    k_syrk_gen(double* C, long long ldc, const double* A, long long lda, int M, int K, int split, int band,
+               unsigned* band_done = nullptr) {
   static_assert(TBM == TBN, "square tiles");
   using S = GenShape<TBM, TBN, WMW, WNW, NSTG>;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + NSTG * BK * S::LDA;
   int tm, tn;
-  if (band > 0) {
+  bool signal = false;
+  long long t = blockIdx.x;
+  if (band < 0) {
+    const int nt = (M + TBM - 1) / TBM;
+    if (t < (long long)nt * -band) {
+      tm = (int)(t % nt);
+      tn = (int)(t / nt);
+      signal = true;
+      if (tn > tm) {
+        if (threadIdx.x == 0) atomicAdd(band_done, 1u);
+        return;
+      }
+    } else {
+      t -= (long long)nt * -band;
+      split = -band;
+      int x = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      while ((long long)(x + 1) * (x + 2) / 2 <= t) ++x;
+      while ((long long)x * (x + 1) / 2 > t) --x;
+      tm = split + x;
+      tn = split + (int)(t - (long long)x * (x + 1) / 2);
+    }
+  } else if (band > 0) {
     tm = blockIdx.x;
     tn = split + blockIdx.y;
     if (tn > tm) return;
   } else {
-    const long long t = blockIdx.x;
     int x = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
     while ((long long)(x + 1) * (x + 2) / 2 <= t) ++x;
     while ((long long)x * (x + 1) / 2 > t) --x;
@@ -347,6 +372,11 @@ __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
         const int col = cw0 + j * 8 + 2 * t4 + e;
         if (row < M && col <= row) C[(long long)col * ldc + row] = cur[j][e] - acc[i][j][e];
       }
+  }
+  if (signal) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(band_done, 1u);
   }
 }
 

@@ -40,6 +40,10 @@ constexpr int NB = 128;       // Cholesky block size (diagonal blocks, trailing-
 // SM (tools/gemm_bench.cu: 28.0 TFLOP/s at K = 128 vs 25.6 for 128 x 64 tiles)
 using UpdShape = GenShape<64, 64, 2, 2, 2>;
 #define kUpdate k_syrk_gen<64, 64, 2, 2, 2, 4>
+// shared memory of an update CTA padded so that only 3 fit on an SM (4 x 61 KB >
+// 228 KB) and a trsm or band CTA (<= 38 KB, <= 16K registers) fits beside them
+constexpr size_t kUpdSmemPadded = 60 * 1024;
+static_assert(UpdShape::SMEM <= kUpdSmemPadded, "padding");
 // Factor the kb x kb (kb <= NB = 128) diagonal block and invert its factor, in
 // shared memory, by 32-column panels:
 //   1. warp 0 factors the 32 x 32 diagonal sub-block in registers (lane i owns
@@ -131,7 +135,8 @@ __device__ __forceinline__ void potrf_inv_part2(double* a, const double* xd, con
 }
 
 __global__ void __launch_bounds__(kPotrfThreads)
-    k_potrf_diag(double* A, long long lda, int kb, int row0, double* Linv, int* info) {
+    k_potrf_diag(double* A, long long lda, int kb, int row0, double* Linv, int* info,
+                 const unsigned* wait_ctr = nullptr, unsigned wait_target = 0) {
   extern __shared__ __align__(16) double sm[];
   constexpr int LD = NB + 1;
   double* a = sm;              // [NB][LD] column-major: a[c*LD + r]
@@ -142,7 +147,21 @@ __global__ void __launch_bounds__(kPotrfThreads)
   // shuffles inside `if (warp == 0)` compile without divergence handling
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   POTRF_TICK(23);
-  // load the block: 8 independent global loads in flight per thread per batch
+  // launched ahead of its producer (the band tiles of a combined update,
+  // k_syrk_gen band < 0): wait until they have all stored
+  if (wait_ctr) {
+    if (tid == 0) {
+      unsigned v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_ctr) : "memory");
+        if (v >= wait_target) break;
+        __nanosleep(64);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  // load the block (L2 loads: the block may have been written during this kernel): 8 independent global loads in flight per thread per batch
   for (int idx0 = tid; idx0 < NB * NB; idx0 += 8 * kPotrfThreads) {
     double v[8];
 #pragma unroll
@@ -150,7 +169,7 @@ __global__ void __launch_bounds__(kPotrfThreads)
       const int idx = idx0 + u * kPotrfThreads, c = idx / NB, r = idx % NB;
       v[u] = 0.0;
       if (idx < NB * NB) {
-        if (r < kb && c < kb) v[u] = r >= c ? A[(long long)c * lda + r] : 0.0;
+        if (r < kb && c < kb) v[u] = r >= c ? __ldcg(A + (long long)c * lda + r) : 0.0;
         else if (r == c) v[u] = 1.0;  // pad the ragged last block with the identity
       }
     }
@@ -1057,7 +1076,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   }
   static bool attr_done = false;
   if (!attr_done) {
-    GBEM_CUDA(ctx, cudaFuncSetAttribute(kUpdate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)UpdShape::SMEM));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(kUpdate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmemPadded));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kPotrfSmem));
@@ -1104,6 +1123,8 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     // Events: P (potrf done), T (trsm done), B (band done), RA (rest_a done).
     cudaStream_t lo = ctx->g_main, hi = ctx->g_main_hi, p = ctx->g_side;
     cudaEvent_t evP = ctx->ev_panel, evB = ctx->ev_col, evT = ctx->ev_gt;
+    if (!ctx->d_band_done) GBEM_CUDA(ctx, cudaMalloc(&ctx->d_band_done, sizeof(unsigned)));
+    GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_band_done, 0, sizeof(unsigned), s));
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_gs, s));
     GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, ctx->ev_gs, 0));
     GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, ctx->ev_gs, 0));
@@ -1116,10 +1137,11 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       A21 = ctx->d_A + (long long)k0 * lda + k0 + kb;
       A22 = ctx->d_A + (long long)(k0 + kb) * lda + (k0 + kb);
     };
-    auto potrf = [&](int b, cudaStream_t st) {
+    auto potrf = [&](int b, cudaStream_t st, unsigned wait_target = 0) {
       const int k0 = b * NB, kb = std::min(NB, n - k0);
       k_potrf_diag<<<1, kPotrfThreads, kPotrfSmem, st>>>(ctx->d_A + (long long)k0 * lda + k0, lda, kb, k0,
-                                                         Linv + (size_t)b * NB * NB, ctx->d_info);
+                                                         Linv + (size_t)b * NB * NB, ctx->d_info,
+                                                         wait_target ? ctx->d_band_done : nullptr, wait_target);
     };
     auto trsm = [&](int b, cudaStream_t st) {
       int m, nt;
@@ -1159,8 +1181,10 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     //   p/hi: stepA(s+1) = potrf, trsm, U(b, b+1), potrf, trsm   (after band2(s))
     //   lo:   band2(s) -> rest2(s) -> [T(s+1)] band2(s+1) -> ...
     // U(., c) for one column never runs concurrently on two streams.
-    auto stepA = [&](int b0, int nb) -> int {
-      GBEM_CUDA(ctx, cudaStreamWaitEvent(p, evB, 0));
+    // wait_target > 0: the first diagonal factor waits on the band counter
+    // (combined band + rest update on lo) instead of an event after the band
+    auto stepA = [&](int b0, int nb, unsigned wait_target) -> int {
+      if (!wait_target) GBEM_CUDA(ctx, cudaStreamWaitEvent(p, evB, 0));
       for (int k = 0; k < nb; ++k) {
         const int bb = b0 + k;
         if (k > 0) {
@@ -1170,7 +1194,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
           GBEM_CUDA(ctx, cudaStreamWaitEvent(p, evB, 0));
         }
         if (prof) cudaEventRecord(pe[6 * bb], p);
-        potrf(bb, p);
+        potrf(bb, p, k == 0 ? wait_target : 0u);
         GBEM_LAUNCH_CHECK(ctx);
         if (prof) cudaEventRecord(pe[6 * bb + 1], p);
         GBEM_CUDA(ctx, cudaEventRecord(evP, p));
@@ -1185,6 +1209,8 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     // U([b0, b0 + nb), block columns >= b0 + nb + j0): band (j0 = 0, one super-
     // block of kBand2 tile columns) or triangular rest (j0 = 2)
     constexpr int kBand2 = 2 * kBand;
+    static const int occ_rows = getenv("GBEM_OCC_ROWS") ? atoi(getenv("GBEM_OCC_ROWS")) : 0;
+    static const bool combined = getenv("GBEM_NO_COMBINED") == nullptr;
     auto update2 = [&](int b0, int nb, bool band_part) {
       const int k0 = b0 * NB, kw = std::min(nb * NB, n - k0);
       const int m = n - k0 - kw + (int)ctx->border;
@@ -1197,13 +1223,19 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
                                                                                             0, std::min(kBand2, nt));
       } else if (nt > kBand2) {
         const long long tiles = (long long)(nt - kBand2) * (nt - kBand2 + 1) / 2;
-        kUpdate<<<(unsigned)tiles, UpdShape::THREADS, UpdShape::SMEM, lo>>>(A22, lda, A21, lda, m, kw, kBand2, 0);
+        // near the end the chain on p / hi is the critical path: the rest update
+        // then runs 3 CTAs per SM (padded shared memory), which keeps one slot
+        // per SM free for the chain's trsm / band kernels instead of queueing
+        // them behind a full wave of update tiles
+        const size_t sm = m < occ_rows ? kUpdSmemPadded : UpdShape::SMEM;
+        kUpdate<<<(unsigned)tiles, UpdShape::THREADS, sm, lo>>>(A22, lda, A21, lda, m, kw, kBand2, 0);
       }
     };
     GBEM_CUDA(ctx, cudaEventRecord(evB, p));  // stepA(0) waits on nothing
     int b = 0;
-    int rc2 = stepA(0, std::min(2, nblk));
+    int rc2 = stepA(0, std::min(2, nblk), 0u);
     if (rc2) return rc2;
+    unsigned band_target = 0;  // cumulative band CTAs of the combined updates
     for (;;) {
       const int nb = std::min(2, nblk - b), next = b + nb;
       GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, evT, 0));
@@ -1214,16 +1246,37 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
         b = nblk;
         break;
       }
-      update2(b, nb, true);  // band2(b): block columns next, next + 1
-      GBEM_LAUNCH_CHECK(ctx);
-      GBEM_CUDA(ctx, cudaEventRecord(evB, lo));
       const bool next_tail = n - next * NB < tail_rows;
-      if (!next_tail) {
-        rc2 = stepA(next, std::min(2, nblk - next));
-        if (rc2) return rc2;
+      if (combined) {
+        // band2(b) and rest2(b) in one launch, band tiles first; stepA(next)
+        // starts on the band counter, so the chain does not wait for the
+        // band launch's partial last wave and rest2 fills the machine at once
+        const int k0 = b * NB, kw = std::min(nb * NB, n - k0);
+        const int m = n - k0 - kw + (int)ctx->border, nt = (m + 63) / 64;
+        const int bw = std::min(kBand2, nt);
+        const long long tiles =
+            (long long)nt * bw + (nt > kBand2 ? (long long)(nt - kBand2) * (nt - kBand2 + 1) / 2 : 0);
+        double* A21 = ctx->d_A + (long long)k0 * lda + k0 + kw;
+        double* A22 = ctx->d_A + (long long)(k0 + kw) * lda + (k0 + kw);
+        kUpdate<<<(unsigned)tiles, UpdShape::THREADS, UpdShape::SMEM, lo>>>(A22, lda, A21, lda, m, kw, 0, -bw,
+                                                                             ctx->d_band_done);
+        GBEM_LAUNCH_CHECK(ctx);
+        band_target += (unsigned)(nt * bw);
+        if (!next_tail) {
+          rc2 = stepA(next, std::min(2, nblk - next), band_target);
+          if (rc2) return rc2;
+        }
+      } else {
+        update2(b, nb, true);  // band2(b): block columns next, next + 1
+        GBEM_LAUNCH_CHECK(ctx);
+        GBEM_CUDA(ctx, cudaEventRecord(evB, lo));
+        if (!next_tail) {
+          rc2 = stepA(next, std::min(2, nblk - next), 0u);
+          if (rc2) return rc2;
+        }
+        update2(b, nb, false);  // rest2(b)
+        GBEM_LAUNCH_CHECK(ctx);
       }
-      update2(b, nb, false);  // rest2(b)
-      GBEM_LAUNCH_CHECK(ctx);
       if (prof) cudaEventRecord(pe[6 * b + 4], lo);
       b = next;
       if (next_tail) break;
