@@ -779,9 +779,12 @@ __global__ void __launch_bounds__(kFlowThreads, 1)
 #pragma unroll
     for (int k = 0; k < 64; ++k) dinv[k] = li[k];
   }
-  double acc[RT];
+  double acc[RT], yb[RT];  // yb: Y_b(i), loaded off the dependency chain
 #pragma unroll
-  for (int q = 0; q < RT; ++q) acc[q] = 0.0;
+  for (int q = 0; q < RT; ++q) {
+    acc[q] = 0.0;
+    yb[q] = (h == 0 && i < kb && q < R) ? Y[(long long)q * n + k0 + i] : 0.0;
+  }
   auto issue_block = [&](int c) {  // L(c0 + r, k0 + i) -> Lb[r][i], zero outside the matrix
     const int c0 = c * NB, kc = min(NB, n - c0);
     for (int idx = tid; idx < NB * NB; idx += kFlowThreads) {
@@ -824,7 +827,7 @@ __global__ void __launch_bounds__(kFlowThreads, 1)
   if (h == 0)
 #pragma unroll
     for (int q = 0; q < RT; ++q)
-      ys[i * RT + q] = (i < kb && q < R) ? Y[(long long)q * n + k0 + i] - (acc[q] + red[i * RT + q]) : 0.0;
+      ys[i * RT + q] = (i < kb && q < R) ? yb[q] - (acc[q] + red[i * RT + q]) : 0.0;
   __syncthreads();
   // X_b(i) = sum_k inv(L_bb)(k, i) y_k (the inverse is zero above its diagonal)
   double o[RT];
