@@ -798,10 +798,13 @@ __global__ void __launch_bounds__(kFlowThreads, 1)
   for (int c = nblk - 1; c > b; --c) {
     const int c0 = c * NB, kc = min(NB, n - c0);
     if (tid == 0) {
+      // relaxed polls (an acquire load per poll also invalidates L1 each time),
+      // then one acquire fence; X_c is read through L2 below
       int f;
       do {
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(flags + c) : "memory");
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(flags + c) : "memory");
       } while (f != epoch);
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
     for (int idx = tid; idx < NB * RT; idx += kFlowThreads) {
