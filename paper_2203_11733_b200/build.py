@@ -27,6 +27,7 @@ NVCC = os.environ.get("NVCC", "nvcc")
 CXX = os.environ.get("GBEM_CXX", "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INCLUDE}"]
+NVFLAGS += os.environ.get("GBEM_NVCC_EXTRA", "").split()  # experiments only (e.g. -DGBEM_FAR_MINB=5)
 # Per-file extra flags: the assembly unit keeps the reference's operation order
 # in the near-field closed forms (explicit fma() is still used in the far field).
 EXTRA = {"gbem_assembly.cu": ["-fmad=false"]}

@@ -647,7 +647,10 @@ __device__ __forceinline__ void emit_list(const FarList& L, const double* gx, co
 // (64 for M > 14, whose slots would not fit 48 KB).
 __host__ __device__ constexpr int far_threads(int M) { return M <= 14 ? 128 : 64; }
 template <int M>
-__global__ void __launch_bounds__(far_threads(M), M <= 12 ? 4 : 2)
+#ifndef GBEM_FAR_MINB
+#define GBEM_FAR_MINB 4  // CTAs per SM for M <= 12 (sweep tools/far_minb_ab.sh: 2, 3, 5, 6 are 27-43% slower)
+#endif
+__global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
     k_far(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue, const uint32_t* __restrict__ plans,
           const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats) {
   constexpr int kFarThreads = far_threads(M);
