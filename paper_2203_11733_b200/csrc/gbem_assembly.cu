@@ -523,6 +523,17 @@ __device__ __forceinline__ double warp_reduce_d(double x) {
   return x;
 }
 
+// 1 / x: MUFU.RCP64H seed and two Newton steps (a few ulp; the far rule's own
+// error is 1e-12), instead of an IEEE division's longer dependent sequence.
+__device__ __forceinline__ double rcp64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // acc + W / sqrt(x): MUFU.RSQ64H seed y (relative error <= 9.1e-7) and one
 // Newton step folded into the weighted accumulation,
 //   W / sqrt(x) ~ W y (1 + e / 2),  e = 1 - x y^2,
@@ -648,7 +659,7 @@ __device__ __forceinline__ void emit_list(const FarList& L, const double* gx, co
 __host__ __device__ constexpr int far_threads(int M) { return M <= 14 ? 128 : 64; }
 template <int M>
 #ifndef GBEM_FAR_MINB
-#define GBEM_FAR_MINB 4  // CTAs per SM for M <= 12 (sweep tools/far_minb_ab.sh: 2, 3, 5, 6 are 27-43% slower)
+#define GBEM_FAR_MINB 4  // CTAs per SM for M <= 12 (sweep tools/far_minb_ab.sh: 2, 3, 5, 6 are 24-43% slower)
 #endif
 __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
     k_far(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue, const uint32_t* __restrict__ plans,
@@ -668,7 +679,7 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
   double* W3s = oW + OUT2 * kFarThreads + threadIdx.x;
   const uint32_t begin = offsets[far_key_first(M)];
   const uint32_t end = offsets[M < kFarListMax ? far_key_first(M + 1) : kNumKeys];
-  double flops = 0.0, evals = 0.0;
+  unsigned long long flops = 0, evals = 0;
   const uint32_t stride = gridDim.x * blockDim.x;
   // Software pipeline over a thread's pairs: the queue entry and plan two runs
   // ahead are loading, and the panel records of the next run are prefetched
@@ -734,18 +745,24 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
         acc = fma(W3 * W2s[b * kFarThreads], t0 + t1, acc);
       }
     }
-    const double U = acc / kFourPi;
-    const double nodes = (double)M * m2 * m3;
+    // counters in integer arithmetic (off the FP64 pipe)
+    const uint32_t nodes = (uint32_t)(M * m2 * m3);
     evals += nodes;
-    flops += 9.0 * nodes + 4.0 * m2 * m3 + 6.0 * (M + m2 + m3) + 30.0;  // per node: DADD, DMUL, 2 DFMA, DMUL, DFMA
-    store_value(o, i, j, A, B, U);
-    if (!o.A && o.conv) o.conv[i] = 1;
+    flops += 9u * nodes + 4u * (uint32_t)(m2 * m3) + 6u * (uint32_t)(M + m2 + m3) + 30u;  // per node: DADD, DMUL, 2 DFMA, DMUL, DFMA
+    if (o.A) {
+      // U / (4 pi area_I area_J) with one reciprocal
+      o.A[(long long)i * o.lda + j] = acc * rcp64(kFourPi * (panel_area(A) * panel_area(B)));
+    } else {
+      o.out[i] = acc * rcp64(kFourPi);
+      if (o.conv) o.conv[i] = 1;
+    }
   }
-  flops = warp_reduce_d(flops);
-  evals = warp_reduce_d(evals);
+  double fl = (double)flops, ev = (double)evals;
+  fl = warp_reduce_d(fl);
+  ev = warp_reduce_d(ev);
   if ((threadIdx.x & 31) == 0) {
-    atomicAdd(reinterpret_cast<double*>(&stats[ST_FAR_FLOPS]), flops);
-    atomicAdd(&stats[ST_FAR_EVALS], (unsigned long long)evals);
+    atomicAdd(reinterpret_cast<double*>(&stats[ST_FAR_FLOPS]), fl);
+    atomicAdd(&stats[ST_FAR_EVALS], (unsigned long long)ev);
   }
 }
 
