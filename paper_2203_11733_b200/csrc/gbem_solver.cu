@@ -62,35 +62,42 @@ static_assert(UpdShape::SMEM <= kUpdSmemPadded, "padding");
 __device__ long long g_potrf_clk[128];
 #define POTRF_TICK(k) \
   if (threadIdx.x == 0) g_potrf_clk[k] = clock64();
+#define POTRF_TICK_T(k, t) \
+  if (threadIdx.x == (t)) g_potrf_clk[k] = clock64();
 #else
 #define POTRF_TICK(k)
+#define POTRF_TICK_T(k, t)
 #endif
 constexpr int kPotrfThreads = 512;
 constexpr int kPotrfWarps = kPotrfThreads / 32;
 constexpr int kPanel = 32;
-constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + NB + 3 * kPanel * (kPanel + 1)) * sizeof(double);
+constexpr int kInvSlots = 6;  // sums T_rp, p < r <= 3
+constexpr size_t kPotrfSmem = (size_t)(NB * (NB + 1) + NB + kInvSlots * kPanel * (kPanel + 1)) * sizeof(double);
 
-// Off-diagonal 32 x 32 blocks of X = inv(L) of the diagonal block, one block row
-// r = rbk at a time: X_rp = -X_rr * T_p with T_p = sum_{q=p}^{r-1} L_rq X_qp, for
-// p < r, on strided 4 x 4 register tiles of one 64-thread group per p.  X(r,c),
-// r > c, lives in the strict upper half a[r*LD + c], its diagonal in xd; T_p is
-// staged in tmp[p][32][33].  Part 1 (T_p) only needs block rows < r of X and the
-// finished L_rq, so it runs while warp 0 factors panel r; part 2 runs beside the
-// panel-row step of panel r (disjoint rows of the same columns).
-__device__ __forceinline__ void potrf_inv_part1(const double* a, const double* xd, double* tmp, int rbk, int pb,
-                                                int tx, int ty) {
+// Off-diagonal 32 x 32 blocks of X = inv(L) of the diagonal block:
+// X_rp = -X_rr * T_rp, T_rp = sum_{q=p}^{r-1} L_rq X_qp, for p < r.  X(r,c), r > c,
+// lives in the strict upper half a[r*LD + c], its diagonal in xd; T_rp
+// accumulates in tmp[r(r-1)/2 + p][32][33].  Part 1: one product L_rq X_qp
+// (32 x 32 x 32, strided 4 x 4 register tiles on a two-warp team, gt = index
+// 0..63 in the team) -- all products with the same q run while warp 0 factors
+// panel q + 1 (L_rq and X_qp are final by then), on the warps off warp 0's
+// sub-partition.  Part 2 applies -X_rr beside the panel-row step of panel r
+// (disjoint rows of the same columns).
+__device__ __forceinline__ int inv_slot(int r, int p) { return r * (r - 1) / 2 + p; }
+__device__ __forceinline__ void potrf_inv_part1(const double* a, const double* xd, double* tmp, int r, int p,
+                                                int q, int gt) {
   constexpr int LD = NB + 1, TLD = kPanel + 1;
-  const int R0 = rbk * kPanel;
+  const int R0 = r * kPanel, tx = gt & 7, ty = gt >> 3;
   double acc[4][4] = {};
 #pragma unroll 4
-  for (int m = pb * kPanel; m < R0; ++m) {
+  for (int m = q * kPanel; m < (q + 1) * kPanel; ++m) {
     double lr[4], xc[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) lr[u] = a[m * LD + R0 + ty + 8 * u];  // L(R0+i, m)
     const double dg = xd[m];
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int c = pb * kPanel + tx + 8 * v;
+      const int c = p * kPanel + tx + 8 * v;
       const double up = a[m * LD + c];
       xc[v] = m > c ? up : 0.0;
       xc[v] = m == c ? dg : xc[v];  // X(m, c)
@@ -100,38 +107,48 @@ __device__ __forceinline__ void potrf_inv_part1(const double* a, const double* x
 #pragma unroll
       for (int v = 0; v < 4; ++v) acc[u][v] = fma(lr[u], xc[v], acc[u][v]);
   }
+  double* t = tmp + inv_slot(r, p) * kPanel * TLD;
+  const bool first = q == p;
 #pragma unroll
   for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) tmp[pb * kPanel * TLD + (ty + 8 * u) * TLD + tx + 8 * v] = acc[u][v];
+    for (int v = 0; v < 4; ++v) {
+      double& d = t[(ty + 8 * u) * TLD + tx + 8 * v];
+      d = first ? acc[u][v] : d + acc[u][v];
+    }
 }
 
+// rows ty + 8 (u0 + u), u < NU, of X_rp (a team of 64 threads per NU = 4 block,
+// two teams per block with NU = 2); X_rr is lower triangular, so the m-loop
+// stops at the last row of the slice
+template <int NU>
 __device__ __forceinline__ void potrf_inv_part2(double* a, const double* xd, const double* tmp, int rbk, int pb,
-                                                int tx, int ty) {
+                                                int tx, int ty, int u0) {
   constexpr int LD = NB + 1, TLD = kPanel + 1;
-  const int R0 = rbk * kPanel;
-  double acc[4][4] = {};
+  const int R0 = rbk * kPanel, mend = 8 * (u0 + NU);
+  double acc[NU][4] = {};
 #pragma unroll 4
-  for (int m = 0; m < kPanel; ++m) {
-    double xr[4], tv[4];
+  for (int m = 0; m < mend; ++m) {
+    double xr[NU], tv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = ty + 8 * u;
+    for (int u = 0; u < NU; ++u) {
+      const int i = ty + 8 * (u0 + u);
       const double up = a[(R0 + i) * LD + R0 + m], dg = xd[R0 + i];
       xr[u] = m < i ? up : 0.0;
       xr[u] = m == i ? dg : xr[u];  // X(R0+i, R0+m)
     }
 #pragma unroll
-    for (int v = 0; v < 4; ++v) tv[v] = tmp[pb * kPanel * TLD + m * TLD + tx + 8 * v];
+    for (int v = 0; v < 4; ++v) tv[v] = tmp[inv_slot(rbk, pb) * kPanel * TLD + m * TLD + tx + 8 * v];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < NU; ++u)
 #pragma unroll
       for (int v = 0; v < 4; ++v) acc[u][v] = fma(xr[u], tv[v], acc[u][v]);
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < NU; ++u)
 #pragma unroll
-    for (int v = 0; v < 4; ++v) a[(R0 + ty + 8 * u) * LD + pb * kPanel + tx + 8 * v] = -acc[u][v];  // X(R0+i, col)
+    for (int v = 0; v < 4; ++v)
+      a[(R0 + ty + 8 * (u0 + u)) * LD + pb * kPanel + tx + 8 * v] = -acc[u][v];  // X(R0+i, col)
 }
 
 __global__ void __launch_bounds__(kPotrfThreads)
@@ -225,19 +242,24 @@ __global__ void __launch_bounds__(kPotrfThreads)
 #pragma unroll
       for (int i = 0; i < kPanel; ++i)
         if (i > lane) a[(c0 + i) * LD + c0 + lane] = x[i];  // X(i, lane) in the strict upper half
-    } else {
-      // odd groups 1, 3, 5 (warps off warp 0's sub-partition): T_q of block row p
-      // of inv(L) (needs block rows < p only)
-      const int grp = tid >> 6, pb = (grp - 1) >> 1;
-      if ((grp & 1) && pb < p) potrf_inv_part1(a, xd, tmp, p, pb, tid & 7, (tid >> 3) & 7);
+    } else if ((warp & 3) != 0 && p > 0) {
+      // the 12 warps off warp 0's sub-partition, in teams of two: the products
+      // L_rq X_qp with q = p - 1 for every later block row r (<= 4 of them)
+      const int slot = warp - 1 - (warp >> 2);  // 0..11 over warps 1,2,3,5,6,7,...
+      const int team = slot >> 1, gt = (slot & 1) * 32 + lane;
+      if (team < (npan - p) * p) potrf_inv_part1(a, xd, tmp, p + team / p, team % p, p - 1, gt);
+      if (p == 3) POTRF_TICK_T(13, 64);
     }
+    if (p == 3) POTRF_TICK(15);
     __syncthreads();
     POTRF_TICK(1 + 3 * p);
     const int r0 = c0 + kPanel, mrest = NB - r0;  // padded rows below the panel
     if (mrest <= 0) {
       // last panel: block row p of inv(L) on groups 0..p-1
-      const int pb = tid >> 6;
-      if (pb < p) potrf_inv_part2(a, xd, tmp, p, pb, tid & 7, (tid >> 3) & 7);
+      const int pb = tid >> 7;  // two 64-thread teams per block (row halves)
+      POTRF_TICK(11);
+      if (pb < p) potrf_inv_part2<2>(a, xd, tmp, p, pb, tid & 7, (tid >> 3) & 7, 2 * ((tid >> 6) & 1));
+      POTRF_TICK(12);
       __syncthreads();
       break;
     }
@@ -250,9 +272,9 @@ __global__ void __launch_bounds__(kPotrfThreads)
       const int G = mrest / kPanel;
       double acc[4][4] = {};
       const int rowb = r0 + kPanel * grp + ty;
-      // groups 4..4+p-1: block row p of inv(L) (rows < c0 of panel p's columns;
+      // groups 4..7 (two per block, row halves): block row p of inv(L) (rows < c0 of panel p's columns;
       // the panel rows below write rows >= r0 of the same columns)
-      if (grp >= 4 && grp - 4 < p) potrf_inv_part2(a, xd, tmp, p, grp - 4, tx, ty);
+      if (grp >= 4 && ((grp - 4) >> 1) < p) potrf_inv_part2<2>(a, xd, tmp, p, (grp - 4) >> 1, tx, ty, 2 * (grp & 1));
       if (grp < G) {
 #pragma unroll 4
         for (int k = 0; k < kPanel; ++k) {  // X(j, k) = 0 for k > j: fixed trip count, no branches

@@ -21,7 +21,7 @@ int main() {
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     long long clk[128]; cudaMemcpyFromSymbol(clk, g_potrf_clk, sizeof(clk));
     printf("kernel %.1f us (%s); phase cycles from start:", ms * 1000, cudaGetErrorString(cudaGetLastError()));
-    int ids[] = {23, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 20, 21, 22};
+    int ids[] = {23, 1, 2, 3, 4, 5, 6, 7, 8, 9, 13, 14, 15, 10, 11, 12, 20, 21, 22};
     for (int k : ids) printf(" [%d]=%lld", k, clk[k] - clk[0]);
     printf("\n");
   }
