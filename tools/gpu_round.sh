@@ -18,7 +18,7 @@ if [ $rc -eq 0 ]; then
   echo "launch list rc=$?"
   python tools/launch_summary.py gpurun_out/launches_$TAG.csv > gpurun_out/launch_summary_$TAG.txt 2>&1
   head -30 gpurun_out/launch_summary_$TAG.txt
-  for KS in "k_syrk_gen:300" "k_far<\(int\)9>:1" "k_potrf_diag:200" "k_bwd_flow:2" "k_near_gl:2" "k_classify:2" "k_trsm_rows:200" "k_symv_upper:1"; do
+  for KS in "k_syrk_gen:1" "k_far<\(int\)9>:1" "k_potrf_diag:200" "k_bwd_flow:2" "k_near_gl:2" "k_classify:2" "k_trsm_rows:200" "k_symv_upper:1"; do
     K=${KS%%:*}; S=${KS##*:}
     NAME=$(echo "$K" | tr -cd 'a-z_0-9')
     timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
