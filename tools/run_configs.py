@@ -51,21 +51,26 @@ def direct(config):
     ast, sst = N.GbemAssemblyStats(), N.GbemSolveStats()
     cfg = ctx.quad()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0 = time.perf_counter()
-    e0.record()
-    ctx.check(ctx.lib.gbem_extract_cmatrix_dev(ctx.h, C.byref(panels), n, C.c_void_p(d_net.data_ptr()), K, eps,
-                                               C.byref(cfg), C.c_void_p(d_C.data_ptr()),
-                                               C.c_void_p(d_res.data_ptr()), C.byref(ast), C.byref(sst)))
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
+    # twice in one context: the first extraction also allocates the context's
+    # buffers (matrix, pair queue) and loads modules; the second is the steady state
+    times = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        e0.record()
+        ctx.check(ctx.lib.gbem_extract_cmatrix_dev(ctx.h, C.byref(panels), n, C.c_void_p(d_net.data_ptr()), K,
+                                                   eps, C.byref(cfg), C.c_void_p(d_C.data_ptr()),
+                                                   C.c_void_p(d_res.data_ptr()), C.byref(ast), C.byref(sst)))
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = times[-1]
     Cm = d_C.cpu().numpy().reshape(K, K)
     res = d_res.cpu().numpy()
     entries = n * (n + 1) // 2
     recip = float(np.max(np.abs(Cm - Cm.T)) / np.max(np.abs(np.diag(Cm))))
     off = Cm[~np.eye(K, dtype=bool)]
     out = dict(config=config, panels=n, nets=K, entries=entries, matrix_gb=n * n * 8 / 1e9,
-               extraction_ms=ms, wall_s=time.perf_counter() - t0, entries_per_s=entries / (ast.ms_total * 1e-3),
+               extraction_ms=ms, first_extraction_ms=times[0], wall_s=time.perf_counter() - t0, entries_per_s=entries / (ast.ms_total * 1e-3),
                assembly=ast.as_dict(), solve=sst.as_dict(),
                cholesky_tflops=(n ** 3 / 3) / (sst.ms_factor * 1e-3) / 1e12,
                max_residual=float(res.max()), reciprocity_defect=recip,
