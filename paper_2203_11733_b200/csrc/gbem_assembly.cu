@@ -462,8 +462,15 @@ __global__ void __launch_bounds__(1024)
   __shared__ uint32_t part[1024];
   int t = threadIdx.x;
   constexpr int per = kNumKeys / 1024;
+  // the thread's 64 counts as 16 independent 16-byte loads, all in flight at once
+  static_assert(per == 64, "16 x uint4 per thread");
+  uint4 cv[per / 4];
+  const uint4* c4 = reinterpret_cast<const uint4*>(counts + t * per);
+#pragma unroll
+  for (int k = 0; k < per / 4; ++k) cv[k] = c4[k];
   uint32_t s = 0;
-  for (int k = 0; k < per; ++k) s += counts[t * per + k];
+#pragma unroll
+  for (int k = 0; k < per / 4; ++k) s += cv[k].x + cv[k].y + cv[k].z + cv[k].w;
   part[t] = s;
   __syncthreads();
   for (int off = 1; off < 1024; off <<= 1) {
@@ -473,10 +480,21 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
   }
   uint32_t run = t ? part[t - 1] : 0;
-  for (int k = 0; k < per; ++k) {
-    offsets[t * per + k] = run;
-    cursors[t * per + k] = run;
-    run += counts[t * per + k];
+  uint4* o4 = reinterpret_cast<uint4*>(offsets + t * per);
+  uint4* u4 = reinterpret_cast<uint4*>(cursors + t * per);
+#pragma unroll
+  for (int k = 0; k < per / 4; ++k) {
+    uint4 o;
+    o.x = run;
+    run += cv[k].x;
+    o.y = run;
+    run += cv[k].y;
+    o.z = run;
+    run += cv[k].z;
+    o.w = run;
+    run += cv[k].w;
+    o4[k] = o;
+    u4[k] = o;
   }
   if (t == 1023) offsets[kNumKeys] = run;
   if (t == 0) {
