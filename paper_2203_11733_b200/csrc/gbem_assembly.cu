@@ -885,25 +885,40 @@ __global__ void __launch_bounds__(128)
 }
 
 // Mirror A[i*lda + j] (j >= i) into A[j*lda + i] over 32x32 tiles (bi <= bj).
+// 64 x 64 tiles, 16 loads per thread issued before any store (32 KB per CTA in
+// flight, 6 CTAs per SM), transposed through shared memory.
+constexpr int kSymTile = 64;
 __global__ void __launch_bounds__(256) k_symmetrize(double* A, long long lda, int n, int nbt) {
-  __shared__ double tile[kTile][kTile + 1];
+  constexpr int TS = kSymTile, RPT = TS * TS / 256 / 2;  // rows per thread per half-tile column
+  __shared__ double tile[TS][TS + 1];
   // linear upper-triangle tile index -> (bi, bj)
   long long t = blockIdx.x;
   int bi = (int)floor((2.0 * nbt + 1.0 - sqrt((2.0 * nbt + 1.0) * (2.0 * nbt + 1.0) - 8.0 * (double)t)) / 2.0);
   auto rowoff = [nbt](long long b) { return b * nbt - b * (b - 1) / 2; };
   while (bi > 0 && rowoff(bi) > t) --bi;
   while (rowoff(bi + 1) <= t) ++bi;
-  int bj = bi + (int)(t - rowoff(bi));
-  int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int r = ty; r < kTile; r += 8) {
-    int i = bi * kTile + r, j = bj * kTile + tx;
-    if (i < n && j < n && j >= i) tile[r][tx] = A[(long long)i * lda + j];
-  }
+  const int bj = bi + (int)(t - rowoff(bi));
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
+  double v[RPT][2];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = ty + 8 * u, i = bi * TS + r, j = bj * TS + h * 32 + tx;
+      v[u][h] = (i < n && j < n && j >= i) ? A[(long long)i * lda + j] : 0.0;
+    }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) tile[ty + 8 * u][h * 32 + tx] = v[u][h];
   __syncthreads();
-  for (int r = ty; r < kTile; r += 8) {
-    int j = bj * kTile + r, i = bi * kTile + tx;
-    if (i < n && j < n && j > i) A[(long long)j * lda + i] = tile[tx][r];
-  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = ty + 8 * u, j = bj * TS + r, i = bi * TS + h * 32 + tx;
+      if (i < n && j < n && j > i) A[(long long)j * lda + i] = tile[h * 32 + tx][r];
+    }
 }
 
 __global__ void k_pack_panels(const uint8_t* axis, const double* level, const double* a0,
@@ -1159,8 +1174,9 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
     if (rc) return rc;
   }
   if (symmetrize) {
-    long long ntiles = (long long)nbt * (nbt + 1) / 2;
-    k_symmetrize<<<(unsigned)ntiles, 256, 0, ctx->stream>>>(ctx->d_A, (long long)ctx->lda, (int)n, nbt);
+    const int snbt = (int)((n + kSymTile - 1) / kSymTile);
+    long long ntiles = (long long)snbt * (snbt + 1) / 2;
+    k_symmetrize<<<(unsigned)ntiles, 256, 0, ctx->stream>>>(ctx->d_A, (long long)ctx->lda, (int)n, snbt);
     GBEM_LAUNCH_CHECK(ctx);
   }
   cudaEventRecord(ctx->ev[1], ctx->stream);
