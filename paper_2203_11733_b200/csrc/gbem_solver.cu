@@ -372,8 +372,9 @@ __global__ void __launch_bounds__(256) k_symv_upper(const double* __restrict__ A
                                                     const double* __restrict__ diag, int n, const double* X,
                                                     long long ldx, int nrhs, double* Y) {
   constexpr int T = 64, LD = T + 1;
+  static_assert(MAXR % 2 == 0, "x rows read as double2");
   __shared__ double sa[T * LD];
-  __shared__ double xs[T * MAXR];
+  __shared__ __align__(16) double xs[T * MAXR];
   double* red = sa;  // [3][T][MAXR] quarter partials, after the tile loop
   static_assert(3 * T * MAXR <= T * LD, "partials fit in the tile buffer");
   const int nbt = (n + T - 1) / T;
@@ -446,8 +447,14 @@ __global__ void __launch_bounds__(256) k_symv_upper(const double* __restrict__ A
     for (int k = 0; k < T / 4; ++k) {
       const int c = quarter * (T / 4) + k;
       const double a = sa[c * LD + row];
+      // x_c as 16-byte broadcasts (MAXR even)
+      const double2* x2 = reinterpret_cast<const double2*>(xs + c * MAXR);
 #pragma unroll
-      for (int q = 0; q < MAXR; ++q) acc[q] = fma(a, xs[c * MAXR + q], acc[q]);
+      for (int q = 0; q < MAXR / 2; ++q) {
+        const double2 xv = x2[q];
+        acc[2 * q] = fma(a, xv.x, acc[2 * q]);
+        acc[2 * q + 1] = fma(a, xv.y, acc[2 * q + 1]);
+      }
     }
 #pragma unroll
     for (int u = 0; u < T / 8; ++u) {
@@ -1502,7 +1509,15 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
       int rq = std::min(8, R - q0);
       const double* Xq = d_X + (long long)q0 * n;
       double* Yq = Ysym + (long long)q0 * n;
-      k_symv_upper<8><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      // the narrowest instantiation that holds rq right-hand sides
+      if (rq <= 2)
+        k_symv_upper<2><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      else if (rq <= 4)
+        k_symv_upper<4><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      else if (rq <= 6)
+        k_symv_upper<6><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      else
+        k_symv_upper<8><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
       GBEM_LAUNCH_CHECK(ctx);
     }
     k_resid_norm<<<R, 256, 0, s>>>(Ysym, d_B, n, d_resid);
