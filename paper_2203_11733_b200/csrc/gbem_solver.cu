@@ -1470,8 +1470,8 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
     int* fl = ctx->d_flags;
     void* args[] = {(void*)&cA, (void*)&lda, (void*)&cL, (void*)&nn, (void*)&RR, (void*)&cY, (void*)&d_X, (void*)&fl,
                     (void*)&ep};
-    void* fn = R <= 2 ? (void*)k_bwd_flow<2> : R <= 4 ? (void*)k_bwd_flow<4> : R <= 8 ? (void*)k_bwd_flow<8>
-                                                                                 : (void*)k_bwd_flow<16>;
+    void* fn = R <= 2 ? (void*)k_bwd_flow<2> : R <= 4 ? (void*)k_bwd_flow<4> : R <= 6 ? (void*)k_bwd_flow<6>
+             : R <= 8 ? (void*)k_bwd_flow<8> : (void*)k_bwd_flow<16>;
     GBEM_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlowSmem));
     GBEM_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3(nblk_s), dim3(kFlowThreads), args, kFlowSmem, s));
     GBEM_LAUNCH_CHECK(ctx);
