@@ -180,6 +180,14 @@ def test_kernel_selftest_on_device(ctx):
     for c in cases:
         assert c["passed"], c
         assert c["pairs"] == 200
+        # the report carries the class's worst pair for follow-up (tools/selftest_recheck.py)
+        assert int(c["worst_test"][0]) in (0, 1, 2) and int(c["worst_source"][0]) in (0, 1, 2), c
+        assert np.isfinite(c["worst_value"]) and np.isfinite(c["worst_oracle"]), c
+        if c["name"].startswith("Q"):
+            assert c["worst_nsign"] in (-1, 1), c
+        if c["name"] != "Q coplanar zero":
+            rel = abs(c["worst_value"] - c["worst_oracle"]) / max(abs(c["worst_oracle"]), 1e-9)
+            assert abs(rel - c["worst_rel"]) <= 1e-6 * max(c["worst_rel"], 1e-12) + 1e-15, c
 
 
 def test_kernel_selftest_cli():
