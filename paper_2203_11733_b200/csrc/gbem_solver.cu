@@ -487,7 +487,7 @@ __global__ void k_resid_norm(const double* Y, const double* B, int n, double* re
     rn += d * d;
     bn += b * b;
   }
-  __shared__ double s1[256], s2[256];
+  __shared__ double s1[1024], s2[1024];  // blockDim.x <= 1024, a power of two
   s1[threadIdx.x] = rn;
   s2[threadIdx.x] = bn;
   __syncthreads();
@@ -1520,7 +1520,7 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
         k_symv_upper<8><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
       GBEM_LAUNCH_CHECK(ctx);
     }
-    k_resid_norm<<<R, 256, 0, s>>>(Ysym, d_B, n, d_resid);
+    k_resid_norm<<<R, 1024, 0, s>>>(Ysym, d_B, n, d_resid);
     GBEM_LAUNCH_CHECK(ctx);
   }
   cudaEventRecord(ctx->ev[3], s);
