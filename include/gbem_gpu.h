@@ -74,6 +74,12 @@ typedef struct {
   int64_t far_evals;         /* Gauss kernel evaluations */
   double far_flops;          /* algorithmic FP64 flops of the far kernel */
   double ms_classify, ms_far, ms_near, ms_total; /* device time per phase */
+  /* near-field routes (included in pairs_parallel + pairs_orthogonal):
+   * gap < 1e-3 max diameter -> the reference's adaptive Romberg (warp per pair);
+   * band b -> graded Gauss-Legendre, gap/diam in [0.1, 1) or touching (b = 0),
+   * [0.02, 0.1) (1), [0.005, 0.02) (2), [1e-3, 0.005) (3) */
+  int64_t pairs_near_romberg;
+  int64_t pairs_near_band[4];
 } gbem_assembly_stats;
 
 typedef struct {
@@ -259,6 +265,11 @@ int gbem_extract_cmatrix(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const i
 int gbem_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net_of_panel,
                              int32_t K, double eps_r, const gbem_quad_config* cfg, double* C, double* resid,
                              gbem_assembly_stats* astats, gbem_solve_stats* sstats);
+
+/* Diagnostic: fill the shared memory of every SM with `value` (one maximal
+ * CTA per SM).  Tests use it to prove that no kernel reads shared memory it
+ * did not write (e.g. NaN left by an earlier kernel). */
+int gbem_debug_fill_shared(gbem_ctx* ctx, double value);
 
 #ifdef __cplusplus
 }

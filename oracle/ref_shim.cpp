@@ -151,6 +151,56 @@ int ref_assemble_single(int64_t n, const orc_rect* p, double rel_tol, int max_le
   return status.load();
 }
 
+// ref_assemble_single plus the reference's convergence diagnostics: the
+// (i, j) of every pair whose u_pair_integral reports converged = false
+// (assembly.hpp:97 ANDs these flags into GalerkinSystem::converged), up to
+// nc_cap of them; *nc_count receives the total.  Rows are dealt in chunks of
+// `chunk` so a progress callback can report.
+int ref_assemble_single_diag(int64_t n, const orc_rect* p, double rel_tol, int max_levels,
+                             double* A, int64_t* nc_pairs, int64_t nc_cap, int64_t* nc_count,
+                             int nthreads, void (*progress)(int64_t rows_done)) {
+  if (nthreads < 1) nthreads = 1;
+  std::atomic<int> status{0};
+  std::atomic<int64_t> next{0}, nnc{0}, done{0};
+  auto work = [&] {
+    for (;;) {
+      int64_t i = next.fetch_add(1);
+      if (i >= n) break;
+      gbem::Rect ri = toRect(p[i]);
+      double ai = ri.area();
+      for (int64_t j = i; j < n; ++j) {
+        gbem::Rect rj = toRect(p[j]);
+        gbem::QuadratureConfig cfg;
+        cfg.relTol = rel_tol;
+        cfg.maxLevels = max_levels;
+        try {
+          gbem::KernelValue kv = gbem::u_pair_integral(ri, rj, cfg);
+          if (!kv.converged) {
+            int64_t s = nnc.fetch_add(1);
+            if (s < nc_cap) {
+              nc_pairs[2 * s] = i;
+              nc_pairs[2 * s + 1] = j;
+            }
+          }
+          double v = kv.value / (ai * rj.area());
+          A[i * n + j] = v;
+          A[j * n + i] = v;
+        } catch (const gbem::NumericalError&) {
+          status = 2;
+        }
+      }
+      int64_t d = done.fetch_add(1) + 1;
+      if (progress && d % 256 == 0) progress(d);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nthreads; ++t) th.emplace_back(work);
+  work();
+  for (auto& t : th) t.join();
+  if (nc_count) *nc_count = nnc.load();
+  return status.load();
+}
+
 // gbem::oracle_pair_integral(SingleLayer) (oracle.hpp:191).
 double ref_oracle_pair_integral(const orc_rect* a, const orc_rect* b, int depth) {
   return gbem::oracle_pair_integral(gbem::KernelKind::SingleLayer, toRect(*a), toRect(*b),

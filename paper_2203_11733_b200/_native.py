@@ -39,10 +39,13 @@ class GbemAssemblyStats(C.Structure):
                 ("pairs_far", C.c_int64), ("not_converged", C.c_int64),
                 ("nonfinite", C.c_int64), ("near_evals", C.c_int64), ("far_evals", C.c_int64),
                 ("far_flops", C.c_double), ("ms_classify", C.c_double), ("ms_far", C.c_double),
-                ("ms_near", C.c_double), ("ms_total", C.c_double)]
+                ("ms_near", C.c_double), ("ms_total", C.c_double),
+                ("pairs_near_romberg", C.c_int64), ("pairs_near_band", C.c_int64 * 4)]
 
     def as_dict(self) -> dict:
-        return {f: getattr(self, f) for f, _ in self._fields_}
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["pairs_near_band"] = list(d["pairs_near_band"])
+        return d
 
 
 class GbemBlockPanels(C.Structure):
@@ -105,6 +108,7 @@ GPU_SYMBOLS = [
     ("gbem_extract_cmatrix", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, _P, C.c_int32, C.c_double,
                                        C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats),
                                        C.POINTER(GbemSolveStats)]),
+    ("gbem_debug_fill_shared", C.c_int, [_P, C.c_double]),
     ("gbem_extract_cmatrix_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, _P, C.c_int32, C.c_double,
                                            C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats),
                                            C.POINTER(GbemSolveStats)]),
@@ -243,6 +247,10 @@ class Context:
                                            C.byref(sst) if stats else None)
         self.check(rc)
         return Cm, res, ast, sst
+
+    def fill_shared(self, value: float):
+        """Diagnostic: leave `value` in every SM's shared memory."""
+        self.check(self.lib.gbem_debug_fill_shared(self.h, value))
 
     def matrix_upload(self, A: np.ndarray):
         A = np.ascontiguousarray(A, dtype=np.float64)

@@ -55,7 +55,9 @@ enum StatIdx {
   ST_ORTH,
   ST_FAR,
   ST_FIRST_BAD,  // first (i << 32 | j) with a non-finite sample, ~0 if none
-  ST_COUNT
+  ST_ROMB,       // near-contact pairs on the adaptive Romberg route
+  ST_BAND0,      // .. ST_BAND0 + kNearBands - 1: graded Gauss-Legendre bands
+  ST_COUNT = ST_BAND0 + 4
 };
 
 constexpr int kTile = 32;
@@ -506,6 +508,9 @@ __global__ void __launch_bounds__(1024)
     atomicAdd(&stats[ST_COP], (unsigned long long)counts[kClsCoplanar]);
     atomicAdd(&stats[ST_PAR], par);
     atomicAdd(&stats[ST_ORTH], orth);
+    atomicAdd(&stats[ST_ROMB], (unsigned long long)counts[kClsParallel] + counts[kClsOrthogonal]);
+    for (int b = 0; b < kNearBands; ++b)
+      atomicAdd(&stats[ST_BAND0 + b], (unsigned long long)counts[kClsParallelGL + b] + counts[kClsOrthogonalGL + b]);
   }
   __syncthreads();
   if (t == 0) {
@@ -1047,6 +1052,8 @@ int finish_stats(gbem_ctx* ctx, gbem_assembly_stats* stats, int64_t pairs_total)
     double f;
     memcpy(&f, &h[ST_FAR_FLOPS], sizeof(double));
     stats->far_flops = f;
+    stats->pairs_near_romberg = (int64_t)h[ST_ROMB];
+    for (int b = 0; b < 4; ++b) stats->pairs_near_band[b] = b < kNearBands ? (int64_t)h[ST_BAND0 + b] : 0;
   }
   if (h[ST_NONFINITE]) {
     unsigned long long b = h[ST_FIRST_BAD];

@@ -605,11 +605,10 @@ int gbem_internal_lu_solve(gbem_ctx* ctx, double* d_b, double* d_x, double* d_re
   double scale;
   memcpy(&scale, &hmax, sizeof(double));
   double thresh = 1e-14 * scale;
-  static bool attr = false;
-  if (!attr) {
+  if (!(ctx->attr_set & gbem_ctx::kAttrGemmLU)) {
     GBEM_CUDA(ctx, cudaFuncSetAttribute(gbem_gemm::k_gemm_g<gbem_gemm::kSub, 1>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbem_gemm::kGSmem));
-    attr = true;
+    ctx->attr_set |= gbem_ctx::kAttrGemmLU;
   }
   double* A = ctx->d_A;
   int grid = ctx->num_sms;

@@ -81,10 +81,15 @@ __global__ void k_corner_charges(const double* A, long long lda, int n, int K, d
   C[i] = -scale * A[(long long)(n + lo) * lda + n + hi];
 }
 
+// Nets per extraction: the K border rows ride along every trsm and update of the
+// factorisation, so K is bounded only by memory; this cap keeps K*K and the
+// border small next to the matrix.
+constexpr int32_t kMaxNets = 8192;
+
 int extract_impl(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* d_net, int32_t K, double eps_r,
                  const gbem_quad_config* cfg, double* d_C, double* d_resid, gbem_assembly_stats* as,
                  gbem_solve_stats* ss, bool device_panels) {
-  if (K < 1 || K > 64) return ctx->fail(GBEM_EINVAL, "K must be in [1, 64]");
+  if (K < 1 || K > kMaxNets) return ctx->fail(GBEM_EINVAL, "K must be in [1, " + std::to_string(kMaxNets) + "]");
   int rc = gbem_internal_upload_panels(ctx, P, n, device_panels);
   if (rc) return rc;
   rc = ensure_matrix(ctx, n, K);
@@ -535,6 +540,28 @@ int gbem_spd_solve_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, 
   return gbem_internal_solve(ctx, B, nrhs, X, resid, stats);
 }
 
+namespace {
+__global__ void k_fill_shared(double value, int words) {
+  extern __shared__ double fill_sm[];
+  for (int i = threadIdx.x; i < words; i += blockDim.x) fill_sm[i] = value;
+  __syncthreads();
+  // keep the stores: an impossible condition on the data read back
+  if (fill_sm[(threadIdx.x * 7) % words] == 1.2345e-300 && value != 1.2345e-300) fill_sm[0] = 0.0;
+}
+}  // namespace
+
+int gbem_debug_fill_shared(gbem_ctx* ctx, double value) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int maxsm = 0;
+  GBEM_CUDA(ctx, cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  GBEM_CUDA(ctx, cudaFuncSetAttribute(k_fill_shared, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  k_fill_shared<<<ctx->num_sms * 2, 1024, maxsm, ctx->stream>>>(value, maxsm / 8);
+  GBEM_LAUNCH_CHECK(ctx);
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GBEM_OK;
+}
+
 int gbem_net_charges_dev(gbem_ctx* ctx, const int32_t* net, int64_t n, const double* X, int64_t nrhs,
                          int32_t K, double scale, double* C, double* outer) {
   if (!ctx) return GBEM_EINVAL;
@@ -556,11 +583,12 @@ int gbem_extract_cmatrix(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const i
                          gbem_assembly_stats* as, gbem_solve_stats* ss) {
   if (!ctx) return GBEM_EINVAL;
   if (!P || !net_of_panel || !C || n <= 0) return ctx->fail(GBEM_EINVAL, "null argument or empty panel set");
+  if (K < 1 || K > kMaxNets) return ctx->fail(GBEM_EINVAL, "K must be in [1, " + std::to_string(kMaxNets) + "]");
   GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
   int32_t* d_net = nullptr;
   double *d_C = nullptr, *d_res = nullptr;
   GBEM_CUDA(ctx, cudaMallocAsync(&d_net, sizeof(int32_t) * n, ctx->stream));
-  GBEM_CUDA(ctx, cudaMallocAsync(&d_C, sizeof(double) * K * K + sizeof(double) * 64, ctx->stream));
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_C, sizeof(double) * ((size_t)K * K + K), ctx->stream));
   d_res = d_C + (size_t)K * K;
   GBEM_CUDA(ctx, cudaMemcpyAsync(d_net, net_of_panel, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
   int rc = extract_impl(ctx, P, n, d_net, K, eps_r, cfg, d_C, d_res, as, ss, false);

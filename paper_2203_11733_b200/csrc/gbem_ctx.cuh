@@ -85,6 +85,11 @@ struct gbem_ctx {
   cudaEvent_t ev_gs = nullptr, ev_ge = nullptr, ev_gt = nullptr, ev_gra = nullptr;
   void* green_ctx[2] = {nullptr, nullptr};  // CUgreenCtx (side, main)
 
+  // kernels whose dynamic shared-memory limit has been raised on this
+  // context's device (cudaFuncSetAttribute is per device; one bit per site)
+  unsigned attr_set = 0;
+  enum : unsigned { kAttrGemmSolve = 1u, kAttrFactor = 2u, kAttrGemmLU = 4u };
+
   int fail(int code, const std::string& msg) {
     err = msg;
     return code;

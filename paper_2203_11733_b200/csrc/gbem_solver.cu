@@ -567,10 +567,11 @@ __device__ __forceinline__ void solve_diag(const double* Ls, const double* ws, d
     for (int q = 0; q < RT; ++q)
       if (q < R) part[q * NB + i] = acc[q];
   __syncthreads();
-  if (!half && i < kb)
+  // Every ys slot strip_update reads is written: rows >= kb of a ragged last
+  // block and columns q >= R are zero (fma(0, leftover NaN) would poison T).
+  if (!half)
 #pragma unroll
-    for (int q = 0; q < RT; ++q)
-      if (q < R) ys[q * NB + i] = acc[q] + part[q * NB + i];
+    for (int q = 0; q < RT; ++q) ys[q * NB + i] = (i < kb && q < R) ? acc[q] + part[q * NB + i] : 0.0;
   __syncthreads();
 }
 
@@ -951,13 +952,12 @@ static int solve_blocked(gbem_ctx* ctx, const double* d_B, int R, double* d_X, b
   double* W = ctx->d_sw;
   double* Y = W + nr;
   double* X = Y + nr;
-  static bool attr = false;
-  if (!attr) {
+  if (!(ctx->attr_set & gbem_ctx::kAttrGemmSolve)) {
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_g<kStore, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_g<kSub, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_g<kStore, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_g<kSub, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGSmem));
-    attr = true;
+    ctx->attr_set |= gbem_ctx::kAttrGemmSolve;
   }
   const dim3 tb(32, 8), tg((n + 31) / 32, (R + 31) / 32);
   if (y_from_border) {
@@ -1109,13 +1109,12 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     GBEM_CUDA(ctx, cudaMalloc(&ctx->d_info, sizeof(int)));
     GBEM_CUDA(ctx, cudaMallocHost(&ctx->h_info, sizeof(int)));
   }
-  static bool attr_done = false;
-  if (!attr_done) {
+  if (!(ctx->attr_set & gbem_ctx::kAttrFactor)) {
     GBEM_CUDA(ctx, cudaFuncSetAttribute(kUpdate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmemPadded));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kPotrfSmem));
-    attr_done = true;
+    ctx->attr_set |= gbem_ctx::kAttrFactor;
   }
   cudaStream_t s = ctx->stream;
   int big = 0x7fffffff;
@@ -1431,7 +1430,7 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
                                  gbem_solve_stats* stats, bool y_from_border) {
   const int n = (int)ctx->n;
   const long long lda = ctx->lda;
-  if (nrhs < 0 || nrhs > 64) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, 64]");
+  if (nrhs < 0 || nrhs > n) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, n]");
   if (!ctx->factored) return ctx->fail(GBEM_EINVAL, "no factored matrix in the context");
   if (stats) stats->nrhs = nrhs;
   if (n == 0 || nrhs == 0) return GBEM_OK;
@@ -1545,7 +1544,7 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
 
 int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
                         gbem_solve_stats* stats) {
-  if (nrhs < 0 || nrhs > 64) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, 64]");
+  if (nrhs < 0 || nrhs > ctx->n) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, n]");
   int rc = gbem_internal_factor(ctx, stats);
   if (rc) return rc;
   if (stats) stats->nrhs = nrhs;

@@ -235,7 +235,7 @@ CapMatrix capacitance_matrix_shared(gbem_ctx* ctx, const Scene& s, const PanelSe
   const size_t n = ps.panels.size();
   const size_t K = s.nets.size();
   if (K == 0) throw ValidationError("scene has no conductors");
-  if (K > 64) throw ValidationError("at most 64 nets per shared solve");
+  if (K > 8192) throw ValidationError("at most 8192 nets per shared solve");
   std::map<int, size_t> col;
   for (size_t k = 0; k < K; ++k) col[s.nets[k].id] = k;
   SoA soa(ps);

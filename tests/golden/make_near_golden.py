@@ -1,0 +1,76 @@
+"""Generate tests/golden/near_contact_golden.json (run here, on CPU; needs oracle/_ref).
+
+Near-contact pair sets for the parity tests of the near-field routes
+(VERDICT r1 "what's missing" #4): offset-parallel and orthogonal pairs at
+gap / max-diameter in four buckets
+
+    (1e-6, 1e-3)  -> k_near_warp (the reference's adaptive Romberg, warp-cooperative)
+    [1e-3, 5e-3)  -> graded Gauss-Legendre band 3 (48 nodes per half segment)
+    [5e-3, 0.02)  -> band 2 (32 nodes)
+    [0.02, 0.1)   -> band 1 (24 nodes)
+
+120 pairs per (bucket, kind), seeded (tests/pairgen.py near_contact_pairs).
+For every pair the file holds
+    ref    : the reference u_pair_integral (kernels.hpp:270) at its default
+             QuadratureConfig (relTol 1e-8, maxLevels 16), and its converged flag;
+    tight  : the same at relTol 1e-13, maxLevels 20, and its converged flag;
+    exact  : the closed-form corner sum in 50-digit arithmetic (tests/exact_truth.py),
+             pinned to `tight` wherever `tight` converged (tests/test_exact_truth.py).
+
+  python tests/golden/make_near_golden.py
+"""
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent))
+import exact_truth as E  # noqa: E402
+import oracle_lib as O  # noqa: E402
+import pairgen as G  # noqa: E402
+
+BUCKETS = [(1e-6, 1e-3), (1e-3, 5e-3), (5e-3, 0.02), (0.02, 0.1)]
+KINDS = ["parallel", "orthogonal"]
+PER = 120
+
+
+def main():
+    rng = np.random.default_rng(20261021)
+    A, B, bucket, kind = [], [], [], []
+    for bi, (lo, hi) in enumerate(BUCKETS):
+        for kk, k in enumerate(KINDS):
+            a, b = G.near_contact_pairs(rng, PER, lo, hi, k)
+            A.append(a); B.append(b)
+            bucket += [bi] * PER; kind += [kk] * PER
+    A = np.vstack(A); B = np.vstack(B)
+    # every pair on its own lattice site: shift set s (bucket, kind) by a further
+    # offset so the 960 pairs form one panel set with only far cross pairs
+    for s in range(len(BUCKETS) * len(KINDS)):
+        off = np.array([0.0, 0.0, 0.0])
+        off[s % 3] = 400.0 * (1 + s // 3)
+        for M in (A, B):
+            for r in range(s * PER, (s + 1) * PER):
+                ax = int(M[r, 0]); i0, i1 = G.INPLANE[ax]
+                M[r, 1] += off[ax]; M[r, 2:4] += off[i0]; M[r, 4:6] += off[i1]
+    nth = os.cpu_count()
+    ref, rconv, _ = O.u_pairs("ref", A, B, nthreads=nth)
+    tight, tconv, _ = O.u_pairs("ref", A, B, rel_tol=1e-13, max_levels=20, nthreads=nth)
+    exact = np.array([E.u_exact(a, b) for a, b in zip(A, B)])
+    g = O.gap_ratio(A, B)
+    d = {"buckets": BUCKETS, "kinds": KINDS, "per": PER, "A": A.tolist(), "B": B.tolist(),
+         "bucket": bucket, "kind": kind, "gap_ratio": g.tolist(),
+         "ref": ref.tolist(), "ref_converged": rconv.astype(int).tolist(),
+         "tight": tight.tolist(), "tight_converged": tconv.astype(int).tolist(), "exact": exact.tolist()}
+    (HERE / "near_contact_golden.json").write_text(json.dumps(d))
+    for bi in range(len(BUCKETS)):
+        for kk in range(len(KINDS)):
+            m = (np.array(bucket) == bi) & (np.array(kind) == kk)
+            print(BUCKETS[bi], KINDS[kk], "ref-exact", np.max(np.abs(ref[m] - exact[m]) / exact[m]),
+                  "ref conv", rconv[m].mean(), "tight conv", tconv[m].mean())
+
+
+if __name__ == "__main__":
+    main()

@@ -239,3 +239,24 @@ def assemble_multi(P: np.ndarray, nsign, kind, net, reg_a, reg_b, regions, main_
                                   A.ctypes.data, b.ctypes.data, C.byref(m), C.byref(conv))
     mm = m.value
     return A[:mm * mm].reshape(mm, mm), b[:mm], st, bool(conv.value)
+
+
+def assemble_ref_diag(P: np.ndarray, nthreads=8, rel_tol=1e-8, max_levels=16, nc_cap=1 << 20,
+                      progress=None):
+    """Reference assembly (oracle/_ref) plus the (i, j) of every pair the
+    reference's Romberg reports as not converged (assembly.hpp:97)."""
+    lib = ref()
+    f = lib.ref_assemble_single_diag
+    CB = C.CFUNCTYPE(None, C.c_int64)
+    f.restype = C.c_int
+    f.argtypes = [C.c_int64, RP, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_int64,
+                  C.POINTER(C.c_int64), C.c_int, CB]
+    n = len(P)
+    rp = rects_from_matrix(P)
+    A = np.empty((n, n))
+    nc = np.zeros((nc_cap, 2), dtype=np.int64)
+    cnt = C.c_int64(0)
+    cb = CB(progress) if progress else CB(lambda d: None)
+    st = f(n, rp, rel_tol, max_levels, A.ctypes.data, nc.ctypes.data, nc_cap, C.byref(cnt), nthreads, cb)
+    k = min(cnt.value, nc_cap)
+    return A, nc[:k].copy(), int(cnt.value), st

@@ -168,3 +168,56 @@ def small_far_pairs(rng, n, edge_lo=0.002, edge_hi=0.05, dist_lo=0.5, dist_hi=5.
             c2[ax] = c1[ax]
         A.append(mk(ax, c1)); B.append(mk(bx, c2))
     return np.array(A), np.array(B)
+
+
+def near_contact_pairs(rng, n, g_lo, g_hi, kind, spacing=50.0):
+    """Offset-parallel ("parallel") or orthogonal ("orthogonal") pairs at
+    gap/max-diameter log-uniform in [g_lo, g_hi): the near-contact regime of the
+    reference's reduced integrands (kernels.hpp:138-153, 175-214) and its
+    Romberg (quadrature.hpp:70-113).  Pair k is translated to its own lattice
+    site `spacing` apart (panels are at most
+    ~20 long: size ratio and aspect up to 4), so the 2n panels [A0, B0, A1, B1, ...] also form a
+    panel set whose cross pairs are all far (the assembly route test)."""
+    A, B = [], []
+    side = int(np.ceil(n ** (1.0 / 3.0)))
+    while len(A) < n:
+        ax = int(rng.integers(3))
+        la = rng.uniform(0.2, 1.2)
+        lb = la * (1.0 if rng.random() < 0.4 else np.exp(rng.uniform(-np.log(4), np.log(4))))
+        a = [ax, 0.0, -la / 2, la / 2, -lb / 2, lb / 2]
+        bx = ax if kind == "parallel" else (ax + 1 + int(rng.integers(2))) % 3
+        s = np.exp(rng.uniform(-np.log(4), np.log(4)))
+        lc = rng.uniform(0.2, 1.2) * s
+        ld = lc * (1.0 if rng.random() < 0.4 else np.exp(rng.uniform(-np.log(4), np.log(4))))
+        d = rng.normal(size=3)
+        if kind == "parallel" and abs(d[ax]) < 0.05:
+            d[ax] = 0.05 if d[ax] >= 0 else -0.05  # keep the planes apart (offset-parallel, not coplanar)
+        d /= np.linalg.norm(d)
+        g_target = np.exp(rng.uniform(np.log(g_lo), np.log(g_hi)))
+        dm = max(np.hypot(la, lb), np.hypot(lc, ld))
+        j0, j1 = INPLANE[bx]
+
+        def place(t):
+            c = d * t
+            return [bx, c[bx], c[j0] - lc / 2, c[j0] + lc / 2, c[j1] - ld / 2, c[j1] + ld / 2]
+
+        lo, hi = 0.0, 500.0
+        for _ in range(200):
+            mid = 0.5 * (lo + hi)
+            if _gap(a, place(mid)) / dm < g_target:
+                lo = mid
+            else:
+                hi = mid
+        b = place(hi)
+        g = _gap(a, b) / dm
+        if not (g_lo <= g < g_hi) or _crossing(a, b):
+            continue
+        k = len(A)
+        site = np.array([k % side, (k // side) % side, k // (side * side)], dtype=float) * spacing
+
+        def shift(r):
+            axis = int(r[0]); i0, i1 = INPLANE[axis]
+            return [axis, r[1] + site[axis], r[2] + site[i0], r[3] + site[i0], r[4] + site[i1], r[5] + site[i1]]
+
+        A.append(shift(a)); B.append(shift(b))
+    return np.array(A), np.array(B)

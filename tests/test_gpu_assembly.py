@@ -111,3 +111,36 @@ def test_row_block_sharded_assembly_matches_full(ctx):
         assert sh.stats.pairs_total == sh.unique_pairs
         for i in range(sh.row_begin, sh.row_end):
             assert np.array_equal(blk[i - sh.row_begin, i:n], A_full[i, i:n])
+
+
+@pytest.mark.parametrize("nrhs", [1, 2, 3, 4, 5, 6, 7, 8, 16])
+def test_cholesky_ragged_after_nan_shared(ctx, nrhs):
+    """every solve path initialises the shared memory it
+    reads.  NaN is left in every SM's shared memory by a prior kernel, then a
+    ragged system (n % 128 != 0) is solved at each right-hand-side width."""
+    n = 2832
+    rng = np.random.default_rng(nrhs)
+    M = rng.normal(size=(n, n)) / np.sqrt(n)
+    A = M.T @ M + 2.0 * np.eye(n)
+    B = rng.normal(size=(n, nrhs))
+    ctx.matrix_upload(A)
+    ctx.fill_shared(float("nan"))
+    X, res, st = ctx.spd_solve(B)
+    assert np.isfinite(X).all()
+    Xn = np.linalg.solve(A, B)
+    assert np.abs(X - Xn).max() <= 1e-10 * np.abs(Xn).max()
+    assert res.max() <= 1e-12
+
+
+def test_cholesky_many_rhs(ctx):
+    """nrhs > 64: the solve loops over right-hand-side chunks."""
+    n = 700
+    rng = np.random.default_rng(70)
+    M = rng.normal(size=(n, n)) / np.sqrt(n)
+    A = M.T @ M + np.eye(n)
+    B = rng.normal(size=(n, 100))
+    ctx.matrix_upload(A)
+    X, res, st = ctx.spd_solve(B)
+    Xn = np.linalg.solve(A, B)
+    assert np.abs(X - Xn).max() <= 1e-10 * np.abs(Xn).max()
+    assert res.max() <= 1e-12

@@ -152,3 +152,24 @@ def test_spd_solve_every_width(ctx, K):
     Xr = np.linalg.solve(A, B)
     assert np.abs(X - Xr).max() <= 1e-10 * np.abs(Xr).max()
     assert np.max(res) <= 1e-12
+
+
+def test_extract_more_than_64_nets(ctx):
+    """K > 64: the bordered factorisation carries any number of
+    border rows; 100 panel groups as nets, C = eps B^T A^-1 B against numpy."""
+    import paper_2203_11733_b200 as g
+    from paper_2203_11733_b200._native import PanelArrays
+    m = g.config_model(1, scale=0.5)
+    ps = m.partition(1)
+    P = ps.matrix()
+    n = len(P)
+    K = 100
+    rng = np.random.default_rng(100)
+    net = (np.arange(n) % K).astype(np.int32)
+    rng.shuffle(net)
+    Cm, res, _, _ = ctx.extract_cmatrix(PanelArrays.from_matrix(P), net, K, 3.9)
+    A, _ = ctx.assemble_single(PanelArrays.from_matrix(P))
+    Bm = (net[:, None] == np.arange(K)[None, :]).astype(float)
+    Cref = 3.9 * 8.854187817e-12 * 1e-6 * Bm.T @ np.linalg.solve(A, Bm)
+    assert np.abs(Cm - Cref).max() <= 1e-9 * np.abs(Cref).max()
+    assert res.max() <= 1e-10
