@@ -271,6 +271,62 @@ int gbem_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, con
  * did not write (e.g. NaN left by an earlier kernel). */
 int gbem_debug_fill_shared(gbem_ctx* ctx, double value);
 
+/* ------------------------------------------------------------------------
+ * Row-block sharded solve (no reference counterpart: the
+ * reference solves with dense Cholesky only, solver.hpp:24-50).  When the
+ * matrix does not fit one GPU, rank r of P holds complete rows
+ * [r*m, min((r+1)*m, n)) of A, m = ceil(n / P), assembled locally with no
+ * communication, and A X = B is solved by block-Jacobi preconditioned CG
+ * (K recurrences sharing every launch and collective).  Per iteration: an
+ * all-gather of the search directions (n x K), the local DMMA product
+ * A_r P, two all-reduces of K-vectors, and the preconditioner as one DMMA
+ * GEMM against the explicit inverse of each Jacobi block.
+ *
+ * Collectives: the context owns an NCCL communicator (gbem_ctx_init_nccl;
+ * libnccl.so.2 is loaded at run time, so a process that already holds NCCL,
+ * e.g. through torch, shares it), or the host plugs its own (MPI, gloo ...)
+ * through gbem_collectives.  With one rank no collective is issued. */
+#define GBEM_NCCL_UNIQUE_ID_BYTES 128
+/* ncclGetUniqueId: rank 0 calls it and distributes the 128 bytes out of band. */
+int gbem_nccl_unique_id(void* id_out);
+/* Attach an NCCL communicator of nranks ranks (ncclCommInitRank) to ctx. */
+int gbem_ctx_init_nccl(gbem_ctx* ctx, int32_t nranks, int32_t rank, const void* id);
+
+/* Host-provided collectives on device buffers of doubles, called on the
+ * calling thread with the context's cudaStream_t; each returns 0 on success.
+ *   all_gather: every rank contributes `count` doubles, recv holds nranks*count
+ *               in rank order;
+ *   all_reduce_sum: in-place sum of `count` doubles. */
+typedef struct {
+  void* user;
+  int (*all_gather)(void* user, const double* send, double* recv, int64_t count, void* stream);
+  int (*all_reduce_sum)(void* user, double* buf, int64_t count, void* stream);
+} gbem_collectives;
+int gbem_ctx_set_collectives(gbem_ctx* ctx, int32_t nranks, int32_t rank, const gbem_collectives* coll);
+
+typedef struct {
+  double tol;              /* stop a column at ||b - A x|| / ||b|| <= tol (default 1e-10) */
+  int32_t max_iter;        /* default 1000 */
+  int32_t jacobi_blocks;   /* Jacobi blocks per rank (default 1: the rank's diagonal block) */
+} gbem_pcg_options;
+
+typedef struct {
+  int64_t n, rows_local, row_begin;
+  int32_t nranks, rank, iterations, converged;
+  double max_rel_resid;     /* max over columns of ||B - A X|| / ||B||, recomputed from A at the end */
+  double ms_assembly, ms_precond, ms_iterations, ms_matvec, ms_total;
+  double matvec_flops;      /* 2 rows n K per product, summed over the products of this rank */
+} gbem_pcg_stats;
+
+/* C-matrix extraction on row-block shards: every rank calls it with the same
+ * (replicated) panels and net_of_panel on its device; C (K x K) and resid (K)
+ * come out identical on every rank.  Device pointers. */
+int gbem_pcg_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P_dev, int64_t n,
+                                 const int32_t* net_of_panel, int32_t K, double eps_r,
+                                 const gbem_quad_config* cfg, const gbem_pcg_options* opt,
+                                 double* C, double* resid, gbem_assembly_stats* astats,
+                                 gbem_pcg_stats* pstats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,29 @@ class GbemSolveStats(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+AllGatherFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+AllReduceFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+class GbemCollectives(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("all_gather", AllGatherFn), ("all_reduce_sum", AllReduceFn)]
+
+
+class GbemPcgOptions(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int32), ("jacobi_blocks", C.c_int32)]
+
+
+class GbemPcgStats(C.Structure):
+    _fields_ = [("n", C.c_int64), ("rows_local", C.c_int64), ("row_begin", C.c_int64),
+                ("nranks", C.c_int32), ("rank", C.c_int32), ("iterations", C.c_int32), ("converged", C.c_int32),
+                ("max_rel_resid", C.c_double), ("ms_assembly", C.c_double), ("ms_precond", C.c_double),
+                ("ms_iterations", C.c_double), ("ms_matvec", C.c_double), ("ms_total", C.c_double),
+                ("matvec_flops", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
 # (name, restype, argtypes) for every symbol of include/gbem_gpu.h
 _P = C.c_void_p
 GPU_SYMBOLS = [
@@ -109,6 +132,12 @@ GPU_SYMBOLS = [
                                        C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats),
                                        C.POINTER(GbemSolveStats)]),
     ("gbem_debug_fill_shared", C.c_int, [_P, C.c_double]),
+    ("gbem_nccl_unique_id", C.c_int, [_P]),
+    ("gbem_ctx_init_nccl", C.c_int, [_P, C.c_int32, C.c_int32, _P]),
+    ("gbem_ctx_set_collectives", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(GbemCollectives)]),
+    ("gbem_pcg_extract_cmatrix_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, _P, C.c_int32, C.c_double,
+                                               C.POINTER(GbemQuadConfig), C.POINTER(GbemPcgOptions), _P, _P,
+                                               C.POINTER(GbemAssemblyStats), C.POINTER(GbemPcgStats)]),
     ("gbem_extract_cmatrix_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, _P, C.c_int32, C.c_double,
                                            C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats),
                                            C.POINTER(GbemSolveStats)]),

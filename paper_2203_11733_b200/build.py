@@ -33,7 +33,7 @@ NVFLAGS += os.environ.get("GBEM_NVCC_EXTRA", "").split()  # experiments only (e.
 EXTRA = {"gbem_assembly.cu": ["-fmad=false"]}
 CXXFLAGS = ["-O2", "-std=c++17", "-fPIC", "-Wall", f"-I{INCLUDE}"]
 
-CU_SOURCES = ["gbem_assembly.cu", "gbem_solver.cu", "gbem_block.cu", "gbem_selftest.cu", "gbem_capi.cu"]
+CU_SOURCES = ["gbem_assembly.cu", "gbem_solver.cu", "gbem_block.cu", "gbem_selftest.cu", "gbem_pcg.cu", "gbem_capi.cu"]
 
 
 def _run(cmd: list[str]) -> None:
@@ -69,7 +69,7 @@ def build_gpu(force: bool = False) -> Path:
         list(ex.map(_run, jobs))
     so = LIB / "libgbem_gpu.so"
     if force or jobs or _stale(so, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", str(so)] + [str(o) for o in objs] + ["-lcudart"])
+        _run([NVCC] + ARCH + ["-shared", "-o", str(so)] + [str(o) for o in objs] + ["-lcudart", "-ldl"])
     return so
 
 

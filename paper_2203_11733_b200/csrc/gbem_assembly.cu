@@ -523,8 +523,9 @@ __global__ void __launch_bounds__(1024)
 // ---------------------------------------------------------------- evaluation
 
 struct OutSpec {
-  double* A;      // matrix mode (nullptr in list mode)
+  double* A;      // matrix mode (nullptr in list mode): entry (i, j) at A[i * lda + j * ldc]
   long long lda;
+  long long ldc;
   double* out;    // list mode: out[i]
   int32_t* conv;  // list mode converged flags (may be null)
 };
@@ -534,7 +535,7 @@ __device__ __forceinline__ double panel_area(const DPanel& p) { return (p.a1 - p
 __device__ __forceinline__ void store_value(const OutSpec& o, uint32_t i, uint32_t j, const DPanel& Pi,
                                             const DPanel& Pj, double U) {
   if (o.A) {
-    o.A[(long long)i * o.lda + j] = U / (panel_area(Pi) * panel_area(Pj));
+    o.A[(long long)i * o.lda + (long long)j * o.ldc] = U / (panel_area(Pi) * panel_area(Pj));
   } else {
     o.out[i] = U;
   }
@@ -774,7 +775,7 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
     flops += 9u * nodes + 4u * (uint32_t)(m2 * m3) + 6u * (uint32_t)(M + m2 + m3) + 30u;  // per node: DADD, DMUL, 2 DFMA, DMUL, DFMA
     if (o.A) {
       // U / (4 pi area_I area_J) with one reciprocal
-      o.A[(long long)i * o.lda + j] = acc * rcp64(kFourPi * (panel_area(A) * panel_area(B)));
+      o.A[(long long)i * o.lda + (long long)j * o.ldc] = acc * rcp64(kFourPi * (panel_area(A) * panel_area(B)));
     } else {
       o.out[i] = acc * rcp64(kFourPi);
       if (o.conv) o.conv[i] = 1;
@@ -1115,7 +1116,7 @@ int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, 
 // Assemble rows [row_begin, row_end) of the upper triangle into ctx->d_A.
 int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,
                            const gbem_quad_config* cfg_in, gbem_assembly_stats* stats, bool symmetrize,
-                           double* out, int64_t ld_out, bool full_rows) {
+                           double* out, int64_t ld_out, bool full_rows, bool out_col_major) {
   gbem_quad_config cfg;
   int rc = prepare_work(ctx, cfg_in, &cfg);
   if (rc) return rc;
@@ -1146,11 +1147,16 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
   GBEM_CUDA(ctx, cudaMemcpyAsync(d_rowoff, rowoff.data(), sizeof(long long) * rowoff.size(),
                                  cudaMemcpyHostToDevice, ctx->stream));
   // destination: the context matrix (entry (i, j >= i) at A[i*lda + j]) or a
-  // caller row block (entry at out[(i - row_begin)*ld_out + j])
-  OutSpec o{ctx->d_A, (long long)ctx->lda, nullptr, nullptr};
-  if (out) {
+  // caller row block, row-major (entry at out[(i - row_begin)*ld_out + j]) or
+  // column-major (out[j*ld_out + i - row_begin], the sharded solve's layout)
+  OutSpec o{ctx->d_A, (long long)ctx->lda, 1, nullptr, nullptr};
+  if (out && !out_col_major) {
     o.A = out - row_begin * ld_out;
     o.lda = (long long)ld_out;
+  } else if (out) {
+    o.A = out - row_begin;
+    o.lda = 1;
+    o.ldc = (long long)ld_out;
   }
   const long long tiles_per_chunk = std::max<long long>(1, ctx->queue_cap / (kTile * kTile));
   float ms_cls = 0, ms_far = 0, ms_near = 0;
@@ -1246,7 +1252,7 @@ int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_confi
                                                          ctx->d_counts, ctx->d_cursors, ctx->d_queue,
                                                          ctx->d_plan);
   GBEM_LAUNCH_CHECK(ctx);
-  OutSpec o{nullptr, 0, d_out, d_conv};
+  OutSpec o{nullptr, 0, 0, d_out, d_conv};
   rc = run_eval(ctx, o, cfg, nullptr, nullptr);
   if (rc) return rc;
   return finish_stats(ctx, stats, npairs);

@@ -178,6 +178,7 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
   if (ctx->stream && ctx->stream != ctx->own_stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->pcg_release) ctx->pcg_release(ctx);
   cudaFree(ctx->d_panels);
   cudaFree(ctx->d_cinfo);
   cudaFree(ctx->d_A);

@@ -85,10 +85,18 @@ struct gbem_ctx {
   cudaEvent_t ev_gs = nullptr, ev_ge = nullptr, ev_gt = nullptr, ev_gra = nullptr;
   void* green_ctx[2] = {nullptr, nullptr};  // CUgreenCtx (side, main)
 
+  // row-block sharded solve (gbem_pcg.cu): ranks and collectives
+  int32_t nranks = 1, rank = 0;
+  void* nccl_comm = nullptr;           // ncclComm_t owned by the context (gbem_ctx_init_nccl)
+  gbem_collectives coll{};             // host-provided collectives (gbem_ctx_set_collectives)
+  bool has_coll = false;
+  void* pcg_ws = nullptr;              // sharded-solve workspace (gbem_pcg.cu)
+  void (*pcg_release)(gbem_ctx*) = nullptr;  // frees pcg_ws and the communicator
+
   // kernels whose dynamic shared-memory limit has been raised on this
   // context's device (cudaFuncSetAttribute is per device; one bit per site)
   unsigned attr_set = 0;
-  enum : unsigned { kAttrGemmSolve = 1u, kAttrFactor = 2u, kAttrGemmLU = 4u };
+  enum : unsigned { kAttrGemmSolve = 1u, kAttrFactor = 2u, kAttrGemmLU = 4u, kAttrPcgGemm = 8u };
 
   int fail(int code, const std::string& msg) {
     err = msg;
@@ -124,7 +132,8 @@ int gbem_internal_upload_panels(gbem_ctx* ctx, const gbem_panels* P, int64_t n, 
 int gbem_internal_check_pending_stats(gbem_ctx* ctx);
 int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t row_end,
                            const gbem_quad_config* cfg, gbem_assembly_stats* stats, bool symmetrize,
-                           double* out = nullptr, int64_t ld_out = 0, bool full_rows = false);
+                           double* out = nullptr, int64_t ld_out = 0, bool full_rows = false,
+                           bool out_col_major = false);
 int gbem_internal_rowblock_matvec(gbem_ctx* ctx, const double* Ab, int64_t ld, int64_t rows, int64_t n,
                                   const double* P, int64_t ldp, int64_t K, double* Q, int64_t ldq);
 int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_config* cfg,

@@ -1430,7 +1430,7 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
                                  gbem_solve_stats* stats, bool y_from_border) {
   const int n = (int)ctx->n;
   const long long lda = ctx->lda;
-  if (nrhs < 0 || nrhs > n) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, n]");
+  if (nrhs < 0 || nrhs > (1 << 20)) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, 2^20]");
   if (!ctx->factored) return ctx->fail(GBEM_EINVAL, "no factored matrix in the context");
   if (stats) stats->nrhs = nrhs;
   if (n == 0 || nrhs == 0) return GBEM_OK;
@@ -1544,7 +1544,7 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
 
 int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
                         gbem_solve_stats* stats) {
-  if (nrhs < 0 || nrhs > ctx->n) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, n]");
+  if (nrhs < 0 || nrhs > (1 << 20)) return ctx->fail(GBEM_EINVAL, "cholesky_solve: nrhs must be in [0, 2^20]");
   int rc = gbem_internal_factor(ctx, stats);
   if (rc) return rc;
   if (stats) stats->nrhs = nrhs;

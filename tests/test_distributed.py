@@ -80,7 +80,8 @@ def test_two_rank_row_blocks_reassemble(tmp_path):
 
 # --- sharded block-Jacobi PCG (paper_2203_11733_b200/pcg.py) -------------------------
 
-from paper_2203_11733_b200.pcg import Comm, block_jacobi_pcg, equal_row_split  # noqa: E402
+from paper_2203_11733_b200.pcg import equal_row_split  # noqa: E402
+from pcg_restatement import Comm, block_jacobi_pcg  # noqa: E402
 
 
 @pytest.mark.parametrize("n,world", [(0, 2), (1, 2), (7, 2), (10, 3), (1344, 8), (100000, 8)])
@@ -156,3 +157,32 @@ def test_sharded_pcg_matches_direct_solve(tmp_path, world):
     assert np.abs(X - Xd).max() <= 1e-9 * np.abs(Xd).max()
     # capacitance-style column sums agree to the solve tolerance
     np.testing.assert_allclose(X.sum(0), Xd.sum(0), rtol=1e-11)
+
+
+# --- host collectives plugged into the C-ABI (paper_2203_11733_b200/pcg.py) ------------
+
+def _coll_worker(rank, world, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2203_11733_b200.pcg import HostCollectives
+    hc = HostCollectives(device=False)
+    # the library calls the C function pointers; call them the same way
+    send = np.arange(5, dtype=np.float64) + 10 * rank
+    recv = np.zeros(5 * world)
+    assert hc.struct.all_gather(None, send.ctypes.data, recv.ctypes.data, 5, None) == 0
+    buf = np.full(3, rank + 1.0)
+    assert hc.struct.all_reduce_sum(None, buf.ctypes.data, 3, None) == 0
+    if rank == 0:
+        np.savez(out_path, recv=recv, buf=buf)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_collectives_callbacks(tmp_path, world):
+    out = str(tmp_path / "c.npz")
+    mp.spawn(_coll_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    d = np.load(out)
+    assert np.array_equal(d["recv"], np.concatenate([np.arange(5) + 10 * r for r in range(world)]))
+    assert np.array_equal(d["buf"], np.full(3, world * (world + 1) / 2))

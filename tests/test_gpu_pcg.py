@@ -1,6 +1,8 @@
-"""Sharded-solver building blocks on the GPU (paper_2203_11733_b200/pcg.py):
-full-row assembly, the row-block product, the kept factor, and the block-Jacobi
-PCG C-matrix against the direct Cholesky extraction."""
+"""Sharded solve on the GPU (gbem_pcg_extract_cmatrix_dev, csrc/gbem_pcg.cu):
+full-row assembly, the row-block product, the kept factor, the block-Jacobi
+PCG C-matrix against the direct Cholesky extraction at world size 1 (1 to 8
+Jacobi blocks), through an NCCL communicator, and with two ranks on the one
+GPU whose collectives are staged through gloo (host collectives)."""
 import ctypes as C
 
 import numpy as np
@@ -9,7 +11,7 @@ import torch
 
 import paper_2203_11733_b200 as g
 from paper_2203_11733_b200._native import PanelArrays
-from paper_2203_11733_b200.pcg import GpuRowBlockOps, sharded_cmatrix
+from paper_2203_11733_b200.pcg import equal_row_split, sharded_cmatrix
 from paper_2203_11733_b200.shard import panels_to_device
 from test_gpu_assembly import two_boxes
 
@@ -37,15 +39,23 @@ def test_full_rows_match_symmetric_assembly(ctx):
     n = len(P)
     A, _ = ctx.assemble_single(PanelArrays.from_matrix(P))
     pd = panels_to_device(PanelArrays.from_matrix(P), torch.device("cuda", 0))
-    ops = GpuRowBlockOps(ctx, pd, n, 1, 3)
+    rb, re = equal_row_split(n, 3)[1]
+    ld = ((n + 7) // 8) * 8
+    blk = torch.zeros((re - rb, ld), dtype=torch.float64, device="cuda")
+    dp = C.POINTER(C.c_double)
+    panels = g._native.GbemPanels(C.cast(C.c_void_p(pd["axis"].data_ptr()), C.POINTER(C.c_uint8)),
+                                  *[C.cast(C.c_void_p(pd[k].data_ptr()), dp) for k in ("level", "a0", "a1", "b0", "b1")])
+    st = g._native.GbemAssemblyStats()
     ctx.set_stream(torch.cuda.current_stream().cuda_stream)
-    blk = ops.assemble(with_stats=True)[:, :n].cpu().numpy()
-    ref = A[ops.row_begin:ops.row_end]
+    ctx.check(ctx.lib.gbem_assemble_rows_full_dev(ctx.h, C.byref(panels), n, rb, re, C.byref(ctx.quad()),
+                                                  C.c_void_p(blk.data_ptr()), ld, C.byref(st)))
+    blk = blk[:, :n].cpu().numpy()
+    ref = A[rb:re]
     rel = np.abs(blk - ref) / np.abs(ref)
     assert rel.max() <= 1e-13, rel.max()
-    assert ops.astats.pairs_total == ops.rows * n
+    assert st.pairs_total == (re - rb) * n
     # the upper triangle is the same computation as the symmetric path
-    iu = np.triu_indices(ops.rows, ops.row_begin, n)
+    iu = np.triu_indices(re - rb, rb, n)
     assert np.array_equal(blk[iu], ref[iu])
 
 
@@ -81,22 +91,111 @@ def test_non_spd_block_reports_pivot(ctx):
     assert "not positive definite" in ctx.lib.gbem_last_error(ctx.h).decode()
 
 
-@pytest.mark.parametrize("sub_blocks", [1, 5])
-def test_pcg_cmatrix_matches_direct(ctx, sub_blocks):
-    m = g.config_model(1, seed=1, scale=0.5)
+def _config_net(cfg, scale):
+    m = g.config_model(cfg, seed=1, scale=scale)
     ps = m.partition(1)
     ids = m.net_ids
     col = {nid: k for k, nid in enumerate(ids)}
     net = np.array([col.get(int(v), -1) if k == 0 else -1 for v, k in zip(ps.net, ps.kind)], dtype=np.int32)
-    K, eps = len(ids), m.info()["eps_r"]
+    return ps, net, len(ids), m.info()["eps_r"]
+
+
+@pytest.mark.parametrize("cfg,scale,blocks", [(1, 0.5, 1), (1, 0.5, 5), (2, 0.5, 8), (4, 0.1, 3)])
+def test_pcg_cmatrix_matches_direct(ctx, cfg, scale, blocks):
+    """C-ABI block-Jacobi PCG (1 rank, `blocks` Jacobi blocks) against the direct
+    bordered-Cholesky extraction; the true residual is recomputed from A."""
+    ps, net, K, eps = _config_net(cfg, scale)
     Cd, _, _, _ = ctx.extract_cmatrix(ps.arrays(), net, K, eps)
-    Cp, res = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-12, sub_blocks=sub_blocks)
-    assert res.converged, res.rel_resid
-    if sub_blocks == 1:
-        assert res.iterations <= 2      # one Jacobi block = the exact inverse
+    Cp, res, st, ast = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=blocks)
+    assert st.converged and st.nranks == 1 and st.rows_local == len(ps)
+    assert ast.pairs_total == len(ps) ** 2
+    if blocks == 1:
+        assert st.iterations <= 1      # one Jacobi block = the exact inverse
     else:
-        assert res.iterations > 2
+        assert st.iterations > 2
+    assert res.max() <= 1e-11 and st.max_rel_resid == res.max()
     assert np.abs(Cp - Cd).max() <= 1e-9 * np.abs(Cd).max(), np.abs(Cp - Cd).max() / np.abs(Cd).max()
+
+
+def test_pcg_iterations_match_restatement(ctx):
+    """The device recurrence takes the same number of iterations as the torch
+    restatement (tests/pcg_restatement.py) on the same matrix and blocks."""
+    import pcg_restatement as R
+    ps, net, K, eps = _config_net(1, 0.5)
+    n = len(ps)
+    A, _ = ctx.assemble_single(ps.arrays())
+    Cp, res, st, _ = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-10, jacobi_blocks=4)
+
+    class Ops:
+        m = n
+        cuts = [0] + [n * b // 4 // 8 * 8 for b in (1, 2, 3)] + [n]
+
+        def matvec(self, p):
+            return torch.from_numpy(A) @ p[:n]
+
+        def precond(self, r):
+            z = torch.empty_like(r)
+            for a, b in zip(self.cuts[:-1], self.cuts[1:]):
+                z[a:b] = torch.linalg.solve(torch.from_numpy(A[a:b, a:b]), r[a:b])
+            return z
+
+    B = torch.from_numpy((net[:, None] == np.arange(K)[None, :]).astype(float))
+    out = R.block_jacobi_pcg(Ops(), B, R.Comm(), tol=1e-10, max_iter=500)
+    assert abs(out.iterations - st.iterations) <= 1, (out.iterations, st.iterations)
+
+
+def test_pcg_with_nccl_communicator(ctx):
+    """gbem_nccl_unique_id + gbem_ctx_init_nccl (one rank): libnccl.so.2 loads at
+    run time and the context owns the communicator."""
+    uid = (C.c_uint8 * 128)()
+    ctx.check(ctx.lib.gbem_nccl_unique_id(C.cast(uid, C.c_void_p)))
+    ctx.check(ctx.lib.gbem_ctx_init_nccl(ctx.h, 1, 0, C.cast(uid, C.c_void_p)))
+    ps, net, K, eps = _config_net(1, 0.5)
+    Cd, _, _, _ = ctx.extract_cmatrix(ps.arrays(), net, K, eps)
+    Cp, res, st, _ = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=2, attach_ranks=False)
+    assert np.abs(Cp - Cd).max() <= 1e-9 * np.abs(Cd).max()
+    ctx.check(ctx.lib.gbem_ctx_set_collectives(ctx.h, 1, 0, None))
+
+
+def _two_rank_worker(rank, world, port, out):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2203_11733_b200._native import Context
+    c = Context(0)
+    ps, net, K, eps = _config_net(2, 0.5)
+    Cp, res, st, ast = sharded_cmatrix(c, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=2, collectives="host")
+    hc = c._coll_keep
+    if rank == 0:
+        np.savez(out, C=Cp, res=res, it=st.iterations, rows=st.rows_local, n=st.n,
+                 ag=hc.calls["all_gather"], ar=hc.calls["all_reduce_sum"])
+    dist.barrier()
+    c.close()
+    dist.destroy_process_group()
+
+
+def test_pcg_two_ranks_host_collectives(ctx, tmp_path):
+    """Two processes on the one GPU, each a rank of the sharded solve with its
+    own row block and Jacobi blocks; the per-iteration all-gather / all-reduce go
+    through gloo (gbem_collectives).  The C-matrix equals the direct one."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = str(tmp_path / "r0.npz")
+    mp.spawn(_two_rank_worker, args=(2, port, out), nprocs=2, join=True)
+    d = np.load(out)
+    ps, net, K, eps = _config_net(2, 0.5)
+    Cd, _, _, _ = ctx.extract_cmatrix(ps.arrays(), net, K, eps)
+    assert int(d["rows"]) == -(-len(ps) // 2) and int(d["n"]) == len(ps)
+    assert int(d["it"]) > 2 and int(d["ag"]) >= int(d["it"]) + 1 and int(d["ar"]) >= 2 * int(d["it"])
+    assert d["res"].max() <= 1e-11
+    assert np.abs(d["C"] - Cd).max() <= 1e-9 * np.abs(Cd).max()
 
 
 def test_async_mode_defers_pivot_check(ctx):
