@@ -797,6 +797,32 @@ int orc_assemble_single(int64_t n, const orc_rect* p, double rel_tol, int max_le
   return status;
 }
 
+/* ---------------- Cholesky factor in the reference's storage order ----------------
+ * solver.hpp:28-37 with L an Eigen::MatrixXd, i.e. COLUMN-major: L(r, k) at
+ * L[k * n + r], so L.row(k).head(k) walks with stride n (what the reference's
+ * CPU loop actually does; the row-major restatement below is the fast
+ * variant).  A is column-major too (symmetric, so either).  Timing only: returns
+ * 0, or 2 with *bad_pivot on a non-positive pivot. */
+int orc_cholesky_factor_colmajor(int64_t n, const double* A, double* L, int64_t* bad_pivot) {
+  for (int64_t e = 0; e < n * n; ++e) L[e] = 0.0;
+  for (int64_t k = 0; k < n; ++k) {
+    double sq = 0.0;
+    for (int64_t t = 0; t < k; ++t) sq += L[t * n + k] * L[t * n + k];
+    double d = A[k * n + k] - sq;
+    if (!(d > 0.0)) {
+      if (bad_pivot) *bad_pivot = k;
+      return 2;
+    }
+    L[k * n + k] = sqrt(d);
+    for (int64_t r = k + 1; r < n; ++r) {
+      double dot = 0.0;
+      for (int64_t t = 0; t < k; ++t) dot += L[t * n + r] * L[t * n + k];
+      L[k * n + r] = (A[k * n + r] - dot) / L[k * n + k];
+    }
+  }
+  return 0;
+}
+
 /* ---------------- Cholesky (solver.hpp:17-50) ---------------- */
 
 int orc_cholesky_solve(int64_t n, const double* A, int64_t nrhs, const double* B, double* X,

@@ -111,6 +111,10 @@ int orc_lu_solve(int64_t n, const double* A, const double* b, double* x, double*
 double orc_quad_test(int which, int mode, double a, double b, int singA, int singB,
                      int* status, int* converged, long* evals);
 
+/* solver.hpp:28-37 factor loop with Eigen's column-major L (timing of the
+ * reference's CPU order; bench.py cpu_baseline / --impl reference). */
+int orc_cholesky_factor_colmajor(int64_t n, const double* A, double* L, int64_t* bad_pivot);
+
 #ifdef __cplusplus
 }
 #endif

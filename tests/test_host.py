@@ -205,3 +205,15 @@ def test_config_panel_lists_match_golden_fixture(cfg):
     P = g.config_model(cfg, seed=fx["seed"]).partition(1).matrix()
     assert len(P) == fx["panels"]
     assert hashlib.sha256(np.ascontiguousarray(P).tobytes()).hexdigest() == fx["panels_sha256"]
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_serialised_workloads_match_generator(cfg):
+    """workloads/config*_panels.npz (what bench.py --impl reference reads) are
+    the host generator's panel lists bit for bit."""
+    import paper_2203_11733_b200 as g
+    d = np.load(ROOT / "workloads" / f"config{cfg}_panels.npz")
+    m = g.config_model(cfg, seed=1)
+    ps = m.partition(1)
+    assert np.array_equal(d["panels"], ps.matrix())
+    assert int(d["nets"]) == len(m.net_ids) and float(d["eps_r"]) == m.info()["eps_r"]

@@ -3,7 +3,7 @@
   configs 1-4: C-matrix extraction through gbem_extract_cmatrix_dev (assembly +
                DMMA Cholesky + K solves + charges), device-timed phases,
                C-matrix sanity (reciprocity, signs, residuals);
-  config 4:    additionally the row-block block-Jacobi PCG (pcg.py) with 8
+  config 4:    additionally the row-block block-Jacobi PCG (gbem_pcg_extract_cmatrix_dev) with 8
                Jacobi blocks (the 8-rank preconditioner on one GPU) against the
                direct C-matrix;
   config 5:    assembly only, streamed through 16 full-row blocks.
@@ -88,14 +88,14 @@ def pcg_vs_direct(config, Cd, blocks=8, tol=1e-10):
     ctx = N.Context(0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    Cp, res = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=tol, max_iter=2000, sub_blocks=blocks)
+    Cp, res, st, ast = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=tol, max_iter=2000, jacobi_blocks=blocks)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     rel = float(np.max(np.abs(Cp - Cd)) / np.max(np.abs(Cd)))
     ctx.close()
     torch.cuda.empty_cache()
-    return dict(config=config, jacobi_blocks=blocks, tol=tol, iterations=res.iterations, converged=res.converged,
-                max_rel_resid=float(res.rel_resid.max()), wall_s=wall, cmatrix_max_rel_diff_vs_direct=rel)
+    return dict(config=config, jacobi_blocks=blocks, tol=tol, wall_s=wall, cmatrix_max_rel_diff_vs_direct=rel,
+                matvec_tflops=st.matvec_flops / (st.ms_matvec * 1e-3) / 1e12, **st.as_dict())
 
 
 def stream_assembly(config=5, chunks=16):
