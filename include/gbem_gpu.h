@@ -190,6 +190,13 @@ typedef struct {
 } gbem_selftest_case;
 int gbem_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gbem_quad_config* cfg,
                   gbem_selftest_case* cases, int32_t* ncases);
+/* oracle_pair_integral (oracle.hpp:191-205) on the device for a pair list:
+ * recursive dyadic subdivision to `depth` (0..6) with 6^4 Gauss leaves, the
+ * single-layer kernel (double_layer = 0) or the double-layer one with source
+ * normal signs nsign[k] (+1/-1; NULL = +1).  I, J: host arrays of npairs panels;
+ * out: host, npairs values (um^3, like u_pair_integral). */
+int gbem_oracle_pair_integrals(gbem_ctx* ctx, const gbem_panels* I, const gbem_panels* J, const int32_t* nsign,
+                               int64_t npairs, int32_t double_layer, int32_t depth, double* out);
 
 /* assemble_multi (assembly.hpp:110-175, replaces gbem::assemble_multi): the
  * Galerkin block system over all dielectric regions (double-layer

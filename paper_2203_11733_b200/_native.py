@@ -132,6 +132,8 @@ GPU_SYMBOLS = [
                                        C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats),
                                        C.POINTER(GbemSolveStats)]),
     ("gbem_debug_fill_shared", C.c_int, [_P, C.c_double]),
+    ("gbem_oracle_pair_integrals", C.c_int, [_P, C.POINTER(GbemPanels), C.POINTER(GbemPanels), _P, C.c_int64,
+                                             C.c_int32, C.c_int32, _P]),
     ("gbem_nccl_unique_id", C.c_int, [_P]),
     ("gbem_ctx_init_nccl", C.c_int, [_P, C.c_int32, C.c_int32, _P]),
     ("gbem_ctx_set_collectives", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(GbemCollectives)]),
@@ -276,6 +278,17 @@ class Context:
                                            C.byref(sst) if stats else None)
         self.check(rc)
         return Cm, res, ast, sst
+
+    def oracle_pair_integrals(self, I: PanelArrays, J: PanelArrays, depth: int, double_layer: bool = False,
+                              nsign: np.ndarray | None = None) -> np.ndarray:
+        """oracle_pair_integral (oracle.hpp:191) on the device, per pair."""
+        out = np.zeros(I.n)
+        ns = None if nsign is None else np.ascontiguousarray(nsign, dtype=np.int32)
+        si, sj = I.struct(), J.struct()
+        self.check(self.lib.gbem_oracle_pair_integrals(self.h, C.byref(si), C.byref(sj),
+                                                       None if ns is None else ptr(ns), I.n,
+                                                       1 if double_layer else 0, depth, ptr(out)))
+        return out
 
     def fill_shared(self, value: float):
         """Diagnostic: leave `value` in every SM's shared memory."""

@@ -420,6 +420,13 @@ int gbem_assemble_multi(gbem_ctx* ctx, const gbem_block_panels* P, int64_t n, co
   return GBEM_OK;
 }
 
+int gbem_oracle_pair_integrals(gbem_ctx* ctx, const gbem_panels* I, const gbem_panels* J, const int32_t* nsign,
+                               int64_t npairs, int32_t double_layer, int32_t depth, double* out) {
+  if (!ctx) return GBEM_EINVAL;
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  return gbem_internal_oracle_pairs(ctx, I, J, nsign, npairs, double_layer, depth, out);
+}
+
 int gbem_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gbem_quad_config* cfg,
                   gbem_selftest_case* cases, int32_t* ncases) {
   if (!ctx) return GBEM_EINVAL;

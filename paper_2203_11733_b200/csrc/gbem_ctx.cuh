@@ -139,6 +139,8 @@ int gbem_internal_rowblock_matvec(gbem_ctx* ctx, const double* Ab, int64_t ld, i
 int gbem_internal_pair_list(gbem_ctx* ctx, int64_t npairs, const gbem_quad_config* cfg,
                             double* d_out, int32_t* d_conv, gbem_assembly_stats* stats);
 int gbem_internal_init_tables(gbem_ctx* ctx);
+int gbem_internal_oracle_pairs(gbem_ctx* ctx, const gbem_panels* I, const gbem_panels* J, const int32_t* nsign,
+                               int64_t npairs, int32_t dbl, int32_t depth, double* out);
 int gbem_internal_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gbem_quad_config* cfg,
                            gbem_selftest_case* cases, int32_t* ncases);
 int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X,

@@ -396,6 +396,47 @@ const CaseDef kCases[10] = {
 
 }  // namespace
 
+int gbem_internal_oracle_pairs(gbem_ctx* ctx, const gbem_panels* I, const gbem_panels* J, const int32_t* nsign,
+                               int64_t npairs, int32_t dbl, int32_t depth, double* out) {
+  if (npairs < 0 || npairs > (1 << 22)) return ctx->fail(GBEM_EINVAL, "npairs must be in [0, 2^22]");
+  if (depth < 0 || depth > 6) return ctx->fail(GBEM_EINVAL, "oracle depth must be in [0, 6]");
+  if (!I || !J || !out) return ctx->fail(GBEM_EINVAL, "null argument");
+  if (npairs == 0) return GBEM_OK;
+  // I then J as one 2 npairs panel list in the context's panel array
+  const size_t n = (size_t)npairs;
+  std::vector<uint8_t> ax(2 * n);
+  std::vector<double> lv(2 * n), a0(2 * n), a1(2 * n), b0(2 * n), b1(2 * n);
+  const gbem_panels* src[2] = {I, J};
+  for (int s = 0; s < 2; ++s)
+    for (size_t k = 0; k < n; ++k) {
+      ax[s * n + k] = src[s]->axis[k];
+      lv[s * n + k] = src[s]->level[k];
+      a0[s * n + k] = src[s]->a_lo[k];
+      a1[s * n + k] = src[s]->a_hi[k];
+      b0[s * n + k] = src[s]->b_lo[k];
+      b1[s * n + k] = src[s]->b_hi[k];
+    }
+  gbem_panels all{ax.data(), lv.data(), a0.data(), a1.data(), b0.data(), b1.data()};
+  int rc = gbem_internal_upload_panels(ctx, &all, 2 * npairs, false);
+  if (rc) return rc;
+  std::vector<int> ns(n, 1);
+  if (nsign)
+    for (size_t k = 0; k < n; ++k) ns[k] = nsign[k] < 0 ? -1 : 1;
+  int* d_ns = nullptr;
+  double* d_out = nullptr;
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_ns, sizeof(int) * n, ctx->stream));
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_out, sizeof(double) * n, ctx->stream));
+  GBEM_CUDA(ctx, cudaMemcpyAsync(d_ns, ns.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->stream));
+  const unsigned ob = (unsigned)((npairs + kOracleWarps - 1) / kOracleWarps);
+  k_st_oracle<<<ob, 32 * kOracleWarps, 0, ctx->stream>>>(ctx->d_panels, d_ns, (int)npairs, dbl ? 1 : 0, depth, d_out);
+  GBEM_LAUNCH_CHECK(ctx);
+  GBEM_CUDA(ctx, cudaMemcpyAsync(out, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  cudaFreeAsync(d_ns, ctx->stream);
+  cudaFreeAsync(d_out, ctx->stream);
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GBEM_OK;
+}
+
 int gbem_internal_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gbem_quad_config* cfg_in,
                            gbem_selftest_case* cases, int32_t* ncases) {
   if (pairs <= 0 || pairs > (1 << 22)) return ctx->fail(GBEM_EINVAL, "pairs per case must be in [1, 2^22]");

@@ -10,8 +10,9 @@ solve is LAPACK Cholesky (scipy; not the reference's loop order, which is
 infeasible here: ~5 h at n = 33,776) and the charges follow net_charges
 (extraction.hpp:55-79).  The file also records the reference's convergence
 diagnostics: every pair its Romberg reports as not converged (assembly.hpp:97),
-with the reference value and a tight-tolerance (relTol 1e-13) reference value,
-so the GPU can be checked on exactly the pairs the reference is unsure of.
+with the reference value, a tight-tolerance (relTol 1e-13) reference value and
+the closed-form 50-digit value (tests/exact_truth.py), so the GPU can be
+checked on exactly the pairs the reference is unsure of.
 
   python tests/golden/make_golden_big.py 3          # ~2.6 h on 8 threads
   python tests/golden/make_golden_big.py 4 0.2      # ~50 min
@@ -28,6 +29,7 @@ import scipy.linalg as sla
 HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE.parents[1]))
 sys.path.insert(0, str(HERE.parent))
+import exact_truth as E  # noqa: E402
 import oracle_lib as O  # noqa: E402
 import paper_2203_11733_b200 as g  # noqa: E402
 from make_golden import EPS0, panels_digest  # noqa: E402
@@ -60,6 +62,7 @@ def run(cfg: int, scale: float, nthreads: int):
                                 nthreads=nthreads)
     else:
         ref_v = tight = np.zeros(0)
+    exact = np.array([E.u_exact(P[i], P[j]) for i, j in keep]) if len(keep) else np.zeros(0)
     B = np.stack([(ps.kind == 0) & (ps.net == nid) for nid in ids], axis=1).astype(float)
     A_keep = A.copy()
     c, low = sla.cho_factor(A, lower=True, overwrite_a=True, check_finite=False)
@@ -72,7 +75,7 @@ def run(cfg: int, scale: float, nthreads: int):
          "net_ids": ids, "eps_r": eps, "kernel": "ref", "all_converged": nnc == 0,
          "not_converged_pairs": nnc,
          "not_converged_sample": {"ij": keep.tolist(), "ref": np.asarray(ref_v).tolist(),
-                                  "tight": np.asarray(tight).tolist()},
+                                  "tight": np.asarray(tight).tolist(), "exact": exact.tolist()},
          "cmatrix_F": Cm.tolist(), "max_residual": float(res.max()),
          "assembly_s": round(t_asm, 1), "threads": nthreads,
          "solve": "scipy LAPACK cho_factor/cho_solve (not the reference loop order)"}
@@ -87,3 +90,14 @@ if __name__ == "__main__":
     name = f"config{cfg}_cmatrix.json" if scale == 1.0 else f"config{cfg}s_cmatrix.json"
     (HERE / name).write_text(json.dumps(d, indent=1))
     print(name, d["panels"], d["cmatrix_F"][0][:2], d["max_residual"], d["not_converged_pairs"])
+
+
+def add_exact(name: str):
+    """Post-process an existing golden: closed-form values of its non-converged sample."""
+    f = HERE / name
+    d = json.loads(f.read_text())
+    m = g.config_model(d["config"], seed=d["seed"], scale=d["scale"])
+    P = m.partition(1).matrix()
+    ij = d["not_converged_sample"]["ij"]
+    d["not_converged_sample"]["exact"] = [E.u_exact(P[i], P[j]) for i, j in ij]
+    f.write_text(json.dumps(d, indent=1))

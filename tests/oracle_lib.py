@@ -260,3 +260,54 @@ def assemble_ref_diag(P: np.ndarray, nthreads=8, rel_tol=1e-8, max_levels=16, nc
     st = f(n, rp, rel_tol, max_levels, A.ctypes.data, nc.ctypes.data, nc_cap, C.byref(cnt), nthreads, cb)
     k = min(cnt.value, nc_cap)
     return A, nc[:k].copy(), int(cnt.value), st
+
+
+def flatten_scene(model_text: str):
+    """Scene text (model_io.hpp grammar) -> the flat arrays the _ref entry points
+    take: dom[6], regions (id, eps, lo, hi) x 8, cells (net, lo, hi) x 7, bc[6]."""
+    lines = [l.split("#")[0].split() for l in model_text.splitlines()]
+
+    def pt(tok):
+        return [float(v) for v in tok[tok.index("(") + 1:-1].split(",")]
+    dom = None
+    regs, cells, bc = [], [], [0] * 6
+    faces = {"-x": 0, "+x": 1, "-y": 2, "+y": 3, "-z": 4, "+z": 5}
+    for t in lines:
+        if not t:
+            continue
+        if t[0] == "domain":
+            dom = pt(t[1]) + pt(t[2])
+        elif t[0] == "region":
+            regs += [float(t[1]), float(t[2])] + pt(t[3]) + pt(t[4])
+        elif t[0] == "net":
+            cells += [float(t[1])] + pt(t[3]) + pt(t[4])
+        elif t[0] == "bc":
+            bc[faces[t[1]]] = 1 if t[2] == "neumann" else 0
+    return (np.array(dom, dtype=float), np.array(regs, dtype=float), np.array(cells, dtype=float),
+            np.array(bc, dtype=np.int32))
+
+
+REF_GPU_SO = ROOT / "oracle" / "_ref" / "libgbem_ref_gpu.so"
+
+
+def ref_gpu_capacitance_row(model_text: str, main_net: int, params, rel_tol=1e-8, max_levels=16):
+    """capacitance_row through the reference-side GPU binding (oracle/ref_gpu_backend.cpp):
+    returns (charges per net in ascending id order, outer charge, panels, residual, converged)."""
+    lib = C.CDLL(str(REF_GPU_SO))
+    f = lib.refgpu_capacitance_row
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                  C.c_double, C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                  C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_char_p, C.c_int]
+    dom, regs, cells, bc = flatten_scene(model_text)
+    par = np.array(params, dtype=float)
+    q = np.zeros(256)
+    outer, res = C.c_double(0), C.c_double(0)
+    npan, conv = C.c_int64(0), C.c_int(0)
+    err = C.create_string_buffer(512)
+    k = f(dom.ctypes.data, len(regs) // 8, regs.ctypes.data, len(cells) // 7, cells.ctypes.data, bc.ctypes.data,
+          par.ctypes.data, main_net, rel_tol, max_levels, q.ctypes.data, 256, C.byref(outer), C.byref(npan),
+          C.byref(res), C.byref(conv), err, 512)
+    if k < 0:
+        raise RuntimeError(f"refgpu_capacitance_row: {err.value.decode()} ({k})")
+    return q[:k], outer.value, npan.value, res.value, bool(conv.value)

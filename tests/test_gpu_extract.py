@@ -173,3 +173,28 @@ def test_extract_more_than_64_nets(ctx):
     Cref = 3.9 * 8.854187817e-12 * 1e-6 * Bm.T @ np.linalg.solve(A, Bm)
     assert np.abs(Cm - Cref).max() <= 1e-9 * np.abs(Cref).max()
     assert res.max() <= 1e-10
+
+
+@pytest.mark.skipif(not O.REF_GPU_SO.exists(), reason="oracle/_ref/libgbem_ref_gpu.so not built")
+def test_reference_side_binding_reproduces_readme():
+    """INTEGRATION.md's gbem::GpuBackend compiled against the unmodified reference
+    headers (oracle/ref_gpu_backend.cpp): the reference's own Scene and
+    partition_scene (partition.hpp:214) per main net, assemble + Cholesky through
+    gbem_assemble_single / gbem_spd_solve, net_charges restated — the README
+    capacitance matrix (proj/README.md:78-84) and the host path's rows."""
+    text = BENCH.read_text()
+    m = g.parse_model(text)
+    p = m.params
+    params = (p["p1"], p["p2"], p["p3"], p["p5"]) if isinstance(p, dict) else tuple(p)
+    rows, panels = [], []
+    for net in (1, 2):
+        q, outer, npan, res, conv = O.ref_gpu_capacitance_row(text, net, params)
+        rows.append(q)
+        panels.append(npan)
+        assert res <= 1e-10 and outer < 0
+    Cb = np.array(rows)
+    assert panels == [83, 56]
+    assert np.all(np.abs(Cb - README_C) <= 5e-9 * np.abs(README_C)), Cb
+    _, js = m.extract(net=-1, mode=0)
+    Ch = np.array([[js["rows"][r]["capacitance"][str(k)] for k in (1, 2)] for r in range(2)])
+    assert np.all(np.abs(Cb - Ch) <= 1e-9 * np.abs(Ch))  # same panels, different summation order of the charges
