@@ -564,6 +564,16 @@ __device__ __forceinline__ double rcp64(double x) {
 // relative error <= 1.3e-12 per node (tools/rsq_acc.cu), an order below the
 // far-field rule's own 1e-12 tolerance and 100x inside the 1e-10 gate;
 // 5 FP64-pipe instructions + MUFU instead of 6 for the Householder form.
+// acc + W y (3 - x y^2): twice W / sqrt(x) after one Newton step from the
+// MUFU.RSQ64H seed (the step wrsq_acc folds differently; the factor 1/2 is
+// applied once per pair): DADD, DMUL, DFMA, DMUL, DFMA per node -- one
+// FP64-pipe instruction fewer than wrsq_acc's form.
+__device__ __forceinline__ double wrsq3_acc(double W, double x, double acc) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e3 = fma(-(x * y), y, 3.0);
+  return fma(W * y, e3, acc);
+}
 __device__ __forceinline__ double wrsq_acc(double W, double x, double acc) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -741,6 +751,7 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
     double w1[M], W1[M];
     {
       // the inner list goes through the middle list's slots into registers
+      // (a direct per-node register emission was 6% slower: code size)
       FarList L;
       far_list(code, s0, A, B, L);
       emit_list<kFarThreads>(L, sgx, sgw, w2s, W2s);
@@ -763,16 +774,17 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
         double t0 = 0.0, t1 = 0.0;
 #pragma unroll
         for (int a = 0; a < M; a += 2) {
-          t0 = wrsq_acc(W1[a], r2 + w1[a], t0);
-          if (a + 1 < M) t1 = wrsq_acc(W1[a + 1], r2 + w1[a + 1], t1);
+          t0 = wrsq3_acc(W1[a], r2 + w1[a], t0);
+          if (a + 1 < M) t1 = wrsq3_acc(W1[a + 1], r2 + w1[a + 1], t1);
         }
         acc = fma(W3 * W2s[b * kFarThreads], t0 + t1, acc);
       }
     }
+    acc *= 0.5;  // the Newton step's 1/2 (wrsq3_acc)
     // counters in integer arithmetic (off the FP64 pipe)
     const uint32_t nodes = (uint32_t)(M * m2 * m3);
     evals += nodes;
-    flops += 9u * nodes + 4u * (uint32_t)(m2 * m3) + 6u * (uint32_t)(M + m2 + m3) + 30u;  // per node: DADD, DMUL, 2 DFMA, DMUL, DFMA
+    flops += 7u * nodes + 4u * (uint32_t)(m2 * m3) + 6u * (uint32_t)(M + m2 + m3) + 31u;  // per node: DADD, DMUL, DFMA, DMUL, DFMA
     if (o.A) {
       // U / (4 pi area_I area_J) with one reciprocal
       o.A[(long long)i * o.lda + (long long)j * o.ldc] = acc * rcp64(kFourPi * (panel_area(A) * panel_area(B)));

@@ -42,15 +42,15 @@
 
 #include "gbem_ctx.cuh"
 #include "gbem_dmma_gemm.cuh"
+#include "gbem_gemm_sk.cuh"
 
 namespace {
 
 using gbem_gemm::BK;
-using gbem_gemm::cp_async16;
-using gbem_gemm::cp_async8;
-using gbem_gemm::cp_async_commit;
-using gbem_gemm::cp_async_wait;
-using gbem_gemm::dmma;
+using gbem_sk::k_gemm_nt_sk;
+using gbem_sk::kSmem;
+using gbem_sk::kT;
+using gbem_sk::kThreads;
 
 // ---------------------------------------------------------------- NCCL, loaded at run time
 struct NcclApi {
@@ -123,99 +123,6 @@ int coll_all_reduce(gbem_ctx* ctx, double* buf, int64_t count) {
   } else
     return ctx->fail(GBEM_EINVAL, "no collectives attached for nranks > 1");
   return GBEM_OK;
-}
-
-// ---------------------------------------------------------------- split-K NT DMMA GEMM
-// C_z (M x N) = A (M x Kz) * B (N x Kz)^T over the z-th slice of the reduction
-// dimension, all column-major: A(i, k) = A[k * lda + i], B(j, k) = B[k * ldb + j],
-// C_z(i, j) = C[z * strideC + j * ldc + i].  64 x 64 tiles, 2 x 2 warps of
-// 32 x 32 (4 x 4 DMMA m8n8k4 fragments each), 4 CTAs per SM, BK = 16 slabs in
-// a STG-stage cp.async ring.  16-byte copies need even lda / ldb and 16-byte
-// aligned bases (vec16), else 8-byte copies.
-constexpr int kT = 64, kThreads = 128, kSTG = 3;
-constexpr int kLA = kT + 8;  // slab row stride: conflict-free fragment loads
-constexpr int kSlab = BK * kLA;
-constexpr size_t kSmem = (size_t)kSTG * 2 * kSlab * sizeof(double);
-
-__global__ void __launch_bounds__(kThreads, 4)
-    k_gemm_nt_sk(double* __restrict__ C, long long ldc, long long strideC, const double* __restrict__ A,
-                 long long lda, const double* __restrict__ B, long long ldb, int M, int N, long long Ktot,
-                 long long kchunk, int vec16) {
-  extern __shared__ __align__(16) double smem[];
-  const int m0 = blockIdx.x * kT, n0 = blockIdx.y * kT;
-  const long long kbeg = (long long)blockIdx.z * kchunk;
-  const long long kend = min(Ktot, kbeg + kchunk);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp & 1, wn = warp >> 1;
-  const int g = lane >> 2, t4 = lane & 3;
-  auto load = [&](long long kt, int buf) {
-    const long long k0 = kbeg + kt * BK;
-    double* as = smem + (size_t)buf * 2 * kSlab;
-    double* bs = as + kSlab;
-#pragma unroll
-    for (int c = tid; c < BK * kT / 2; c += kThreads) {
-      const int kk = c / (kT / 2), xx = (c % (kT / 2)) * 2;
-      const long long gk = k0 + kk;
-      const int gm = m0 + xx, gn = n0 + xx;
-      if (vec16) {
-        const bool oka = gk < kend && gm < M, okb = gk < kend && gn < N;
-        cp_async16(as + kk * kLA + xx, oka ? A + gk * lda + gm : A, oka ? (gm + 1 < M ? 16 : 8) : 0);
-        cp_async16(bs + kk * kLA + xx, okb ? B + gk * ldb + gn : B, okb ? (gn + 1 < N ? 16 : 8) : 0);
-      } else {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const bool oka = gk < kend && gm + e < M, okb = gk < kend && gn + e < N;
-          cp_async8(as + kk * kLA + xx + e, oka ? A + gk * lda + gm + e : A, oka ? 8 : 0);
-          cp_async8(bs + kk * kLA + xx + e, okb ? B + gk * ldb + gn + e : B, okb ? 8 : 0);
-        }
-      }
-    }
-  };
-  double acc[4][4][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const long long KT = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-#pragma unroll
-  for (int s = 0; s < kSTG - 1; ++s) {
-    if (s < KT) load(s, s);
-    cp_async_commit();
-  }
-  for (long long kt = 0; kt < KT; ++kt) {
-    if (kt + kSTG - 1 < KT) load(kt + kSTG - 1, (int)((kt + kSTG - 1) % kSTG));
-    cp_async_commit();
-    cp_async_wait<kSTG - 1>();
-    __syncthreads();
-    const double* as = smem + (size_t)(kt % kSTG) * 2 * kSlab;
-    const double* bs = as + kSlab;
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[4], bf[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = as[(kk + t4) * kLA + wm * 32 + i * 8 + g];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = bs[(kk + t4) * kLA + wn * 32 + j * 8 + g];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-    __syncthreads();
-  }
-  double* Cz = C + (long long)blockIdx.z * strideC;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int row = m0 + wm * 32 + i * 8 + g;
-    if (row >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int col = n0 + wn * 32 + j * 8 + 2 * t4 + e;
-        if (col < N) Cz[(long long)col * ldc + row] = acc[i][j][e];
-      }
-  }
 }
 
 // ---------------------------------------------------------------- CG vector kernels
@@ -464,7 +371,7 @@ int gemm_nt(gbem_ctx* ctx, double* C, long long ldc, long long strideC, const do
             const double* B, long long ldb, int M, int N, long long Ktot, int S) {
   static_assert(kSmem <= 227 * 1024, "smem");
   if (!(ctx->attr_set & gbem_ctx::kAttrPcgGemm)) {
-    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt_sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt_sk<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     ctx->attr_set |= gbem_ctx::kAttrPcgGemm;
   }
   long long kchunk = (Ktot + S - 1) / S;
@@ -473,19 +380,25 @@ int gemm_nt(gbem_ctx* ctx, double* C, long long ldc, long long strideC, const do
   for (int m0 = 0; m0 < M; m0 += kT) {
     const int mm = std::min(kT, M - m0);
     dim3 grid(1, (unsigned)((N + kT - 1) / kT), (unsigned)S);
-    k_gemm_nt_sk<<<grid, kThreads, kSmem, ctx->stream>>>(C + m0, ldc, strideC, A + m0, lda, B, ldb, mm, N, Ktot,
-                                                        kchunk, vec16 && (m0 % 2 == 0));
+    k_gemm_nt_sk<64><<<grid, kThreads, kSmem, ctx->stream>>>(C + m0, ldc, strideC, A + m0, lda, B, ldb, mm, N,
+                                                            Ktot, kchunk, vec16 && (m0 % 2 == 0));
     GBEM_LAUNCH_CHECK(ctx);
   }
   return GBEM_OK;
 }
 
-// split count that fills ~4 CTAs on every SM for `tiles` output tiles
+// Split count of the reduction dimension: at least ~2.2 waves of CTAs (a
+// single partial wave leaves SMs with unequal CTA counts) and at least 4 slices
+// of a large product (a shorter tail wave), each slice >= 32 BK steps.
+// tools/pcg_gemm_bench.cu at Kp = 64, n = 96,200: rows 12,032 -> S = 7
+// (30.2 TFLOP/s vs 27.4 at S = 3); rows 96,200 -> S = 4 (31.8 vs 28.7 at S = 1).
 int splits_for(gbem_ctx* ctx, long long tiles, long long Ktot) {
   const long long slots = 4LL * ctx->num_sms;
-  long long s = std::max<long long>(1, slots / std::max<long long>(1, tiles));
-  s = std::min<long long>(s, std::max<long long>(1, Ktot / 512));  // >= 32 BK steps per slice
-  return (int)std::min<long long>(s, 16);
+  tiles = std::max<long long>(1, tiles);
+  const long long target = std::max<long long>(22 * slots / 10, 4 * tiles);
+  long long s = (target + tiles - 1) / tiles;
+  s = std::min<long long>(s, std::max<long long>(1, Ktot / 512));
+  return (int)std::max<long long>(1, std::min<long long>(s, 8));
 }
 
 }  // namespace

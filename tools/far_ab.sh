@@ -1,2 +1,8 @@
-# bench twice, far/assembly phases
-for k in 1 2; do python bench.py --no-cpu-baseline --steps 8 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); p=d['phases_ms']; print(round(d['ms_per_step'],3), round(p['far_ms'],3), round(p['assembly_ms'],3), round(p['factor_ms'],3))"; done
+#!/bin/bash
+# far-field timing on configs 2 and 3 (assembly phases of one instrumented extraction step)
+for c in 2 3; do
+  python bench.py --config $c --steps 3 --warmup 2 --no-sharded --no-cpu-baseline | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); p=d['phases_ms']
+r=d['roofline'] if d['roofline']['kernel']=='k_far' else d['roofline_secondary']
+print('config', d['config']['panels'], 'step', round(d['ms_per_step'],2), 'far', round(p['far_ms'],3), 'near', round(p['near_ms'],3), 'classify', round(p['classify_ms'],3), 'factor', round(p['factor_ms'],2), 'far_frac', round(r['frac'],4))"
+done
