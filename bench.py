@@ -366,7 +366,7 @@ def sharded_extract_steps(ctx, P, net, K, eps, warmup, steps, world, jacobi_rows
     def step():
         ctx.check(ctx.lib.gbem_pcg_extract_cmatrix_dev(ctx.h, C.byref(panels), n, C.c_void_p(d_net.data_ptr()), K,
                                                        eps, C.byref(cfg), C.byref(opt), C.c_void_p(d_C.data_ptr()),
-                                                       C.c_void_p(d_res.data_ptr()), C.byref(ast), C.byref(pst)))
+                                                       C.c_void_p(d_res.data_ptr()), None, C.byref(ast), C.byref(pst)))
 
     for _ in range(warmup):
         step()
@@ -395,8 +395,8 @@ def sharded_extract_steps(ctx, P, net, K, eps, warmup, steps, world, jacobi_rows
         dist.barrier(group)
     t0 = time.perf_counter()
     for _ in range(max(1, steps // 2)):
-        Cm, res, st2, _ = sharded_cmatrix(ctx, Pa, net, K, eps, tol=1e-10, max_iter=2000, jacobi_blocks=jb,
-                                          attach_ranks=False)
+        Cm, res, _, st2, _ = sharded_cmatrix(ctx, Pa, net, K, eps, tol=1e-10, max_iter=2000, jacobi_blocks=jb,
+                                             attach_ranks=False)
     e2e_s = (time.perf_counter() - t0) / max(1, steps // 2)
     if world > 1:
         tt = torch.tensor([e2e_s], device=dev)

@@ -326,13 +326,23 @@ typedef struct {
 } gbem_pcg_stats;
 
 /* C-matrix extraction on row-block shards: every rank calls it with the same
- * (replicated) panels and net_of_panel on its device; C (K x K) and resid (K)
- * come out identical on every rank.  Device pointers. */
+ * (replicated) panels and net_of_panel (net -1: grounded outer panels); C (K x K),
+ * resid (K) and outer (K: the charge on the net -1 panels per row, may be NULL)
+ * come out identical on every rank.  Device pointers; the _dev variant is
+ * stream-ordered apart from the convergence polling. */
 int gbem_pcg_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P_dev, int64_t n,
                                  const int32_t* net_of_panel, int32_t K, double eps_r,
                                  const gbem_quad_config* cfg, const gbem_pcg_options* opt,
-                                 double* C, double* resid, gbem_assembly_stats* astats,
+                                 double* C, double* resid, double* outer, gbem_assembly_stats* astats,
                                  gbem_pcg_stats* pstats);
+/* Host-buffer variant (panels, net_of_panel, C, resid, outer in host memory). */
+int gbem_pcg_extract_cmatrix(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net_of_panel,
+                             int32_t K, double eps_r, const gbem_quad_config* cfg, const gbem_pcg_options* opt,
+                             double* C, double* resid, double* outer, gbem_assembly_stats* astats,
+                             gbem_pcg_stats* pstats);
+/* Ranks attached to the context (1 until gbem_ctx_init_nccl / gbem_ctx_set_collectives). */
+int32_t gbem_ctx_nranks(const gbem_ctx* ctx);
+int32_t gbem_ctx_rank(const gbem_ctx* ctx);
 
 #ifdef __cplusplus
 }

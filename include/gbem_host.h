@@ -60,6 +60,16 @@ typedef struct {
   double* cap_out;         /* NULL or rows x nets, full precision (farads), rows in solve order */
   double* outer_out;       /* NULL or per-row induced charge on the outer boundary */
   int32_t collocation;     /* 1: the collocation baseline (--baseline collocation, cli.hpp:37-38) */
+  /* shared mode (mode 1) only: the solver.  0 auto (block-Jacobi PCG on row
+   * shards when the context has several ranks, else the direct DMMA Cholesky),
+   * 1 direct, 2 PCG (also at one rank).  Ranks: nranks > 1 attaches an NCCL
+   * communicator (rank 0 writes the unique id to nccl_id_file, the others read
+   * it); only rank 0 fills csv / json. */
+  int32_t solver;
+  int32_t nranks, rank;
+  const char* nccl_id_file;
+  int32_t jacobi_blocks;   /* Jacobi blocks per rank (PCG; 0 = 1) */
+  double pcg_tol;          /* 0 = 1e-10 */
 } gbem_extract_opts;
 
 int gbem_model_extract(const gbem_model* m, const gbem_extract_opts* o, char* csv, int64_t csv_cap,

@@ -138,8 +138,13 @@ GPU_SYMBOLS = [
     ("gbem_ctx_init_nccl", C.c_int, [_P, C.c_int32, C.c_int32, _P]),
     ("gbem_ctx_set_collectives", C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(GbemCollectives)]),
     ("gbem_pcg_extract_cmatrix_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, _P, C.c_int32, C.c_double,
-                                               C.POINTER(GbemQuadConfig), C.POINTER(GbemPcgOptions), _P, _P,
+                                               C.POINTER(GbemQuadConfig), C.POINTER(GbemPcgOptions), _P, _P, _P,
                                                C.POINTER(GbemAssemblyStats), C.POINTER(GbemPcgStats)]),
+    ("gbem_pcg_extract_cmatrix", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, _P, C.c_int32, C.c_double,
+                                           C.POINTER(GbemQuadConfig), C.POINTER(GbemPcgOptions), _P, _P, _P,
+                                           C.POINTER(GbemAssemblyStats), C.POINTER(GbemPcgStats)]),
+    ("gbem_ctx_nranks", C.c_int32, [_P]),
+    ("gbem_ctx_rank", C.c_int32, [_P]),
     ("gbem_extract_cmatrix_dev", C.c_int, [_P, C.POINTER(GbemPanels), C.c_int64, _P, C.c_int32, C.c_double,
                                            C.POINTER(GbemQuadConfig), _P, _P, C.POINTER(GbemAssemblyStats),
                                            C.POINTER(GbemSolveStats)]),

@@ -205,7 +205,9 @@ HOST_SYMBOLS = ["gbem_model_parse", "gbem_model_config", "gbem_model_free", "gbe
 class ExtractOpts(C.Structure):
     _fields_ = [("device", C.c_int32), ("mode", C.c_int32), ("net", C.c_int32), ("rel_tol", C.c_double),
                 ("max_levels", C.c_int32), ("dump_matrix", C.c_char_p), ("cap_out", C.c_void_p),
-                ("outer_out", C.c_void_p), ("collocation", C.c_int32)]
+                ("outer_out", C.c_void_p), ("collocation", C.c_int32), ("solver", C.c_int32),
+                ("nranks", C.c_int32), ("rank", C.c_int32), ("nccl_id_file", C.c_char_p),
+                ("jacobi_blocks", C.c_int32), ("pcg_tol", C.c_double)]
 
 
 @dataclass
@@ -314,8 +316,10 @@ class Model:
         return PanelSet(**arrs, main_net=main_net)
 
     def extract(self, net: int = -1, mode: int = 0, device: int = 0, dump_matrix: str | None = None,
-                rel_tol: float = 1e-8, max_levels: int = 16, baseline: str | None = None) -> tuple[str, dict]:
+                rel_tol: float = 1e-8, max_levels: int = 16, baseline: str | None = None, solver: int = 0,
+                jacobi_blocks: int = 1, pcg_tol: float = 1e-10) -> tuple[str, dict]:
         """Run capacitance_matrix (net=-1) or capacitance_row; returns (csv, json dict).
+        Shared mode (mode=1): solver 0 auto / 1 direct / 2 block-Jacobi PCG.
         Full-precision values are left in self.last_cap (rows x nets) / self.last_outer."""
         ids = self.net_ids
         rows = 1 if net >= 0 else len(ids)
@@ -324,7 +328,8 @@ class Model:
         if baseline not in (None, "collocation"):
             raise ValidationError("baseline must be 'collocation'")
         o = ExtractOpts(device, mode, net, rel_tol, max_levels, dump_matrix.encode() if dump_matrix else None,
-                        self.last_cap.ctypes.data, self.last_outer.ctypes.data, 1 if baseline else 0)
+                        self.last_cap.ctypes.data, self.last_outer.ctypes.data, 1 if baseline else 0, solver,
+                        1, 0, None, jacobi_blocks, pcg_tol)
         cap = 1 << 20
         csv, js = C.create_string_buffer(cap), C.create_string_buffer(cap)
         cl, jl = C.c_int64(), C.c_int64()

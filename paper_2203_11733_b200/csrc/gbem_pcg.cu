@@ -294,14 +294,19 @@ __global__ void k_identity(double* I, long long m) {
     I[e] = (e / m == e % m) ? 1.0 : 0.0;
 }
 
-// Ct[r * K + k] += scale * X(i, r) for the local rows i with net(row_begin + i) = k
+// Ct[r * K + k] += scale * X(i, r) for the local rows i with net(row_begin + i) = k;
+// panels with net -1 (grounded outer panels) add to the outer charge Ct[K * K + r]
+// (net_charges, extraction.hpp:55-79)
 __global__ void k_rank_charges(const int32_t* __restrict__ net, long long row_begin, long long rows, int K, int Kp,
                                const double* __restrict__ X, double scale, double* Ct) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < rows * K; e += (long long)gridDim.x * blockDim.x) {
     const long long i = e / K;
     const int r = (int)(e % K);
     const int k = net[row_begin + i];
-    if (k >= 0 && k < K) atomicAdd(&Ct[(long long)r * K + k], scale * X[i * Kp + r]);
+    if (k >= 0 && k < K)
+      atomicAdd(&Ct[(long long)r * K + k], scale * X[i * Kp + r]);
+    else
+      atomicAdd(&Ct[(long long)K * K + r], scale * X[i * Kp + r]);
   }
 }
 
@@ -453,14 +458,13 @@ int gbem_ctx_set_collectives(gbem_ctx* ctx, int32_t nranks, int32_t rank, const 
   return GBEM_OK;
 }
 
-int gbem_pcg_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net, int32_t K,
-                                 double eps_r, const gbem_quad_config* cfg, const gbem_pcg_options* opt_in,
-                                 double* C_out, double* resid_out, gbem_assembly_stats* astats,
-                                 gbem_pcg_stats* pstats) {
-  if (!ctx) return GBEM_EINVAL;
-  if (!P || !net || !C_out || n <= 0) return ctx->fail(GBEM_EINVAL, "null argument or empty panel set");
-  if (K < 1 || K > 2048) return ctx->fail(GBEM_EINVAL, "K must be in [1, 2048]");
-  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+}  // extern "C"
+
+namespace {
+
+int pcg_extract(gbem_ctx* ctx, const gbem_panels* P, bool device_panels, int64_t n, const int32_t* net, int32_t K,
+                double eps_r, const gbem_quad_config* cfg, const gbem_pcg_options* opt_in, double* C_out,
+                double* resid_out, double* outer_out, gbem_assembly_stats* astats, gbem_pcg_stats* pstats) {
   gbem_pcg_options opt{1e-10, 1000, 1};
   if (opt_in) {
     if (opt_in->tol > 0) opt.tol = opt_in->tol;
@@ -489,7 +493,7 @@ int gbem_pcg_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n,
   // --- 1. assembly of complete rows, no communication (column-major m x n)
   rc = grow(ctx, &w->A, &w->cap_A, (size_t)mA * (size_t)n);
   if (rc) return rc;
-  rc = gbem_internal_upload_panels(ctx, P, n, true);
+  rc = gbem_internal_upload_panels(ctx, P, n, device_panels);
   if (rc) return rc;
   cudaEventRecord(w->ev[0], s);
   if (rows > 0) {
@@ -539,12 +543,12 @@ int gbem_pcg_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n,
   const int S_max = std::max(S_mv, S_pc);
   rc = grow(ctx, &w->part, &w->cap_part, (size_t)S_max * (size_t)cnt);
   if (rc) return rc;
-  rc = grow(ctx, &w->sc, &w->cap_sc, (size_t)(S_COUNT + 1) * Kp + (size_t)K * K);
+  rc = grow(ctx, &w->sc, &w->cap_sc, (size_t)(S_COUNT + 1) * Kp + (size_t)K * K + K);
   if (rc) return rc;
   double* sc = w->sc;
   double* rres = sc + S_COUNT * Kp;
   double* Ct = rres + Kp;
-  GBEM_CUDA(ctx, cudaMemsetAsync(sc, 0, sizeof(double) * ((size_t)(S_COUNT + 1) * Kp + (size_t)K * K), s));
+  GBEM_CUDA(ctx, cudaMemsetAsync(sc, 0, sizeof(double) * ((size_t)(S_COUNT + 1) * Kp + (size_t)K * K + K), s));
   GBEM_CUDA(ctx, cudaMemsetAsync(vZ, 0, sizeof(double) * 3 * (size_t)cnt, s));  // Z, P, Q
   const unsigned vgrid = (unsigned)std::min<long long>((cnt + 255) / 256, 8LL * ctx->num_sms);
   const size_t red1 = sizeof(double) * Kp, red2 = 2 * red1;
@@ -649,9 +653,11 @@ int gbem_pcg_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n,
         net, rb, rows, K, Kp, vX, eps_r * 8.854187817e-12 * 1e-6, Ct);
     GBEM_LAUNCH_CHECK(ctx);
   }
-  rc = coll_all_reduce(ctx, Ct, (int64_t)K * K);
+  rc = coll_all_reduce(ctx, Ct, (int64_t)K * K + K);
   if (rc) return rc;
   GBEM_CUDA(ctx, cudaMemcpyAsync(C_out, Ct, sizeof(double) * K * K, cudaMemcpyDeviceToDevice, s));
+  if (outer_out)
+    GBEM_CUDA(ctx, cudaMemcpyAsync(outer_out, Ct + (size_t)K * K, sizeof(double) * K, cudaMemcpyDeviceToDevice, s));
   double* dres = resid_out;
   if (!dres) dres = rres;  // in place (Kp >= K)
   k_finish_resid<<<1, 256, 0, s>>>(rres, sc, K, Kp, dres);
@@ -691,5 +697,52 @@ int gbem_pcg_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n,
   (void)mv_flops;
   return GBEM_OK;
 }
+
+}  // namespace
+
+extern "C" {
+
+int gbem_pcg_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net, int32_t K,
+                                 double eps_r, const gbem_quad_config* cfg, const gbem_pcg_options* opt,
+                                 double* C, double* resid, double* outer, gbem_assembly_stats* astats,
+                                 gbem_pcg_stats* pstats) {
+  if (!ctx) return GBEM_EINVAL;
+  if (!P || !net || !C || n <= 0) return ctx->fail(GBEM_EINVAL, "null argument or empty panel set");
+  if (K < 1 || K > 2048) return ctx->fail(GBEM_EINVAL, "K must be in [1, 2048]");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  return pcg_extract(ctx, P, true, n, net, K, eps_r, cfg, opt, C, resid, outer, astats, pstats);
+}
+
+int gbem_pcg_extract_cmatrix(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net, int32_t K,
+                             double eps_r, const gbem_quad_config* cfg, const gbem_pcg_options* opt, double* C,
+                             double* resid, double* outer, gbem_assembly_stats* astats, gbem_pcg_stats* pstats) {
+  if (!ctx) return GBEM_EINVAL;
+  if (!P || !net || !C || n <= 0) return ctx->fail(GBEM_EINVAL, "null argument or empty panel set");
+  if (K < 1 || K > 2048) return ctx->fail(GBEM_EINVAL, "K must be in [1, 2048]");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int32_t* d_net = nullptr;
+  double* d_out = nullptr;
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_net, sizeof(int32_t) * n, ctx->stream));
+  GBEM_CUDA(ctx, cudaMallocAsync(&d_out, sizeof(double) * ((size_t)K * K + 2 * K), ctx->stream));
+  GBEM_CUDA(ctx, cudaMemcpyAsync(d_net, net, sizeof(int32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = pcg_extract(ctx, P, false, n, d_net, K, eps_r, cfg, opt, d_out, d_out + (size_t)K * K,
+                       d_out + (size_t)K * K + K, astats, pstats);
+  if (rc == GBEM_OK || ctx->err.find("did not reach") != std::string::npos) {
+    GBEM_CUDA(ctx, cudaMemcpyAsync(C, d_out, sizeof(double) * K * K, cudaMemcpyDeviceToHost, ctx->stream));
+    if (resid)
+      GBEM_CUDA(ctx, cudaMemcpyAsync(resid, d_out + (size_t)K * K, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    if (outer)
+      GBEM_CUDA(ctx, cudaMemcpyAsync(outer, d_out + (size_t)K * K + K, sizeof(double) * K, cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+  }
+  cudaFreeAsync(d_net, ctx->stream);
+  cudaFreeAsync(d_out, ctx->stream);
+  GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return rc;
+}
+
+int32_t gbem_ctx_nranks(const gbem_ctx* ctx) { return ctx ? ctx->nranks : 0; }
+int32_t gbem_ctx_rank(const gbem_ctx* ctx) { return ctx ? ctx->rank : -1; }
 
 }  // extern "C"

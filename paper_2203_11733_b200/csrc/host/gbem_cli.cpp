@@ -6,6 +6,8 @@
 //                [--format csv|json] [--output P] [--dump-matrix P]
 //                [--mode per-net|shared] [--uniform H | --graded H0,R,HMAX] [--device D]
 //                [--baseline collocation]
+//                [--solver auto|direct|pcg] [--jacobi-blocks B] [--pcg-tol X]
+//                [--ranks N --rank R --nccl-id FILE]   (shared mode on row-block shards, one process per GPU)
 //   gbem validate --input F
 //   gbem kernels selftest [--pairs N] [--seed S] [--device D]   (cli.hpp:48-75, on the GPU)
 //   gbem config --id N [--seed S] [--scale X]      (prints the config scene + panel count)
@@ -134,8 +136,8 @@ int main(int argc, char** argv) {
     return 0;
   }
   if (cmd != "extract") return usage(("unknown subcommand " + cmd).c_str());
-  std::string in, out, format = "csv", dump, mode = "per-net", v, baseline;
-  double p[4] = {-1, -1, -1, -1}, netd = -1, dev = 0, uni = -1;
+  std::string in, out, format = "csv", dump, mode = "per-net", v, baseline, solver = "auto", ncclid;
+  double p[4] = {-1, -1, -1, -1}, netd = -1, dev = 0, uni = -1, ranks = 1, rank = 0, jblocks = 1, ptol = 0;
   double graded[3] = {-1, -1, -1};
   bool all = false, have_net = false;
   for (size_t i = 0; i < a.size(); ++i) {
@@ -146,6 +148,12 @@ int main(int argc, char** argv) {
     if (k == "--dump-matrix" && value(i, dump)) continue;
     if (k == "--mode" && value(i, mode) && (mode == "per-net" || mode == "shared")) continue;
     if (k == "--baseline" && value(i, baseline) && baseline == "collocation") continue;  // cli.hpp:37-38
+    if (k == "--solver" && value(i, solver) && (solver == "auto" || solver == "direct" || solver == "pcg")) continue;
+    if (k == "--jacobi-blocks" && value(i, v) && num(v, jblocks) && jblocks >= 1) continue;
+    if (k == "--pcg-tol" && value(i, v) && num(v, ptol) && ptol > 0) continue;
+    if (k == "--ranks" && value(i, v) && num(v, ranks) && ranks >= 1) continue;
+    if (k == "--rank" && value(i, v) && num(v, rank) && rank >= 0) continue;
+    if (k == "--nccl-id" && value(i, ncclid)) continue;
     if (k == "--all") {
       all = true;
       continue;
@@ -200,6 +208,17 @@ int main(int argc, char** argv) {
   o.net = have_net ? (int32_t)netd : -1;
   o.dump_matrix = dump.empty() ? nullptr : dump.c_str();
   o.collocation = baseline == "collocation" ? 1 : 0;
+  o.solver = solver == "direct" ? 1 : (solver == "pcg" ? 2 : 0);
+  o.jacobi_blocks = (int32_t)jblocks;
+  o.pcg_tol = ptol;
+  o.nranks = (int32_t)ranks;
+  o.rank = (int32_t)rank;
+  o.nccl_id_file = ncclid.empty() ? nullptr : ncclid.c_str();
+  if (o.nranks > 1 && o.mode != 1) {
+    std::cerr << "input error: --ranks needs --mode shared\n";
+    gbem_model_free(m);
+    return 1;
+  }
   if (o.collocation && o.mode == 1) {
     std::cerr << "input error: --baseline collocation runs per net (--mode per-net)\n";
     gbem_model_free(m);
@@ -251,6 +270,7 @@ int main(int argc, char** argv) {
     std::cerr << "error: " << err << "\n";
     return 3;
   }
+  if (o.nranks > 1 && o.rank != 0) return 0;  // every rank holds the same matrix; rank 0 reports
   const std::string& report = format == "json" ? json : csv;
   if (out.empty()) {
     std::cout << report;

@@ -242,18 +242,38 @@ CapMatrix capacitance_matrix_shared(gbem_ctx* ctx, const Scene& s, const PanelSe
   gbem_panels view = soa.view();
   gbem_quad_config q = quad(o);
   gbem_assembly_stats ast{};
+  std::vector<double> X, res(K, 0.0), Cpcg, outer_pcg;
+  const bool pcg = o.solver == 2 || (o.solver == 0 && gbem_ctx_nranks(ctx) > 1);
   auto t0 = std::chrono::steady_clock::now();
-  raise(ctx, gbem_assemble_single(ctx, &view, (int64_t)n, &q, nullptr, 0, &ast));
-  if (!o.dump_matrix.empty()) {
-    std::vector<double> A(n * n);
-    raise(ctx, gbem_matrix_download(ctx, A.data(), (int64_t)n));
-    dump_matrix_file(o.dump_matrix, A, n);
+  if (pcg) {
+    // row-block sharded block-Jacobi PCG (gbem_pcg_extract_cmatrix; every rank
+    // runs this with the same panels, the context's collectives join them)
+    if (!o.dump_matrix.empty()) throw ValidationError("--dump-matrix needs the direct solver");
+    std::vector<int32_t> net(n, -1);
+    for (size_t p = 0; p < n; ++p)
+      if (ps.panels[p].kind == kConductor) net[p] = (int32_t)col.at(ps.panels[p].net);
+    const Region* reg = s.region(ps.panels.empty() ? 0 : ps.panels.front().regA);
+    if (!reg) throw ValidationError("missing permittivity");
+    gbem_pcg_options po{o.pcg_tol, 5000, std::max(1, o.jacobi_blocks)};
+    gbem_pcg_stats pst{};
+    Cpcg.assign(K * K, 0.0);
+    outer_pcg.assign(K, 0.0);
+    raise(ctx, gbem_pcg_extract_cmatrix(ctx, &view, (int64_t)n, net.data(), (int32_t)K, reg->eps, &q, &po,
+                                        Cpcg.data(), res.data(), outer_pcg.data(), &ast, &pst));
+  } else {
+    raise(ctx, gbem_assemble_single(ctx, &view, (int64_t)n, &q, nullptr, 0, &ast));
+    if (!o.dump_matrix.empty()) {
+      std::vector<double> A(n * n);
+      raise(ctx, gbem_matrix_download(ctx, A.data(), (int64_t)n));
+      dump_matrix_file(o.dump_matrix, A, n);
+    }
+    std::vector<double> B(n * K, 0.0);
+    X.assign(n * K, 0.0);
+    for (size_t p = 0; p < n; ++p)
+      if (ps.panels[p].kind == kConductor) B[col.at(ps.panels[p].net) * n + p] = 1.0;
+    gbem_solve_stats sst{};
+    raise(ctx, gbem_spd_solve(ctx, B.data(), (int64_t)K, X.data(), res.data(), &sst));
   }
-  std::vector<double> B(n * K, 0.0), X(n * K, 0.0), res(K, 0.0);
-  for (size_t p = 0; p < n; ++p)
-    if (ps.panels[p].kind == kConductor) B[col.at(ps.panels[p].net) * n + p] = 1.0;
-  gbem_solve_stats sst{};
-  raise(ctx, gbem_spd_solve(ctx, B.data(), (int64_t)K, X.data(), res.data(), &sst));
   auto t1 = std::chrono::steady_clock::now();
   const double secs = std::chrono::duration<double>(t1 - t0).count();
   CapMatrix cm;
@@ -262,21 +282,26 @@ CapMatrix capacitance_matrix_shared(gbem_ctx* ctx, const Scene& s, const PanelSe
     Row row;
     row.main_net = s.nets[r].id;
     row.diag.panels = n;
-    row.diag.method = "galerkin-shared";
+    row.diag.method = pcg ? "galerkin-shared-pcg" : "galerkin-shared";
     row.diag.seconds = secs;
     row.diag.residual = res[r];
     row.diag.converged = ast.not_converged == 0;
     for (const Net& nn : s.nets) row.cap[nn.id] = 0.0;
     double outer = 0;
-    for (size_t p = 0; p < n; ++p) {
-      const Panel& pn = ps.panels[p];
-      const Region* reg = s.region(pn.regA);
-      if (!reg) throw ValidationError("missing permittivity for region " + std::to_string(pn.regA));
-      const double qv = reg->eps * kEps0 * X[r * n + p] * kUnitScale;
-      if (pn.kind == kConductor)
-        row.cap[pn.net] += qv;
-      else
-        outer += qv;
+    if (pcg) {
+      for (size_t k = 0; k < K; ++k) row.cap[s.nets[k].id] = Cpcg[r * K + k];
+      outer = outer_pcg[r];
+    } else {
+      for (size_t p = 0; p < n; ++p) {
+        const Panel& pn = ps.panels[p];
+        const Region* reg = s.region(pn.regA);
+        if (!reg) throw ValidationError("missing permittivity for region " + std::to_string(pn.regA));
+        const double qv = reg->eps * kEps0 * X[r * n + p] * kUnitScale;
+        if (pn.kind == kConductor)
+          row.cap[pn.net] += qv;
+        else
+          outer += qv;
+      }
     }
     row.outer = outer;
     double total = outer;

@@ -180,6 +180,9 @@ struct Options {
   double rel_tol = 1e-8;
   int max_levels = 16;
   bool collocation = false;  // ExtractionOptions::baselineCollocation (extraction.hpp:110-114)
+  int solver = 0;            // shared mode: 0 auto (PCG iff the context has several ranks), 1 direct, 2 PCG
+  int jacobi_blocks = 1;     // PCG: Jacobi blocks per rank
+  double pcg_tol = 1e-10;
 };
 
 struct RowDiag {

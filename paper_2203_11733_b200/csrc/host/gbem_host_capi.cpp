@@ -1,6 +1,10 @@
 // gbem_host_capi.cpp — extern "C" surface of the C++ host (include/gbem_host.h).
+#include <chrono>
+#include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <memory>
+#include <thread>
 
 #include "../../../include/gbem_gpu.h"
 #include "../../../include/gbem_host.h"
@@ -192,6 +196,37 @@ int gbem_model_panels(const gbem_model* m, uint8_t* axis, double* level, double*
   return 0;
 }
 
+namespace {
+
+// NCCL ranks for the sharded shared-mode solve: rank 0 writes the unique id to
+// `path` (atomically, through a rename), the other ranks poll for it.
+void attach_ranks(gbem_ctx* ctx, int nranks, int rank, const char* path) {
+  if (!path || !*path) throw gbh::ValidationError("several ranks need an NCCL id file");
+  if (rank < 0 || rank >= nranks) throw gbh::ValidationError("rank out of range");
+  std::vector<char> id(GBEM_NCCL_UNIQUE_ID_BYTES);
+  if (rank == 0) {
+    if (gbem_nccl_unique_id(id.data()) != GBEM_OK) throw std::runtime_error("ncclGetUniqueId failed");
+    const std::string tmp = std::string(path) + ".tmp";
+    {
+      std::ofstream f(tmp, std::ios::binary);
+      f.write(id.data(), (std::streamsize)id.size());
+      if (!f) throw std::runtime_error("cannot write " + tmp);
+    }
+    if (std::rename(tmp.c_str(), path) != 0) throw std::runtime_error(std::string("cannot rename to ") + path);
+  } else {
+    for (int t = 0;; ++t) {
+      std::ifstream f(path, std::ios::binary);
+      if (f && f.read(id.data(), (std::streamsize)id.size()) && f.gcount() == (std::streamsize)id.size()) break;
+      if (t > 12000) throw std::runtime_error(std::string("timed out waiting for ") + path);
+      std::this_thread::sleep_for(std::chrono::milliseconds(10));
+    }
+  }
+  if (gbem_ctx_init_nccl(ctx, nranks, rank, id.data()) != GBEM_OK)
+    throw std::runtime_error(std::string("NCCL: ") + gbem_last_error(ctx));
+}
+
+}  // namespace
+
 int gbem_model_extract(const gbem_model* m, const gbem_extract_opts* o, char* csv, int64_t csv_cap,
                        int64_t* csv_len, char* json, int64_t json_cap, int64_t* json_len, char* err,
                        int errlen) {
@@ -204,8 +239,12 @@ int gbem_model_extract(const gbem_model* m, const gbem_extract_opts* o, char* cs
     return 3;
   }
   int rc = guarded(err, errlen, [&] {
+    if (o->nranks > 1) attach_ranks(ctx, o->nranks, o->rank, o->nccl_id_file);
     gbh::Options opt;
     opt.device = o->device;
+    opt.solver = o->solver;
+    opt.jacobi_blocks = o->jacobi_blocks > 0 ? o->jacobi_blocks : 1;
+    if (o->pcg_tol > 0) opt.pcg_tol = o->pcg_tol;
     if (o->rel_tol > 0) opt.rel_tol = o->rel_tol;
     if (o->max_levels > 0) opt.max_levels = o->max_levels;
     if (o->dump_matrix) opt.dump_matrix = o->dump_matrix;

@@ -145,27 +145,29 @@ def attach(ctx, group=None, collectives: str = "auto"):
 def sharded_cmatrix(ctx, P, net_of_panel: np.ndarray, K: int, eps_r: float, cfg=None, group=None,
                     tol: float = 1e-10, max_iter: int = 1000, jacobi_blocks: int = 1, collectives: str = "auto",
                     attach_ranks: bool = True):
-    """C-matrix on row-block shards; every rank of ``group`` calls it with the
-    same panels (``_native.PanelArrays``).  Returns (C (K, K), resid (K,),
-    GbemPcgStats, GbemAssemblyStats); C is identical on every rank.
+    """C-matrix on row-block shards through the host-buffer entry point
+    ``gbem_pcg_extract_cmatrix`` (panel and net upload, C / resid / outer
+    download inside the call); every rank of ``group`` calls it with the same
+    panels (``_native.PanelArrays``).  Returns (C (K, K), resid (K,), outer (K,),
+    GbemPcgStats, GbemAssemblyStats); identical on every rank.
     ``attach_ranks=False`` reuses the ranks / collectives attached earlier."""
-    import torch
-    from .shard import panels_to_device
-    dev = torch.device("cuda", torch.cuda.current_device())
     if attach_ranks:
         attach(ctx, group, collectives)
-    ctx.set_stream(torch.cuda.current_stream(dev).cuda_stream)
-    pd = panels_to_device(P, dev)
-    dp = C.POINTER(C.c_double)
-    panels = N.GbemPanels(C.cast(C.c_void_p(pd["axis"].data_ptr()), C.POINTER(C.c_uint8)),
-                          *[C.cast(C.c_void_p(pd[k].data_ptr()), dp) for k in ("level", "a0", "a1", "b0", "b1")])
-    net = torch.from_numpy(np.ascontiguousarray(net_of_panel, dtype=np.int32)).to(dev)
-    Cm = torch.zeros(K * K, dtype=torch.float64, device=dev)
-    res = torch.zeros(K, dtype=torch.float64, device=dev)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    except ImportError:
+        pass
+    net = np.ascontiguousarray(net_of_panel, dtype=np.int32)
+    Cm = np.zeros((K, K))
+    res = np.zeros(K)
+    outer = np.zeros(K)
     opt = N.GbemPcgOptions(tol, max_iter, jacobi_blocks)
     pst, ast = N.GbemPcgStats(), N.GbemAssemblyStats()
-    rc = ctx.lib.gbem_pcg_extract_cmatrix_dev(ctx.h, C.byref(panels), P.n, C.c_void_p(net.data_ptr()), K, eps_r,
-                                              C.byref(cfg or ctx.quad()), C.byref(opt), C.c_void_p(Cm.data_ptr()),
-                                              C.c_void_p(res.data_ptr()), C.byref(ast), C.byref(pst))
+    sp = P.struct()
+    rc = ctx.lib.gbem_pcg_extract_cmatrix(ctx.h, C.byref(sp), P.n, N.ptr(net), K, eps_r, C.byref(cfg or ctx.quad()),
+                                          C.byref(opt), N.ptr(Cm), N.ptr(res), N.ptr(outer), C.byref(ast),
+                                          C.byref(pst))
     ctx.check(rc)
-    return Cm.view(K, K).cpu().numpy(), res.cpu().numpy(), pst, ast
+    return Cm, res, outer, pst, ast

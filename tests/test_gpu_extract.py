@@ -198,3 +198,22 @@ def test_reference_side_binding_reproduces_readme():
     _, js = m.extract(net=-1, mode=0)
     Ch = np.array([[js["rows"][r]["capacitance"][str(k)] for k in (1, 2)] for r in range(2)])
     assert np.all(np.abs(Cb - Ch) <= 1e-9 * np.abs(Ch))  # same panels, different summation order of the charges
+
+
+def test_shared_mode_pcg_solver_matches_direct():
+    """The C++ host runs the sharded solve (gbem_pcg_extract_cmatrix) from the
+    shared mode: CLI --solver pcg against --solver direct on the same panels."""
+    args = [str(CLI), "extract", "--input", str(BENCH), "--all", "--mode", "shared", "--graded", "0.05,1.5,0.3",
+            "--format", "json"]
+    rd = subprocess.run(args + ["--solver", "direct"], capture_output=True, text=True, timeout=600)
+    rp = subprocess.run(args + ["--solver", "pcg", "--jacobi-blocks", "3", "--pcg-tol", "1e-12"],
+                        capture_output=True, text=True, timeout=600)
+    assert rd.returncode == 0 and rp.returncode == 0, (rd.stderr, rp.stderr)
+    jd, jp = json.loads(rd.stdout), json.loads(rp.stdout)
+    for a, b in zip(jd["rows"], jp["rows"]):  # reports carry 9 significant digits
+        assert b["method"] == "galerkin-shared-pcg" and a["method"] == "galerkin-shared"
+        self_c = abs(a["capacitance"][str(a["net"])])
+        for k, v in a["capacitance"].items():
+            assert abs(b["capacitance"][k] - v) <= 2e-8 * self_c, (k, v, b["capacitance"][k])
+        assert abs(b["outerCharge"] - a["outerCharge"]) <= 2e-8 * self_c
+        assert b["residual"] <= 1e-11

@@ -106,7 +106,7 @@ def test_pcg_cmatrix_matches_direct(ctx, cfg, scale, blocks):
     bordered-Cholesky extraction; the true residual is recomputed from A."""
     ps, net, K, eps = _config_net(cfg, scale)
     Cd, _, _, _ = ctx.extract_cmatrix(ps.arrays(), net, K, eps)
-    Cp, res, st, ast = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=blocks)
+    Cp, res, outer, st, ast = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=blocks)
     assert st.converged and st.nranks == 1 and st.rows_local == len(ps)
     assert ast.pairs_total == len(ps) ** 2
     if blocks == 1:
@@ -124,7 +124,7 @@ def test_pcg_iterations_match_restatement(ctx):
     ps, net, K, eps = _config_net(1, 0.5)
     n = len(ps)
     A, _ = ctx.assemble_single(ps.arrays())
-    Cp, res, st, _ = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-10, jacobi_blocks=4)
+    Cp, res, _, st, _ = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-10, jacobi_blocks=4)
 
     class Ops:
         m = n
@@ -152,7 +152,7 @@ def test_pcg_with_nccl_communicator(ctx):
     ctx.check(ctx.lib.gbem_ctx_init_nccl(ctx.h, 1, 0, C.cast(uid, C.c_void_p)))
     ps, net, K, eps = _config_net(1, 0.5)
     Cd, _, _, _ = ctx.extract_cmatrix(ps.arrays(), net, K, eps)
-    Cp, res, st, _ = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=2, attach_ranks=False)
+    Cp, res, _, st, _ = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=2, attach_ranks=False)
     assert np.abs(Cp - Cd).max() <= 1e-9 * np.abs(Cd).max()
     ctx.check(ctx.lib.gbem_ctx_set_collectives(ctx.h, 1, 0, None))
 
@@ -167,7 +167,7 @@ def _two_rank_worker(rank, world, port, out):
     from paper_2203_11733_b200._native import Context
     c = Context(0)
     ps, net, K, eps = _config_net(2, 0.5)
-    Cp, res, st, ast = sharded_cmatrix(c, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=2, collectives="host")
+    Cp, res, _, st, ast = sharded_cmatrix(c, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=2, collectives="host")
     hc = c._coll_keep
     if rank == 0:
         np.savez(out, C=Cp, res=res, it=st.iterations, rows=st.rows_local, n=st.n,

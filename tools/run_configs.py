@@ -88,7 +88,7 @@ def pcg_vs_direct(config, Cd, blocks=8, tol=1e-10):
     ctx = N.Context(0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    Cp, res, st, ast = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=tol, max_iter=2000, jacobi_blocks=blocks)
+    Cp, res, _, st, ast = sharded_cmatrix(ctx, ps.arrays(), net, K, eps, tol=tol, max_iter=2000, jacobi_blocks=blocks)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     rel = float(np.max(np.abs(Cp - Cd)) / np.max(np.abs(Cd)))
