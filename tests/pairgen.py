@@ -171,7 +171,8 @@ def small_far_pairs(rng, n, edge_lo=0.002, edge_hi=0.05, dist_lo=0.5, dist_hi=5.
 
 
 def near_contact_pairs(rng, n, g_lo, g_hi, kind, spacing=50.0):
-    """Offset-parallel ("parallel") or orthogonal ("orthogonal") pairs at
+    """Offset-parallel ("parallel"), orthogonal ("orthogonal") or coplanar
+    ("coplanar": same plane, the closed form kernels.hpp:48-94) pairs at
     gap/max-diameter log-uniform in [g_lo, g_hi): the near-contact regime of the
     reference's reduced integrands (kernels.hpp:138-153, 175-214) and its
     Romberg (quadrature.hpp:70-113).  Pair k is translated to its own lattice
@@ -185,13 +186,15 @@ def near_contact_pairs(rng, n, g_lo, g_hi, kind, spacing=50.0):
         la = rng.uniform(0.2, 1.2)
         lb = la * (1.0 if rng.random() < 0.4 else np.exp(rng.uniform(-np.log(4), np.log(4))))
         a = [ax, 0.0, -la / 2, la / 2, -lb / 2, lb / 2]
-        bx = ax if kind == "parallel" else (ax + 1 + int(rng.integers(2))) % 3
+        bx = ax if kind in ("parallel", "coplanar") else (ax + 1 + int(rng.integers(2))) % 3
         s = np.exp(rng.uniform(-np.log(4), np.log(4)))
         lc = rng.uniform(0.2, 1.2) * s
         ld = lc * (1.0 if rng.random() < 0.4 else np.exp(rng.uniform(-np.log(4), np.log(4))))
         d = rng.normal(size=3)
         if kind == "parallel" and abs(d[ax]) < 0.05:
             d[ax] = 0.05 if d[ax] >= 0 else -0.05  # keep the planes apart (offset-parallel, not coplanar)
+        if kind == "coplanar":
+            d[ax] = 0.0
         d /= np.linalg.norm(d)
         g_target = np.exp(rng.uniform(np.log(g_lo), np.log(g_hi)))
         dm = max(np.hypot(la, lb), np.hypot(lc, ld))

@@ -1,11 +1,12 @@
 """Near-contact parity of the near-field routes (VERDICT r1 "missing" #4).
 
-960 seeded offset-parallel / orthogonal pairs at gap / max-diameter in
+1,440 seeded offset-parallel / orthogonal / coplanar pairs at gap / max-diameter in
 (1e-6, 1e-3), [1e-3, 5e-3), [5e-3, 0.02), [0.02, 0.1) — 120 per (bucket, kind),
 tests/golden/near_contact_golden.json (tests/golden/make_near_golden.py) — run
 through BOTH the pair-list entry point (gbem_u_pair_integrals) and a full
-matrix assembly of the 1,920 panels (gbem_assemble_single, where k_classify
-routes them), with the routes confirmed by the per-route stats.
+matrix assembly of the 2,880 panels (gbem_assemble_single, where k_classify
+routes them), with the routes confirmed by the per-route stats (coplanar
+pairs take the closed form on every bucket).
 
 Truth: the closed-form corner sum in 50-digit arithmetic (tests/exact_truth.py),
 pinned to the tight-tolerance reference (relTol 1e-13) on every pair where that
@@ -39,6 +40,7 @@ def _gate(gpu, m):
     lim = np.full(err.shape, 1e-10)
     near = BUCKET[m] == 0
     lim[near] = np.maximum(1e-10, 2 * np.abs(ref[near] - ex[near]) / ex[near])
+    lim[KIND[m] == 2] = 1e-10  # coplanar: the closed form on every bucket
     return err, lim
 
 
@@ -47,15 +49,17 @@ def _area(P):
 
 
 @pytest.mark.parametrize("bucket", [0, 1, 2, 3])
-@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("kind", [0, 1, 2])
 def test_near_contact_pair_list(ctx, bucket, kind):
     m = (BUCKET == bucket) & (KIND == kind)
     assert m.sum() >= 100
     out, conv, st = ctx.u_pair_integrals(PanelArrays.from_matrix(A[m]), PanelArrays.from_matrix(B[m]))
     d = st.as_dict()
     # route: every pair is near, of this kind, on this bucket's route
-    assert (d["pairs_parallel"] if kind == 0 else d["pairs_orthogonal"]) == m.sum(), d
-    if bucket == 0:
+    assert d[("pairs_parallel", "pairs_orthogonal", "pairs_coplanar")[kind]] == m.sum(), d
+    if kind == 2:
+        pass  # the closed form
+    elif bucket == 0:
         assert d["pairs_near_romberg"] == m.sum(), d
     else:
         assert d["pairs_near_band"][4 - bucket] == m.sum(), d
@@ -65,8 +69,9 @@ def test_near_contact_pair_list(ctx, bucket, kind):
 
 
 def test_near_contact_full_assembly(ctx):
-    """The 960 pairs as one 1,920-panel set: every designated pair is routed by
-    the assembly classifier (all other pairs are far, >= 6 diameters)."""
+    """The 1,440 pairs as one 2,880-panel set: every designated pair is routed
+    by the assembly classifier (all other pairs are far, >= 6 diameters; the
+    coplanar count also holds the n self pairs)."""
     n2 = len(A)
     P = np.empty((2 * n2, 6))
     P[0::2] = A
@@ -78,9 +83,10 @@ def test_near_contact_full_assembly(ctx):
     Ut = Amat[2 * k + 1, 2 * k] * _area(A) * _area(B)
     assert np.array_equal(U, Ut)  # symmetric storage
     assert d["pairs_parallel"] == (KIND == 0).sum() and d["pairs_orthogonal"] == (KIND == 1).sum(), d
-    assert d["pairs_near_romberg"] == (BUCKET == 0).sum(), d
+    assert d["pairs_coplanar"] == (KIND == 2).sum() + 2 * n2, d
+    assert d["pairs_near_romberg"] == ((BUCKET == 0) & (KIND < 2)).sum(), d
     for b in (1, 2, 3):
-        assert d["pairs_near_band"][4 - b] == (BUCKET == b).sum(), d
+        assert d["pairs_near_band"][4 - b] == ((BUCKET == b) & (KIND < 2)).sum(), d
     m = np.ones(n2, bool)
     err, lim = _gate(U, m)
     bad = err > lim
