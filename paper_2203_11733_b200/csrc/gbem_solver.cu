@@ -1222,8 +1222,10 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       for (int k = 0; k < nb; ++k) {
         const int bb = b0 + k;
         if (k > 0) {
-          update_col(b0, 0, hi);  // U(b0, b0 + 1)
-          GBEM_LAUNCH_CHECK(ctx);
+          for (int j = 0; j < k; ++j) {  // U(b0 + j, b0 + k): the super-block's own columns
+            update_col(b0 + j, k - 1 - j, hi);
+            GBEM_LAUNCH_CHECK(ctx);
+          }
           GBEM_CUDA(ctx, cudaEventRecord(evB, hi));
           GBEM_CUDA(ctx, cudaStreamWaitEvent(p, evB, 0));
         }
@@ -1242,7 +1244,15 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     };
     // U([b0, b0 + nb), block columns >= b0 + nb + j0): band (j0 = 0, one super-
     // block of kBand2 tile columns) or triangular rest (j0 = 2)
-    constexpr int kBand2 = 2 * kBand;
+    // super-block width in 128-column blocks (K of the trailing update = SB * 128;
+    // tools/gemm_bench.cu at m = 20,000: K = 256 / 384 / 512 -> 32.0 / 33.0 / 33.4 TFLOP/s).
+    // The intra-super-block updates lengthen the potrf / trsm chain by O(SB^2)
+    // thin updates, which a small matrix cannot hide: config 2 (n = 11,340) is
+    // fastest at SB = 2 (18.46 ms vs 18.96 at 4), config 3 (n = 33,776) at
+    // SB >= 5 (426.1 / 416.6 / 412.7 / 411.2 / 411.0 ms at SB = 2 / 3 / 4 / 5 / 6)
+    static const int sb_env = getenv("GBEM_SUPERBLOCK") ? std::max(1, atoi(getenv("GBEM_SUPERBLOCK"))) : 0;
+    const int SB = sb_env > 0 ? sb_env : (n < 16384 ? 2 : 5);
+    const int kBand2 = SB * kBand;
     static const int occ_rows = getenv("GBEM_OCC_ROWS") ? atoi(getenv("GBEM_OCC_ROWS")) : 0;
     static const bool combined = getenv("GBEM_NO_COMBINED") == nullptr;
     auto update2 = [&](int b0, int nb, bool band_part) {
@@ -1267,11 +1277,11 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     };
     GBEM_CUDA(ctx, cudaEventRecord(evB, p));  // stepA(0) waits on nothing
     int b = 0;
-    int rc2 = stepA(0, std::min(2, nblk), 0u);
+    int rc2 = stepA(0, std::min(SB, nblk), 0u);
     if (rc2) return rc2;
     unsigned band_target = 0;  // cumulative band CTAs of the combined updates
     for (;;) {
-      const int nb = std::min(2, nblk - b), next = b + nb;
+      const int nb = std::min(SB, nblk - b), next = b + nb;
       GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, evT, 0));
       if (prof) cudaEventRecord(pe[6 * b + 5], lo);
       if (next >= nblk) {  // the last super-block: its trsm covered the border rows
@@ -1297,7 +1307,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
         GBEM_LAUNCH_CHECK(ctx);
         band_target += (unsigned)(nt * bw);
         if (!next_tail) {
-          rc2 = stepA(next, std::min(2, nblk - next), band_target);
+          rc2 = stepA(next, std::min(SB, nblk - next), band_target);
           if (rc2) return rc2;
         }
       } else {
@@ -1305,7 +1315,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
         GBEM_LAUNCH_CHECK(ctx);
         GBEM_CUDA(ctx, cudaEventRecord(evB, lo));
         if (!next_tail) {
-          rc2 = stepA(next, std::min(2, nblk - next), 0u);
+          rc2 = stepA(next, std::min(SB, nblk - next), 0u);
           if (rc2) return rc2;
         }
         update2(b, nb, false);  // rest2(b)
