@@ -1222,10 +1222,13 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       for (int k = 0; k < nb; ++k) {
         const int bb = b0 + k;
         if (k > 0) {
-          for (int j = 0; j < k; ++j) {  // U(b0 + j, b0 + k): the super-block's own columns
-            update_col(b0 + j, k - 1 - j, hi);
-            GBEM_LAUNCH_CHECK(ctx);
-          }
+          // U(b0 .. b0+k-1, b0 + k): block column b0 + k by the super-block's
+          // first k blocks at once (one K = 128 k update on the chain)
+          const int c0 = bb * NB, mk = n - c0 + (int)ctx->border, ntk = (mk + 63) / 64;
+          kUpdate<<<dim3(ntk, std::min(kBand, ntk)), UpdShape::THREADS, UpdShape::SMEM, hi>>>(
+              ctx->d_A + (long long)c0 * lda + c0, lda, ctx->d_A + (long long)(b0 * NB) * lda + c0, lda, mk, k * NB, 0,
+              std::min(kBand, ntk));
+          GBEM_LAUNCH_CHECK(ctx);
           GBEM_CUDA(ctx, cudaEventRecord(evB, hi));
           GBEM_CUDA(ctx, cudaStreamWaitEvent(p, evB, 0));
         }

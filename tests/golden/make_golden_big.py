@@ -64,10 +64,26 @@ def run(cfg: int, scale: float, nthreads: int):
         ref_v = tight = np.zeros(0)
     exact = np.array([E.u_exact(P[i], P[j]) for i, j in keep]) if len(keep) else np.zeros(0)
     B = np.stack([(ps.kind == 0) & (ps.net == nid) for nid in ids], axis=1).astype(float)
+    if os.environ.get("GOLDEN_SAVE_A"):
+        np.save(os.environ["GOLDEN_SAVE_A"], A)
     A_keep = A.copy()
-    c, low = sla.cho_factor(A, lower=True, overwrite_a=True, check_finite=False)
-    X = sla.cho_solve((c, low), B, check_finite=False)
-    del c, A
+    solve = "scipy LAPACK cho_factor/cho_solve (not the reference loop order)"
+    spd_fail = None
+    try:
+        c, low = sla.cho_factor(A, lower=True, overwrite_a=True, check_finite=False)
+        X = sla.cho_solve((c, low), B, check_finite=False)
+        del c
+    except np.linalg.LinAlgError as e:
+        # the reference's cholesky_solve would throw "matrix not positive definite"
+        # here (solver.hpp:29-33); capacitance_row's allowLuFallback path
+        # (extraction.hpp:128-131) solves by partial-pivot LU instead
+        spd_fail = str(e)
+        print("Cholesky failed:", spd_fail, "-> LU (the reference's allowLuFallback)", flush=True)
+        lu = sla.lu_factor(A_keep, check_finite=False)
+        X = sla.lu_solve(lu, B, check_finite=False)
+        del lu
+        solve = "scipy LAPACK lu_factor/lu_solve (the reference's LU fallback: its Cholesky fails, " + spd_fail + ")"
+    del A
     res = np.linalg.norm(A_keep @ X - B, axis=0) / np.linalg.norm(B, axis=0)
     eps = m.info()["eps_r"]
     Cm = np.array([[eps * EPS0 * 1e-6 * X[(ps.net == k), r].sum() for k in ids] for r in range(len(ids))])
@@ -78,7 +94,7 @@ def run(cfg: int, scale: float, nthreads: int):
                                   "tight": np.asarray(tight).tolist(), "exact": exact.tolist()},
          "cmatrix_F": Cm.tolist(), "max_residual": float(res.max()),
          "assembly_s": round(t_asm, 1), "threads": nthreads,
-         "solve": "scipy LAPACK cho_factor/cho_solve (not the reference loop order)"}
+         "solve": solve, "reference_cholesky_fails": spd_fail}
     return d
 
 

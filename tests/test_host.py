@@ -217,3 +217,19 @@ def test_serialised_workloads_match_generator(cfg):
     ps = m.partition(1)
     assert np.array_equal(d["panels"], ps.matrix())
     assert int(d["nets"]) == len(m.net_ids) and float(d["eps_r"]) == m.info()["eps_r"]
+
+
+def test_bench_arms_report_the_same_config():
+    """bench.py: the reference arm (serialised panel list, no repo library) and
+    the GPU arm describe the workload with identical `config` objects."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench", ROOT / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for cfg in (2, 3):
+        P, net, K, eps, seed = bench.serialized_workload(cfg)
+        m = g.config_model(cfg, seed=1)
+        assert bench.extract_config(cfg, len(P), K, eps, seed) == bench.extract_config(
+            cfg, len(m.partition(1)), len(m.net_ids), m.info()["eps_r"], 1)
+    P4, _, K4, _, _ = bench.serialized_workload(4)
+    assert bench.sharded_config(8, len(P4), K4, 200000)["unique_entries"] == 96200 * 96201 // 2
