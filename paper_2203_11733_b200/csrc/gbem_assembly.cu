@@ -765,6 +765,8 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
       far_list(code, mid_second ? r0 : r1, A, B, L);
       emit_list<kFarThreads>(L, sgx, sgw, w3s, W3s);
     }
+    // the output scale now, so the panel records are dead during the node loop
+    const double out_scale = 0.5 * (o.A ? rcp64(kFourPi * (panel_area(A) * panel_area(B))) : rcp64(kFourPi));
     double acc = 0.0;
     for (int c = 0; c < m3; ++c) {
       const double w3 = w3s[c * kFarThreads], W3 = W3s[c * kFarThreads];
@@ -780,16 +782,15 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
         acc = fma(W3 * W2s[b * kFarThreads], t0 + t1, acc);
       }
     }
-    acc *= 0.5;  // the Newton step's 1/2 (wrsq3_acc)
+    acc *= out_scale;  // 1/2 of the Newton step (wrsq3_acc), 1 / (4 pi area_I area_J)
     // counters in integer arithmetic (off the FP64 pipe)
     const uint32_t nodes = (uint32_t)(M * m2 * m3);
     evals += nodes;
     flops += 7u * nodes + 4u * (uint32_t)(m2 * m3) + 6u * (uint32_t)(M + m2 + m3) + 31u;  // per node: DADD, DMUL, DFMA, DMUL, DFMA
     if (o.A) {
-      // U / (4 pi area_I area_J) with one reciprocal
-      o.A[(long long)i * o.lda + (long long)j * o.ldc] = acc * rcp64(kFourPi * (panel_area(A) * panel_area(B)));
+      o.A[(long long)i * o.lda + (long long)j * o.ldc] = acc;
     } else {
-      o.out[i] = acc * rcp64(kFourPi);
+      o.out[i] = acc;
       if (o.conv) o.conv[i] = 1;
     }
   }

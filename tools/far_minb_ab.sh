@@ -1,6 +1,10 @@
-# A/B of the far kernel's minimum CTAs per SM (register cap): rebuild, bench
-for mb in ${MBS:-5 6 4}; do
+#!/bin/bash
+# k_far CTAs-per-SM sweep: rebuild the assembly unit with GBEM_FAR_MINB=N, time configs 2 and 3
+for mb in "$@"; do
   touch paper_2203_11733_b200/csrc/gbem_assembly.cu
-  GBEM_NVCC_EXTRA="-DGBEM_FAR_MINB=$mb" python -c "from paper_2203_11733_b200 import build as b; b.build()" > /dev/null 2>&1 || echo "build $mb failed"
-  echo "minb=$mb"; bash tools/far_ab.sh
+  GBEM_NVCC_EXTRA="-DGBEM_FAR_MINB=$mb" python -m paper_2203_11733_b200.build > /dev/null 2>&1
+  echo "GBEM_FAR_MINB=$mb"
+  tools/far_ab.sh
 done
+touch paper_2203_11733_b200/csrc/gbem_assembly.cu
+python -m paper_2203_11733_b200.build > /dev/null 2>&1
