@@ -263,7 +263,10 @@ int gbem_net_charges_dev(gbem_ctx* ctx, const int32_t* net_of_panel, int64_t n,
  * assemble, factor, solve with B[:, r] = 1 on the panels of net r, and reduce
  * C[r*K + k] = eps_r * eps0 * 1e-6 * sum_{p in net k} X[p, r] (farads).
  * net_of_panel[p] in [0, K) for conductor panels, -1 for grounded outer panels.
- * Host buffers (every host<->device copy happens inside the call). */
+ * Host buffers (every host<->device copy happens inside the call).  With several
+ * ranks attached to the context (gbem_ctx_init_nccl / gbem_ctx_set_collectives)
+ * every rank calls it and the solve runs on row-block shards
+ * (gbem_pcg_extract_cmatrix, Jacobi blocks of ~12k rows); sstats is then zeroed. */
 int gbem_extract_cmatrix(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const int32_t* net_of_panel,
                          int32_t K, double eps_r, const gbem_quad_config* cfg, double* C, double* resid,
                          gbem_assembly_stats* astats, gbem_solve_stats* sstats);

@@ -593,6 +593,15 @@ int gbem_extract_cmatrix(gbem_ctx* ctx, const gbem_panels* P, int64_t n, const i
   if (!P || !net_of_panel || !C || n <= 0) return ctx->fail(GBEM_EINVAL, "null argument or empty panel set");
   if (K < 1 || K > kMaxNets) return ctx->fail(GBEM_EINVAL, "K must be in [1, " + std::to_string(kMaxNets) + "]");
   GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  if (ctx->nranks > 1) {
+    // ranks attached (gbem_ctx_init_nccl / gbem_ctx_set_collectives): the matrix is
+    // sharded by row blocks and solved by block-Jacobi PCG (gbem_pcg.cu), Jacobi
+    // blocks of ~12k rows (the 8-rank config-4 shape)
+    const int64_t rows = (n + ctx->nranks - 1) / ctx->nranks;
+    gbem_pcg_options po{1e-10, 5000, (int32_t)std::max<int64_t>(1, (rows + 12031) / 12032)};
+    if (ss) *ss = gbem_solve_stats{};
+    return gbem_pcg_extract_cmatrix(ctx, P, n, net_of_panel, K, eps_r, cfg, &po, C, resid, nullptr, as, nullptr);
+  }
   int32_t* d_net = nullptr;
   double *d_C = nullptr, *d_res = nullptr;
   GBEM_CUDA(ctx, cudaMallocAsync(&d_net, sizeof(int32_t) * n, ctx->stream));
@@ -616,6 +625,12 @@ int gbem_extract_cmatrix_dev(gbem_ctx* ctx, const gbem_panels* P, int64_t n, con
   if (!ctx) return GBEM_EINVAL;
   if (!P || !net_of_panel || !C || n <= 0) return ctx->fail(GBEM_EINVAL, "null argument or empty panel set");
   GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  if (ctx->nranks > 1) {  // sharded solve, as in gbem_extract_cmatrix
+    const int64_t rows = (n + ctx->nranks - 1) / ctx->nranks;
+    gbem_pcg_options po{1e-10, 5000, (int32_t)std::max<int64_t>(1, (rows + 12031) / 12032)};
+    if (ss) *ss = gbem_solve_stats{};
+    return gbem_pcg_extract_cmatrix_dev(ctx, P, n, net_of_panel, K, eps_r, cfg, &po, C, resid, nullptr, as, nullptr);
+  }
   return extract_impl(ctx, P, n, net_of_panel, K, eps_r, cfg, C, resid, as, ss, true);
 }
 

@@ -169,9 +169,11 @@ def _two_rank_worker(rank, world, port, out):
     ps, net, K, eps = _config_net(2, 0.5)
     Cp, res, _, st, ast = sharded_cmatrix(c, ps.arrays(), net, K, eps, tol=1e-12, jacobi_blocks=2, collectives="host")
     hc = c._coll_keep
+    # the plain extraction entry point dispatches to the sharded solve once ranks are attached
+    C2, res2, _, _ = c.extract_cmatrix(ps.arrays(), net, K, eps)
     if rank == 0:
         np.savez(out, C=Cp, res=res, it=st.iterations, rows=st.rows_local, n=st.n,
-                 ag=hc.calls["all_gather"], ar=hc.calls["all_reduce_sum"])
+                 ag=hc.calls["all_gather"], ar=hc.calls["all_reduce_sum"], C2=C2, res2=res2)
     dist.barrier()
     c.close()
     dist.destroy_process_group()
@@ -196,6 +198,7 @@ def test_pcg_two_ranks_host_collectives(ctx, tmp_path):
     assert int(d["it"]) > 2 and int(d["ag"]) >= int(d["it"]) + 1 and int(d["ar"]) >= 2 * int(d["it"])
     assert d["res"].max() <= 1e-11
     assert np.abs(d["C"] - Cd).max() <= 1e-9 * np.abs(Cd).max()
+    assert np.abs(d["C2"] - Cd).max() <= 1e-8 * np.abs(Cd).max() and d["res2"].max() <= 1e-9
 
 
 def test_async_mode_defers_pivot_check(ctx):
