@@ -96,7 +96,7 @@ struct gbem_ctx {
   // kernels whose dynamic shared-memory limit has been raised on this
   // context's device (cudaFuncSetAttribute is per device; one bit per site)
   uint64_t attr_set = 0;
-  enum : uint64_t { kAttrGemmSolve = 1u, kAttrFactor = 2u, kAttrGemmLU = 4u, kAttrPcgGemm = 8u };
+  enum : uint64_t { kAttrGemmSolve = 1u, kAttrFactor = 2u, kAttrGemmLU = 4u, kAttrPcgGemm = 8u, kAttrSymm = 16u };
 
   int fail(int code, const std::string& msg) {
     err = msg;

@@ -478,6 +478,127 @@ __global__ void __launch_bounds__(256) k_symv_upper(const double* __restrict__ A
 }
 
 // resid[q] = ||Y[:,q] - B[:,q]|| / ||B[:,q]|| (one CTA per rhs)
+// Y = A X on the FP64 tensor cores for the residual, with A symmetric and only
+// its strict upper triangle (col-major, A[c*lda + r], r < c) and the saved
+// diagonal intact (the lower triangle holds L).  CTA: 64 rows of Y x NR
+// right-hand sides, 4 warps of 16 x NR (2 x NR/8 DMMA m8n8k4 fragments); the
+// reduction runs over all n columns in BK = 16 slabs, double-buffered by
+// cp.async.  A slab right of the CTA's rows is read as stored (A(r, c) at
+// c*lda + r, contiguous in r) into a [k][m] buffer, a slab left of them
+// through the symmetry (A(r, c) = A[r*lda + c], contiguous in c) into an
+// [m][k] buffer, and the few slabs crossing the diagonal element-wise; the
+// fragment loads index whichever layout the slab used.  X (n x R, col-major)
+// arrives as an [q][k] slab.  One pass over the matrix for up to NR
+// right-hand sides (the scalar k_symv_upper streams it once per 8).
+constexpr int kSyT = 64, kSyThreads = 128, kSyLU = kSyT + 8, kSyLL = BK + 4;
+template <int NR>
+struct SymmShape {
+  static constexpr int LX = BK + 4;
+  static constexpr int SLAB = BK * kSyLU + kSyT * kSyLL + NR * LX;  // upper layout, lower layout, X
+  static constexpr size_t SMEM = 2 * SLAB * sizeof(double);
+};
+template <int NR>
+__global__ void __launch_bounds__(kSyThreads, 4)
+    k_symm_dmma(const double* __restrict__ A, long long lda, const double* __restrict__ diag, int n,
+                const double* __restrict__ X, long long ldx, int R, double* __restrict__ Y) {
+  using S = SymmShape<NR>;
+  constexpr int FN = NR / 8;
+  extern __shared__ __align__(16) double ssm[];
+  const int r0 = blockIdx.x * kSyT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nslab = (n + BK - 1) / BK;
+  // slab kind: 0 upper (stored), 1 lower (transposed read), 2 crosses the diagonal
+  auto kind = [&](int k0) { return k0 >= r0 + kSyT ? 0 : (k0 + BK <= r0 ? 1 : 2); };
+  auto load = [&](int sl, int buf) {
+    double* su = ssm + buf * S::SLAB;
+    double* sL = su + BK * kSyLU;
+    double* sx = sL + kSyT * kSyLL;
+    const int k0 = sl * BK, kd = kind(k0);
+    if (kd == 0) {
+      for (int c = tid; c < BK * kSyT / 2; c += kSyThreads) {  // 16 columns x 64 rows, 16 B along r
+        const int kk = c / (kSyT / 2), mm = (c % (kSyT / 2)) * 2;
+        const int col = k0 + kk, row = r0 + mm;
+        const bool ok = col < n && row < n;
+        gbem_gemm::cp_async16(su + kk * kSyLU + mm, ok ? A + (long long)col * lda + row : A,
+                              ok ? (row + 1 < n ? 16 : 8) : 0);
+      }
+    } else if (kd == 1) {
+      for (int c = tid; c < kSyT * BK / 2; c += kSyThreads) {  // 64 rows x 16 columns, 16 B along c
+        const int mm = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+        const int row = r0 + mm, col = k0 + kk;
+        const bool ok = row < n && col < n;
+        gbem_gemm::cp_async16(sL + mm * kSyLL + kk, ok ? A + (long long)row * lda + col : A,
+                              ok ? (col + 1 < n ? 16 : 8) : 0);
+      }
+    } else {
+      for (int e = tid; e < BK * kSyT; e += kSyThreads) {
+        const int kk = e / kSyT, mm = e % kSyT;
+        const int col = k0 + kk, row = r0 + mm;
+        double v = 0.0;
+        if (row < n && col < n)
+          v = col > row ? A[(long long)col * lda + row] : (col < row ? A[(long long)row * lda + col] : diag[row]);
+        su[kk * kSyLU + mm] = v;
+      }
+    }
+    for (int c = tid; c < NR * BK / 2; c += kSyThreads) {  // X: NR columns x 16 rows, 16 B along k
+      const int q = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+      const int col = k0 + kk;
+      const bool ok = q < R && col < n;
+      gbem_gemm::cp_async16(sx + q * S::LX + kk, ok ? X + (long long)q * ldx + col : X,
+                            ok ? (col + 1 < n ? 16 : 8) : 0);
+    }
+    gbem_gemm::cp_async_commit();
+  };
+  double acc[2][FN][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  load(0, 0);
+  for (int sl = 0; sl < nslab; ++sl) {
+    if (sl + 1 < nslab) {
+      load(sl + 1, (sl + 1) & 1);
+      gbem_gemm::cp_async_wait<1>();
+    } else {
+      gbem_gemm::cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* su = ssm + (sl & 1) * S::SLAB;
+    const double* sL = su + BK * kSyLU;
+    const double* sx = sL + kSyT * kSyLL;
+    const bool lower = kind(sl * BK) == 1;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[2], bf[FN];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int m = warp * 16 + i * 8 + g;
+        af[i] = lower ? sL[m * kSyLL + kk + t4] : su[(kk + t4) * kSyLU + m];
+      }
+#pragma unroll
+      for (int j = 0; j < FN; ++j) bf[j] = sx[(j * 8 + g) * S::LX + kk + t4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) gbem_gemm::dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int row = r0 + warp * 16 + i * 8 + g;
+    if (row >= n) continue;
+#pragma unroll
+    for (int j = 0; j < FN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int q = j * 8 + 2 * t4 + e;
+        if (q < R) Y[(long long)q * n + row] = acc[i][j][e];
+      }
+  }
+}
+
 __global__ void k_resid_norm(const double* Y, const double* B, int n, double* resid) {
   int q = blockIdx.x;
   double rn = 0.0, bn = 0.0;
@@ -1514,7 +1635,41 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
   }
   cudaEventRecord(ctx->ev[2], s);
   if (d_resid) {
-    GBEM_CUDA(ctx, cudaMemsetAsync(Ysym, 0, sizeof(double) * (size_t)n * R, s));
+    // A X on the tensor cores, one pass over A per 32 right-hand sides
+    // (k_symm_dmma: config 3 6.2 -> 2.6 ms); below n = 16,384 its 64-row CTAs
+    // cannot fill the machine and the scalar k_symv_upper (column chunks) is
+    // faster (config 2: 0.27 vs 0.55 ms).  GBEM_SYMV_SCALAR=1 forces the scalar one.
+    static const bool force_scalar = getenv("GBEM_SYMV_SCALAR") != nullptr;
+    const bool scalar = force_scalar || n < 16384;
+    if (!scalar) {
+      if (!(ctx->attr_set & gbem_ctx::kAttrSymm)) {
+        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SymmShape<8>::SMEM));
+        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SymmShape<16>::SMEM));
+        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SymmShape<24>::SMEM));
+        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SymmShape<32>::SMEM));
+        ctx->attr_set |= gbem_ctx::kAttrSymm;
+      }
+      const unsigned grid = (unsigned)((n + kSyT - 1) / kSyT);
+      for (int q0 = 0; q0 < R; q0 += 32) {
+        const int rq = std::min(32, R - q0);
+        const double* Xq = d_X + (long long)q0 * n;
+        double* Yq = Ysym + (long long)q0 * n;
+        if (rq <= 8)
+          k_symm_dmma<8><<<grid, kSyThreads, SymmShape<8>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+        else if (rq <= 16)
+          k_symm_dmma<16><<<grid, kSyThreads, SymmShape<16>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+        else if (rq <= 24)
+          k_symm_dmma<24><<<grid, kSyThreads, SymmShape<24>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+        else
+          k_symm_dmma<32><<<grid, kSyThreads, SymmShape<32>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+        GBEM_LAUNCH_CHECK(ctx);
+      }
+    } else {
+        GBEM_CUDA(ctx, cudaMemsetAsync(Ysym, 0, sizeof(double) * (size_t)n * R, s));
     int nbt = (n + 63) / 64;
     const dim3 sgrid((unsigned)nbt, (unsigned)std::min(kSymvChunks, nbt));
     for (int q0 = 0; q0 < R; q0 += 8) {
@@ -1531,6 +1686,7 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
       else
         k_symv_upper<8><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
       GBEM_LAUNCH_CHECK(ctx);
+    }
     }
     k_resid_norm<<<R, 1024, 0, s>>>(Ysym, d_B, n, d_resid);
     GBEM_LAUNCH_CHECK(ctx);
