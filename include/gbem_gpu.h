@@ -167,6 +167,11 @@ int gbem_rowblock_matvec_dev(gbem_ctx* ctx, const double* Ablk, int64_t ld, int6
  * the factor for repeated gbem_spd_solve_factored_dev calls (block-Jacobi
  * preconditioner of the sharded solver). */
 int gbem_spd_factor_dev(gbem_ctx* ctx, const double* M, int64_t m, int64_t ldm, gbem_solve_stats* stats);
+/* Y = A X with the context matrix (the original symmetric A: its preserved
+ * strict upper triangle and diagonal, so also after a factorisation), X and Y
+ * n x nrhs column-major on the device; the residual product of solver.hpp:47
+ * (FP64 tensor cores for n >= 16,384). */
+int gbem_matrix_apply_dev(gbem_ctx* ctx, const double* X, int64_t nrhs, double* Y);
 int gbem_spd_solve_factored_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
                                 gbem_solve_stats* stats);
 

@@ -112,6 +112,7 @@ GPU_SYMBOLS = [
     ("gbem_rowblock_matvec_dev", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64, _P, C.c_int64, C.c_int64, _P,
                                            C.c_int64]),
     ("gbem_spd_factor_dev", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.POINTER(GbemSolveStats)]),
+    ("gbem_matrix_apply_dev", C.c_int, [_P, _P, C.c_int64, _P]),
     ("gbem_spd_solve_factored_dev", C.c_int, [_P, _P, C.c_int64, _P, _P, C.POINTER(GbemSolveStats)]),
     ("gbem_assemble_collocation", C.c_int, [_P, C.POINTER(GbemBlockPanels), C.c_int64, C.POINTER(GbemRegion),
                                             C.c_int32, C.c_int32, _P, C.c_int64, _P, C.POINTER(C.c_int64)]),

@@ -370,6 +370,16 @@ int gbem_spd_factor_dev(gbem_ctx* ctx, const double* M, int64_t m, int64_t ldm, 
   return gbem_internal_factor(ctx, stats);
 }
 
+int gbem_matrix_apply_dev(gbem_ctx* ctx, const double* X, int64_t nrhs, double* Y) {
+  if (!ctx) return GBEM_EINVAL;
+  if (!X || !Y) return ctx->fail(GBEM_EINVAL, "null argument");
+  GBEM_CUDA(ctx, cudaSetDevice(ctx->device));
+  int rc = gbem_internal_apply(ctx, X, nrhs, Y);
+  if (rc) return rc;
+  if (!ctx->async) GBEM_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GBEM_OK;
+}
+
 int gbem_spd_solve_factored_dev(gbem_ctx* ctx, const double* B, int64_t nrhs, double* X, double* resid,
                                 gbem_solve_stats* stats) {
   if (!ctx) return GBEM_EINVAL;

@@ -143,6 +143,7 @@ int gbem_internal_oracle_pairs(gbem_ctx* ctx, const gbem_panels* I, const gbem_p
                                int64_t npairs, int32_t dbl, int32_t depth, double* out);
 int gbem_internal_selftest(gbem_ctx* ctx, int32_t pairs, uint64_t seed, const gbem_quad_config* cfg,
                            gbem_selftest_case* cases, int32_t* ncases);
+int gbem_internal_apply(gbem_ctx* ctx, const double* d_X, int64_t nrhs, double* d_Y);
 int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X,
                         double* d_resid, gbem_solve_stats* stats);
 int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats);

@@ -1558,6 +1558,69 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   return GBEM_OK;
 }
 
+// Y = A X (n x R each, column-major) with the symmetric matrix given by the
+// preserved strict upper triangle and the saved diagonal: valid before and
+// after the factorisation (the residual of solver.hpp:47, gbem_matrix_apply_dev).
+static int apply_sym(gbem_ctx* ctx, const double* X, int R, double* Y) {
+  const int n = (int)ctx->n;
+  const long long lda = ctx->lda;
+  cudaStream_t s = ctx->stream;
+    // A X on the tensor cores, one pass over A per 32 right-hand sides
+    // (k_symm_dmma: config 3 6.2 -> 2.6 ms); below n = 16,384 its 64-row CTAs
+    // cannot fill the machine and the scalar k_symv_upper (column chunks) is
+    // faster (config 2: 0.27 vs 0.55 ms).  GBEM_SYMV_SCALAR=1 forces the scalar one.
+    static const bool force_scalar = getenv("GBEM_SYMV_SCALAR") != nullptr;
+    const bool scalar = force_scalar || n < 16384;
+    if (!scalar) {
+      if (!(ctx->attr_set & gbem_ctx::kAttrSymm)) {
+        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SymmShape<8>::SMEM));
+        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SymmShape<16>::SMEM));
+        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SymmShape<24>::SMEM));
+        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)SymmShape<32>::SMEM));
+        ctx->attr_set |= gbem_ctx::kAttrSymm;
+      }
+      const unsigned grid = (unsigned)((n + kSyT - 1) / kSyT);
+      for (int q0 = 0; q0 < R; q0 += 32) {
+        const int rq = std::min(32, R - q0);
+        const double* Xq = X + (long long)q0 * n;
+        double* Yq = Y + (long long)q0 * n;
+        if (rq <= 8)
+          k_symm_dmma<8><<<grid, kSyThreads, SymmShape<8>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+        else if (rq <= 16)
+          k_symm_dmma<16><<<grid, kSyThreads, SymmShape<16>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+        else if (rq <= 24)
+          k_symm_dmma<24><<<grid, kSyThreads, SymmShape<24>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+        else
+          k_symm_dmma<32><<<grid, kSyThreads, SymmShape<32>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+        GBEM_LAUNCH_CHECK(ctx);
+      }
+    } else {
+        GBEM_CUDA(ctx, cudaMemsetAsync(Y, 0, sizeof(double) * (size_t)n * R, s));
+    int nbt = (n + 63) / 64;
+    const dim3 sgrid((unsigned)nbt, (unsigned)std::min(kSymvChunks, nbt));
+    for (int q0 = 0; q0 < R; q0 += 8) {
+      int rq = std::min(8, R - q0);
+      const double* Xq = X + (long long)q0 * n;
+      double* Yq = Y + (long long)q0 * n;
+      // the narrowest instantiation that holds rq right-hand sides
+      if (rq <= 2)
+        k_symv_upper<2><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      else if (rq <= 4)
+        k_symv_upper<4><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      else if (rq <= 6)
+        k_symv_upper<6><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      else
+        k_symv_upper<8><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
+      GBEM_LAUNCH_CHECK(ctx);
+    }
+    }
+  return GBEM_OK;
+}
+
 // Triangular solves L L^T X = B with the stored factor (gbem_internal_factor),
 // residual ||A x - b|| / ||b|| from the preserved upper triangle when d_resid.
 int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
@@ -1635,59 +1698,8 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
   }
   cudaEventRecord(ctx->ev[2], s);
   if (d_resid) {
-    // A X on the tensor cores, one pass over A per 32 right-hand sides
-    // (k_symm_dmma: config 3 6.2 -> 2.6 ms); below n = 16,384 its 64-row CTAs
-    // cannot fill the machine and the scalar k_symv_upper (column chunks) is
-    // faster (config 2: 0.27 vs 0.55 ms).  GBEM_SYMV_SCALAR=1 forces the scalar one.
-    static const bool force_scalar = getenv("GBEM_SYMV_SCALAR") != nullptr;
-    const bool scalar = force_scalar || n < 16384;
-    if (!scalar) {
-      if (!(ctx->attr_set & gbem_ctx::kAttrSymm)) {
-        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)SymmShape<8>::SMEM));
-        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)SymmShape<16>::SMEM));
-        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)SymmShape<24>::SMEM));
-        GBEM_CUDA(ctx, cudaFuncSetAttribute(k_symm_dmma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)SymmShape<32>::SMEM));
-        ctx->attr_set |= gbem_ctx::kAttrSymm;
-      }
-      const unsigned grid = (unsigned)((n + kSyT - 1) / kSyT);
-      for (int q0 = 0; q0 < R; q0 += 32) {
-        const int rq = std::min(32, R - q0);
-        const double* Xq = d_X + (long long)q0 * n;
-        double* Yq = Ysym + (long long)q0 * n;
-        if (rq <= 8)
-          k_symm_dmma<8><<<grid, kSyThreads, SymmShape<8>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-        else if (rq <= 16)
-          k_symm_dmma<16><<<grid, kSyThreads, SymmShape<16>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-        else if (rq <= 24)
-          k_symm_dmma<24><<<grid, kSyThreads, SymmShape<24>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-        else
-          k_symm_dmma<32><<<grid, kSyThreads, SymmShape<32>::SMEM, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-        GBEM_LAUNCH_CHECK(ctx);
-      }
-    } else {
-        GBEM_CUDA(ctx, cudaMemsetAsync(Ysym, 0, sizeof(double) * (size_t)n * R, s));
-    int nbt = (n + 63) / 64;
-    const dim3 sgrid((unsigned)nbt, (unsigned)std::min(kSymvChunks, nbt));
-    for (int q0 = 0; q0 < R; q0 += 8) {
-      int rq = std::min(8, R - q0);
-      const double* Xq = d_X + (long long)q0 * n;
-      double* Yq = Ysym + (long long)q0 * n;
-      // the narrowest instantiation that holds rq right-hand sides
-      if (rq <= 2)
-        k_symv_upper<2><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-      else if (rq <= 4)
-        k_symv_upper<4><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-      else if (rq <= 6)
-        k_symv_upper<6><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-      else
-        k_symv_upper<8><<<sgrid, 256, 0, s>>>(ctx->d_A, lda, ctx->d_diag, n, Xq, n, rq, Yq);
-      GBEM_LAUNCH_CHECK(ctx);
-    }
-    }
+    rc = apply_sym(ctx, d_X, R, Ysym);
+    if (rc) return rc;
     k_resid_norm<<<R, 1024, 0, s>>>(Ysym, d_B, n, d_resid);
     GBEM_LAUNCH_CHECK(ctx);
   }
@@ -1709,6 +1721,22 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
     }
   }
   return GBEM_OK;
+}
+
+int gbem_internal_apply(gbem_ctx* ctx, const double* d_X, int64_t nrhs, double* d_Y) {
+  const int n = (int)ctx->n;
+  if (nrhs < 0 || nrhs > (1 << 20)) return ctx->fail(GBEM_EINVAL, "nrhs out of range");
+  if (n == 0 || nrhs == 0) return GBEM_OK;
+  if (!ctx->factored) {  // the diagonal is still in place: save it for apply_sym
+    if (ctx->diag_cap < n) {
+      cudaFree(ctx->d_diag);
+      GBEM_CUDA(ctx, cudaMalloc(&ctx->d_diag, sizeof(double) * n));
+      ctx->diag_cap = n;
+    }
+    k_save_diag<<<(n + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_A, ctx->lda, n, ctx->d_diag);
+    GBEM_LAUNCH_CHECK(ctx);
+  }
+  return apply_sym(ctx, d_X, (int)nrhs, d_Y);
 }
 
 int gbem_internal_solve(gbem_ctx* ctx, const double* d_B, int64_t nrhs, double* d_X, double* d_resid,
