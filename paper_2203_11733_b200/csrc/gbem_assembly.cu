@@ -749,6 +749,11 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
     const int r0 = s0 == 0 ? 1 : 0, r1 = s0 == 2 ? 1 : 2;
     const bool mid_second = (code >> 30) & 1u;
     double w1[M], W1[M];
+#if defined(GBEM_FAR_SETUP_ONLY) && GBEM_FAR_SETUP_ONLY == 1  // timing: no list work at all
+    for (int a = 0; a < M; ++a) w1[a] = W1[a] = A.a0 + B.b1 + code;
+    w2s[0] = W2s[0] = w3s[0] = W3s[0] = 1.0;
+    if (false)
+#endif
     {
       // the inner list goes through the middle list's slots into registers
       // (a direct per-node register emission was 6% slower: code size)
@@ -768,6 +773,10 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
     // the output scale now, so the panel records are dead during the node loop
     const double out_scale = 0.5 * (o.A ? rcp64(kFourPi * (panel_area(A) * panel_area(B))) : rcp64(kFourPi));
     double acc = 0.0;
+#ifdef GBEM_FAR_SETUP_ONLY  // timing experiment: the per-pair setup without the node loop (results wrong)
+    acc = w1[M - 1] + W1[M - 1] + w2s[0] + w3s[0];
+    if (false)
+#endif
     for (int c = 0; c < m3; ++c) {
       const double w3 = w3s[c * kFarThreads], W3 = W3s[c * kFarThreads];
       for (int b = 0; b < m2; ++b) {
