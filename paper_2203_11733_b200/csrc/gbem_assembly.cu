@@ -17,6 +17,7 @@
 // A[i*lda + j] so consecutive lanes (consecutive j) store contiguously.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "gbem_ctx.cuh"
@@ -40,6 +41,9 @@ __constant__ float c_cd2f[kQMax + 1];
 // Gauss-Legendre nodes / weights of the graded near-field rule (near_nodes(band) entries per band)
 __constant__ double c_nx[kNearBands][48];
 __constant__ double c_nw[kNearBands][48];
+// list descriptor (type | (q1-1) << 2 | q2 << 5) -> index of its specialised
+// far-field kernel (kFastDescs below), or -1
+__constant__ __align__(16) int8_t c_fast_idx[512];
 }  // namespace gbem_gpu
 
 namespace {
@@ -245,8 +249,8 @@ __device__ __forceinline__ uint32_t shared_axis_desc(const CPanel& A, const CPan
   return (uint32_t)kListProduct | (uint32_t)(qi - 1) << 2 | (uint32_t)qj << 5;
 }
 
-__device__ __forceinline__ uint32_t far_plan_code(const CPanel& A, const CPanel& B, float g2, int& m1, int& m2,
-                                                  int& m3) {
+__device__ __forceinline__ uint32_t far_plan_code(const CPanel& A, const CPanel& B, float g2, const int8_t* fast_idx,
+                                                  uint32_t& key) {
   uint32_t d[3];
   int m[3];
   const bool orth = A.axis != B.axis;
@@ -267,14 +271,26 @@ __device__ __forceinline__ uint32_t far_plan_code(const CPanel& A, const CPanel&
   const int s0 = (m[0] >= m[1] && m[0] >= m[2]) ? 0 : (m[1] >= m[2] ? 1 : 2);
   const int r0 = s0 == 0 ? 1 : 0, r1 = s0 == 2 ? 1 : 2;  // remaining sources in index order
   const int mid_second = m[r1] > m[r0] ? 1 : 0;
-  m1 = m[s0];
-  m2 = mid_second ? m[r1] : m[r0];
-  m3 = mid_second ? m[r0] : m[r1];
+  const int m1 = m[s0];
+  const int m2 = mid_second ? m[r1] : m[r0];
+  const int m3 = mid_second ? m[r0] : m[r1];
+  // specialised kernels (k_far_orth / k_far_par) when the inner list has one of their descriptors
+  const uint32_t di = s0 == 0 ? d[0] : (s0 == 1 ? d[1] : d[2]);
+  const uint32_t dm = mid_second ? (r1 == 1 ? d[1] : d[2]) : (r0 == 0 ? d[0] : d[1]);
+  const int fi = fast_idx[di];
+  if (fi >= 0 && orth && s0 == 0) {
+    key = kFastOrthBase + (uint32_t)(fi << 6 | (m2 - 1) << 3 | (m3 - 1));
+  } else if (fi >= 0 && !orth && (dm & 3u) >= (uint32_t)kListProduct) {
+    const uint32_t c2 = ((dm & 3u) == (uint32_t)kListTent ? 1u : 0u) | ((dm >> 2) & 7u) << 1 | (dm >> 5) << 4;
+    key = kFastParBase + ((uint32_t)fi << 8 | c2);
+  } else {
+    key = far_key(m1, m2, m3);
+  }
   return (orth ? 1u : 0u) | d[0] << 1 | d[1] << 10 | d[2] << 19 | (uint32_t)s0 << 28 | (uint32_t)mid_second << 30;
 }
 
 __device__ __forceinline__ uint32_t classify_pair(const CPanel& A, const CPanel& B, bool same, double near_ratio,
-                                                  uint32_t& plan) {
+                                                  const int8_t* fast_idx, uint32_t& plan) {
   plan = 0;
   if (same) return kClsCoplanar;
   double gap2 = 0.0;
@@ -300,9 +316,9 @@ __device__ __forceinline__ uint32_t classify_pair(const CPanel& A, const CPanel&
       return same_axis ? kClsParallel : kClsOrthogonal;  // near contact: adaptive Romberg
     return (same_axis ? kClsParallelGL : kClsOrthogonalGL) + band;
   }
-  int m1, m2, m3;
-  plan = far_plan_code(A, B, (float)gap2, m1, m2, m3);
-  return far_key(m1, m2, m3);
+  uint32_t key;
+  plan = far_plan_code(A, B, (float)gap2, fast_idx, key);
+  return key;
 }
 
 // Per-CTA key aggregation: warp groups of equal keys (__match_any_sync) add
@@ -332,6 +348,9 @@ __global__ void __launch_bounds__(kClassifyThreads)
   constexpr int kIter = kTile / (kClassifyThreads / 32);
   __shared__ CPanel si[kTile], sj[kTile];
   __shared__ uint32_t hkey[kHash], hcnt[kHash];
+  __shared__ __align__(4) int8_t sfast[512];
+  if (!FILL && threadIdx.x < 128)
+    reinterpret_cast<uint32_t*>(sfast)[threadIdx.x] = reinterpret_cast<const uint32_t*>(c_fast_idx)[threadIdx.x];
   const long long t = tile_begin + blockIdx.x;
   // tile row of t: full rows hold nbt tiles each; upper-triangle rows hold
   // nbt - bi tiles, so tile_row_off[r] = r c - r (r - 1) / 2 with c = nbt - bi0,
@@ -379,7 +398,7 @@ __global__ void __launch_bounds__(kClassifyThreads)
     // pass 1 classifies and keeps (key, plan) in tile order; pass 2 reads them back
     uint64_t* kp_at = kp + (size_t)blockIdx.x * (kTile * kTile) + r * kTile + lane;
     if (!FILL) {
-      key[it] = valid ? classify_pair(si[r], sj[lane], i == j, near_ratio, plan[it]) : kEmpty;
+      key[it] = valid ? classify_pair(si[r], sj[lane], i == j, near_ratio, sfast, plan[it]) : kEmpty;
       *kp_at = (uint64_t)key[it] << 32 | plan[it];
     } else {
       const uint64_t v = *kp_at;
@@ -449,10 +468,14 @@ template <bool FILL>
 __global__ void __launch_bounds__(256)
     k_classify_list(const CPanel* __restrict__ P, int npairs, double near_ratio, uint32_t* counts,
                     uint32_t* cursors, uint64_t* queue, uint32_t* plans) {
+  __shared__ __align__(4) int8_t sfast[512];
+  if (threadIdx.x < 128)
+    reinterpret_cast<uint32_t*>(sfast)[threadIdx.x] = reinterpret_cast<const uint32_t*>(c_fast_idx)[threadIdx.x];
+  __syncthreads();
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = k < npairs;
   uint32_t key = 0, plan = 0;
-  if (valid) key = classify_pair(P[k], P[npairs + k], false, near_ratio, plan);
+  if (valid) key = classify_pair(P[k], P[npairs + k], false, near_ratio, sfast, plan);
   warp_append<FILL>(valid, key, plan, (uint32_t)k, (uint32_t)(npairs + k), counts, cursors, queue, plans);
 }
 
@@ -712,7 +735,7 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
   double* w3s = ow2 + OUT2 * kFarThreads + threadIdx.x;
   double* W3s = oW + OUT2 * kFarThreads + threadIdx.x;
   const uint32_t begin = offsets[far_key_first(M)];
-  const uint32_t end = offsets[M < kFarListMax ? far_key_first(M + 1) : kNumKeys];
+  const uint32_t end = offsets[far_key_first(M + 1)];
   unsigned long long flops = 0, evals = 0;
   const uint32_t stride = gridDim.x * blockDim.x;
   // Software pipeline over a thread's pairs: the queue entry and plan two runs
@@ -807,6 +830,307 @@ __global__ void __launch_bounds__(far_threads(M), M <= 12 ? GBEM_FAR_MINB : 2)
   fl = warp_reduce_d(fl);
   ev = warp_reduce_d(ev);
   if ((threadIdx.x & 31) == 0) {
+    atomicAdd(reinterpret_cast<double*>(&stats[ST_FAR_FLOPS]), fl);
+    atomicAdd(&stats[ST_FAR_EVALS], (unsigned long long)ev);
+  }
+}
+
+// ---------------------------------------------------------------- far field, specialised
+//
+// Most far pairs share a handful of inner-list shapes (configs 2-4: 22
+// descriptors cover 98%).  For those the generic kernel's per-pair setup --
+// three descriptor decodes, three run-time emission loops through
+// shared-memory slots and the reload of the inner list, more warp instructions
+// than the node loops themselves (DESIGN 9) -- is replaced by kernels compiled
+// per inner descriptor: the inner list is emitted straight into registers by
+// fully unrolled code whose Gauss nodes are constant-bank operands, and the
+// other two lists are never stored: the single rules of an orthogonal pair and
+// the second shared axis of a parallel pair are generated inside the (c, b)
+// loops (3-5 FP64 operations per M-node row).  The descriptor is part of the
+// queue key, so a kernel's segment is contiguous and its loops warp-uniform.
+#define GBEM_FAST_DESCS(X)                                                                              \
+  X(0, kListProduct, 2, 2) X(1, kListProduct, 2, 3) X(2, kListProduct, 3, 2) X(3, kListProduct, 3, 3)     \
+  X(4, kListTent, 3, 0) X(5, kListTent, 3, 1) X(6, kListTent, 3, 2) X(7, kListTent, 3, 3)                \
+  X(8, kListTent, 3, 4) X(9, kListTent, 3, 5) X(10, kListTent, 4, 0) X(11, kListTent, 4, 1)              \
+  X(12, kListTent, 4, 2) X(13, kListTent, 4, 3) X(14, kListTent, 4, 4) X(15, kListTent, 4, 5)            \
+  X(16, kListTent, 5, 0) X(17, kListTent, 5, 1) X(18, kListTent, 5, 2) X(19, kListTent, 5, 3)            \
+  X(20, kListTent, 5, 4) X(21, kListTent, 6, 0) X(22, kListTent, 6, 1) X(23, kListProduct, 2, 4)         \
+  X(24, kListProduct, 4, 2)
+
+__host__ __device__ constexpr int fast_inner_size(int type, int q1, int q2) {
+  return type == kListTent ? 2 * q1 + q2 : q1 * q2;
+}
+
+// Inner list of a shared axis, I = [s0, s1], J = [u0, u1], into registers.
+// Tent nodes and weights are the generic emit_list's, operation for operation;
+// a product list leaves its constant factor h_I h_J to `scale`.
+template <int TYPE, int Q1, int Q2>
+__device__ __forceinline__ void emit_inner(double s0, double s1, double u0, double u1,
+                                           double (&w2)[fast_inner_size(TYPE, Q1, Q2)],
+                                           double (&W)[fast_inner_size(TYPE, Q1, Q2)], double& scale) {
+  if (TYPE == kListTent) {
+    const double p0 = s0 - u1, p1 = fmin(s0 - u0, s1 - u1), p2 = fmax(s0 - u0, s1 - u1), p3 = s1 - u0;
+    const double p4 = fmin(s1 - s0, u1 - u0);
+    {
+      const double c = 0.5 * (p0 + p1), h = 0.5 * (p1 - p0);
+#pragma unroll
+      for (int k = 0; k < Q1; ++k) {
+        const double w = fma(h, c_gx[Q1][k], c);
+        w2[k] = w * w;
+        W[k] = (h * c_gw[Q1][k]) * (w - p0);
+      }
+    }
+    if (Q2 > 0) {
+      const double c = 0.5 * (p1 + p2), h = 0.5 * (p2 - p1);
+#pragma unroll
+      for (int k = 0; k < Q2; ++k) {
+        const double w = fma(h, c_gx[Q2][k], c);
+        w2[Q1 + k] = w * w;
+        W[Q1 + k] = (h * c_gw[Q2][k]) * p4;
+      }
+    }
+    {
+      const double c = 0.5 * (p2 + p3), h = 0.5 * (p3 - p2);
+#pragma unroll
+      for (int k = 0; k < Q1; ++k) {
+        const double w = fma(h, c_gx[Q1][k], c);
+        w2[Q1 + Q2 + k] = w * w;
+        W[Q1 + Q2 + k] = (h * c_gw[Q1][k]) * (p3 - w);
+      }
+    }
+  } else {
+    const double p0 = 0.5 * (s0 + s1) - 0.5 * (u0 + u1), p1 = 0.5 * (s1 - s0), p2 = 0.5 * (u1 - u0);
+    scale *= p1 * p2;
+#pragma unroll
+    for (int a = 0; a < Q1; ++a) {
+      const double ca = fma(p1, c_gx[Q1][a], p0);
+#pragma unroll
+      for (int b = 0; b < Q2; ++b) {
+        const double w = fma(-p2, c_gx[Q2][b], ca);
+        w2[a * Q2 + b] = w * w;
+        W[a * Q2 + b] = c_gw[Q1][a] * c_gw[Q2][b];
+      }
+    }
+  }
+}
+
+// sum_a W1_a * 2 / sqrt(r2 + w1_a) (wrsq3_acc; two partial sums)
+template <int M>
+__device__ __forceinline__ double inner_row(const double (&w1)[M], const double (&W1)[M], double r2) {
+  double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+  for (int a = 0; a < M; a += 2) {
+    t0 = wrsq3_acc(W1[a], r2 + w1[a], t0);
+    if (a + 1 < M) t1 = wrsq3_acc(W1[a + 1], r2 + w1[a + 1], t1);
+  }
+  return t0 + t1;
+}
+
+#ifndef GBEM_FAST_MINB
+#define GBEM_FAST_MINB 4
+#endif
+
+// Orthogonal pairs: inner = the shared axis (descriptor TYPE, Q1, Q2), middle
+// and outer = the single rules of orders m2 >= m3 (I along J's normal, J along
+// I's normal; the plan's mid_second bit says which is the middle one).
+template <int TYPE, int Q1, int Q2>
+__global__ void __launch_bounds__(128, GBEM_FAST_MINB)
+    k_far_orth(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue, const uint32_t* __restrict__ plans,
+               const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats, int d) {
+  constexpr int M = fast_inner_size(TYPE, Q1, Q2);
+  __shared__ double sgx[(kQMax + 1) * kQMax], sgw[(kQMax + 1) * kQMax];
+  for (int t = threadIdx.x; t < (kQMax + 1) * kQMax; t += blockDim.x) {
+    sgx[t] = (&c_gx[0][0])[t];
+    sgw[t] = (&c_gw[0][0])[t];
+  }
+  __syncthreads();
+  const uint32_t begin = offsets[kFastOrthBase + (uint32_t)(d << 6)];
+  const uint32_t end = offsets[kFastOrthBase + (uint32_t)((d + 1) << 6)];
+  unsigned long long flops = 0, evals = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t base = begin + (blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
+  uint32_t nidx = base + (threadIdx.x & 31u);
+  uint64_t ne = nidx < end ? queue[nidx] : 0;
+  uint32_t ncode = nidx < end ? plans[nidx] : 0;
+  uint32_t nnidx = nidx + stride;
+  uint64_t nne = nnidx < end ? queue[nnidx] : 0;
+  uint32_t nncode = nnidx < end ? plans[nnidx] : 0;
+  for (; base < end; base += stride) {
+    const uint32_t idx = nidx;
+    const uint64_t e = ne;
+    const uint32_t code = ncode;
+    nidx = nnidx;
+    ne = nne;
+    ncode = nncode;
+    nnidx += stride;
+    if (nnidx < end) {
+      nne = queue[nnidx];
+      nncode = plans[nnidx];
+    }
+    if (nidx < end) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_i(ne)));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_j(ne)));
+    }
+    if (idx >= end) continue;
+    const uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e);
+    const int m2 = (int)((key >> 3) & 7u) + 1, m3 = (int)(key & 7u) + 1;
+    const DPanel A = load_panel(P, i), B = load_panel(P, j);
+    double scale = 0.5 * (o.A ? rcp64(kFourPi * (panel_area(A) * panel_area(B))) : rcp64(kFourPi));
+    double w1[M], W1[M];
+    {
+      double s0, s1, u0, u1;
+      const int k = 3 - A.axis - B.axis;
+      panel_extent(A, k, s0, s1);
+      panel_extent(B, k, u0, u1);
+      emit_inner<TYPE, Q1, Q2>(s0, s1, u0, u1, w1, W1, scale);
+    }
+    // single rules: w = c + h x_k, W = h g_k (h folded into the scale)
+    double c0, c1;
+    panel_extent(A, B.axis, c0, c1);
+    const double ca = 0.5 * (c0 + c1) - B.level, ha = 0.5 * (c1 - c0);
+    panel_extent(B, A.axis, c0, c1);
+    const double cb = 0.5 * (c0 + c1) - A.level, hb = 0.5 * (c1 - c0);
+    scale *= ha * hb;
+    const bool mid_second = (code >> 30) & 1u;
+    const double cm = mid_second ? cb : ca, hm = mid_second ? hb : ha;
+    const double co = mid_second ? ca : cb, ho = mid_second ? ha : hb;
+    const double *gx2 = sgx + m2 * kQMax, *gw2 = sgw + m2 * kQMax;
+    const double *gx3 = sgx + m3 * kQMax, *gw3 = sgw + m3 * kQMax;
+    double acc = 0.0;
+    for (int c = 0; c < m3; ++c) {
+      const double w3 = fma(ho, gx3[c], co);
+      const double w3s = w3 * w3, W3 = gw3[c];
+      for (int b = 0; b < m2; ++b) {
+        const double w2 = fma(hm, gx2[b], cm);
+        acc = fma(W3 * gw2[b], inner_row<M>(w1, W1, fma(w2, w2, w3s)), acc);
+      }
+    }
+    acc *= scale;
+    const uint32_t rows = (uint32_t)(m2 * m3);
+    evals += (uint32_t)M * rows;
+    flops += 7u * (uint32_t)M * rows + 7u * rows + 5u * (uint32_t)M + 40u;
+    if (o.A) {
+      o.A[(long long)i * o.lda + (long long)j * o.ldc] = acc;
+    } else {
+      o.out[i] = acc;
+      if (o.conv) o.conv[i] = 1;
+    }
+  }
+  double fl = (double)flops, ev = (double)evals;
+  fl = warp_reduce_d(fl);
+  ev = warp_reduce_d(ev);
+  if ((threadIdx.x & 31) == 0 && ev > 0.0) {
+    atomicAdd(reinterpret_cast<double*>(&stats[ST_FAR_FLOPS]), fl);
+    atomicAdd(&stats[ST_FAR_EVALS], (unsigned long long)ev);
+  }
+}
+
+// Parallel pairs: inner = the larger shared-axis list (descriptor TYPE, Q1, Q2;
+// plan bits 28-29 say which in-plane axis), middle = the other shared axis,
+// generated piece by piece inside the loop from the descriptor in the key;
+// the normal offset is a constant.
+template <int TYPE, int Q1, int Q2>
+__global__ void __launch_bounds__(128, GBEM_FAST_MINB)
+    k_far_par(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue, const uint32_t* __restrict__ plans,
+              const uint32_t* __restrict__ offsets, OutSpec o, unsigned long long* stats, int d) {
+  constexpr int M = fast_inner_size(TYPE, Q1, Q2);
+  __shared__ double sgx[(kQMax + 1) * kQMax], sgw[(kQMax + 1) * kQMax];
+  for (int t = threadIdx.x; t < (kQMax + 1) * kQMax; t += blockDim.x) {
+    sgx[t] = (&c_gx[0][0])[t];
+    sgw[t] = (&c_gw[0][0])[t];
+  }
+  __syncthreads();
+  const uint32_t begin = offsets[kFastParBase + (uint32_t)(d << 8)];
+  const uint32_t end = offsets[kFastParBase + (uint32_t)((d + 1) << 8)];
+  unsigned long long flops = 0, evals = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t base = begin + (blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
+  uint32_t nidx = base + (threadIdx.x & 31u);
+  uint64_t ne = nidx < end ? queue[nidx] : 0;
+  uint32_t ncode = nidx < end ? plans[nidx] : 0;
+  uint32_t nnidx = nidx + stride;
+  uint64_t nne = nnidx < end ? queue[nnidx] : 0;
+  uint32_t nncode = nnidx < end ? plans[nnidx] : 0;
+  for (; base < end; base += stride) {
+    const uint32_t idx = nidx;
+    const uint64_t e = ne;
+    const uint32_t code = ncode;
+    nidx = nnidx;
+    ne = nne;
+    ncode = nncode;
+    nnidx += stride;
+    if (nnidx < end) {
+      nne = queue[nnidx];
+      nncode = plans[nnidx];
+    }
+    if (nidx < end) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_i(ne)));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_j(ne)));
+    }
+    if (idx >= end) continue;
+    const uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e);
+    const bool tent2 = key & 1u;
+    const int q1 = (int)((key >> 1) & 7u) + 1, q2 = (int)((key >> 4) & 15u);
+    const DPanel A = load_panel(P, i), B = load_panel(P, j);
+    double scale = 0.5 * (o.A ? rcp64(kFourPi * (panel_area(A) * panel_area(B))) : rcp64(kFourPi));
+    const bool inner_first = ((code >> 28) & 3u) == 0u;  // inner list on ip0, middle on ip1 (else swapped)
+    double w1[M], W1[M];
+    {
+      // a parallel pair's in-plane axes are the panels' own a / b spans
+      const double s0 = inner_first ? A.a0 : A.b0, s1 = inner_first ? A.a1 : A.b1;
+      const double u0 = inner_first ? B.a0 : B.b0, u1 = inner_first ? B.a1 : B.b1;
+      emit_inner<TYPE, Q1, Q2>(s0, s1, u0, u1, w1, W1, scale);
+    }
+    const double s0 = inner_first ? A.b0 : A.a0, s1 = inner_first ? A.b1 : A.a1;
+    const double u0 = inner_first ? B.b0 : B.a0, u1 = inner_first ? B.b1 : B.a1;
+    const double dz = A.level - B.level, dz2 = dz * dz;
+    double acc = 0.0;
+    int rows;
+    if (tent2) {
+      rows = 2 * q1 + q2;
+      const double p0 = s0 - u1, p1 = fmin(s0 - u0, s1 - u1), p2 = fmax(s0 - u0, s1 - u1), p3 = s1 - u0;
+      const double p4 = fmin(s1 - s0, u1 - u0);
+      for (int piece = 0; piece < 3; ++piece) {
+        const bool up = piece == 0, flat = piece == 1;
+        const int q = flat ? q2 : q1;
+        const double lo = up ? p0 : (flat ? p1 : p2), hi = up ? p1 : (flat ? p2 : p3);
+        const double c = 0.5 * (lo + hi), h = 0.5 * (hi - lo);
+        const double al = up ? -p0 : (flat ? p4 : p3), be = up ? 1.0 : (flat ? 0.0 : -1.0);
+        const double *gx = sgx + q * kQMax, *gw = sgw + q * kQMax;
+        for (int k = 0; k < q; ++k) {
+          const double w = fma(h, gx[k], c);
+          const double Wn = (h * gw[k]) * fma(be, w, al);
+          acc = fma(Wn, inner_row<M>(w1, W1, fma(w, w, dz2)), acc);
+        }
+      }
+    } else {
+      rows = q1 * q2;
+      const double p0 = 0.5 * (s0 + s1) - 0.5 * (u0 + u1), p1 = 0.5 * (s1 - s0), p2 = 0.5 * (u1 - u0);
+      scale *= p1 * p2;
+      const double *gxa = sgx + q1 * kQMax, *gwa = sgw + q1 * kQMax;
+      const double *gxb = sgx + q2 * kQMax, *gwb = sgw + q2 * kQMax;
+      for (int a = 0; a < q1; ++a) {
+        const double ca = fma(p1, gxa[a], p0), fa = gwa[a];
+        for (int b = 0; b < q2; ++b) {
+          const double w = fma(-p2, gxb[b], ca);
+          acc = fma(fa * gwb[b], inner_row<M>(w1, W1, fma(w, w, dz2)), acc);
+        }
+      }
+    }
+    acc *= scale;
+    evals += (uint32_t)(M * rows);
+    flops += 7u * (uint32_t)(M * rows) + 8u * (uint32_t)rows + 5u * (uint32_t)M + 40u;
+    if (o.A) {
+      o.A[(long long)i * o.lda + (long long)j * o.ldc] = acc;
+    } else {
+      o.out[i] = acc;
+      if (o.conv) o.conv[i] = 1;
+    }
+  }
+  double fl = (double)flops, ev = (double)evals;
+  fl = warp_reduce_d(fl);
+  ev = warp_reduce_d(ev);
+  if ((threadIdx.x & 31) == 0 && ev > 0.0) {
     atomicAdd(reinterpret_cast<double*>(&stats[ST_FAR_FLOPS]), fl);
     atomicAdd(&stats[ST_FAR_EVALS], (unsigned long long)ev);
   }
@@ -1037,6 +1361,15 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
   GBEM_FAR(9) GBEM_FAR(10) GBEM_FAR(11) GBEM_FAR(12) GBEM_FAR(13) GBEM_FAR(14) GBEM_FAR(15) GBEM_FAR(16)
   GBEM_FAR(17) GBEM_FAR(18) GBEM_FAR(19) GBEM_FAR(20) GBEM_FAR(21) GBEM_FAR(22) GBEM_FAR(23) GBEM_FAR(24)
 #undef GBEM_FAR
+#define GBEM_FAST(D, TYPE, Q1, Q2)                                                                                \
+  k_far_orth<TYPE, Q1, Q2><<<sms * GBEM_FAST_MINB, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan, \
+                                                                         ctx->d_offsets, o, ctx->d_stats, D);      \
+  GBEM_LAUNCH_CHECK(ctx);                                                                                         \
+  k_far_par<TYPE, Q1, Q2><<<sms * GBEM_FAST_MINB, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan,  \
+                                                                        ctx->d_offsets, o, ctx->d_stats, D);       \
+  GBEM_LAUNCH_CHECK(ctx);
+  GBEM_FAST_DESCS(GBEM_FAST)
+#undef GBEM_FAST
   cudaEventRecord(ctx->ev[3], ctx->stream);
   k_coplanar<<<sms * 4, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o);
   GBEM_LAUNCH_CHECK(ctx);
@@ -1098,6 +1431,16 @@ int gbem_internal_init_tables(gbem_ctx* ctx) {
   for (int b = 0; b < kNearBands; ++b) legendre_nodes(near_nodes(b), nx[b], nw[b]);
   GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_nx, nx, sizeof(nx)));
   GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_nw, nw, sizeof(nw)));
+  int8_t fast[512];
+  for (int k = 0; k < 512; ++k) fast[k] = -1;
+  if (!getenv("GBEM_NO_FAST_FAR")) {  // experiments: every far pair through the generic kernels
+#define GBEM_FAST_ENTRY(D, TYPE, Q1, Q2) \
+  static_assert(D < kFastMax, "descriptor index"); \
+  fast[(int)TYPE | (Q1 - 1) << 2 | Q2 << 5] = D;
+    GBEM_FAST_DESCS(GBEM_FAST_ENTRY)
+#undef GBEM_FAST_ENTRY
+  }
+  GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_fast_idx, fast, sizeof(fast)));
   return GBEM_OK;
 }
 

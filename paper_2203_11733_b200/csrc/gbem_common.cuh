@@ -48,6 +48,17 @@ __host__ __device__ inline uint32_t far_key(int m1, int m2, int m3) {
 }
 __host__ __device__ inline uint32_t far_key_first(int m1) { return 16u + (uint32_t)((m1 - 1) << 8); }
 
+// Specialised far keys (gbem_assembly.cu, k_far_orth / k_far_par): pairs whose
+// inner list has one of the kFastDescs descriptors (index d) run in a kernel
+// compiled for that descriptor, the other two lists generated inside the node
+// loops.  Orthogonal pairs (inner = the shared axis; two single rules of
+// orders m2 >= m3):   key = kFastOrthBase + (d << 6 | (m2-1) << 3 | (m3-1))
+// Parallel pairs (middle = the other shared axis with descriptor
+// c2 = tent | (q1-1) << 1 | q2 << 4; the normal offset is a constant):
+//                     key = kFastParBase + (d << 8 | c2)
+constexpr uint32_t kFastOrthBase = 8192, kFastParBase = 16384;
+constexpr int kFastMax = 32;  // descriptor indices d < kFastMax
+
 // Queue entry: i (24 bits) | j (24 bits) | key (16 bits).
 __host__ __device__ inline uint64_t pack_entry(uint32_t i, uint32_t j, uint32_t key) {
   return ((uint64_t)i << 40) | ((uint64_t)j << 16) | (uint64_t)key;
