@@ -44,6 +44,15 @@ __constant__ double c_nw[kNearBands][48];
 // list descriptor (type | (q1-1) << 2 | q2 << 5) -> index of its specialised
 // far-field kernel (kFastDescs below), or -1
 __constant__ __align__(16) int8_t c_fast_idx[512];
+// Weight-folded nodes of the specialised far-field kernels: W / sqrt(x) = S / sqrt(x kappa)
+// with kappa = (S / W)^2 a constant of the rule once the geometric scale S is factored out:
+//   tent ramp of order q (S = h^2):      W_k = h^2 g_k (1 + x_k)   c_kr[q][k]  = 1 / (g_k (1 + x_k))^2
+//   tent plateau of order q (S = h T):   W_k = h T g_k             c_kp[q][k]  = 1 / g_k^2
+//   product rule q1 x q2 (S = h_I h_J):  W   = S g_a g_b           c_kpp[q1][q2][a q2 + b] = 1 / (g_a g_b)^2
+constexpr int kQProd = 4;  // product inner lists up to 4 x 4
+__constant__ double c_kr[kQMax + 1][kQMax];
+__constant__ double c_kp[kQMax + 1][kQMax];
+__constant__ double c_kpp[kQProd + 1][kQProd + 1][kQProd * kQProd];
 }  // namespace gbem_gpu
 
 namespace {
@@ -581,27 +590,16 @@ __device__ __forceinline__ double rcp64(double x) {
   return fma(r, e, r);
 }
 
-// acc + W / sqrt(x): MUFU.RSQ64H seed y (relative error <= 9.1e-7) and one
-// Newton step folded into the weighted accumulation,
-//   W / sqrt(x) ~ W y (1 + e / 2),  e = 1 - x y^2,
-// relative error <= 1.3e-12 per node (tools/rsq_acc.cu), an order below the
-// far-field rule's own 1e-12 tolerance and 100x inside the 1e-10 gate;
-// 5 FP64-pipe instructions + MUFU instead of 6 for the Householder form.
 // acc + W y (3 - x y^2): twice W / sqrt(x) after one Newton step from the
-// MUFU.RSQ64H seed (the step wrsq_acc folds differently; the factor 1/2 is
-// applied once per pair): DADD, DMUL, DFMA, DMUL, DFMA per node -- one
-// FP64-pipe instruction fewer than wrsq_acc's form.
+// MUFU.RSQ64H seed y (relative error <= 9.1e-7; after the step <= 1.3e-12 per
+// node, tools/rsq_acc.cu: an order below the far-field rule's own 1e-12
+// tolerance and 100x inside the 1e-10 gate).  The factor 1/2 is applied once
+// per pair.  With the DADD that forms x: DADD, DMUL, DFMA, DMUL, DFMA per node.
 __device__ __forceinline__ double wrsq3_acc(double W, double x, double acc) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double e3 = fma(-(x * y), y, 3.0);
   return fma(W * y, e3, acc);
-}
-__device__ __forceinline__ double wrsq_acc(double W, double x, double acc) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double e = fma(-x * y, y, 1.0);
-  return fma(W * y, fma(0.5, e, 1.0), acc);
 }
 
 // One decoded list: type, orders, and the geometry of its nodes
@@ -861,42 +859,41 @@ __host__ __device__ constexpr int fast_inner_size(int type, int q1, int q2) {
   return type == kListTent ? 2 * q1 + q2 : q1 * q2;
 }
 
-// Inner list of a shared axis, I = [s0, s1], J = [u0, u1], into registers.
-// Tent nodes and weights are the generic emit_list's, operation for operation;
-// a product list leaves its constant factor h_I h_J to `scale`.
+// Inner list of a shared axis, I = [s0, s1], J = [u0, u1], into registers, weights folded into
+// the nodes: slot k holds cw_k = w_k^2 kappa_k, so that inside the node loops
+//   W_k / sqrt(r2 + w_k^2) = S / sqrt(fma(r2, kappa_k, cw_k))
+// with kappa_k a constant-bank operand (c_kr / c_kp / c_kpp) and S one scale per piece.  Tent:
+// ramps [p0, p0 + 2 hr] and [p3 - 2 hr, p3] (T = w - p0, p3 - w; hr = min(L_I, L_J) / 2, scale
+// hr^2 in sr) around the plateau of half-length hp = |L_I - L_J| / 2 (T = 2 hr, scale 2 hr hp in
+// sp); product: every node carries h_I h_J, which goes to `scale`.
 template <int TYPE, int Q1, int Q2>
 __device__ __forceinline__ void emit_inner(double s0, double s1, double u0, double u1,
-                                           double (&w2)[fast_inner_size(TYPE, Q1, Q2)],
-                                           double (&W)[fast_inner_size(TYPE, Q1, Q2)], double& scale) {
+                                           double (&cw)[fast_inner_size(TYPE, Q1, Q2)], double& sr, double& sp,
+                                           double& scale) {
   if (TYPE == kListTent) {
-    const double p0 = s0 - u1, p1 = fmin(s0 - u0, s1 - u1), p2 = fmax(s0 - u0, s1 - u1), p3 = s1 - u0;
-    const double p4 = fmin(s1 - s0, u1 - u0);
-    {
-      const double c = 0.5 * (p0 + p1), h = 0.5 * (p1 - p0);
+    const double p0 = s0 - u1, p3 = s1 - u0;
+    const double li = s1 - s0, lj = u1 - u0;
+    const double hr = 0.5 * fmin(li, lj);
+    sr = hr * hr;
+    const double cu = p0 + hr, cd = p3 - hr;
 #pragma unroll
-      for (int k = 0; k < Q1; ++k) {
-        const double w = fma(h, c_gx[Q1][k], c);
-        w2[k] = w * w;
-        W[k] = (h * c_gw[Q1][k]) * (w - p0);
-      }
+    for (int k = 0; k < Q1; ++k) {
+      const double w = fma(hr, c_gx[Q1][k], cu);
+      cw[k] = (w * w) * c_kr[Q1][k];
     }
     if (Q2 > 0) {
-      const double c = 0.5 * (p1 + p2), h = 0.5 * (p2 - p1);
+      const double hp = 0.5 * fabs(li - lj), c = 0.5 * (p0 + p3);
+      sp = (2.0 * hr) * hp;
 #pragma unroll
       for (int k = 0; k < Q2; ++k) {
-        const double w = fma(h, c_gx[Q2][k], c);
-        w2[Q1 + k] = w * w;
-        W[Q1 + k] = (h * c_gw[Q2][k]) * p4;
+        const double w = fma(hp, c_gx[Q2][k], c);
+        cw[Q1 + k] = (w * w) * c_kp[Q2][k];
       }
     }
-    {
-      const double c = 0.5 * (p2 + p3), h = 0.5 * (p3 - p2);
 #pragma unroll
-      for (int k = 0; k < Q1; ++k) {
-        const double w = fma(h, c_gx[Q1][k], c);
-        w2[Q1 + Q2 + k] = w * w;
-        W[Q1 + Q2 + k] = (h * c_gw[Q1][k]) * (p3 - w);
-      }
+    for (int k = 0; k < Q1; ++k) {
+      const double w = fma(hr, c_gx[Q1][k], cd);
+      cw[Q1 + Q2 + k] = (w * w) * c_kr[Q1][Q1 - 1 - k];  // T = hr (1 - x_k): the mirrored ramp
     }
   } else {
     const double p0 = 0.5 * (s0 + s1) - 0.5 * (u0 + u1), p1 = 0.5 * (s1 - s0), p2 = 0.5 * (u1 - u0);
@@ -907,23 +904,47 @@ __device__ __forceinline__ void emit_inner(double s0, double s1, double u0, doub
 #pragma unroll
       for (int b = 0; b < Q2; ++b) {
         const double w = fma(-p2, c_gx[Q2][b], ca);
-        w2[a * Q2 + b] = w * w;
-        W[a * Q2 + b] = c_gw[Q1][a] * c_gw[Q2][b];
+        cw[a * Q2 + b] = (w * w) * c_kpp[Q1][Q2][a * Q2 + b];
       }
     }
   }
 }
 
-// sum_a W1_a * 2 / sqrt(r2 + w1_a) (wrsq3_acc; two partial sums)
-template <int M>
-__device__ __forceinline__ double inner_row(const double (&w1)[M], const double (&W1)[M], double r2) {
-  double t0 = 0.0, t1 = 0.0;
+// acc + 2 / sqrt(x): MUFU.RSQ64H seed and one Newton step, y (3 - x y^2) (the 1/2 is applied
+// once per pair): DMUL, DFMA, DFMA -- with the DFMA that forms x, 4 FP64-pipe instructions per
+// node beside the MUFU (wrsq3_acc, which carries a weight per node, needs 5).
+__device__ __forceinline__ double rsq3_acc(double x, double acc) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return fma(y, fma(-(x * y), y, 3.0), acc);
+}
+
+// sum_k W_k * 2 / sqrt(r2 + w_k^2) over the inner list (weight-folded nodes, emit_inner)
+template <int TYPE, int Q1, int Q2>
+__device__ __forceinline__ double inner_row(const double (&cw)[fast_inner_size(TYPE, Q1, Q2)], double r2, double sr,
+                                            double sp) {
+  if (TYPE == kListTent) {
+    double tu = 0.0, td = 0.0;
 #pragma unroll
-  for (int a = 0; a < M; a += 2) {
-    t0 = wrsq3_acc(W1[a], r2 + w1[a], t0);
-    if (a + 1 < M) t1 = wrsq3_acc(W1[a + 1], r2 + w1[a + 1], t1);
+    for (int k = 0; k < Q1; ++k) {
+      tu = rsq3_acc(fma(r2, c_kr[Q1][k], cw[k]), tu);
+      td = rsq3_acc(fma(r2, c_kr[Q1][Q1 - 1 - k], cw[Q1 + Q2 + k]), td);
+    }
+    if (Q2 == 0) return sr * (tu + td);
+    double tp = 0.0;
+#pragma unroll
+    for (int k = 0; k < Q2; ++k) tp = rsq3_acc(fma(r2, c_kp[Q2][k], cw[Q1 + k]), tp);
+    return fma(sr, tu + td, sp * tp);
+  } else {
+    constexpr int M = Q1 * Q2;
+    double t0 = 0.0, t1 = 0.0;
+#pragma unroll
+    for (int a = 0; a < M; a += 2) {
+      t0 = rsq3_acc(fma(r2, c_kpp[Q1][Q2][a], cw[a]), t0);
+      if (a + 1 < M) t1 = rsq3_acc(fma(r2, c_kpp[Q1][Q2][a + 1], cw[a + 1]), t1);
+    }
+    return t0 + t1;
   }
-  return t0 + t1;
 }
 
 #ifndef GBEM_FAST_MINB
@@ -955,6 +976,7 @@ __global__ void __launch_bounds__(128, GBEM_FAST_MINB)
   uint32_t nnidx = nidx + stride;
   uint64_t nne = nnidx < end ? queue[nnidx] : 0;
   uint32_t nncode = nnidx < end ? plans[nnidx] : 0;
+  DPanel nA = load_panel(P, nidx < end ? entry_i(ne) : 0u), nB = load_panel(P, nidx < end ? entry_j(ne) : 0u);
   for (; base < end; base += stride) {
     const uint32_t idx = nidx;
     const uint64_t e = ne;
@@ -967,22 +989,24 @@ __global__ void __launch_bounds__(128, GBEM_FAST_MINB)
       nne = queue[nnidx];
       nncode = plans[nnidx];
     }
+    // this pair's panel records were loaded during the previous pair's node loops
+    // (an L1 prefetch covers one 128-byte line; 3 of 8 48-byte records straddle two)
+    const DPanel A = nA, B = nB;
     if (nidx < end) {
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_i(ne)));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_j(ne)));
+      nA = load_panel(P, entry_i(ne));
+      nB = load_panel(P, entry_j(ne));
     }
     if (idx >= end) continue;
     const uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e);
     const int m2 = (int)((key >> 3) & 7u) + 1, m3 = (int)(key & 7u) + 1;
-    const DPanel A = load_panel(P, i), B = load_panel(P, j);
     double scale = 0.5 * (o.A ? rcp64(kFourPi * (panel_area(A) * panel_area(B))) : rcp64(kFourPi));
-    double w1[M], W1[M];
+    double cw[M], sr = 1.0, sp = 0.0;
     {
       double s0, s1, u0, u1;
       const int k = 3 - A.axis - B.axis;
       panel_extent(A, k, s0, s1);
       panel_extent(B, k, u0, u1);
-      emit_inner<TYPE, Q1, Q2>(s0, s1, u0, u1, w1, W1, scale);
+      emit_inner<TYPE, Q1, Q2>(s0, s1, u0, u1, cw, sr, sp, scale);
     }
     // single rules: w = c + h x_k, W = h g_k (h folded into the scale)
     double c0, c1;
@@ -1002,7 +1026,7 @@ __global__ void __launch_bounds__(128, GBEM_FAST_MINB)
       const double w3s = w3 * w3, W3 = gw3[c];
       for (int b = 0; b < m2; ++b) {
         const double w2 = fma(hm, gx2[b], cm);
-        acc = fma(W3 * gw2[b], inner_row<M>(w1, W1, fma(w2, w2, w3s)), acc);
+        acc = fma(W3 * gw2[b], inner_row<TYPE, Q1, Q2>(cw, fma(w2, w2, w3s), sr, sp), acc);
       }
     }
     acc *= scale;
@@ -1051,6 +1075,7 @@ __global__ void __launch_bounds__(128, GBEM_FAST_MINB)
   uint32_t nnidx = nidx + stride;
   uint64_t nne = nnidx < end ? queue[nnidx] : 0;
   uint32_t nncode = nnidx < end ? plans[nnidx] : 0;
+  DPanel nA = load_panel(P, nidx < end ? entry_i(ne) : 0u), nB = load_panel(P, nidx < end ? entry_j(ne) : 0u);
   for (; base < end; base += stride) {
     const uint32_t idx = nidx;
     const uint64_t e = ne;
@@ -1063,23 +1088,25 @@ __global__ void __launch_bounds__(128, GBEM_FAST_MINB)
       nne = queue[nnidx];
       nncode = plans[nnidx];
     }
+    // this pair's panel records were loaded during the previous pair's node loops
+    // (an L1 prefetch covers one 128-byte line; 3 of 8 48-byte records straddle two)
+    const DPanel A = nA, B = nB;
     if (nidx < end) {
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_i(ne)));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(P + entry_j(ne)));
+      nA = load_panel(P, entry_i(ne));
+      nB = load_panel(P, entry_j(ne));
     }
     if (idx >= end) continue;
     const uint32_t i = entry_i(e), j = entry_j(e), key = entry_key(e);
     const bool tent2 = key & 1u;
     const int q1 = (int)((key >> 1) & 7u) + 1, q2 = (int)((key >> 4) & 15u);
-    const DPanel A = load_panel(P, i), B = load_panel(P, j);
     double scale = 0.5 * (o.A ? rcp64(kFourPi * (panel_area(A) * panel_area(B))) : rcp64(kFourPi));
     const bool inner_first = ((code >> 28) & 3u) == 0u;  // inner list on ip0, middle on ip1 (else swapped)
-    double w1[M], W1[M];
+    double cw[M], sr = 1.0, sp = 0.0;
     {
       // a parallel pair's in-plane axes are the panels' own a / b spans
       const double s0 = inner_first ? A.a0 : A.b0, s1 = inner_first ? A.a1 : A.b1;
       const double u0 = inner_first ? B.a0 : B.b0, u1 = inner_first ? B.a1 : B.b1;
-      emit_inner<TYPE, Q1, Q2>(s0, s1, u0, u1, w1, W1, scale);
+      emit_inner<TYPE, Q1, Q2>(s0, s1, u0, u1, cw, sr, sp, scale);
     }
     const double s0 = inner_first ? A.b0 : A.a0, s1 = inner_first ? A.b1 : A.a1;
     const double u0 = inner_first ? B.b0 : B.a0, u1 = inner_first ? B.b1 : B.a1;
@@ -1100,7 +1127,7 @@ __global__ void __launch_bounds__(128, GBEM_FAST_MINB)
         for (int k = 0; k < q; ++k) {
           const double w = fma(h, gx[k], c);
           const double Wn = (h * gw[k]) * fma(be, w, al);
-          acc = fma(Wn, inner_row<M>(w1, W1, fma(w, w, dz2)), acc);
+          acc = fma(Wn, inner_row<TYPE, Q1, Q2>(cw, fma(w, w, dz2), sr, sp), acc);
         }
       }
     } else {
@@ -1113,7 +1140,7 @@ __global__ void __launch_bounds__(128, GBEM_FAST_MINB)
         const double ca = fma(p1, gxa[a], p0), fa = gwa[a];
         for (int b = 0; b < q2; ++b) {
           const double w = fma(-p2, gxb[b], ca);
-          acc = fma(fa * gwb[b], inner_row<M>(w1, W1, fma(w, w, dz2)), acc);
+          acc = fma(fa * gwb[b], inner_row<TYPE, Q1, Q2>(cw, fma(w, w, dz2), sr, sp), acc);
         }
       }
     }
@@ -1431,6 +1458,26 @@ int gbem_internal_init_tables(gbem_ctx* ctx) {
   for (int b = 0; b < kNearBands; ++b) legendre_nodes(near_nodes(b), nx[b], nw[b]);
   GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_nx, nx, sizeof(nx)));
   GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_nw, nw, sizeof(nw)));
+  {
+    double kr[kQMax + 1][kQMax] = {}, kp[kQMax + 1][kQMax] = {};
+    static double kpp[kQProd + 1][kQProd + 1][kQProd * kQProd];
+    for (int q = 1; q <= kQMax; ++q)
+      for (int k = 0; k < q; ++k) {
+        const double t = gw[q][k] * (1.0 + gx[q][k]);
+        kr[q][k] = 1.0 / (t * t);
+        kp[q][k] = 1.0 / (gw[q][k] * gw[q][k]);
+      }
+    for (int q1 = 1; q1 <= kQProd; ++q1)
+      for (int q2 = 1; q2 <= kQProd; ++q2)
+        for (int a = 0; a < q1; ++a)
+          for (int b = 0; b < q2; ++b) {
+            const double t = gw[q1][a] * gw[q2][b];
+            kpp[q1][q2][a * q2 + b] = 1.0 / (t * t);
+          }
+    GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_kr, kr, sizeof(kr)));
+    GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_kp, kp, sizeof(kp)));
+    GBEM_CUDA(ctx, cudaMemcpyToSymbol(c_kpp, kpp, sizeof(kpp)));
+  }
   int8_t fast[512];
   for (int k = 0; k < 512; ++k) fast[k] = -1;
   if (!getenv("GBEM_NO_FAST_FAR")) {  // experiments: every far pair through the generic kernels
