@@ -203,6 +203,9 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
   if (ctx->ev_panel) cudaEventDestroy(ctx->ev_panel);
+  for (auto& e : ctx->ev_bw)
+    if (e) cudaEventDestroy(e);
+  if (ctx->bw_graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)ctx->bw_graph_exec);
   if (ctx->ev_col) cudaEventDestroy(ctx->ev_col);
   if (ctx->g_side) cudaStreamDestroy(ctx->g_side);
   if (ctx->g_main) cudaStreamDestroy(ctx->g_main);

@@ -74,6 +74,19 @@ struct gbem_ctx {
   cudaEvent_t ev[8] = {};
   cudaStream_t side_stream = nullptr;  // high-priority look-ahead stream of the factorisation
   cudaEvent_t ev_panel = nullptr, ev_col = nullptr;
+  cudaEvent_t ev_bw[5] = {};  // look-ahead backward substitution: start, step done, bulk done x 3
+  // its captured sweep (cudaGraphExec_t), valid for one (matrix, factor, work, output, shape) tuple
+  struct BwdGraphKey {
+    const void *A = nullptr, *linv = nullptr, *work = nullptr, *out = nullptr;
+    int64_t lda = 0;
+    int n = 0, R = 0;
+    bool operator==(const BwdGraphKey& o) const {
+      return A == o.A && linv == o.linv && work == o.work && out == o.out && lda == o.lda && n == o.n && R == o.R;
+    }
+  };
+  void* bw_graph_exec = nullptr;
+  BwdGraphKey bw_graph_key;
+  int64_t bw_graph_launches = 0;
   // SM-partitioned factorisation (green contexts): the diagonal-block factor
   // runs on a reserved SM pair (g_side) while the trailing updates run on the
   // other SMs (g_main); otherwise the update CTAs fill every SM and the
@@ -96,7 +109,7 @@ struct gbem_ctx {
   // kernels whose dynamic shared-memory limit has been raised on this
   // context's device (cudaFuncSetAttribute is per device; one bit per site)
   uint64_t attr_set = 0;
-  enum : uint64_t { kAttrGemmSolve = 1u, kAttrFactor = 2u, kAttrGemmLU = 4u, kAttrPcgGemm = 8u, kAttrSymm = 16u };
+  enum : uint64_t { kAttrGemmSolve = 1u, kAttrFactor = 2u, kAttrGemmLU = 4u, kAttrPcgGemm = 8u, kAttrSymm = 16u, kAttrBwdStep = 32u };
 
   int fail(int code, const std::string& msg) {
     err = msg;

@@ -1008,7 +1008,9 @@ __global__ void __launch_bounds__(kFlowThreads, 1)
 
 // Column-major (R x n, ld n: one right-hand side per column of the caller's
 // layout) <-> row-major (n x R: the R values of a panel contiguous).
-__global__ void k_rhs_transpose(const double* __restrict__ in, int n, int R, double* __restrict__ out, int to_rows) {
+__global__ void k_rhs_transpose(const double* __restrict__ in, int n, int R, double* __restrict__ out, int to_rows,
+                                int ldr = 0) {
+  if (ldr == 0) ldr = R;  // row stride of the row-major side
   __shared__ double t[32][33];
   const int i0 = blockIdx.x * 32, q0 = blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
@@ -1017,14 +1019,14 @@ __global__ void k_rhs_transpose(const double* __restrict__ in, int n, int R, dou
     if (to_rows) t[k][tx] = (i < n && q < R) ? in[(long long)q * n + i] : 0.0;
     else {
       const int ii = i0 + k, qq = q0 + tx;  // row-major source: coalesced along q
-      t[k][tx] = (ii < n && qq < R) ? in[(long long)ii * R + qq] : 0.0;
+      t[k][tx] = (ii < n && qq < R) ? in[(long long)ii * ldr + qq] : 0.0;
     }
   }
   __syncthreads();
   for (int k = ty; k < 32; k += 8) {
     if (to_rows) {
       const int i = i0 + k, q = q0 + tx;
-      if (i < n && q < R) out[(long long)i * R + q] = t[tx][k];
+      if (i < n && q < R) out[(long long)i * ldr + q] = t[tx][k];
     } else {
       const int q = q0 + k, i = i0 + tx;
       if (i < n && q < R) out[(long long)q * n + i] = t[tx][k];
@@ -1119,6 +1121,319 @@ static int solve_blocked(gbem_ctx* ctx, const double* d_B, int R, double* d_X, b
   }
   k_rhs_transpose<<<tg, tb, 0, s>>>(X, n, R, d_X, 0);
   GBEM_LAUNCH_CHECK(ctx);
+  return GBEM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Look-ahead backward substitution L^T X = Y for the bordered extraction with
+// 17..64 right-hand sides.  The plain blocked sweep above runs two dependent
+// launches per 128-row block (31 us per block on config 3: latency, not HBM).
+// Here the dependency chain and the bulk of the work are separated:
+//   chain (high-priority stream), one 8-CTA cluster launch per block b:
+//     X_b = inv(L_bb)^T (Y1_b + Y2_b);   Y1_{b-1} -= L_{b,b-1}^T X_b
+//   bulk (the caller's stream), one DMMA GEMM per block b:
+//     Y2_{0..b-2} -= L_{b,0..b-2}^T X_b
+// Y1 is only touched by the chain and Y2 only by the bulk stream, so the two never
+// write the same rows; step b waits for bulk(b + 2), which had a whole step to
+// finish.  In the step kernel cluster rank r owns 16 of the block's 128 columns:
+// its slabs of inv(L_bb) and L_{b,b-1} are staged by cp.async before anything that
+// depends on the previous step, the 16 x R slice of X_b is written to every CTA of
+// the cluster through distributed shared memory, and after one cluster barrier the
+// same CTA forms its 16 rows of the Y1_{b-1} update.  Work arrays are row-major
+// n x Rs (Rs = R rounded up to even: 16-byte cp.async in the bulk GEMM).
+constexpr int kStepCluster = 8, kStepThreads = 512, kStepCols = NB / kStepCluster, kStepKG = 8;
+// shared-memory strides (doubles) that spread the DMMA fragment loads over all banks: slab rows
+// (k contiguous) = 4 mod 16, right-hand-side rows (m contiguous) = 8 mod 16
+constexpr int kSlabLd = NB + 4;
+constexpr int kStepRMax = 64;
+__host__ __device__ constexpr int rhs_stride(int NF) { return NF % 2 ? 8 * NF : 8 * NF + 8; }
+static int rhs_frags(int Rs) { return Rs <= 8 ? 1 : Rs <= 16 ? 2 : Rs <= 24 ? 3 : Rs <= 32 ? 4 : Rs <= 48 ? 6 : 8; }
+static size_t step_smem(int NF) { return (size_t)(2 * kStepCols * kSlabLd + 2 * NB * rhs_stride(NF)) * sizeof(double); }
+
+// y of the bordered factorisation as rows of stride Rs (columns >= R zero)
+__global__ void k_border_to_rows(const double* __restrict__ A, long long lda, int n, int R, int Rs,
+                                 double* __restrict__ Y) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= (long long)n * Rs) return;
+  const long long c = i / Rs;
+  const int q = (int)(i % Rs);
+  Y[i] = q < R ? A[c * lda + n + q] : 0.0;
+}
+
+// acc (8 slab rows x 8 NF right-hand sides) += slab rows (k in [k0, k0 + 4 ksteps)) * V rows:
+// a = this lane's slab element (row g, k0 + t4), v = V + (k0 + t4) * Vs + g
+template <int NF>
+__device__ __forceinline__ void dmma_rows(const double* __restrict__ a, const double* __restrict__ v, int Vs, int ksteps,
+                                          double (&acc)[NF][2]) {
+#pragma unroll 4
+  for (int ks = 0; ks < ksteps; ++ks) {
+    const double av = a[4 * ks];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) dmma(acc[f][0], acc[f][1], av, v[4 * ks * Vs + 8 * f]);
+  }
+}
+
+// rows [r0, r0 + rows) of a row-major (rows x Rs) global block into shared rows of stride Vs
+// (16-byte cp.async; Rs even), rows >= live zero-filled
+__device__ __forceinline__ void stage_rows(double* dst, int Vs, const double* src, int Rs, int live, int tid, int nthreads) {
+  const int cpr = Rs / 2;  // 16-byte chunks per row
+  for (int c = tid; c < NB * cpr; c += nthreads) {
+    const int r = c / cpr, q = 2 * (c % cpr);
+    cp_async16(&dst[r * Vs + q], r < live ? src + (size_t)r * Rs + q : src, r < live ? 16 : 0);
+  }
+}
+
+template <int NF>  // 8-wide right-hand-side fragments (Rs <= 8 NF)
+__global__ void __cluster_dims__(kStepCluster, 1, 1) __launch_bounds__(kStepThreads)
+    k_bwd_step(const double* __restrict__ Linv_b, const double* __restrict__ L, long long lda, double* Y1,
+               const double* Y2, double* X, int Rs, int k0, int kb) {
+  constexpr int Vs = rhs_stride(NF);
+  extern __shared__ __align__(16) double smem[];
+  double* Ai = smem;                      // [16][kSlabLd]: Ai[j][k] = inv(L_bb)(k, j0 + j)
+  double* Lb = Ai + kStepCols * kSlabLd;  // [16][kSlabLd]: Lb[j][k] = L(k0 + k, k0 - NB + j0 + j)
+  double* T = Lb + kStepCols * kSlabLd;   // [NB][Vs]: Y1_b + Y2_b; then the partial sums red[kg][16][8 NF]
+  double* Xs = T + NB * Vs;               // [NB][Vs]: X_b, gathered from the cluster
+  double* red = T;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nf = warp & 1, kg = warp >> 1;  // this warp: slab rows [8 nf, 8 nf + 8), k in [16 kg, 16 kg + 16)
+  const int j0 = rank * kStepCols;
+  // everything this step reads is requested at once: the two slabs (they do not depend on
+  // the previous step) and Y1_b by cp.async, Y2_b into registers
+  for (int c = tid; c < kStepCols * (NB / 2); c += kStepThreads) {
+    const int jj = c / (NB / 2), k = 2 * (c % (NB / 2));
+    const bool ok1 = k < kb && j0 + jj < kb;
+    cp_async16(&Ai[jj * kSlabLd + k], ok1 ? Linv_b + (size_t)(j0 + jj) * NB + k : Linv_b,
+               ok1 ? (k + 1 < kb ? 16 : 8) : 0);
+    const bool ok2 = k0 > 0 && k < kb;
+    cp_async16(&Lb[jj * kSlabLd + k], ok2 ? L + (long long)(k0 - NB + j0 + jj) * lda + k0 + k : L,
+               ok2 ? (k + 1 < kb ? 16 : 8) : 0);
+  }
+  stage_rows(T, Vs, Y1 + (size_t)k0 * Rs, Rs, kb, tid, kStepThreads);
+  cp_async_commit();
+  double y2[2 * NF];
+#pragma unroll
+  for (int u = 0; u < 2 * NF; ++u) {
+    const int c = tid + u * kStepThreads;
+    y2[u] = c < kb * Rs ? Y2[(size_t)k0 * Rs + c] : 0.0;
+  }
+  for (int c = tid; c < NB * (Vs - Rs); c += kStepThreads) {  // zero the padding columns of T and Xs
+    const int r = c / (Vs - Rs), q = Rs + c % (Vs - Rs);
+    T[r * Vs + q] = 0.0;
+    Xs[r * Vs + q] = 0.0;
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 2 * NF; ++u) {
+    const int c = tid + u * kStepThreads;
+    if (c < NB * Rs) T[(c / Rs) * Vs + c % Rs] += y2[u];
+  }
+  __syncthreads();
+  // x(j0 + j, m) = sum_k inv(L_bb)(k, j0 + j) T(k, m)  (zero for rows >= kb: zero-filled slab)
+  double acc[NF][2];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
+  dmma_rows<NF>(Ai + (8 * nf + g) * kSlabLd + 16 * kg + t4, T + (16 * kg + t4) * Vs + g, Vs, 4, acc);
+  __syncthreads();  // T is dead: its space takes the partial sums
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    red[(kg * kStepCols + 8 * nf + g) * (8 * NF) + 8 * f + 2 * t4] = acc[f][0];
+    red[(kg * kStepCols + 8 * nf + g) * (8 * NF) + 8 * f + 2 * t4 + 1] = acc[f][1];
+  }
+  __syncthreads();
+  for (int o = tid; o < kStepCols * Rs; o += kStepThreads) {
+    const int jj = o / Rs, m = o % Rs;
+    double x = 0.0;
+#pragma unroll
+    for (int q = 0; q < kStepKG; ++q) x += red[(q * kStepCols + jj) * (8 * NF) + m];
+    if (j0 + jj < kb) X[(size_t)(k0 + j0) * Rs + o] = x;
+#pragma unroll
+    for (int r = 0; r < kStepCluster; ++r) cluster.map_shared_rank(Xs, r)[(j0 + jj) * Vs + m] = x;
+  }
+  cluster.sync();
+  if (k0 == 0) return;
+  // Y1(k0 - NB + j0 + j, m) -= sum_k L(k0 + k, k0 - NB + j0 + j) x(k, m)
+#pragma unroll
+  for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
+  dmma_rows<NF>(Lb + (8 * nf + g) * kSlabLd + 16 * kg + t4, Xs + (16 * kg + t4) * Vs + g, Vs, 4, acc);
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    red[(kg * kStepCols + 8 * nf + g) * (8 * NF) + 8 * f + 2 * t4] = acc[f][0];
+    red[(kg * kStepCols + 8 * nf + g) * (8 * NF) + 8 * f + 2 * t4 + 1] = acc[f][1];
+  }
+  __syncthreads();
+  double* y = Y1 + (size_t)(k0 - NB + j0) * Rs;
+  for (int o = tid; o < kStepCols * Rs; o += kStepThreads) {
+    const int jj = o / Rs, m = o % Rs;
+    double d = 0.0;
+#pragma unroll
+    for (int q = 0; q < kStepKG; ++q) d += red[(q * kStepCols + jj) * (8 * NF) + m];
+    y[o] -= d;
+  }
+}
+
+// Bulk update of the sweep: Y2(n, m) -= sum_k L(k0 + k, n) X_b(k, m) for the columns n < cols of the
+// factor's row block b, on the FP64 tensor cores.  A CTA owns 32 columns (one 8-column DMMA
+// fragment row per warp); its 128 x 32 tile of L (one 1 KB run per column) and X_b are requested in
+// one burst of cp.async, so the kernel pays the memory latency once (the 64 x 64-tile GEMM walks its
+// K = 128 in eight dependent slabs: ~20 us per launch whatever the size).
+constexpr int kBulkCols = 32, kBulkThreads = 128;
+static size_t bulk_smem(int NF) { return (size_t)(kBulkCols * kSlabLd + NB * rhs_stride(NF)) * sizeof(double); }
+
+template <int NF>
+__global__ void __launch_bounds__(kBulkThreads)
+    k_bwd_bulk(const double* __restrict__ L, long long lda, const double* __restrict__ X, double* __restrict__ Y2,
+               int Rs, int k0, int kb, int cols) {
+  constexpr int Vs = rhs_stride(NF);
+  extern __shared__ __align__(16) double smem[];
+  double* Ls = smem;                        // [32][kSlabLd]: Ls[c][k] = L(k0 + k, n0 + c)
+  double* Xs = smem + kBulkCols * kSlabLd;  // [NB][Vs]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, n0 = blockIdx.x * kBulkCols;
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int c = tid; c < kBulkCols * (NB / 2); c += kBulkThreads) {
+    const int cc = c / (NB / 2), k = 2 * (c % (NB / 2));
+    const bool ok = k < kb && n0 + cc < cols;
+    cp_async16(&Ls[cc * kSlabLd + k], ok ? L + (long long)(n0 + cc) * lda + k0 + k : L, ok ? (k + 1 < kb ? 16 : 8) : 0);
+  }
+  stage_rows(Xs, Vs, X + (size_t)k0 * Rs, Rs, kb, tid, kBulkThreads);
+  cp_async_commit();
+  for (int c = tid; c < NB * (Vs - Rs); c += kBulkThreads) Xs[(c / (Vs - Rs)) * Vs + Rs + c % (Vs - Rs)] = 0.0;
+  cp_async_wait<0>();
+  __syncthreads();
+  double acc[NF][2];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) acc[f][0] = acc[f][1] = 0.0;
+  dmma_rows<NF>(Ls + (8 * warp + g) * kSlabLd + t4, Xs + t4 * Vs + g, Vs, NB / 4, acc);
+  const int nn = n0 + 8 * warp + g;
+  if (nn >= cols) return;
+  double* y = Y2 + (size_t)nn * Rs;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int m = 8 * f + 2 * t4;  // Rs even: the pair (m, m + 1) is in or out together
+    if (m < Rs) {
+      double2 v = *reinterpret_cast<double2*>(y + m);
+      v.x -= acc[f][0];
+      v.y -= acc[f][1];
+      *reinterpret_cast<double2*>(y + m) = v;
+    }
+  }
+}
+
+// The whole sweep (one cluster launch and one GEMM per block, joined by events) is
+// captured once into a CUDA graph per (matrix, right-hand-side) shape and replayed:
+// issued launch by launch it is bound by the host's enqueue rate (~20 us per block for
+// two launches, two event records and two waits against ~4 us of device time).
+static int enqueue_backward_lookahead(gbem_ctx* ctx, int R, int Rs, double* Y1, double* Y2, double* X, double* d_X,
+                                      cudaStream_t s, cudaStream_t chain) {
+  const int n = (int)ctx->n;
+  const long long lda = ctx->lda;
+  const size_t nr = (size_t)n * Rs;
+  const int NF = rhs_frags(Rs);
+  void (*step)(const double*, const double*, long long, double*, const double*, double*, int, int, int) =
+      NF == 1 ? k_bwd_step<1> : NF == 2 ? k_bwd_step<2> : NF == 3 ? k_bwd_step<3> : NF == 4 ? k_bwd_step<4>
+      : NF == 6 ? k_bwd_step<6> : k_bwd_step<8>;
+  void (*bulk)(const double*, long long, const double*, double*, int, int, int, int) =
+      NF == 1 ? k_bwd_bulk<1> : NF == 2 ? k_bwd_bulk<2> : NF == 3 ? k_bwd_bulk<3> : NF == 4 ? k_bwd_bulk<4>
+      : NF == 6 ? k_bwd_bulk<6> : k_bwd_bulk<8>;
+  const size_t smem = step_smem(NF);
+  cudaEvent_t ev_start = ctx->ev_bw[0], ev_step = ctx->ev_bw[1];
+  cudaEvent_t* ev_bulk = &ctx->ev_bw[2];  // [3]
+  k_border_to_rows<<<(unsigned)((nr + 255) / 256), 256, 0, s>>>(ctx->d_A, lda, n, R, Rs, Y1);
+  GBEM_LAUNCH_CHECK(ctx);
+  GBEM_CUDA(ctx, cudaMemsetAsync(Y2, 0, nr * sizeof(double), s));
+  GBEM_CUDA(ctx, cudaEventRecord(ev_start, s));
+  GBEM_CUDA(ctx, cudaStreamWaitEvent(chain, ev_start, 0));
+  const double* L = ctx->d_A;
+  const int nblk = (n + NB - 1) / NB;
+  for (int b = nblk - 1; b >= 0; --b) {
+    const int k0 = b * NB, kb = std::min(NB, n - k0);
+    if (b + 2 < nblk) GBEM_CUDA(ctx, cudaStreamWaitEvent(chain, ev_bulk[(b + 2) % 3], 0));
+    step<<<kStepCluster, kStepThreads, smem, chain>>>(ctx->d_linv + (size_t)b * NB * NB, L, lda, Y1, Y2, X, Rs, k0, kb);
+    GBEM_LAUNCH_CHECK(ctx);
+    GBEM_CUDA(ctx, cudaEventRecord(ev_step, chain));
+    if (b >= 2) {
+      GBEM_CUDA(ctx, cudaStreamWaitEvent(s, ev_step, 0));
+      const int cols = k0 - NB;  // rows of Y2 above block b - 1
+      bulk<<<(unsigned)((cols + kBulkCols - 1) / kBulkCols), kBulkThreads, bulk_smem(NF), s>>>(L, lda, X, Y2, Rs, k0, kb,
+                                                                                             cols);
+      GBEM_LAUNCH_CHECK(ctx);
+      GBEM_CUDA(ctx, cudaEventRecord(ev_bulk[b % 3], s));
+    }
+  }
+  GBEM_CUDA(ctx, cudaStreamWaitEvent(s, ev_step, 0));
+  const dim3 tb(32, 8), tg((n + 31) / 32, (R + 31) / 32);
+  k_rhs_transpose<<<tg, tb, 0, s>>>(X, n, R, d_X, 0, Rs);
+  GBEM_LAUNCH_CHECK(ctx);
+  return GBEM_OK;
+}
+
+static int solve_backward_lookahead(gbem_ctx* ctx, int R, double* d_X) {
+  const int n = (int)ctx->n;
+  const int Rs = (R + 1) & ~1;
+  cudaStream_t s = ctx->stream, chain = ctx->side_stream;
+  const size_t nr = (size_t)n * Rs;
+  if (ctx->sw_cap < 3 * nr) {
+    cudaFree(ctx->d_sw);
+    ctx->d_sw = nullptr;
+    ctx->sw_cap = 0;
+    GBEM_CUDA(ctx, cudaMalloc(&ctx->d_sw, 3 * nr * sizeof(double)));
+    ctx->sw_cap = 3 * nr;
+  }
+  double* Y1 = ctx->d_sw;
+  double* Y2 = Y1 + nr;
+  double* X = Y2 + nr;
+  if (!(ctx->attr_set & gbem_ctx::kAttrBwdStep)) {
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_step<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step_smem(1)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_step<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step_smem(2)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_step<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step_smem(3)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_step<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step_smem(4)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_step<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step_smem(6)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_step<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)step_smem(8)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_bulk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem(1)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_bulk<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem(2)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_bulk<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem(3)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_bulk<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem(4)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_bulk<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem(6)));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_bwd_bulk<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bulk_smem(8)));
+    ctx->attr_set |= gbem_ctx::kAttrBwdStep;
+  }
+  for (auto& e : ctx->ev_bw)
+    if (!e) GBEM_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  static const bool no_graph = getenv("GBEM_NO_BWD_GRAPH") != nullptr;
+  // (the legacy default stream cannot be captured: issue the launches directly)
+  if (no_graph || s == nullptr || s == cudaStreamLegacy)
+    return enqueue_backward_lookahead(ctx, R, Rs, Y1, Y2, X, d_X, s, chain);
+  // graph cache: one instantiated sweep per (shape, buffers)
+  gbem_ctx::BwdGraphKey key{ctx->d_A, ctx->d_linv, Y1, d_X, ctx->lda, n, R};
+  if (!ctx->bw_graph_exec || !(ctx->bw_graph_key == key)) {
+    if (ctx->bw_graph_exec) {
+      cudaGraphExecDestroy((cudaGraphExec_t)ctx->bw_graph_exec);
+      ctx->bw_graph_exec = nullptr;
+    }
+    const int64_t launches0 = ctx->launches;
+    GBEM_CUDA(ctx, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_backward_lookahead(ctx, R, Rs, Y1, Y2, X, d_X, s, chain);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    ctx->launches = launches0;
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return ctx->fail(GBEM_ECUDA, std::string("backward-sweep graph capture: ") + cudaGetErrorString(e));
+    cudaGraphExec_t exec = nullptr;
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return ctx->fail(GBEM_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    ctx->bw_graph_exec = exec;
+    ctx->bw_graph_key = key;
+    ctx->bw_graph_launches = 2 * ((n + NB - 1) / NB);  // kernels per replay: nblk steps, nblk - 2 bulk GEMMs, 2 copies
+  }
+  GBEM_CUDA(ctx, cudaGraphLaunch((cudaGraphExec_t)ctx->bw_graph_exec, s));
+  ctx->launches += ctx->bw_graph_launches;
   return GBEM_OK;
 }
 
@@ -1260,6 +1575,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   // and main-stream timings on stderr (diagnostics only)
   static const bool prof = getenv("GBEM_FACTOR_PROFILE") != nullptr;
   std::vector<cudaEvent_t> pe;
+  std::vector<int> sb_starts;  // first block of every pipelined super-block (profile mode)
   if (prof) {
     pe.resize(6 * (size_t)nblk);
     for (auto& e : pe) cudaEventCreate(&e);
@@ -1406,6 +1722,10 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     unsigned band_target = 0;  // cumulative band CTAs of the combined updates
     for (;;) {
       const int nb = std::min(SB, nblk - b), next = b + nb;
+      if (prof) {
+        cudaEventRecord(pe[6 * b + 3], lo);  // previous update done: lo idle until the chain's trsm (evT)
+        sb_starts.push_back(b);
+      }
       GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, evT, 0));
       if (prof) cudaEventRecord(pe[6 * b + 5], lo);
       if (next >= nblk) {  // the last super-block: its trsm covered the border rows
@@ -1528,19 +1848,25 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     fprintf(stderr, "[factor profile] n=%d blocks=%d mode=%s side=%.3f ms band-update=%.3f ms "
             "band->next-potrf gap=%.3f ms\n", n, nblk, green ? "green" : "streams", side, band, gap);
     if (green) {
-      // per pipelined block (us): potrf, trsm (after potrf); per super-block: band2 + rest2 on lo
-      double tp = 0, tt = 0, tr = 0;
-      for (int b = 0; b < nblk && n - b * NB >= tail_rows; ++b) {
-        float pf = 0, t = 0, r = 0;
-        cudaEventElapsedTime(&pf, pe[6 * b], pe[6 * b + 1]);
-        cudaEventElapsedTime(&t, pe[6 * b + 1], pe[6 * b + 2]);
-        if (b % 2 == 0) cudaEventElapsedTime(&r, pe[6 * b + 5], pe[6 * b + 4]);
-        tp += pf; tt += t; tr += r;
-        if (b % 8 == 0)
-          fprintf(stderr, "  blk %3d potrf %6.1f trsm %6.1f update2(lo) %7.1f\n", b, 1e3 * pf, 1e3 * t, 1e3 * r);
+      // per super-block on lo (us): idle wait for the chain's last trsm, then the combined
+      // band + rest update; potrf includes its spin on the band counter
+      double tw = 0, tu = 0, tfl = 0;
+      for (size_t k = 0; k < sb_starts.size(); ++k) {
+        const int b = sb_starts[k];
+        float w = 0, u = 0;
+        cudaEventElapsedTime(&w, pe[6 * b + 3], pe[6 * b + 5]);
+        if (cudaEventElapsedTime(&u, pe[6 * b + 5], pe[6 * b + 4]) != cudaSuccess) u = 0;
         cudaGetLastError();
+        const int k0 = b * NB, kw = std::min((int)NB * (k + 1 < sb_starts.size() ? sb_starts[k + 1] - b : nblk - b), n - k0);
+        const double m = n - k0 - kw + (double)ctx->border;
+        const double fl = m * (m + 1) * kw;  // lower triangle, 2 flops per entry and k
+        tw += w; tu += u; tfl += u > 0 ? fl : 0;
+        if (k % 4 == 0 || k + 8 >= sb_starts.size())
+          fprintf(stderr, "  sb %3d (blk %3d, m %6.0f, K %4d): lo idle %7.1f us, update %8.1f us = %5.2f TFLOP/s\n", (int)k, b,
+                  m, kw, 1e3 * w, 1e3 * u, u > 0 ? fl / (u * 1e-3) * 1e-12 : 0.0);
       }
-      fprintf(stderr, "  totals: potrf %.3f trsm %.3f update2(lo) %.3f ms\n", tp, tt, tr);
+      fprintf(stderr, "  totals: lo idle %.3f ms, updates %.3f ms (%.2f TFLOP/s while running)\n", tw, tu,
+              tu > 0 ? tfl / (tu * 1e-3) * 1e-12 : 0.0);
     }
     for (auto& e : pe) cudaEventDestroy(e);
   }
@@ -1671,6 +1997,10 @@ int gbem_internal_solve_factored(gbem_ctx* ctx, const double* d_B, int64_t nrhs,
     GBEM_CUDA(ctx, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFlowSmem));
     GBEM_CUDA(ctx, cudaLaunchCooperativeKernel(fn, dim3(nblk_s), dim3(kFlowThreads), args, kFlowSmem, s));
     GBEM_LAUNCH_CHECK(ctx);
+  } else if (y_from_border && R <= kStepRMax && ctx->side_stream && !getenv("GBEM_NO_BWD_LOOKAHEAD")) {
+    // bordered, 17..64 right-hand sides (or more blocks than SMs): look-ahead backward substitution
+    rc = solve_backward_lookahead(ctx, R, d_X);
+    if (rc) return rc;
   } else if (R >= blocked_min || y_from_border) {
     // (bordered: y sits in the border rows; the DMMA-blocked backward sweep takes it for any width)
     rc = solve_blocked(ctx, d_B, R, d_X, y_from_border);

@@ -115,12 +115,13 @@ def test_matrix_dump_round_trip(tmp_path):
     assert n == len(ps) and np.array_equal(A, sysm.A)
 
 
-@pytest.mark.parametrize("K", [1, 3, 6, 8, 9, 12, 16, 17, 24])
+@pytest.mark.parametrize("K", [1, 3, 6, 8, 9, 12, 16, 17, 24, 33, 48, 64])
 def test_bordered_extraction_every_solve_path(ctx, K):
     """gbem_extract_cmatrix's bordered factorisation (C = B^T A^-1 B from the
     border corner, X from the backward substitution) across the right-hand-side
-    widths that select the dataflow (K <= 16) and DMMA-blocked (>= 17) backward substitutions; n = 2,832 also runs the
-    SM-partitioned look-ahead (n >= 2 * 1024).  Reference: the GPU-assembled A
+    widths that select the dataflow (K <= 16) and the look-ahead cluster (17..64: every
+    right-hand-side-per-thread instantiation) backward substitutions; n = 2,832 = 22 * 128 + 16 has a
+    ragged last block and also runs the SM-partitioned factorisation (n >= 2 * 1024).  Reference: the GPU-assembled A
     solved densely by numpy."""
     m = g.config_model(1, scale=1.4)
     ps = m.partition(1)

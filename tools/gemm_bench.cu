@@ -82,6 +82,8 @@ int main(int argc, char** argv) {
   GEN(128, 128, 2, 4, 2, 1);
   GEN(96, 96, 3, 2, 2, 2);
   GEN(64, 64, 2, 2, 4, 3);
+  GEN(64, 64, 2, 2, 3, 4);
+  GEN(64, 64, 2, 2, 2, 5);
   cublasHandle_t h;
   cublasCreate(&h);
   double alpha = -1.0, beta = 1.0;
