@@ -26,17 +26,30 @@ if [ $rc -eq 0 ]; then
   head -40 gpurun_out/${TAG}_launch_summary.txt
   timeout 300 python tools/prof_assembly.py 3 1 > gpurun_out/asm_plain_$TAG.log 2>&1 && \
   SECS="--section SpeedOfLight --section ComputeWorkloadAnalysis --section Occupancy --section LaunchStats --section WarpStateStats --section SchedulerStats --section MemoryWorkloadAnalysis"
-  # every far-field launch of the assembly with the pipe / occupancy / stall sections (no source: small reports)
+  # every far-field launch of the assembly's first chunk with the pipe / occupancy / stall sections (no source)
   timeout 1200 ncu $SECS --clock-control none --kernel-name-base demangled --kernel-name "regex:k_far" -c 80 \
     -o gpurun_out/prof_${TAG}_far_all -f python tools/prof_assembly.py 3 1 > gpurun_out/ncu_${TAG}_far_all.log 2>&1
   echo "ncu far_all rc=$?"
-  for KS in "k_classify<\(bool\)0>:classify0" "k_classify<\(bool\)1>:classify1"; do
+  python tools/ncu_far_all.py gpurun_out/prof_${TAG}_far_all.ncu-rep 80 > gpurun_out/${TAG}_ncu_far_kernels.txt 2>&1
+  rm -f gpurun_out/prof_${TAG}_far_all.ncu-rep
+  : > gpurun_out/${TAG}_ncu_summary.txt
+  for KS in "k_classify<.bool.0>:classify0" "k_classify<.bool.1>:classify1" "k_far_orth<.int.2, .int.3, .int.3>:far_orth233"; do
     K=${KS%%:*}; NAME=${KS##*:}
     timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
       --kernel-name "regex:$K" -c 1 -o gpurun_out/prof_${TAG}_$NAME -f \
       python tools/prof_assembly.py 3 1 > gpurun_out/ncu_${TAG}_$NAME.log 2>&1
     echo "ncu $K rc=$?"
+    python tools/ncu_summary.py gpurun_out/prof_${TAG}_$NAME.ncu-rep >> gpurun_out/${TAG}_ncu_summary.txt 2>&1
+    python tools/ncu_stalls.py gpurun_out/prof_${TAG}_$NAME.ncu-rep 15 >> gpurun_out/${TAG}_ncu_summary.txt 2>&1
+    ncu -i gpurun_out/prof_${TAG}_$NAME.ncu-rep --page details 2>/dev/null | grep -E "Issue Slots Busy|One or More Eligible|Active Warps Per Scheduler|Eligible Warps Per|Cycles Per Issued|Executed Ipc Active|highest-utilized|DRAM Throughput|Achieved Occupancy" >> gpurun_out/${TAG}_ncu_summary.txt
+    case "$NAME" in far_orth233) ;; *) rm -f gpurun_out/prof_${TAG}_$NAME.ncu-rep ;; esac
   done
+  # the look-ahead backward sweep's kernels (graph nodes) from one bench step
+  GBEM_NO_GREEN=1 timeout 900 ncu $SECS --clock-control none --kernel-name-base demangled --kernel-name "regex:k_bwd_step|k_bwd_bulk" -s 20 -c 4 \
+    -o gpurun_out/prof_${TAG}_bwd -f python bench.py --steps 1 --warmup 0 --no-sharded --no-cpu-baseline > gpurun_out/ncu_${TAG}_bwd.log 2>&1
+  echo "ncu bwd rc=$?"
+  python tools/ncu_summary.py gpurun_out/prof_${TAG}_bwd.ncu-rep >> gpurun_out/${TAG}_ncu_summary.txt 2>&1
+  rm -f gpurun_out/prof_${TAG}_bwd.ncu-rep
   gzip -f gpurun_out/${TAG}_launches.csv
   du -sh gpurun_out
 fi
