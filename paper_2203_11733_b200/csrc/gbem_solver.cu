@@ -1685,17 +1685,43 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     // U([b0, b0 + nb), block columns >= b0 + nb + j0): band (j0 = 0, one super-
     // block of kBand2 tile columns) or triangular rest (j0 = 2)
     // super-block width in 128-column blocks (K of the trailing update = SB * 128;
-    // tools/gemm_bench.cu at m = 20,000: K = 256 / 384 / 512 -> 32.0 / 33.0 / 33.4 TFLOP/s).
+    // tools/gemm_bench.cu at m = 20,000: K = 256 / 384 / 512 / 640 -> 32.0 / 33.0 / 33.4 / 33.8 TFLOP/s).
     // The intra-super-block updates lengthen the potrf / trsm chain by O(SB^2)
-    // thin updates, which a small matrix cannot hide: config 2 (n = 11,340) is
-    // fastest at SB = 2 (18.46 ms vs 18.96 at 4), config 3 (n = 33,776) at
-    // SB >= 5 (426.1 / 416.6 / 412.7 / 411.2 / 411.0 ms at SB = 2 / 3 / 4 / 5 / 6)
+    // thin updates, which a small trailing matrix cannot hide.
     static const int sb_env = getenv("GBEM_SUPERBLOCK") ? std::max(1, atoi(getenv("GBEM_SUPERBLOCK"))) : 0;
-    const int SB = sb_env > 0 ? sb_env : (n < 16384 ? 2 : 5);
-    const int kBand2 = SB * kBand;
+    // Adaptive width: wide super-blocks while the trailing matrix is large (the update amortises
+    // its C read-modify-write over K = 128 SB and hides the O(SB^2) chain), narrower ones as it
+    // shrinks and the chain (SB diagonal factors of ~47 us, SB trsms, the intra-super-block
+    // updates) would outlast the update.  GBEM_SB_SCHED="sb:rows,..." overrides the table
+    // (first entry whose rows <= remaining rows), GBEM_SUPERBLOCK=k fixes the width.
+    struct SbRule { int sb, rows; };
+    static const std::vector<SbRule> sb_env_rules = [] {
+      std::vector<SbRule> r;
+      if (const char* e = getenv("GBEM_SB_SCHED")) {
+        int sb = 0, rows = 0, used = 0;
+        while (sscanf(e, "%d:%d%n", &sb, &rows, &used) == 2) {
+          r.push_back({std::max(1, sb), rows});
+          e += used;
+          if (*e == ',') ++e;
+        }
+      }
+      return r;
+    }();
+    // config 3: 411.1 ms at a fixed SB = 5, 405.5 at 10, 403.3 with the large table;
+    // config 2: 18.47 ms at a fixed SB = 2, 18.23 with the small one
+    static const std::vector<SbRule> sb_large = {{12, 16000}, {10, 12000}, {8, 9000}, {6, 7000},
+                                                 {4, 5000},   {3, 3500},   {2, 0}};
+    static const std::vector<SbRule> sb_small = {{4, 9000}, {3, 6000}, {2, 3000}, {1, 0}};
+    auto sb_at = [&](int blk) {
+      if (sb_env > 0) return sb_env;
+      const int rows = n - blk * NB;
+      for (const SbRule& r : !sb_env_rules.empty() ? sb_env_rules : (n < 16384 ? sb_small : sb_large))
+        if (rows >= r.rows) return r.sb;
+      return 1;
+    };
     static const int occ_rows = getenv("GBEM_OCC_ROWS") ? atoi(getenv("GBEM_OCC_ROWS")) : 0;
     static const bool combined = getenv("GBEM_NO_COMBINED") == nullptr;
-    auto update2 = [&](int b0, int nb, bool band_part) {
+    auto update2 = [&](int b0, int nb, bool band_part, int kBand2) {
       const int k0 = b0 * NB, kw = std::min(nb * NB, n - k0);
       const int m = n - k0 - kw + (int)ctx->border;
       if (m <= 0) return;
@@ -1717,11 +1743,14 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     };
     GBEM_CUDA(ctx, cudaEventRecord(evB, p));  // stepA(0) waits on nothing
     int b = 0;
-    int rc2 = stepA(0, std::min(SB, nblk), 0u);
+    int rc2 = stepA(0, std::min(sb_at(0), nblk), 0u);
     if (rc2) return rc2;
     unsigned band_target = 0;  // cumulative band CTAs of the combined updates
     for (;;) {
-      const int nb = std::min(SB, nblk - b), next = b + nb;
+      const int nb = std::min(sb_at(b), nblk - b), next = b + nb;
+      // the band of this update = the next super-block's columns
+      const int nb_next = next < nblk ? std::min(sb_at(next), nblk - next) : 1;
+      const int kBand2 = nb_next * kBand;
       if (prof) {
         cudaEventRecord(pe[6 * b + 3], lo);  // previous update done: lo idle until the chain's trsm (evT)
         sb_starts.push_back(b);
@@ -1729,7 +1758,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, evT, 0));
       if (prof) cudaEventRecord(pe[6 * b + 5], lo);
       if (next >= nblk) {  // the last super-block: its trsm covered the border rows
-        update2(b, nb, true);
+        update2(b, nb, true, kBand2);
         GBEM_LAUNCH_CHECK(ctx);
         b = nblk;
         break;
@@ -1751,18 +1780,18 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
         GBEM_LAUNCH_CHECK(ctx);
         band_target += (unsigned)(nt * bw);
         if (!next_tail) {
-          rc2 = stepA(next, std::min(SB, nblk - next), band_target);
+          rc2 = stepA(next, nb_next, band_target);
           if (rc2) return rc2;
         }
       } else {
-        update2(b, nb, true);  // band2(b): block columns next, next + 1
+        update2(b, nb, true, kBand2);  // band2(b): the next super-block's columns
         GBEM_LAUNCH_CHECK(ctx);
         GBEM_CUDA(ctx, cudaEventRecord(evB, lo));
         if (!next_tail) {
-          rc2 = stepA(next, std::min(SB, nblk - next), 0u);
+          rc2 = stepA(next, nb_next, 0u);
           if (rc2) return rc2;
         }
-        update2(b, nb, false);  // rest2(b)
+        update2(b, nb, false, kBand2);  // rest2(b)
         GBEM_LAUNCH_CHECK(ctx);
       }
       if (prof) cudaEventRecord(pe[6 * b + 4], lo);
