@@ -242,6 +242,48 @@ __host__ __device__ inline long long gen_tiles_before(long long tm) {
 // tiles of tile columns [0, -band) (nt = tile rows), dispatched first, then the
 // triangle from split = -band; each band CTA bumps *band_done when its tile is
 // stored (release), which is what the next diagonal factor waits for.
+// Lower-triangle tile t of an X x X tile grid -> (row r, column c), enumerated in column strips
+// of kSyrkStrip tile columns, row-major inside a strip: the CTAs in flight at one time then share
+// the strip's column operands and a few dozen row operands (~40 MB at K = 1,536 for a strip of 16; 32 measured the same speed), which stay in
+// the 126 MB L2.  Plain row-major order walks the whole panel once per tile row; at K >= 640 the
+// panel no longer fits the L2 and was re-read from HBM (ncu: 62 GB of DRAM reads for a 0.3 GB
+// panel + 2.7 GB of C at m = 26,000, K = 1,536).
+#ifndef GBEM_SYRK_STRIP
+#define GBEM_SYRK_STRIP 32
+#endif
+__device__ __forceinline__ void lower_tile_strips(long long t, int X, int& r, int& c) {
+#if GBEM_SYRK_STRIP > 0
+  constexpr int W = GBEM_SYRK_STRIP;
+  int c0 = 0;
+  for (;; c0 += W) {
+    const int w = min(W, X - c0);
+    const long long total = (long long)w * (w + 1) / 2 + (long long)(X - c0 - w) * w;
+    if (t < total || c0 + W >= X) {
+      const long long tri = (long long)w * (w + 1) / 2;
+      if (t < tri) {
+        int x = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+        while ((long long)(x + 1) * (x + 2) / 2 <= t) ++x;
+        while ((long long)x * (x + 1) / 2 > t) --x;
+        r = c0 + x;
+        c = c0 + (int)(t - (long long)x * (x + 1) / 2);
+      } else {
+        t -= tri;
+        r = c0 + w + (int)(t / w);
+        c = c0 + (int)(t % w);
+      }
+      return;
+    }
+    t -= total;
+  }
+#else
+  int x = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((long long)(x + 1) * (x + 2) / 2 <= t) ++x;
+  while ((long long)x * (x + 1) / 2 > t) --x;
+  r = x;
+  c = (int)(t - (long long)x * (x + 1) / 2);
+#endif
+}
+
 template <int TBM, int TBN, int WMW, int WNW, int NSTG, int MINB>
 __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
     k_syrk_gen(double* C, long long ldc, const double* A, long long lda, int M, int K, int split, int band,
@@ -267,22 +309,20 @@ __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
     } else {
       t -= (long long)nt * -band;
       split = -band;
-      int x = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-      while ((long long)(x + 1) * (x + 2) / 2 <= t) ++x;
-      while ((long long)x * (x + 1) / 2 > t) --x;
-      tm = split + x;
-      tn = split + (int)(t - (long long)x * (x + 1) / 2);
+      int r, c;
+      lower_tile_strips(t, nt - split, r, c);
+      tm = split + r;
+      tn = split + c;
     }
   } else if (band > 0) {
     tm = blockIdx.x;
     tn = split + blockIdx.y;
     if (tn > tm) return;
   } else {
-    int x = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
-    while ((long long)(x + 1) * (x + 2) / 2 <= t) ++x;
-    while ((long long)x * (x + 1) / 2 > t) --x;
-    tm = split + x;
-    tn = split + (int)(t - (long long)x * (x + 1) / 2);
+    int r, c;
+    lower_tile_strips(t, (M + TBM - 1) / TBM - split, r, c);
+    tm = split + r;
+    tn = split + c;
   }
   const int m0 = tm * TBM, n0 = tn * TBN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

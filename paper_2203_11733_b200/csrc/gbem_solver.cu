@@ -1601,6 +1601,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     GBEM_CUDA(ctx, cudaStreamWaitEvent(hi, ctx->ev_gs, 0));
     GBEM_CUDA(ctx, cudaStreamWaitEvent(p, ctx->ev_gs, 0));
     constexpr int kBand = NB / 64;  // tile columns per block column
+    static const int fdbg = getenv("GBEM_FACTOR_DBG") ? atoi(getenv("GBEM_FACTOR_DBG")) : 0;  // timing experiments (results wrong)
     auto trailing = [&](int b, int& m, int& nt, double*& A21, double*& A22) {
       const int k0 = b * NB, kb = std::min(NB, n - k0);
       m = n - k0 - kb + (int)ctx->border;
@@ -1619,7 +1620,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       double *A21, *A22;
       trailing(b, m, nt, A21, A22);
       const int kb = std::min(NB, n - b * NB);
-      if (m > 0)
+      if (m > 0 && !(fdbg & 1))
         k_trsm_rows<<<(unsigned)((m + kTrsmRows - 1) / kTrsmRows), kTrsmThreads, kTrsmSmem, st>>>(
             A21, lda, A21, lda, Linv + (size_t)b * NB * NB, NB, m, kb, kb);
     };
@@ -1662,7 +1663,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
           // U(b0 .. b0+k-1, b0 + k): block column b0 + k by the super-block's
           // first k blocks at once (one K = 128 k update on the chain)
           const int c0 = bb * NB, mk = n - c0 + (int)ctx->border, ntk = (mk + 63) / 64;
-          kUpdate<<<dim3(ntk, std::min(kBand, ntk)), UpdShape::THREADS, UpdShape::SMEM, hi>>>(
+          if (!(fdbg & 2)) kUpdate<<<dim3(ntk, std::min(kBand, ntk)), UpdShape::THREADS, UpdShape::SMEM, hi>>>(
               ctx->d_A + (long long)c0 * lda + c0, lda, ctx->d_A + (long long)(b0 * NB) * lda + c0, lda, mk, k * NB, 0,
               std::min(kBand, ntk));
           GBEM_LAUNCH_CHECK(ctx);
@@ -1712,11 +1713,37 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     static const std::vector<SbRule> sb_large = {{12, 16000}, {10, 12000}, {8, 9000}, {6, 7000},
                                                  {4, 5000},   {3, 3500},   {2, 0}};
     static const std::vector<SbRule> sb_small = {{4, 9000}, {3, 6000}, {2, 3000}, {1, 0}};
+    static const bool ramp_on = getenv("GBEM_SB_NO_RAMP") == nullptr;
+    static const std::vector<int> ramp_widths = [] {
+      std::vector<int> w;
+      if (const char* e = getenv("GBEM_SB_RAMP")) {
+        int v = 0, used = 0;
+        while (sscanf(e, "%d%n", &v, &used) == 1) {
+          w.push_back(std::max(1, v));
+          e += used;
+          if (*e == ',') ++e;
+        }
+      }
+      return w;
+    }();
+    static const bool ramp_env = getenv("GBEM_SB_RAMP") != nullptr;
+    static const std::vector<int> ramp_small = {2}, ramp_large = {4, 8};
     auto sb_at = [&](int blk) {
       if (sb_env > 0) return sb_env;
       const int rows = n - blk * NB;
+      // ramp: nothing overlaps the first super-block's chain (12 diagonal factors, trsms and
+      // intra-super-block updates at full height: 3.6 ms), so the first ones are narrower
+      // (worth 0.1 ms on config 2; on config 3 the early K = 512 / 1,024 updates give it back)
+      int ramp = 1 << 20;
+      if (ramp_on) {
+        int at = 0;
+        for (int w : ramp_env ? ramp_widths : (n < 16384 ? ramp_small : ramp_large)) {
+          if (blk == at) ramp = w;
+          at += w;
+        }
+      }
       for (const SbRule& r : !sb_env_rules.empty() ? sb_env_rules : (n < 16384 ? sb_small : sb_large))
-        if (rows >= r.rows) return r.sb;
+        if (rows >= r.rows) return std::min(r.sb, ramp);
       return 1;
     };
     static const int occ_rows = getenv("GBEM_OCC_ROWS") ? atoi(getenv("GBEM_OCC_ROWS")) : 0;
