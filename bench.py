@@ -282,8 +282,14 @@ def run_extract(args):
                 "algorithmic": "counted FP64 flops of the Gauss evaluations (dadd, dmul = 1, dfma = 2) / device time",
                 "peak_source": "tools/fp64_peaks.cu DFMA loop (no FP64 in MEASURED_PEAKS.json)"}
     roof_far["frac"] = roof_far["achieved"] / roof_far["peak"]
-    rsq_rate = peaks.get("rsqrt_f64_custom_per_s", 2.2e12)
-    roof_far["mufu_rsq64_bound_frac"] = (ast.far_evals / rsq_rate) / (ast.ms_far * 1e-3)
+    # one MUFU.RSQ64H per node against its measured issue rate, and the node's whole instruction
+    # mix (3 DFMA + DMUL + MUFU + the seed's low-word move) against its measured rate
+    roof_far["mufu_rsq64h_frac"] = (ast.far_evals / peaks.get("mufu_rsq64h_per_s", 4.62e12)) / (ast.ms_far * 1e-3)
+    roof_far["node_mix_frac"] = (ast.far_evals / peaks.get("far_node_mix_per_s", 3.22e12)) / (ast.ms_far * 1e-3)
+    pipe = _ncu_traffic_file().get("fp64_pipe_active", {})
+    if pipe:
+        roof_far["fp64_pipe_active_ncu"] = pipe.get("k_far")
+        roof_far["fp64_pipe_active_ncu_source"] = pipe.get("source")
     step_flops = chol_flops + ast.far_flops + 2.0 * n * n * K
     fp64_step = {"flops_per_step": step_flops, "achieved_tflops": step_flops / (ms * 1e-3) / 1e12,
                  "peak_tflops": dmma_peak, "frac": step_flops / (ms * 1e-3) / 1e12 / dmma_peak,
@@ -511,6 +517,14 @@ def run_sharded(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _ncu_traffic_file() -> dict:
+    """profiles/ncu_traffic.json (committed ncu evidence: per-launch DRAM bytes, pipe utilisation)."""
+    try:
+        return json.load(open(ROOT / "profiles" / "ncu_traffic.json"))
+    except (OSError, ValueError):
+        return {}
 
 
 def _ncu_traffic() -> dict:
