@@ -220,10 +220,13 @@ __device__ __forceinline__ double neg_hi(double x) {
 // WMW x WNW warps, warp tile (TBM/WMW) x (TBN/WNW), NSTG-stage cp.async
 // pipeline of BK = 16 slabs, accumulators preloaded with C.  Small tiles with
 // several CTAs per SM overlap one CTA's prologue/epilogue with the others' DMMA.
+#ifndef GBEM_GEN_PAD
+#define GBEM_GEN_PAD 8
+#endif
 template <int TBM, int TBN, int WMW, int WNW, int NSTG>
 struct GenShape {
   static constexpr int THREADS = 32 * WMW * WNW;
-  static constexpr int LDA = TBM + 8, LDB = TBN + 8;
+  static constexpr int LDA = TBM + GBEM_GEN_PAD, LDB = TBN + GBEM_GEN_PAD;
   static constexpr int FM = TBM / WMW / 8, FN = TBN / WNW / 8;
   static constexpr size_t SMEM = (size_t)NSTG * BK * (LDA + LDB) * sizeof(double);
 };
@@ -373,11 +376,15 @@ __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
     cp_async_commit();
   }
   for (int kt = 0; kt < KT; ++kt) {
+#if !defined(GBEM_EXP_NOSYNC)
     cp_async_wait<NSTG - 2>();
     __syncthreads();
+#endif
     const int nxt = kt + NSTG - 1;
+#if !defined(GBEM_EXP_NOLOAD)
     if (nxt < KT) load_stage(nxt, nxt % NSTG);
     cp_async_commit();
+#endif
     const double* as = As + (kt % NSTG) * BK * S::LDA + (wm * (TBM / WMW)) + g;
     const double* bs = Bs + (kt % NSTG) * BK * S::LDB + (wn * (TBN / WNW)) + g;
 #pragma unroll
@@ -407,6 +414,200 @@ __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
       }
 #pragma unroll
     for (int j = 0; j < S::FN; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = cw0 + j * 8 + 2 * t4 + e;
+        if (row < M && col <= row) C[(long long)col * ldc + row] = cur[j][e] - acc[i][j][e];
+      }
+  }
+  if (signal) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(band_done, 1u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Trailing update with bulk-copy (TMA engine) operand staging.  Same tiles, warp layout, DMMA
+// order and rounding as k_syrk_gen<64, 64, 2, 2, ., .>, but the operand slabs are not fetched by
+// the DMMA warps' own cp.async (LDGSTS) instructions: measured on a B200 (tools/sync_ab.sh) the
+// update runs at 34.3 TFLOP/s with those loads, 36.4 with them removed and 34.2 with only the
+// block barrier removed -- the LDGSTS stream (8 per thread per 16-column slab, plus addresses and
+// predicates) costs the DMMA pipe 6%, the barrier nothing.  Here one warp per slab (rotating)
+// issues a single predicated cp.async.bulk: lanes 0 .. BKS-1 each copy one 64-double column
+// segment of the row operand, lanes BKS .. 2 BKS - 1 one of the column operand (512 bytes each,
+// SASS UBLKCP) into a padded slab (row stride 68 doubles: conflict-free fragment loads); the
+// copies signal a per-stage "full" mbarrier (expect_tx), the four warps release a stage through
+// an "empty" mbarrier, and a slab is requested two slabs ahead of its use so a lagging warp does
+// not stall the producer.  Requirements (checked by the host launcher, which falls back to
+// k_syrk_gen): K % BKS == 0, lda even, 16-byte aligned operands, and the element after an odd row
+// count readable (the copies are rounded up to 16 bytes; the extra value only reaches accumulator
+// rows >= M, which are never stored).
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int BKS, int NST>
+struct BulkShape {
+  static constexpr int T = 64, THREADS = 128, LD = T + 4;
+  static constexpr int SLAB = BKS * LD;  // doubles per operand slab
+  static constexpr size_t SMEM = (size_t)NST * 2 * SLAB * sizeof(double) + 2 * NST * sizeof(unsigned long long);
+  static_assert(2 * BKS <= 32 && BKS % 4 == 0, "one copy per lane");
+  static_assert(NST >= 3, "slabs are requested NST - 2 ahead");
+};
+
+template <int BKS, int NST, int MINB, bool SPLIT = false>
+__global__ void __launch_bounds__(128, MINB)
+    k_syrk_bulk(double* C, long long ldc, const double* A, long long lda, int M, int K, int split, int band,
+                unsigned* band_done = nullptr) {
+  using S = BulkShape<BKS, NST>;
+  constexpr int T = S::T;
+  extern __shared__ __align__(16) double smem[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NST * 2 * S::SLAB);
+  unsigned long long* empty = full + NST;
+  int tm, tn;
+  bool signal = false;
+  long long t = blockIdx.x;
+  if (band < 0) {
+    const int nt = (M + T - 1) / T;
+    if (t < (long long)nt * -band) {
+      tm = (int)(t % nt);
+      tn = (int)(t / nt);
+      signal = true;
+      if (tn > tm) {
+        if (threadIdx.x == 0) atomicAdd(band_done, 1u);
+        return;
+      }
+    } else {
+      t -= (long long)nt * -band;
+      split = -band;
+      int r, c;
+      lower_tile_strips(t, nt - split, r, c);
+      tm = split + r;
+      tn = split + c;
+    }
+  } else if (band > 0) {
+    tm = blockIdx.x;
+    tn = split + blockIdx.y;
+    if (tn > tm) return;
+  } else {
+    int r, c;
+    lower_tile_strips(t, (M + T - 1) / T - split, r, c);
+    tm = split + r;
+    tn = split + c;
+  }
+  const int m0 = tm * T, n0 = tn * T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int rw0 = m0 + wm * 32, cw0 = n0 + wn * 32;
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  __syncthreads();
+  // this lane's copy.  One warp per slab (SPLIT = false): lanes [0, BKS) the row operand's column
+  // k0 + lane, [BKS, 2 BKS) the column operand's.  SPLIT: every warp copies a quarter of each slab
+  // (segment warp * BKS / 2 + lane, lanes [0, BKS / 2)) and arrives on the full barrier itself.
+  constexpr int kSeg = SPLIT ? BKS / 2 : 2 * BKS;       // segments per producing warp
+  const int seg = SPLIT ? warp * kSeg + (lane % kSeg) : lane % kSeg;
+  const bool copier = lane < kSeg;
+  const int ck = seg % BKS;
+  const int crow = seg < BKS ? m0 : n0;
+  const int crows = min(T, M - crow);  // >= 1: both tile origins are below M
+  const unsigned cbytes = (unsigned)(((crows + 1) & ~1) * 8);
+  const double* csrc = A + (long long)ck * lda + crow;
+  const int cdst = (seg < BKS ? 0 : S::SLAB) + ck * S::LD;
+  // bytes of one whole slab (both operands); one thread (warp 0's lane 0 when SPLIT, else the
+  // producing warp's) posts them on the stage's full barrier, every copy subtracts its own
+  const unsigned slab_bytes =
+      (unsigned)BKS * 8u * (unsigned)(((min(T, M - m0) + 1) & ~1) + ((min(T, M - n0) + 1) & ~1));
+  const int KT = K / BKS;
+  auto request = [&](int p) {  // whole warp
+    const int sp = p % NST;
+    if (p >= NST) mbar_wait(&empty[sp], ((p / NST) - 1) & 1);
+    if (lane == 0 && (!SPLIT || warp == 0)) mbar_expect_tx(&full[sp], slab_bytes);
+    __syncwarp();
+    if (copier) bulk_g2s(smem + sp * 2 * S::SLAB + cdst, csrc + (long long)p * BKS * lda, cbytes, &full[sp]);
+  };
+  if (SPLIT || warp == 0) {
+#pragma unroll
+    for (int p = 0; p < NST - 2; ++p)
+      if (p < KT) request(p);
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int aoff = wm * 32 + g, boff = S::SLAB + wn * 32 + g;
+  for (int kt = 0; kt < KT; ++kt) {
+    const int s = kt % NST;
+    if ((SPLIT || warp == (kt & 3)) && kt + NST - 2 < KT) request(kt + NST - 2);
+    mbar_wait(&full[s], (kt / NST) & 1);
+    const double* as = smem + s * 2 * S::SLAB + aoff;
+    const double* bs = smem + s * 2 * S::SLAB + boff;
+#pragma unroll
+    for (int kk = 0; kk < BKS; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = as[(kk + t4) * S::LD + i * 8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = bs[(kk + t4) * S::LD + j * 8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+#ifndef GBEM_BULK_NOFENCE
+    // the stage is re-filled through the async proxy: order this warp's (generic-proxy) fragment
+    // loads before that write
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+#endif
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int row = rw0 + i * 8 + g;
+    double cur[4][2];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int col = cw0 + j * 8 + 2 * t4 + e;
+        cur[j][e] = (row < M && col <= row) ? C[(long long)col * ldc + row] : 0.0;
+      }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = cw0 + j * 8 + 2 * t4 + e;

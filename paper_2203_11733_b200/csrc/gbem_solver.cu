@@ -44,6 +44,28 @@ using UpdShape = GenShape<64, 64, 2, 2, 2>;
 // 228 KB) and a trsm or band CTA (<= 38 KB, <= 16K registers) fits beside them
 constexpr size_t kUpdSmemPadded = 60 * 1024;
 static_assert(UpdShape::SMEM <= kUpdSmemPadded, "padding");
+// The same update with its operand slabs staged by bulk copies (TMA engine, mbarrier pipeline;
+// gbem_dmma_gemm.cuh): 35.9 vs 34.3 TFLOP/s at K = 1,536, bit-identical results.  It needs
+// K % 16 == 0 and 16-byte copies, so ragged panels take the cp.async kernel.
+using BulkUpd = BulkShape<16, 3>;
+#define kUpdateBulk k_syrk_bulk<16, 3, 4, true>
+static_assert(BulkUpd::SMEM <= kUpdSmemPadded, "padding");
+
+inline void launch_update(gbem_ctx* ctx, dim3 grid, bool padded, cudaStream_t st, double* C, long long ldc,
+                          const double* A, long long lda, int M, int K, int split, int band,
+                          unsigned* band_done = nullptr) {
+  static const bool use_bulk = getenv("GBEM_UPDATE_CPASYNC") == nullptr;
+  // an odd row count is copied rounded up to 16 bytes: the next element must lie inside the column
+  const long long row0 = (A - ctx->d_A) % lda;
+  const bool bulk = use_bulk && K % 16 == 0 && lda % 2 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+                    ((M & 1) == 0 || row0 + M < lda);
+  if (bulk)
+    kUpdateBulk<<<grid, BulkUpd::THREADS, padded ? kUpdSmemPadded : BulkUpd::SMEM, st>>>(C, ldc, A, lda, M, K, split,
+                                                                                         band, band_done);
+  else
+    kUpdate<<<grid, UpdShape::THREADS, padded ? kUpdSmemPadded : UpdShape::SMEM, st>>>(C, ldc, A, lda, M, K, split,
+                                                                                       band, band_done);
+}
 // Factor the kb x kb (kb <= NB = 128) diagonal block and invert its factor, in
 // shared memory, by 32-column panels:
 //   1. warp 0 factors the 32 x 32 diagonal sub-block in registers (lane i owns
@@ -1547,6 +1569,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
   }
   if (!(ctx->attr_set & gbem_ctx::kAttrFactor)) {
     GBEM_CUDA(ctx, cudaFuncSetAttribute(kUpdate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmemPadded));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(kUpdateBulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUpdSmemPadded));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_trsm_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTrsmSmem));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_potrf_diag, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)kPotrfSmem));
@@ -1631,8 +1654,8 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       trailing(b, m, nt, A21, A22);
       const int t0 = kBand * j0;
       if (t0 >= nt) return;
-      kUpdate<<<dim3(nt, std::min(kBand, nt - t0)), UpdShape::THREADS, UpdShape::SMEM, st>>>(
-          A22, lda, A21, lda, m, std::min(NB, n - b * NB), t0, std::min(kBand, nt - t0));
+      launch_update(ctx, dim3(nt, std::min(kBand, nt - t0)), false, st, A22, lda, A21, lda, m, std::min(NB, n - b * NB),
+                    t0, std::min(kBand, nt - t0));
     };
     // U(b, >= b+1+j0)
     auto update_from = [&](int b, int j0, cudaStream_t st) {
@@ -1642,8 +1665,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       const int t0 = kBand * j0;
       if (t0 >= nt) return;
       const long long tiles = (long long)(nt - t0) * (nt - t0 + 1) / 2;
-      kUpdate<<<(unsigned)tiles, UpdShape::THREADS, UpdShape::SMEM, st>>>(A22, lda, A21, lda, m,
-                                                                           std::min(NB, n - b * NB), t0, 0);
+      launch_update(ctx, dim3((unsigned)tiles), false, st, A22, lda, A21, lda, m, std::min(NB, n - b * NB), t0, 0);
     };
     // Super-blocks of two 128-column blocks: the diagonal factors and panel
     // trsms stay at 128 columns (chain on p / hi), the trailing update of a
@@ -1663,9 +1685,9 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
           // U(b0 .. b0+k-1, b0 + k): block column b0 + k by the super-block's
           // first k blocks at once (one K = 128 k update on the chain)
           const int c0 = bb * NB, mk = n - c0 + (int)ctx->border, ntk = (mk + 63) / 64;
-          if (!(fdbg & 2)) kUpdate<<<dim3(ntk, std::min(kBand, ntk)), UpdShape::THREADS, UpdShape::SMEM, hi>>>(
-              ctx->d_A + (long long)c0 * lda + c0, lda, ctx->d_A + (long long)(b0 * NB) * lda + c0, lda, mk, k * NB, 0,
-              std::min(kBand, ntk));
+          if (!(fdbg & 2))
+            launch_update(ctx, dim3(ntk, std::min(kBand, ntk)), false, hi, ctx->d_A + (long long)c0 * lda + c0, lda,
+                          ctx->d_A + (long long)(b0 * NB) * lda + c0, lda, mk, k * NB, 0, std::min(kBand, ntk));
           GBEM_LAUNCH_CHECK(ctx);
           GBEM_CUDA(ctx, cudaEventRecord(evB, hi));
           GBEM_CUDA(ctx, cudaStreamWaitEvent(p, evB, 0));
@@ -1756,16 +1778,15 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       double* A21 = ctx->d_A + (long long)k0 * lda + k0 + kw;
       double* A22 = ctx->d_A + (long long)(k0 + kw) * lda + (k0 + kw);
       if (band_part) {
-        kUpdate<<<dim3(nt, std::min(kBand2, nt)), UpdShape::THREADS, UpdShape::SMEM, lo>>>(A22, lda, A21, lda, m, kw,
-                                                                                            0, std::min(kBand2, nt));
+        launch_update(ctx, dim3(nt, std::min(kBand2, nt)), false, lo, A22, lda, A21, lda, m, kw, 0,
+                      std::min(kBand2, nt));
       } else if (nt > kBand2) {
         const long long tiles = (long long)(nt - kBand2) * (nt - kBand2 + 1) / 2;
         // near the end the chain on p / hi is the critical path: the rest update
         // then runs 3 CTAs per SM (padded shared memory), which keeps one slot
         // per SM free for the chain's trsm / band kernels instead of queueing
         // them behind a full wave of update tiles
-        const size_t sm = m < occ_rows ? kUpdSmemPadded : UpdShape::SMEM;
-        kUpdate<<<(unsigned)tiles, UpdShape::THREADS, sm, lo>>>(A22, lda, A21, lda, m, kw, kBand2, 0);
+        launch_update(ctx, dim3((unsigned)tiles), m < occ_rows, lo, A22, lda, A21, lda, m, kw, kBand2, 0);
       }
     };
     GBEM_CUDA(ctx, cudaEventRecord(evB, p));  // stepA(0) waits on nothing
@@ -1802,8 +1823,7 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
             (long long)nt * bw + (nt > kBand2 ? (long long)(nt - kBand2) * (nt - kBand2 + 1) / 2 : 0);
         double* A21 = ctx->d_A + (long long)k0 * lda + k0 + kw;
         double* A22 = ctx->d_A + (long long)(k0 + kw) * lda + (k0 + kw);
-        kUpdate<<<(unsigned)tiles, UpdShape::THREADS, UpdShape::SMEM, lo>>>(A22, lda, A21, lda, m, kw, 0, -bw,
-                                                                             ctx->d_band_done);
+        launch_update(ctx, dim3((unsigned)tiles), false, lo, A22, lda, A21, lda, m, kw, 0, -bw, ctx->d_band_done);
         GBEM_LAUNCH_CHECK(ctx);
         band_target += (unsigned)(nt * bw);
         if (!next_tail) {
@@ -1873,13 +1893,13 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
     double* A22 = ctx->d_A + (long long)(k0 + kb) * lda + (k0 + kb);
     constexpr int kBand = NB / 64;
     const int band = std::min(kBand, nt);
-    kUpdate<<<dim3(nt, band), UpdShape::THREADS, UpdShape::SMEM, s>>>(A22, lda, A21, lda, m, kb, 0, band);
+    launch_update(ctx, dim3(nt, band), false, s, A22, lda, A21, lda, m, kb, 0, band);
     GBEM_LAUNCH_CHECK(ctx);
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_col, s));
     if (prof) cudaEventRecord(pe[6 * b + 3], s);
     if (nt > kBand) {
       const long long rest = (long long)(nt - kBand) * (nt - kBand + 1) / 2;
-      kUpdate<<<(unsigned)rest, UpdShape::THREADS, UpdShape::SMEM, s>>>(A22, lda, A21, lda, m, kb, kBand, 0);
+      launch_update(ctx, dim3((unsigned)rest), false, s, A22, lda, A21, lda, m, kb, kBand, 0);
       GBEM_LAUNCH_CHECK(ctx);
     }
   }

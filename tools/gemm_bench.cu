@@ -77,6 +77,16 @@ int main(int argc, char** argv) {
 #define GEN(a, b, c, d, e, f) \
   run_gen(k_syrk_gen<a, b, c, d, e, f>, a, b, 32 * c * d, GenShape<a, b, c, d, e>::SMEM, "gen " #a "x" #b " w" #c "x" #d " st" #e " min" #f)
   GEN(64, 64, 2, 2, 2, 4);
+#define BULK(a, b, c) \
+  run_gen(k_syrk_bulk<a, b, c>, 64, 64, 128, BulkShape<a, b>::SMEM, "bulk bks" #a " st" #b " min" #c)
+  if (k % 16 == 0 && m % 2 == 0) {
+    BULK(8, 4, 4);
+    BULK(8, 6, 4);
+    BULK(16, 3, 4);
+    run_gen(k_syrk_bulk<16, 3, 4, true>, 64, 64, 128, BulkShape<16, 3>::SMEM, "bulk-split bks16 st3 min4");
+    run_gen(k_syrk_bulk<8, 4, 4, true>, 64, 64, 128, BulkShape<8, 4>::SMEM, "bulk-split bks8 st4 min4");
+  }
+  if (getenv("GEMM_BENCH_SHORT")) goto check;
   GEN(64, 64, 2, 2, 3, 3);
   GEN(128, 128, 4, 2, 2, 1);
   GEN(128, 128, 2, 4, 2, 1);
@@ -84,6 +94,7 @@ int main(int argc, char** argv) {
   GEN(64, 64, 2, 2, 4, 3);
   GEN(64, 64, 2, 2, 3, 4);
   GEN(64, 64, 2, 2, 2, 5);
+check:
   cublasHandle_t h;
   cublasCreate(&h);
   double alpha = -1.0, beta = 1.0;
@@ -111,5 +122,16 @@ int main(int argc, char** argv) {
   for (int c = 0; c < m; ++c)
     for (int r = c; r < m; ++r) md = fmax(md, fabs(h1[(size_t)c * ldc + r] - h2[(size_t)c * ldc + r]));
   printf("{\"max_abs_diff_vs_cublas\": %.3e}\n", md);
+  if (k % 16 == 0 && m % 2 == 0) {
+    fill<<<(unsigned)((ldc * m + 255) / 256), 256>>>(C2, ldc * m, 1);
+    k_syrk_bulk<16, 3, 4, true><<<(unsigned)((long long)((m + 63) / 64) * ((m + 63) / 64 + 1) / 2), 128, BulkShape<16, 3>::SMEM>>>(
+        C2, ldc, A, m, m, k, 0, 0);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(h2.data(), C2, sizeof(double) * ldc * m, cudaMemcpyDeviceToHost));
+    md = 0;
+    for (int c = 0; c < m; ++c)
+      for (int r = c; r < m; ++r) md = fmax(md, fabs(h1[(size_t)c * ldc + r] - h2[(size_t)c * ldc + r]));
+    printf("{\"max_abs_diff_bulk_vs_gen\": %.3e}\n", md);
+  }
   return 0;
 }
