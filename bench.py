@@ -270,13 +270,16 @@ def run_extract(args):
     dmma_peak = peaks.get("fp64_dmma_tflops", 37.09)
     dfma_peak = peaks.get("fp64_dfma_tflops", 36.75)
     traffic = _ncu_traffic()
-    roof_chol = {"bound": "tensor", "kernel": "Cholesky factor (k_potrf_diag + k_trsm_rows + k_syrk_gen DMMA update, "
+    roof_chol = {"bound": "tensor", "kernel": "Cholesky factor (k_potrf_diag + k_trsm_rows + k_syrk_bulk DMMA update, "
                                               "bordered: forward substitution fused)",
                  "achieved": chol_flops / (sst.ms_factor * 1e-3) / 1e12, "peak": dmma_peak, "unit": "TFLOP/s",
-                 "traffic": traffic.get("k_syrk_gen"),
+                 "traffic": traffic.get("k_syrk_bulk", traffic.get("k_syrk_gen")),
                  "algorithmic": f"n^3/3 = {chol_flops:.3e} flop per factorisation (n = {n}) / device time of the factor",
                  "peak_source": "tools/fp64_peaks.cu DMMA m8n8k4 loop (no FP64 in MEASURED_PEAKS.json)"}
     roof_chol["frac"] = roof_chol["achieved"] / roof_chol["peak"]
+    upd = _ncu_traffic_file().get("update_kernel", {})
+    if upd:
+        roof_chol["update_kernel_ncu"] = upd
     roof_far = {"bound": "fp64_pipe", "kernel": "k_far", "achieved": ast.far_flops / (ast.ms_far * 1e-3) / 1e12,
                 "peak": dfma_peak, "unit": "TFLOP/s", "traffic": traffic.get("k_far"),
                 "algorithmic": "counted FP64 flops of the Gauss evaluations (dadd, dmul = 1, dfma = 2) / device time",

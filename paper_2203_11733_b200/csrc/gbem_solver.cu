@@ -1731,10 +1731,11 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       return r;
     }();
     // config 3: 411.1 ms at a fixed SB = 5, 405.5 at 10, 403.3 with the large table;
-    // config 2: 18.47 ms at a fixed SB = 2, 18.23 with the small one
+    // config 2: 18.47 ms at a fixed SB = 2, 18.23 with the small one (bulk-staged update: 17.49 with
+    // {4, 3, 2, 1}, 17.34 with {6, 4, 2, 1})
     static const std::vector<SbRule> sb_large = {{12, 16000}, {10, 12000}, {8, 9000}, {6, 7000},
                                                  {4, 5000},   {3, 3500},   {2, 0}};
-    static const std::vector<SbRule> sb_small = {{4, 9000}, {3, 6000}, {2, 3000}, {1, 0}};
+    static const std::vector<SbRule> sb_small = {{6, 9000}, {4, 6000}, {2, 3000}, {1, 0}};
     static const bool ramp_on = getenv("GBEM_SB_NO_RAMP") == nullptr;
     static const std::vector<int> ramp_widths = [] {
       std::vector<int> w;

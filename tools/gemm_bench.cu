@@ -79,6 +79,10 @@ int main(int argc, char** argv) {
   GEN(64, 64, 2, 2, 2, 4);
 #define BULK(a, b, c) \
   run_gen(k_syrk_bulk<a, b, c>, 64, 64, 128, BulkShape<a, b>::SMEM, "bulk bks" #a " st" #b " min" #c)
+  if (getenv("GEMM_BENCH_BULK_ONLY")) {
+    run_gen(k_syrk_bulk<16, 3, 4, true>, 64, 64, 128, BulkShape<16, 3>::SMEM, "bulk-split bks16 st3 min4");
+    goto check;
+  }
   if (k % 16 == 0 && m % 2 == 0) {
     BULK(8, 4, 4);
     BULK(8, 6, 4);
