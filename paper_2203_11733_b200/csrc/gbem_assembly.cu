@@ -1230,11 +1230,38 @@ __global__ void __launch_bounds__(128)
   if (evals) atomicAdd(&stats[ST_NEAR_EVALS], (unsigned long long)evals);
 }
 
+// Near-contact pairs are few (42 of 2.5e9 in a config-5 row chunk) and slow (the adaptive Romberg of
+// one pair keeps a warp busy for 1-4 ms), so a kernel over one chunk's pairs is a 1-4 ms launch that
+// occupies two or three warps.  The chunks of an assembly therefore only collect them
+// (k_romb_collect moves the chunk's Romberg-route queue entries to a list that persists over the
+// chunks) and one k_near_warp launch at the end evaluates the whole list, one warp per pair.  What does
+// not fit the list is evaluated in place (skip = the number taken from this chunk).
+constexpr uint32_t kRombCap = 1u << 20;
+
+__global__ void __launch_bounds__(256)
+    k_romb_collect(const uint64_t* __restrict__ queue, const uint32_t* __restrict__ offsets, uint64_t* list,
+                   uint32_t* cnt) {
+  const uint32_t begin = offsets[kClsParallel], end = offsets[kClsOrthogonal + 1];  // keys 10, 11
+  __shared__ uint32_t s_base, s_take;
+  if (threadIdx.x == 0) {  // one CTA, launches ordered on their stream
+    s_base = cnt[0];
+    s_take = min(end - begin, kRombCap - s_base);
+    cnt[0] = s_base + s_take;
+    cnt[1] = s_take;
+  }
+  __syncthreads();
+  for (uint32_t k = threadIdx.x; k < s_take; k += blockDim.x) list[s_base + k] = queue[begin + k];
+}
+
+// list_cnt == nullptr: the Romberg-route entries of the queue, from `skip` entries in (nullptr: 0);
+// else queue is the collected list of *list_cnt entries.
 __global__ void __launch_bounds__(128)
     k_near_warp(const DPanel* __restrict__ P, const uint64_t* __restrict__ queue,
                 const uint32_t* __restrict__ offsets, OutSpec o, double rel_tol, int max_levels,
-                unsigned long long* stats) {
-  const uint32_t begin = offsets[kClsParallel], end = offsets[kClsOrthogonal + 1];  // keys 10, 11
+                unsigned long long* stats, const uint32_t* skip = nullptr, const uint32_t* list_cnt = nullptr) {
+  const uint32_t begin = list_cnt ? 0u : offsets[kClsParallel] + (skip ? *skip : 0u);
+  const uint32_t end = list_cnt ? *list_cnt : offsets[kClsOrthogonal + 1];
+  if (begin >= end) return;
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -1377,8 +1404,48 @@ int prepare_work(gbem_ctx* ctx, const gbem_quad_config* cfg_in, gbem_quad_config
 
 // Evaluate every queued class for the current chunk.
 int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float* ms_far,
-             float* ms_near) {
+             float* ms_near, bool defer_romberg = false) {
   int sms = ctx->num_sms;
+  // The near-field kernels (closed-form coplanar, graded Gauss-Legendre, warp Romberg) write
+  // entries no far-field kernel touches and are latency-bound -- a chunk's handful of
+  // near-contact pairs keeps one warp each busy for ~1 ms in k_near_warp -- so they run on a
+  // second stream beside the far-field kernels (config 5: near 588 of 2,690 ms when serial).
+  // With per-phase timing requested the phases run one after the other, as their times are defined.
+  static const bool near_serial = getenv("GBEM_NEAR_SERIAL") != nullptr;
+  const bool overlap = !ms_far && !ms_near && !near_serial;
+  cudaStream_t ns = ctx->stream;
+  if (overlap) {
+    if (!ctx->near_stream) {
+      GBEM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->near_stream, cudaStreamNonBlocking));
+      GBEM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_near_fork, cudaEventDisableTiming));
+      GBEM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_near_join, cudaEventDisableTiming));
+    }
+    ns = ctx->near_stream;
+    GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_near_fork, ctx->stream));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(ns, ctx->ev_near_fork, 0));
+  }
+  static const int near_skip = getenv("GBEM_DBG_SKIP_NEAR") ? atoi(getenv("GBEM_DBG_SKIP_NEAR")) : 0;  // timing experiments
+  auto near_kernels = [&]() -> int {
+    if (near_skip == 3) return GBEM_OK;
+    // the longest-running kernel first
+    if (defer_romberg && near_skip != 1) {
+      k_romb_collect<<<1, 256, 0, ns>>>(ctx->d_queue, ctx->d_offsets, ctx->d_romb, ctx->d_romb_cnt);
+      GBEM_LAUNCH_CHECK(ctx);
+    }
+    if (near_skip != 1)
+      k_near_warp<<<sms * 8, 128, 0, ns>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, cfg.rel_tol,
+                                           cfg.max_levels, ctx->d_stats, defer_romberg ? ctx->d_romb_cnt + 1 : nullptr);
+    GBEM_LAUNCH_CHECK(ctx);
+    k_near_gl<<<sms * 8, 128, 0, ns>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, ctx->d_stats);
+    GBEM_LAUNCH_CHECK(ctx);
+    k_coplanar<<<sms * 4, 128, 0, ns>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o);
+    GBEM_LAUNCH_CHECK(ctx);
+    return GBEM_OK;
+  };
+  if (overlap) {
+    if (int rc = near_kernels()) return rc;
+    GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_near_join, ns));
+  }
   cudaEventRecord(ctx->ev[2], ctx->stream);
 #define GBEM_FAR(M) \
   k_far<M><<<sms * 4, far_threads(M), 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan, \
@@ -1398,13 +1465,11 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
   GBEM_FAST_DESCS(GBEM_FAST)
 #undef GBEM_FAST
   cudaEventRecord(ctx->ev[3], ctx->stream);
-  k_coplanar<<<sms * 4, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o);
-  GBEM_LAUNCH_CHECK(ctx);
-  k_near_gl<<<sms * 8, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o, ctx->d_stats);
-  GBEM_LAUNCH_CHECK(ctx);
-  k_near_warp<<<sms * 8, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_offsets, o,
-                                                cfg.rel_tol, cfg.max_levels, ctx->d_stats);
-  GBEM_LAUNCH_CHECK(ctx);
+  if (overlap) {
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_near_join, 0));
+  } else {
+    if (int rc = near_kernels()) return rc;
+  }
   cudaEventRecord(ctx->ev[4], ctx->stream);
   if (ms_far || ms_near) {
     GBEM_CUDA(ctx, cudaEventSynchronize(ctx->ev[4]));
@@ -1573,6 +1638,14 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
   const long long tiles_per_chunk = std::max<long long>(1, ctx->queue_cap / (kTile * kTile));
   float ms_cls = 0, ms_far = 0, ms_near = 0;
   bool timing = stats != nullptr;
+  static const bool defer_romberg = getenv("GBEM_NO_ROMBERG_DEFER") == nullptr;
+  if (defer_romberg) {
+    if (!ctx->d_romb) {
+      GBEM_CUDA(ctx, cudaMalloc(&ctx->d_romb, sizeof(uint64_t) * kRombCap));
+      GBEM_CUDA(ctx, cudaMalloc(&ctx->d_romb_cnt, sizeof(uint32_t) * 2));
+    }
+    GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_romb_cnt, 0, sizeof(uint32_t) * 2, ctx->stream));
+  }
   cudaEventRecord(ctx->ev[0], ctx->stream);
   for (long long t0 = 0; t0 < total_tiles; t0 += tiles_per_chunk) {
     long long nt = std::min(tiles_per_chunk, total_tiles - t0);
@@ -1595,8 +1668,21 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
       cudaEventElapsedTime(&a, ctx->ev[5], ctx->ev[6]);
       ms_cls += a;
     }
-    rc = run_eval(ctx, o, cfg, timing ? &ms_far : nullptr, timing ? &ms_near : nullptr);
+    rc = run_eval(ctx, o, cfg, timing ? &ms_far : nullptr, timing ? &ms_near : nullptr, defer_romberg);
     if (rc) return rc;
+  }
+  if (defer_romberg) {  // the near-contact pairs of every chunk, one warp each
+    cudaEventRecord(ctx->ev[2], ctx->stream);
+    k_near_warp<<<ctx->num_sms * 8, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_romb, ctx->d_offsets, o, cfg.rel_tol,
+                                                          cfg.max_levels, ctx->d_stats, nullptr, ctx->d_romb_cnt);
+    GBEM_LAUNCH_CHECK(ctx);
+    cudaEventRecord(ctx->ev[3], ctx->stream);
+    if (timing) {
+      GBEM_CUDA(ctx, cudaEventSynchronize(ctx->ev[3]));
+      float a = 0;
+      cudaEventElapsedTime(&a, ctx->ev[2], ctx->ev[3]);
+      ms_near += a;
+    }
   }
   if (symmetrize) {
     const int snbt = (int)((n + kSymTile - 1) / kSymTile);

@@ -194,6 +194,8 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   cudaFree(ctx->d_flags);
   cudaFree(ctx->d_band_done);
   cudaFree(ctx->d_kp);
+  cudaFree(ctx->d_romb);
+  cudaFree(ctx->d_romb_cnt);
   cudaFree(ctx->d_rhs);
   cudaFree(ctx->d_linv);
   cudaFree(ctx->d_sw);
@@ -202,6 +204,9 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+  if (ctx->near_stream) cudaStreamDestroy(ctx->near_stream);
+  if (ctx->ev_near_fork) cudaEventDestroy(ctx->ev_near_fork);
+  if (ctx->ev_near_join) cudaEventDestroy(ctx->ev_near_join);
   if (ctx->ev_panel) cudaEventDestroy(ctx->ev_panel);
   for (auto& e : ctx->ev_bw)
     if (e) cudaEventDestroy(e);

@@ -50,6 +50,10 @@ struct gbem_ctx {
   int64_t plan_cap = 0;
   uint64_t* d_kp = nullptr;  // (key, plan) per pair in tile order between the two classification passes
   int64_t kp_cap = 0;
+  // near-contact (Romberg-route) pairs collected over the chunks of one assembly and evaluated
+  // together at its end: entries, then {count, taken from the current chunk}
+  uint64_t* d_romb = nullptr;
+  uint32_t* d_romb_cnt = nullptr;
   uint32_t* d_counts = nullptr;   // per key
   uint32_t* d_offsets = nullptr;  // exclusive scan of counts (kNumKeys + 1)
   uint32_t* d_cursors = nullptr;
@@ -74,6 +78,9 @@ struct gbem_ctx {
   cudaEvent_t ev[8] = {};
   cudaStream_t side_stream = nullptr;  // high-priority look-ahead stream of the factorisation
   cudaEvent_t ev_panel = nullptr, ev_col = nullptr;
+  // near-field kernels of an assembly chunk run beside its far-field kernels (gbem_assembly.cu run_eval)
+  cudaStream_t near_stream = nullptr;
+  cudaEvent_t ev_near_fork = nullptr, ev_near_join = nullptr;
   cudaEvent_t ev_bw[5] = {};  // look-ahead backward substitution: start, step done, bulk done x 3
   // its captured sweep (cudaGraphExec_t), valid for one (matrix, factor, work, output, shape) tuple
   struct BwdGraphKey {

@@ -11,6 +11,7 @@ from paper_2203_11733_b200.shard import ShardedAssembler, panels_to_device, bala
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 scale = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 chunks = int(sys.argv[3]) if len(sys.argv) > 3 else 16
+with_stats = (sys.argv[4] != '0') if len(sys.argv) > 4 else True  # 0: no per-phase timing (near field overlaps far)
 t0 = time.time()
 ps = g.config_model(cfg, seed=1, scale=scale).partition(1)
 n = len(ps)
@@ -27,8 +28,12 @@ torch.cuda.synchronize()
 ev0.record()
 for c in range(chunks):
     sh = ShardedAssembler(ctx, pdev, n, c, chunks)
-    blk = sh.assemble(with_stats=True)
+    blk = sh.assemble(with_stats=with_stats)
     chk += blk.sum()
+    if not with_stats:
+        tot_pairs += sh.unique_pairs
+        del sh, blk
+        continue
     st = sh.stats
     tot_pairs += st.pairs_total
     for k, f in (("far", "pairs_far"), ("cop", "pairs_coplanar"), ("par", "pairs_parallel"), ("orth", "pairs_orthogonal"),
