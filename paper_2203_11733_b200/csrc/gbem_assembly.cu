@@ -335,6 +335,10 @@ __device__ __forceinline__ uint32_t classify_pair(const CPanel& A, const CPanel&
 // distinct key per CTA then counts (pass 1) or reserves the CTA's queue range
 // (pass 2), and each warp group writes at range base + its offset.
 constexpr int kHash = 1024;  // >= pairs per CTA: the table never fills
+#ifndef GBEM_STAGE_MIN_KEYS
+#define GBEM_STAGE_MIN_KEYS 40
+#endif
+constexpr int kStageMinKeys = GBEM_STAGE_MIN_KEYS;  // threads holding a used table slot above which the fill pass stages by key
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
 __device__ __forceinline__ int hash_slot(uint32_t* hkey, uint32_t key) {
@@ -423,27 +427,90 @@ __global__ void __launch_bounds__(kClassifyThreads)
     }
   }
   __syncthreads();
-  // one global atomic per distinct key of the tile; hcnt becomes the range base (FILL)
-  for (int s = tid; s < kHash; s += kClassifyThreads) {
-    const uint32_t k = hkey[s];
-    if (k == kEmpty) continue;
-    if (FILL)
-      hcnt[s] = atomicAdd(&cursors[k], hcnt[s]);
-    else
-      atomicAdd(&counts[k], hcnt[s]);
-  }
-  if (!FILL) return;
-  __syncthreads();
+  if constexpr (!FILL) {
+    // one global atomic per distinct key of the tile
+    for (int s = tid; s < kHash; s += kClassifyThreads) {
+      const uint32_t k = hkey[s];
+      if (k != kEmpty) atomicAdd(&counts[k], hcnt[s]);
+    }
+  } else {
+    // The tile's entries are first grouped by key in shared memory (position = exclusive prefix of
+    // the key's table slot + the warp group's offset + the lane's rank) and then written out in
+    // that order, so consecutive threads store consecutive entries of one key's queue range: with
+    // ~100 distinct keys per tile (config 5) a warp row holds 2-3 pairs per key, and storing from
+    // the classification layout wrote 12 bytes into a separate 32-byte sector for almost every pair.
+    __shared__ uint32_t slpre[kHash];
+    __shared__ uint64_t s_entry[kTile * kTile];
+    __shared__ uint32_t s_plan[kTile * kTile];
+    __shared__ uint16_t s_slot[kTile * kTile];
+    __shared__ uint32_t s_wsum[kClassifyThreads / 32];
+    static_assert(kHash == 4 * kClassifyThreads, "four table slots per thread");
+    uint32_t c[4], sum = 0;
 #pragma unroll
-  for (int it = 0; it < kIter; ++it) {
-    if (key[it] == kEmpty) continue;
-    const int leader = __ffs(peers[it]) - 1;
-    uint32_t base = slot[it] >= 0 ? hcnt[slot[it]] + leader_off[it] : 0;
-    base = __shfl_sync(peers[it], base, leader);
-    const int r = warp + it * (kClassifyThreads / 32);
-    const uint32_t rank = __popc(peers[it] & ((1u << lane) - 1u));
-    queue[base + rank] = pack_entry((uint32_t)(bi * kTile + r), (uint32_t)j, key[it]);
-    plans[base + rank] = plan[it];
+    for (int q = 0; q < 4; ++q) {
+      const int sl = 4 * tid + q;
+      const uint32_t k = hkey[sl];
+      c[q] = k == kEmpty ? 0u : hcnt[sl];
+      if (c[q]) hcnt[sl] = atomicAdd(&cursors[k], c[q]);  // hcnt becomes the key's range base for this tile
+      sum += c[q];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    // few distinct keys in the tile (config 3: ~20): the classification layout already stores
+    // long runs per key, and the staging pass would only cost (11.1 -> 12.3 ms on config 3)
+    const int busy = __syncthreads_count(sum != 0);
+    if (busy <= kStageMinKeys) {
+#pragma unroll
+      for (int it = 0; it < kIter; ++it) {
+        if (key[it] == kEmpty) continue;
+        const int leader = __ffs(peers[it]) - 1;
+        uint32_t base = slot[it] >= 0 ? hcnt[slot[it]] + leader_off[it] : 0;
+        base = __shfl_sync(peers[it], base, leader);
+        const int r = warp + it * (kClassifyThreads / 32);
+        const uint32_t rank = __popc(peers[it] & ((1u << lane) - 1u));
+        queue[base + rank] = pack_entry((uint32_t)(bi * kTile + r), (uint32_t)j, key[it]);
+        plans[base + rank] = plan[it];
+      }
+      return;
+    }
+    uint32_t wbase = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < kClassifyThreads / 32; ++w) {
+      if (w < warp) wbase += s_wsum[w];
+      total += s_wsum[w];
+    }
+    uint32_t run = wbase + incl - sum;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      slpre[4 * tid + q] = run;
+      run += c[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < kIter; ++it) {
+      if (key[it] == kEmpty) continue;
+      const int leader = __ffs(peers[it]) - 1;
+      const int sl = __shfl_sync(peers[it], slot[it], leader);
+      const uint32_t lo = __shfl_sync(peers[it], leader_off[it], leader);
+      const int r = warp + it * (kClassifyThreads / 32);
+      const uint32_t rank = __popc(peers[it] & ((1u << lane) - 1u));
+      const uint32_t lpos = slpre[sl] + lo + rank;
+      s_entry[lpos] = pack_entry((uint32_t)(bi * kTile + r), (uint32_t)j, key[it]);
+      s_plan[lpos] = plan[it];
+      s_slot[lpos] = (uint16_t)sl;
+    }
+    __syncthreads();
+    for (uint32_t t2 = tid; t2 < total; t2 += kClassifyThreads) {
+      const int sl = s_slot[t2];
+      const uint32_t gpos = hcnt[sl] + (t2 - slpre[sl]);
+      queue[gpos] = s_entry[t2];
+      plans[gpos] = s_plan[t2];
+    }
   }
 }
 
