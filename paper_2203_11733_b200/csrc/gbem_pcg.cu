@@ -48,6 +48,7 @@ namespace {
 
 using gbem_gemm::BK;
 using gbem_sk::k_gemm_nt_sk;
+using gbem_sk::k_gemm_nt_sk_bulk;
 using gbem_sk::kSmem;
 using gbem_sk::kT;
 using gbem_sk::kThreads;
@@ -377,16 +378,25 @@ int gemm_nt(gbem_ctx* ctx, double* C, long long ldc, long long strideC, const do
   static_assert(kSmem <= 227 * 1024, "smem");
   if (!(ctx->attr_set & gbem_ctx::kAttrPcgGemm)) {
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt_sk<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt_sk_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)gbem_sk::SkBulk::SMEM));
     ctx->attr_set |= gbem_ctx::kAttrPcgGemm;
   }
+  static const bool use_bulk = getenv("GBEM_PCG_CPASYNC") == nullptr;
   long long kchunk = (Ktot + S - 1) / S;
   kchunk = (kchunk + BK - 1) / BK * BK;
   const int vec16 = (lda % 2 == 0 && ldb % 2 == 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0) ? 1 : 0;
   for (int m0 = 0; m0 < M; m0 += kT) {
     const int mm = std::min(kT, M - m0);
     dim3 grid(1, (unsigned)((N + kT - 1) / kT), (unsigned)S);
-    k_gemm_nt_sk<64><<<grid, kThreads, kSmem, ctx->stream>>>(C + m0, ldc, strideC, A + m0, lda, B, ldb, mm, N,
-                                                            Ktot, kchunk, vec16 && (m0 % 2 == 0));
+    // bulk-copy staging: 16-byte copies rounded up from an odd row count must stay inside the column
+    const bool bulk = use_bulk && vec16 && (mm % 2 == 0 || m0 + mm < lda) && (N % 2 == 0 || N < ldb);
+    if (bulk)
+      k_gemm_nt_sk_bulk<<<grid, 128, gbem_sk::SkBulk::SMEM, ctx->stream>>>(C + m0, ldc, strideC, A + m0, lda, B, ldb,
+                                                                          mm, N, Ktot, kchunk);
+    else
+      k_gemm_nt_sk<64><<<grid, kThreads, kSmem, ctx->stream>>>(C + m0, ldc, strideC, A + m0, lda, B, ldb, mm, N,
+                                                              Ktot, kchunk, vec16 && (m0 % 2 == 0));
     GBEM_LAUNCH_CHECK(ctx);
   }
   return GBEM_OK;
