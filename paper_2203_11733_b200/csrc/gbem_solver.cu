@@ -1504,7 +1504,12 @@ static int init_green(gbem_ctx* ctx) {
   if (p_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return ctx->green_state;
   const int want = getenv("GBEM_GREEN_SIDE") ? atoi(getenv("GBEM_GREEN_SIDE")) : 2;
   unsigned ng = 1;
-  if (p_split(&side, &ng, &all, &rest, 0, (unsigned)want) != CUDA_SUCCESS || ng != 1) return ctx->green_state;
+  // CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING: without it a request for 2 SMs reserves 8 on
+  // sm_100 (tools/green_probe.cu: side 8 / rest 140), and the trailing updates lose 6 SMs = 4% of
+  // the machine; with it the split is 2 / 146.  No kernel of either partition uses clusters.
+  const unsigned split_flags = getenv("GBEM_GREEN_FLAGS") ? (unsigned)atoi(getenv("GBEM_GREEN_FLAGS"))
+                                                          : (unsigned)CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING;
+  if (p_split(&side, &ng, &all, &rest, split_flags, (unsigned)want) != CUDA_SUCCESS || ng != 1) return ctx->green_state;
   CUdevResourceDesc d_side, d_rest;
   if (p_desc(&d_side, &side, 1) != CUDA_SUCCESS || p_desc(&d_rest, &rest, 1) != CUDA_SUCCESS) return ctx->green_state;
   CUgreenCtx g_side, g_main;

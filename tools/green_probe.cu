@@ -18,6 +18,12 @@ int main() {
   CUdevice dev; CU(cuDeviceGet(&dev, 0));
   CUdevResource res; CU(cuDeviceGetDevResource(dev, &res, CU_DEV_RESOURCE_TYPE_SM));
   printf("SMs: %u\n", res.sm.smCount);
+  for (unsigned flags = 0; flags < 2; ++flags)
+    for (unsigned want : {1u, 2u, 4u, 8u}) {  // what a request for `want` SMs really reserves
+      CUdevResource p2, r2; unsigned n2 = 1;
+      CUresult rc = cuDevSmResourceSplitByCount(&p2, &n2, &res, &r2, flags, want);
+      printf("split flags=%u minCount=%u -> rc=%d side %u SMs, rest %u SMs\n", flags, want, (int)rc, p2.sm.smCount, r2.sm.smCount);
+    }
   CUdevResource part, rest; unsigned ng = 1;
   CU(cuDevSmResourceSplitByCount(&part, &ng, &res, &rest, 0, 8));
   printf("groups %u: side %u SMs, rest %u SMs\n", ng, part.sm.smCount, rest.sm.smCount);
