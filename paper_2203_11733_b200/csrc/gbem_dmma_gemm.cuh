@@ -479,7 +479,10 @@ struct BulkShape {
   static_assert(NST >= 3, "slabs are requested NST - 2 ahead");
 };
 
-template <int BKS, int NST, int MINB, bool SPLIT = false>
+// TRI_STORE: C = A A^T (lower tiles, stored, C not read) for an upper-triangular A -- tile (tm, tn)
+// starts its reduction at column 64 tm, the first one where rows >= 64 tm of A are non-zero (the
+// block-Jacobi inverses of the sharded solve: inv(M) = N N^T with N = -inv(L)^T).
+template <int BKS, int NST, int MINB, bool SPLIT = false, bool TRI_STORE = false>
 __global__ void __launch_bounds__(128, MINB)
     k_syrk_bulk(double* C, long long ldc, const double* A, long long lda, int M, int K, int split, int band,
                 unsigned* band_done = nullptr) {
@@ -544,13 +547,14 @@ __global__ void __launch_bounds__(128, MINB)
   const int crow = seg < BKS ? m0 : n0;
   const int crows = min(T, M - crow);  // >= 1: both tile origins are below M
   const unsigned cbytes = (unsigned)(((crows + 1) & ~1) * 8);
-  const double* csrc = A + (long long)ck * lda + crow;
+  const int kt0 = TRI_STORE ? m0 / BKS : 0;  // slabs skipped (zero rows of a triangular operand)
+  const double* csrc = A + ((long long)kt0 * BKS + ck) * lda + crow;
   const int cdst = (seg < BKS ? 0 : S::SLAB) + ck * S::LD;
   // bytes of one whole slab (both operands); one thread (warp 0's lane 0 when SPLIT, else the
   // producing warp's) posts them on the stage's full barrier, every copy subtracts its own
   const unsigned slab_bytes =
       (unsigned)BKS * 8u * (unsigned)(((min(T, M - m0) + 1) & ~1) + ((min(T, M - n0) + 1) & ~1));
-  const int KT = K / BKS;
+  const int KT = K / BKS - kt0;
   auto request = [&](int p) {  // whole warp
     const int sp = p % NST;
     if (p >= NST) mbar_wait(&empty[sp], ((p / NST) - 1) & 1);
@@ -604,14 +608,14 @@ __global__ void __launch_bounds__(128, MINB)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = cw0 + j * 8 + 2 * t4 + e;
-        cur[j][e] = (row < M && col <= row) ? C[(long long)col * ldc + row] : 0.0;
+        cur[j][e] = (!TRI_STORE && row < M && col <= row) ? C[(long long)col * ldc + row] : 0.0;
       }
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int col = cw0 + j * 8 + 2 * t4 + e;
-        if (row < M && col <= row) C[(long long)col * ldc + row] = cur[j][e] - acc[i][j][e];
+        if (row < M && col <= row) C[(long long)col * ldc + row] = TRI_STORE ? acc[i][j][e] : cur[j][e] - acc[i][j][e];
       }
   }
   if (signal) {

@@ -295,6 +295,58 @@ __global__ void k_identity(double* I, long long m) {
     I[e] = (e / m == e % m) ? 1.0 : 0.0;
 }
 
+// ---- explicit inverse of a factored Jacobi block from its Cholesky factor (n^3 flops instead of
+// the 2.3 n^3 of two dense triangular solves against the identity):
+//   N = -inv(L)^T (upper) and Y = N^T (lower) are built bottom-up over groups of 128-row blocks,
+//   [[L11, 0], [L21, L22]] -> N12 = N11 L21^T N22 (two NT GEMMs: T = N11 L21^T, N12 = T Y22^T; the
+//   signs cancel), Y21 = N12^T; the 128 x 128 base blocks come from the factorisation's own
+//   inverses of its diagonal blocks; then inv(M) = N N^T (k_syrk_bulk<TRI_STORE>, the reduction of a
+//   tile starting at its first non-zero column) and a mirror into the upper triangle.
+constexpr int kInvNB = 128;
+
+__global__ void __launch_bounds__(256)
+    k_inv_base(const double* __restrict__ Linv, int n, double* Nm, double* Ym, long long ld) {
+  const int b = blockIdx.x, r0 = b * kInvNB;
+  for (int idx = threadIdx.x; idx < kInvNB * kInvNB; idx += blockDim.x) {
+    const int c = idx / kInvNB, r = idx % kInvNB;
+    if (r0 + r < n && r0 + c < n && r >= c) {
+      const double v = -Linv[(size_t)b * kInvNB * kInvNB + c * kInvNB + r];  // inv(L_bb)(r, c)
+      Ym[(long long)(r0 + c) * ld + r0 + r] = v;
+      Nm[(long long)(r0 + r) * ld + r0 + c] = v;
+    }
+  }
+}
+
+// dst(j, i) = src(i, j), src rows x cols (column-major, lds), 32 x 32 tiles through shared memory
+__global__ void __launch_bounds__(256)
+    k_transpose(const double* __restrict__ src, long long lds, double* __restrict__ dst, long long ldd, int rows,
+                int cols) {
+  __shared__ double t[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int jj = ty; jj < 32; jj += 8)
+    if (i0 + tx < rows && j0 + jj < cols) t[jj][tx] = src[(long long)(j0 + jj) * lds + i0 + tx];
+  __syncthreads();
+  for (int ii = ty; ii < 32; ii += 8)
+    if (j0 + tx < cols && i0 + ii < rows) dst[(long long)(i0 + ii) * ldd + j0 + tx] = t[tx][ii];
+}
+
+// A(c, r) = A(r, c) for r > c (lower triangle mirrored into the upper), n x n column-major
+__global__ void __launch_bounds__(256) k_mirror_lower(double* A, long long ld, int n) {
+  __shared__ double t[32][33];
+  const int bi = blockIdx.x, bj = blockIdx.y;  // tile rows bi >= tile columns bj
+  if (bj > bi) return;
+  const int i0 = bi * 32, j0 = bj * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int jj = ty; jj < 32; jj += 8)
+    if (i0 + tx < n && j0 + jj < n) t[jj][tx] = A[(long long)(j0 + jj) * ld + i0 + tx];
+  __syncthreads();
+  for (int ii = ty; ii < 32; ii += 8) {
+    const int r = j0 + tx, c = i0 + ii;  // destination (row r, column c) = source (row c, column r)
+    if (r < n && c < n && c > r) A[(long long)c * ld + r] = t[tx][ii];
+  }
+}
+
 // Ct[r * K + k] += scale * X(i, r) for the local rows i with net(row_begin + i) = k;
 // panels with net -1 (grounded outer panels) add to the outer charge Ct[K * K + r]
 // (net_charges, extraction.hpp:55-79)
@@ -320,13 +372,14 @@ __global__ void k_finish_resid(const double* sc_rres, const double* sc, int K, i
 
 // ---------------------------------------------------------------- workspace
 struct Ws {
-  size_t cap_A = 0, cap_vec = 0, cap_full = 0, cap_part = 0, cap_minv = 0, cap_tmp = 0;
+  size_t cap_A = 0, cap_vec = 0, cap_full = 0, cap_part = 0, cap_minv = 0, cap_tmp = 0, cap_inv = 0;
   double* A = nullptr;      // m x n column-major rows of this rank (ld mA)
   double* vec = nullptr;    // B, X, R, Z, P, Q : 6 x (m Kp)
   double* full = nullptr;   // P_full: nranks m x Kp
   double* part = nullptr;   // split-K partials
   double* minv = nullptr;   // explicit inverses of the Jacobi blocks
   double* tmp = nullptr;    // identity for the inverse solves
+  double* inv = nullptr;    // N, Y, T of the GEMM-form block inverse
   double* sc = nullptr;     // scalars: S_COUNT x Kp, then rres (Kp), then C (K x K)
   size_t cap_sc = 0;
   int* d_done = nullptr;
@@ -343,6 +396,7 @@ void release(gbem_ctx* ctx) {
     cudaFree(w->part);
     cudaFree(w->minv);
     cudaFree(w->tmp);
+    cudaFree(w->inv);
     cudaFree(w->sc);
     cudaFree(w->d_done);
     if (w->h_done) cudaFreeHost(w->h_done);
@@ -372,16 +426,66 @@ int grow(gbem_ctx* ctx, double** p, size_t* cap, size_t need) {
   return GBEM_OK;
 }
 
-// C_z = A * B^T split over `S` slices of Ktot (Kp rows of C handled in 64-row chunks)
-int gemm_nt(gbem_ctx* ctx, double* C, long long ldc, long long strideC, const double* A, long long lda,
-            const double* B, long long ldb, int M, int N, long long Ktot, int S) {
-  static_assert(kSmem <= 227 * 1024, "smem");
+int ensure_gemm_attrs(gbem_ctx* ctx) {
   if (!(ctx->attr_set & gbem_ctx::kAttrPcgGemm)) {
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt_sk<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     GBEM_CUDA(ctx, cudaFuncSetAttribute(k_gemm_nt_sk_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)gbem_sk::SkBulk::SMEM));
+    GBEM_CUDA(ctx, cudaFuncSetAttribute(gbem_gemm::k_syrk_bulk<16, 3, 4, true, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gbem_sk::SkBulk::SMEM));
     ctx->attr_set |= gbem_ctx::kAttrPcgGemm;
   }
+  return GBEM_OK;
+}
+
+// Explicit inverse of the Jacobi block whose Cholesky factor is in ctx->d_A (mb x mb, the
+// factorisation's diagonal-block inverses in ctx->d_linv) into out (column-major, ld = mb); see the
+// kernels above.  `ws` holds N, Y (ld x ld each, ld = mb rounded up to 16) and T.
+int block_inverse_gemm(gbem_ctx* ctx, double* ws, long long mb, double* out) {
+  cudaStream_t s = ctx->stream;
+  if (int rc = ensure_gemm_attrs(ctx)) return rc;
+  const long long ld = (mb + 15) / 16 * 16;
+  double *Nm = ws, *Ym = ws + ld * ld, *T = Ym + ld * ld;
+  GBEM_CUDA(ctx, cudaMemsetAsync(Nm, 0, sizeof(double) * 2 * (size_t)(ld * ld), s));
+  const int nblk = (int)((mb + kInvNB - 1) / kInvNB);
+  k_inv_base<<<nblk, 256, 0, s>>>(ctx->d_linv, (int)mb, Nm, Ym, ld);
+  GBEM_LAUNCH_CHECK(ctx);
+  auto gemm_store = [&](double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb, int M,
+                        int N, int K) -> int {
+    const long long kchunk = ((long long)K + BK - 1) / BK * BK;
+    dim3 grid((unsigned)((M + kT - 1) / kT), (unsigned)((N + kT - 1) / kT), 1);
+    k_gemm_nt_sk_bulk<<<grid, 128, gbem_sk::SkBulk::SMEM, s>>>(C, ldc, 0, A, lda, B, ldb, M, N, K, kchunk);
+    GBEM_LAUNCH_CHECK(ctx);
+    return GBEM_OK;
+  };
+  const long long lda = ctx->lda;
+  for (int len = 1; len < nblk; len *= 2)
+    for (int g = 0; g + len < nblk; g += 2 * len) {
+      const long long r0 = (long long)g * kInvNB, r1 = (long long)(g + len) * kInvNB;
+      const long long r2 = std::min<long long>((long long)(g + 2 * len) * kInvNB, mb);
+      const int s1 = (int)(r1 - r0), s2 = (int)(r2 - r1);
+      // T = N11 L21^T (s1 x s2), then N12 = T Y22^T, then Y21 = N12^T
+      if (int rc = gemm_store(T, s1, Nm + r0 * ld + r0, ld, ctx->d_A + r0 * lda + r1, lda, s1, s2, s1)) return rc;
+      if (int rc = gemm_store(Nm + r1 * ld + r0, ld, T, s1, Ym + r1 * ld + r1, ld, s1, s2, s2)) return rc;
+      k_transpose<<<dim3((unsigned)((s1 + 31) / 32), (unsigned)((s2 + 31) / 32)), 256, 0, s>>>(
+          Nm + r1 * ld + r0, ld, Ym + r0 * ld + r1, ld, s1, s2);
+      GBEM_LAUNCH_CHECK(ctx);
+    }
+  const long long nt = (mb + 63) / 64;
+  gbem_gemm::k_syrk_bulk<16, 3, 4, true, true><<<(unsigned)(nt * (nt + 1) / 2), 128, gbem_sk::SkBulk::SMEM, s>>>(
+      out, mb, Nm, ld, (int)mb, (int)ld, 0, 0, nullptr);
+  GBEM_LAUNCH_CHECK(ctx);
+  const unsigned n32 = (unsigned)((mb + 31) / 32);
+  k_mirror_lower<<<dim3(n32, n32), 256, 0, s>>>(out, mb, (int)mb);
+  GBEM_LAUNCH_CHECK(ctx);
+  return GBEM_OK;
+}
+
+// C_z = A * B^T split over `S` slices of Ktot (Kp rows of C handled in 64-row chunks)
+int gemm_nt(gbem_ctx* ctx, double* C, long long ldc, long long strideC, const double* A, long long lda,
+            const double* B, long long ldb, int M, int N, long long Ktot, int S) {
+  static_assert(kSmem <= 227 * 1024, "smem");
+  if (int rc = ensure_gemm_attrs(ctx)) return rc;
   static const bool use_bulk = getenv("GBEM_PCG_CPASYNC") == nullptr;
   long long kchunk = (Ktot + S - 1) / S;
   kchunk = (kchunk + BK - 1) / BK * BK;
@@ -520,7 +624,14 @@ int pcg_extract(gbem_ctx* ctx, const gbem_panels* P, bool device_panels, int64_t
   if (rc) return rc;
   long long mbmax = 0;
   for (int b = 0; b < nb; ++b) mbmax = std::max(mbmax, cut[b + 1] - cut[b]);
-  rc = grow(ctx, &w->tmp, &w->cap_tmp, (size_t)std::max<long long>(mbmax * mbmax, 1));
+  // GEMM-form inverse (N, Y, T: 2.25 ld^2 doubles) unless the block is too large for its workspace
+  static const bool inv_solve_env = getenv("GBEM_PCG_INVERSE_BY_SOLVE") != nullptr;
+  const long long ldi = (mbmax + 15) / 16 * 16;
+  const bool inv_gemm = !inv_solve_env && mbmax >= 2 * kInvNB && mbmax <= 36000;
+  if (inv_gemm)
+    rc = grow(ctx, &w->inv, &w->cap_inv, (size_t)(2 * ldi * ldi + ldi * ldi / 4 + ldi * kInvNB));
+  else
+    rc = grow(ctx, &w->tmp, &w->cap_tmp, (size_t)std::max<long long>(mbmax * mbmax, 1));
   if (rc) return rc;
   for (int b = 0; b < nb; ++b) {
     const long long c0 = cut[b], mb = cut[b + 1] - cut[b];
@@ -531,6 +642,15 @@ int pcg_extract(gbem_ctx* ctx, const gbem_panels* P, bool device_panels, int64_t
                                      sizeof(double) * mA, sizeof(double) * mb, mb, cudaMemcpyDeviceToDevice, s));
     rc = gbem_internal_factor(ctx, nullptr);
     if (rc) return rc;
+    if (inv_gemm && mb >= 2 * kInvNB) {
+      rc = block_inverse_gemm(ctx, w->inv, mb, w->minv + moff[b]);
+      if (rc) return rc;
+      continue;
+    }
+    if (!w->tmp || w->cap_tmp < (size_t)(mb * mb)) {
+      rc = grow(ctx, &w->tmp, &w->cap_tmp, (size_t)std::max<long long>(mb * mb, 1));
+      if (rc) return rc;
+    }
     k_identity<<<(unsigned)std::min<long long>((mb * mb + 255) / 256, 65535), 256, 0, s>>>(w->tmp, mb);
     GBEM_LAUNCH_CHECK(ctx);
     rc = gbem_internal_solve_factored(ctx, w->tmp, mb, w->minv + moff[b], nullptr, nullptr);
