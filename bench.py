@@ -512,7 +512,7 @@ def run_sharded(args):
             "config": sharded_config(world, n4, K4, n5),
             "e2e": r4["e2e"], "gpu_launches": r4["gpu_launches"], "clocks": clk.summary(),
             "config4_pcg": r4, "config5_assembly": r5,
-            "roofline": {"bound": "tensor", "kernel": "k_gemm_nt_sk (row-block product A_r P, split-K DMMA)",
+            "roofline": {"bound": "tensor", "kernel": "k_gemm_nt_sk_bulk (row-block product A_r P, split-K DMMA, bulk-copy staged)",
                          "achieved": r4["matvec"]["tflops"], "peak": _peaks().get("fp64_dmma_tflops", 37.09),
                          "unit": "TFLOP/s", "frac": r4["matvec"]["frac_dmma"], "traffic": None,
                          "algorithmic": "2 rows n K flop per product / device time of one product"}}

@@ -154,15 +154,20 @@ using SkBulk = BulkShape<kBulkBKS, kBulkNST>;
 static __global__ void __launch_bounds__(128, 4)
     k_gemm_nt_sk_bulk(double* __restrict__ C, long long ldc, long long strideC, const double* __restrict__ A,
                       long long lda, const double* __restrict__ B, long long ldb, int M, int N, long long Ktot,
-                      long long kchunk) {
+                      long long kchunk, int tri = 0) {
+  // tri (single-slice products of the block inverse): 1 = A is upper triangular (A(i, k) = 0 for
+  // k < i: the tile's reduction starts at its first row), 2 = B is lower triangular (B(j, k) = 0
+  // for k > j: it ends with the tile's last row)
   using S = SkBulk;
   constexpr int BKS = kBulkBKS, NST = kBulkNST, T = 64;
   extern __shared__ __align__(16) double smem[];
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NST * 2 * S::SLAB);
   unsigned long long* empty = full + NST;
   const int m0 = blockIdx.x * T, n0 = blockIdx.y * T;
-  const long long kbeg = (long long)blockIdx.z * kchunk;
-  const long long kend = min(Ktot, kbeg + kchunk);
+  long long kbeg = (long long)blockIdx.z * kchunk;
+  long long kend = min(Ktot, kbeg + kchunk);
+  if (tri == 1) kbeg = max(kbeg, (long long)m0);
+  if (tri == 2) kend = min(kend, (long long)n0 + T);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;
   const int g = lane >> 2, t4 = lane & 3;

@@ -299,7 +299,7 @@ __global__ void k_identity(double* I, long long m) {
 // the 2.3 n^3 of two dense triangular solves against the identity):
 //   N = -inv(L)^T (upper) and Y = N^T (lower) are built bottom-up over groups of 128-row blocks,
 //   [[L11, 0], [L21, L22]] -> N12 = N11 L21^T N22 (two NT GEMMs: T = N11 L21^T, N12 = T Y22^T; the
-//   signs cancel), Y21 = N12^T; the 128 x 128 base blocks come from the factorisation's own
+//   signs cancel; each skips the zero half of its triangular operand), Y21 = N12^T; the 128 x 128 base blocks come from the factorisation's own
 //   inverses of its diagonal blocks; then inv(M) = N N^T (k_syrk_bulk<TRI_STORE>, the reduction of a
 //   tile starting at its first non-zero column) and a mirror into the upper triangle.
 constexpr int kInvNB = 128;
@@ -451,10 +451,10 @@ int block_inverse_gemm(gbem_ctx* ctx, double* ws, long long mb, double* out) {
   k_inv_base<<<nblk, 256, 0, s>>>(ctx->d_linv, (int)mb, Nm, Ym, ld);
   GBEM_LAUNCH_CHECK(ctx);
   auto gemm_store = [&](double* C, long long ldc, const double* A, long long lda, const double* B, long long ldb, int M,
-                        int N, int K) -> int {
+                        int N, int K, int tri) -> int {
     const long long kchunk = ((long long)K + BK - 1) / BK * BK;
     dim3 grid((unsigned)((M + kT - 1) / kT), (unsigned)((N + kT - 1) / kT), 1);
-    k_gemm_nt_sk_bulk<<<grid, 128, gbem_sk::SkBulk::SMEM, s>>>(C, ldc, 0, A, lda, B, ldb, M, N, K, kchunk);
+    k_gemm_nt_sk_bulk<<<grid, 128, gbem_sk::SkBulk::SMEM, s>>>(C, ldc, 0, A, lda, B, ldb, M, N, K, kchunk, tri);
     GBEM_LAUNCH_CHECK(ctx);
     return GBEM_OK;
   };
@@ -465,8 +465,8 @@ int block_inverse_gemm(gbem_ctx* ctx, double* ws, long long mb, double* out) {
       const long long r2 = std::min<long long>((long long)(g + 2 * len) * kInvNB, mb);
       const int s1 = (int)(r1 - r0), s2 = (int)(r2 - r1);
       // T = N11 L21^T (s1 x s2), then N12 = T Y22^T, then Y21 = N12^T
-      if (int rc = gemm_store(T, s1, Nm + r0 * ld + r0, ld, ctx->d_A + r0 * lda + r1, lda, s1, s2, s1)) return rc;
-      if (int rc = gemm_store(Nm + r1 * ld + r0, ld, T, s1, Ym + r1 * ld + r1, ld, s1, s2, s2)) return rc;
+      if (int rc = gemm_store(T, s1, Nm + r0 * ld + r0, ld, ctx->d_A + r0 * lda + r1, lda, s1, s2, s1, 1)) return rc;
+      if (int rc = gemm_store(Nm + r1 * ld + r0, ld, T, s1, Ym + r1 * ld + r1, ld, s1, s2, s2, 2)) return rc;
       k_transpose<<<dim3((unsigned)((s1 + 31) / 32), (unsigned)((s2 + 31) / 32)), 256, 0, s>>>(
           Nm + r1 * ld + r0, ld, Ym + r0 * ld + r1, ld, s1, s2);
       GBEM_LAUNCH_CHECK(ctx);
