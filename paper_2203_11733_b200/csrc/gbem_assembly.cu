@@ -1491,6 +1491,24 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
     GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_near_fork, ctx->stream));
     GBEM_CUDA(ctx, cudaStreamWaitEvent(ns, ctx->ev_near_fork, 0));
   }
+  // The ~75 far-field kernels of a chunk (one per inner-list descriptor / size) write disjoint
+  // entries; most are small, and run one after the other each pays its launch gap and the tail
+  // where its last CTAs drain.  Dealt round robin over four streams the tails fill with the next
+  // kernels' CTAs.
+  static const int far_nstreams = getenv("GBEM_FAR_STREAMS") ? std::max(1, std::min(1 + gbem_ctx::kFarStreams, atoi(getenv("GBEM_FAR_STREAMS")))) : 1 + gbem_ctx::kFarStreams;
+  const int nfs = overlap ? far_nstreams : 1;
+  cudaStream_t fs[1 + gbem_ctx::kFarStreams];
+  fs[0] = ctx->stream;
+  for (int k = 1; k < nfs; ++k) {
+    if (!ctx->far_stream[k - 1]) {
+      GBEM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->far_stream[k - 1], cudaStreamNonBlocking));
+      GBEM_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_far_join[k - 1], cudaEventDisableTiming));
+    }
+    fs[k] = ctx->far_stream[k - 1];
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(fs[k], ctx->ev_near_fork, 0));
+  }
+  int far_rr = 0;
+#define GBEM_FS (fs[far_rr++ % nfs])
   static const int near_skip = getenv("GBEM_DBG_SKIP_NEAR") ? atoi(getenv("GBEM_DBG_SKIP_NEAR")) : 0;  // timing experiments
   auto near_kernels = [&]() -> int {
     if (near_skip == 3) return GBEM_OK;
@@ -1515,7 +1533,7 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
   }
   cudaEventRecord(ctx->ev[2], ctx->stream);
 #define GBEM_FAR(M) \
-  k_far<M><<<sms * 4, far_threads(M), 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan, \
+  k_far<M><<<sms * 4, far_threads(M), 0, GBEM_FS>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan, \
                                                                      ctx->d_offsets, o, ctx->d_stats); \
   GBEM_LAUNCH_CHECK(ctx);
   GBEM_FAR(1) GBEM_FAR(2) GBEM_FAR(3) GBEM_FAR(4) GBEM_FAR(5) GBEM_FAR(6) GBEM_FAR(7) GBEM_FAR(8)
@@ -1523,14 +1541,19 @@ int run_eval(gbem_ctx* ctx, const OutSpec& o, const gbem_quad_config& cfg, float
   GBEM_FAR(17) GBEM_FAR(18) GBEM_FAR(19) GBEM_FAR(20) GBEM_FAR(21) GBEM_FAR(22) GBEM_FAR(23) GBEM_FAR(24)
 #undef GBEM_FAR
 #define GBEM_FAST(D, TYPE, Q1, Q2)                                                                                \
-  k_far_orth<TYPE, Q1, Q2><<<sms * GBEM_FAST_MINB, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan, \
+  k_far_orth<TYPE, Q1, Q2><<<sms * GBEM_FAST_MINB, 128, 0, GBEM_FS>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan, \
                                                                          ctx->d_offsets, o, ctx->d_stats, D);      \
   GBEM_LAUNCH_CHECK(ctx);                                                                                         \
-  k_far_par<TYPE, Q1, Q2><<<sms * GBEM_FAST_MINB, 128, 0, ctx->stream>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan,  \
+  k_far_par<TYPE, Q1, Q2><<<sms * GBEM_FAST_MINB, 128, 0, GBEM_FS>>>(ctx->d_panels, ctx->d_queue, ctx->d_plan,  \
                                                                         ctx->d_offsets, o, ctx->d_stats, D);       \
   GBEM_LAUNCH_CHECK(ctx);
   GBEM_FAST_DESCS(GBEM_FAST)
 #undef GBEM_FAST
+#undef GBEM_FS
+  for (int k = 1; k < nfs; ++k) {
+    GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_far_join[k - 1], fs[k]));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_far_join[k - 1], 0));
+  }
   cudaEventRecord(ctx->ev[3], ctx->stream);
   if (overlap) {
     GBEM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_near_join, 0));

@@ -207,6 +207,10 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   if (ctx->near_stream) cudaStreamDestroy(ctx->near_stream);
   if (ctx->ev_near_fork) cudaEventDestroy(ctx->ev_near_fork);
   if (ctx->ev_near_join) cudaEventDestroy(ctx->ev_near_join);
+  for (int k = 0; k < gbem_ctx::kFarStreams; ++k) {
+    if (ctx->far_stream[k]) cudaStreamDestroy(ctx->far_stream[k]);
+    if (ctx->ev_far_join[k]) cudaEventDestroy(ctx->ev_far_join[k]);
+  }
   if (ctx->ev_panel) cudaEventDestroy(ctx->ev_panel);
   for (auto& e : ctx->ev_bw)
     if (e) cudaEventDestroy(e);

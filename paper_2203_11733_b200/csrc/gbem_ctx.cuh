@@ -81,6 +81,10 @@ struct gbem_ctx {
   // near-field kernels of an assembly chunk run beside its far-field kernels (gbem_assembly.cu run_eval)
   cudaStream_t near_stream = nullptr;
   cudaEvent_t ev_near_fork = nullptr, ev_near_join = nullptr;
+  // the far-field kernels of a chunk are dealt over the caller's stream and these (their tails overlap)
+  static constexpr int kFarStreams = 3;
+  cudaStream_t far_stream[kFarStreams] = {};
+  cudaEvent_t ev_far_join[kFarStreams] = {};
   cudaEvent_t ev_bw[5] = {};  // look-ahead backward substitution: start, step done, bulk done x 3
   // its captured sweep (cudaGraphExec_t), valid for one (matrix, factor, work, output, shape) tuple
   struct BwdGraphKey {
