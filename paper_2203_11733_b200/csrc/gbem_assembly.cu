@@ -1736,30 +1736,74 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
     }
     GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_romb_cnt, 0, sizeof(uint32_t) * 2, ctx->stream));
   }
+  // Classification of chunk t + 1 runs on its own stream, into a second queue / plan / offsets set,
+  // while chunk t is evaluated: the classifier is integer / FP32 issue-bound, the far field FP64-pipe
+  // bound, and its CTAs fit beside the far-field kernels' as those drain.  Per-phase timing
+  // (stats) keeps the phases one after the other.
+  static const bool pipeline_env = getenv("GBEM_NO_CLASSIFY_PIPELINE") == nullptr;
+  const long long nchunks = (total_tiles + tiles_per_chunk - 1) / tiles_per_chunk;
+  const bool pipelined = !timing && pipeline_env && nchunks >= 2;
+  uint64_t* qbuf[2] = {ctx->d_queue, ctx->d_queue};
+  uint32_t* pbuf[2] = {ctx->d_plan, ctx->d_plan};
+  uint32_t* obuf[2] = {ctx->d_offsets, ctx->d_offsets};
+  cudaStream_t cs = ctx->stream;
+  if (pipelined) {
+    rc = grow(ctx, (void**)&ctx->d_queue2, sizeof(uint64_t) * (size_t)ctx->queue_cap, &ctx->queue2_cap, sizeof(uint64_t));
+    if (rc) return rc;
+    rc = grow(ctx, (void**)&ctx->d_plan2, sizeof(uint32_t) * (size_t)ctx->queue_cap, &ctx->plan2_cap, sizeof(uint32_t));
+    if (rc) return rc;
+    if (!ctx->d_offsets2) GBEM_CUDA(ctx, cudaMalloc(&ctx->d_offsets2, sizeof(uint32_t) * (kNumKeys + 1)));
+    if (!ctx->cls_stream) {
+      GBEM_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cls_stream, cudaStreamNonBlocking));
+      for (cudaEvent_t& e : ctx->ev_cls) GBEM_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    qbuf[1] = ctx->d_queue2;
+    pbuf[1] = ctx->d_plan2;
+    obuf[1] = ctx->d_offsets2;
+    cs = ctx->cls_stream;
+    GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_cls[0], ctx->stream));
+    GBEM_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_cls[0], 0));
+  }
   cudaEventRecord(ctx->ev[0], ctx->stream);
-  for (long long t0 = 0; t0 < total_tiles; t0 += tiles_per_chunk) {
+  long long chunk = 0;
+  for (long long t0 = 0; t0 < total_tiles; t0 += tiles_per_chunk, ++chunk) {
     long long nt = std::min(tiles_per_chunk, total_tiles - t0);
-    cudaEventRecord(ctx->ev[5], ctx->stream);
-    GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, ctx->stream));
-    k_classify<false><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
+    const int b = pipelined ? (int)(chunk & 1) : 0;
+    if (pipelined && chunk >= 2)  // the evaluation of chunk - 2 has finished with this buffer set
+      GBEM_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_cls[3 + b], 0));
+    cudaEventRecord(ctx->ev[5], cs);
+    GBEM_CUDA(ctx, cudaMemsetAsync(ctx->d_counts, 0, sizeof(uint32_t) * kNumKeys, cs));
+    k_classify<false><<<(unsigned)nt, kClassifyThreads, 0, cs>>>(
         (const CPanel*)ctx->d_cinfo, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
-        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, ctx->d_plan, ctx->d_kp, full_rows ? 1 : 0);
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, qbuf[b], pbuf[b], ctx->d_kp, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
-    k_scan<<<1, 1024, 0, ctx->stream>>>(ctx->d_counts, ctx->d_offsets, ctx->d_cursors, ctx->d_stats);
+    k_scan<<<1, 1024, 0, cs>>>(ctx->d_counts, obuf[b], ctx->d_cursors, ctx->d_stats);
     GBEM_LAUNCH_CHECK(ctx);
-    k_classify<true><<<(unsigned)nt, kClassifyThreads, 0, ctx->stream>>>(
+    k_classify<true><<<(unsigned)nt, kClassifyThreads, 0, cs>>>(
         (const CPanel*)ctx->d_cinfo, (int)n, (int)row_begin, (int)row_end, bi0, nbt, d_rowoff, nrows_t, t0,
-        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, ctx->d_queue, ctx->d_plan, ctx->d_kp, full_rows ? 1 : 0);
+        cfg.near_ratio, ctx->d_counts, ctx->d_cursors, qbuf[b], pbuf[b], ctx->d_kp, full_rows ? 1 : 0);
     GBEM_LAUNCH_CHECK(ctx);
-    cudaEventRecord(ctx->ev[6], ctx->stream);
+    cudaEventRecord(ctx->ev[6], cs);
     if (timing) {
       GBEM_CUDA(ctx, cudaEventSynchronize(ctx->ev[6]));
       float a = 0;
       cudaEventElapsedTime(&a, ctx->ev[5], ctx->ev[6]);
       ms_cls += a;
     }
+    if (pipelined) {
+      GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_cls[1 + b], cs));
+      GBEM_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, ctx->ev_cls[1 + b], 0));
+    }
+    // the evaluation kernels take their queue from the context: point it at this chunk's set
+    ctx->d_queue = qbuf[b];
+    ctx->d_plan = pbuf[b];
+    ctx->d_offsets = obuf[b];
     rc = run_eval(ctx, o, cfg, timing ? &ms_far : nullptr, timing ? &ms_near : nullptr, defer_romberg);
+    ctx->d_queue = qbuf[0];
+    ctx->d_plan = pbuf[0];
+    ctx->d_offsets = obuf[0];
     if (rc) return rc;
+    if (pipelined) GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_cls[3 + b], ctx->stream));
   }
   if (defer_romberg) {  // the near-contact pairs of every chunk, one warp each
     cudaEventRecord(ctx->ev[2], ctx->stream);

@@ -195,6 +195,12 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   cudaFree(ctx->d_band_done);
   cudaFree(ctx->d_kp);
   cudaFree(ctx->d_romb);
+  cudaFree(ctx->d_queue2);
+  cudaFree(ctx->d_plan2);
+  cudaFree(ctx->d_offsets2);
+  if (ctx->cls_stream) cudaStreamDestroy(ctx->cls_stream);
+  for (cudaEvent_t e : ctx->ev_cls)
+    if (e) cudaEventDestroy(e);
   cudaFree(ctx->d_romb_cnt);
   cudaFree(ctx->d_rhs);
   cudaFree(ctx->d_linv);

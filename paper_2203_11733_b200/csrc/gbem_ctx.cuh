@@ -50,6 +50,14 @@ struct gbem_ctx {
   int64_t plan_cap = 0;
   uint64_t* d_kp = nullptr;  // (key, plan) per pair in tile order between the two classification passes
   int64_t kp_cap = 0;
+  // second queue / plan / offsets set: chunk t + 1 is classified (on cls_stream) while chunk t is evaluated
+  uint64_t* d_queue2 = nullptr;
+  int64_t queue2_cap = 0;
+  uint32_t* d_plan2 = nullptr;
+  int64_t plan2_cap = 0;
+  uint32_t* d_offsets2 = nullptr;
+  cudaStream_t cls_stream = nullptr;
+  cudaEvent_t ev_cls[5] = {};  // fork, classified[2], evaluated[2]
   // near-contact (Romberg-route) pairs collected over the chunks of one assembly and evaluated
   // together at its end: entries, then {count, taken from the current chunk}
   uint64_t* d_romb = nullptr;
