@@ -375,7 +375,7 @@ def sharded_extract_steps(ctx, P, net, K, eps, warmup, steps, world, jacobi_rows
     def step():
         ctx.check(ctx.lib.gbem_pcg_extract_cmatrix_dev(ctx.h, C.byref(panels), n, C.c_void_p(d_net.data_ptr()), K,
                                                        eps, C.byref(cfg), C.byref(opt), C.c_void_p(d_C.data_ptr()),
-                                                       C.c_void_p(d_res.data_ptr()), None, C.byref(ast), C.byref(pst)))
+                                                       C.c_void_p(d_res.data_ptr()), None, None, C.byref(pst)))
 
     for _ in range(warmup):
         step()

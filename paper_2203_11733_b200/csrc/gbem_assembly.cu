@@ -1701,6 +1701,8 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
   rowoff[(size_t)nrows_t] = total_tiles;
   // queue capacity: 2^27 entries (1 GiB) or what the problem needs
   long long need = std::min<long long>(total_tiles * kTile * kTile, 1ll << 27);
+  // test hook: a small queue splits a small problem into many chunks (tests/test_gpu_assembly.py)
+  if (const char* e = getenv("GBEM_QUEUE_CAP")) need = std::min<long long>(need, std::max<long long>(kTile * kTile, atoll(e)));
   rc = grow(ctx, (void**)&ctx->d_queue, sizeof(uint64_t) * (size_t)need, &ctx->queue_cap, sizeof(uint64_t));
   if (rc) return rc;
   rc = grow(ctx, (void**)&ctx->d_plan, sizeof(uint32_t) * (size_t)ctx->queue_cap, &ctx->plan_cap, sizeof(uint32_t));
@@ -1725,7 +1727,8 @@ int gbem_internal_assemble(gbem_ctx* ctx, int64_t n, int64_t row_begin, int64_t 
     o.lda = 1;
     o.ldc = (long long)ld_out;
   }
-  const long long tiles_per_chunk = std::max<long long>(1, ctx->queue_cap / (kTile * kTile));
+  const long long tiles_per_chunk =
+      std::max<long long>(1, (getenv("GBEM_QUEUE_CAP") ? need : (long long)ctx->queue_cap) / (kTile * kTile));
   float ms_cls = 0, ms_far = 0, ms_near = 0;
   bool timing = stats != nullptr;
   static const bool defer_romberg = getenv("GBEM_NO_ROMBERG_DEFER") == nullptr;
