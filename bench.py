@@ -154,7 +154,9 @@ def extract_config(config: int, n: int, K: int, eps: float, seed: int) -> dict:
     """The `config` object of the N = 1 extraction line (identical in both arms)."""
     return {"workload": f"config{config}: {m_name(config)}", "panels": n, "unique_entries": n * (n + 1) // 2,
             "nets": K, "eps_r": eps, "seed": seed,
-            "l2": f"working set {n * n * 8 / 1e9:.2f} GB matrix > 126 MB L2 (no flush needed)",
+            "l2": (f"working set {n * n * 8 / 1e9:.2f} GB matrix > 126 MB L2 (no flush needed)" if n * n * 8 > 126e6
+                   else f"working set {n * n * 8 / 1e6:.1f} MB matrix fits the 126 MB L2 and is not flushed "
+                        "(a secondary config, not the headline)"),
             "parallelism": "single"}
 
 
@@ -624,6 +626,51 @@ def cpu_baseline(P, n, K, budget_s=20.0):
             "extrapolated_step_s": d["extrapolated_step_s"]}
 
 
+def run_reference_full(args, P, n, K, cfgd):
+    """A config small enough for the CPU (config 1, the reference's own runnable case): every step is
+    the COMPLETE reference step, nothing sampled or extrapolated -- all n(n+1)/2 entries through the
+    reference u_pair_integral on all host threads (assemble_single, assembly.hpp:82-104), then the
+    reference Cholesky loop (solver.hpp:28-37, column-major) on that matrix, one thread as in the
+    reference.  The step count is capped so the run stays within a few minutes."""
+    O, which, kind = _ref_libs()
+    threads = os.cpu_count() or 1
+    lib = O.orc()
+    f = lib.orc_cholesky_factor_colmajor
+    f.restype = C.c_int
+    f.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
+    times = []
+    steps = max(1, min(args.steps, 12))
+    warm = min(args.warmup, 1)
+    for s in range(warm + steps):
+        t0 = time.perf_counter()
+        A, _, st = O.assemble(which, P, nthreads=threads)
+        t1 = time.perf_counter()
+        Af = np.asfortranarray(A)
+        L = np.empty((n, n))
+        piv = C.c_int64(-1)
+        t2 = time.perf_counter()
+        rc = f(n, Af.ctypes.data, L.ctypes.data, C.byref(piv))
+        t3 = time.perf_counter()
+        assert st == 0 and rc == 0, (st, rc, piv.value)
+        if s >= warm:
+            times.append(((t1 - t0) + (t3 - t2), t1 - t0, t3 - t2))
+    step_s = float(np.mean([t[0] for t in times]))
+    value = n * (n + 1) / 2 / step_s
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1,
+            "steps": steps, "warmup": warm, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE config geometry)", "config": cfgd,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": f"the complete step, measured: all {n * (n + 1) // 2} entries through the "
+                                       f"reference u_pair_integral on {threads} threads "
+                                       f"({np.mean([t[1] for t in times]):.2f} s) + the reference Cholesky loop at "
+                                       f"n={n} on one thread ({np.mean([t[2] for t in times]):.2f} s); nothing "
+                                       "sampled or extrapolated"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
@@ -636,6 +683,8 @@ def run_reference(args):
         P, net, K, eps, seed = serialized_workload(args.config)
         n = len(P)
         cfgd = extract_config(args.config, n, K, eps, seed)
+    if world == 1 and args.workload != "sharded" and n <= 2000:
+        return run_reference_full(args, P, n, K, cfgd)
     per = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     vals = []
     for s in range(args.warmup + args.steps):
