@@ -1927,8 +1927,9 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
       if (b > 0 && cudaEventElapsedTime(&x, pe[6 * (b - 1) + 3], pe[6 * b]) == cudaSuccess) gap += x;
     }
     cudaGetLastError();
-    fprintf(stderr, "[factor profile] n=%d blocks=%d mode=%s side=%.3f ms band-update=%.3f ms "
-            "band->next-potrf gap=%.3f ms\n", n, nblk, green ? "green" : "streams", side, band, gap);
+    fprintf(stderr, "[factor profile] n=%d blocks=%d mode=%s (SM partition %d + %d) side=%.3f ms band-update=%.3f ms "
+            "band->next-potrf gap=%.3f ms\n", n, nblk, green ? "green" : "streams", green ? ctx->green_side_sms : 0,
+            green ? ctx->num_sms - ctx->green_side_sms : ctx->num_sms, side, band, gap);
     if (green) {
       // per super-block on lo (us): idle wait for the chain's last trsm, then the combined
       // band + rest update; potrf includes its spin on the band counter
