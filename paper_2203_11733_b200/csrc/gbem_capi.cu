@@ -223,9 +223,10 @@ void gbem_ctx_destroy(gbem_ctx* ctx) {
   if (ctx->bw_graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)ctx->bw_graph_exec);
   if (ctx->ev_col) cudaEventDestroy(ctx->ev_col);
   if (ctx->g_side) cudaStreamDestroy(ctx->g_side);
+  if (ctx->g_side_lo) cudaStreamDestroy(ctx->g_side_lo);
   if (ctx->g_main) cudaStreamDestroy(ctx->g_main);
   if (ctx->g_main_hi) cudaStreamDestroy(ctx->g_main_hi);
-  for (cudaEvent_t e : {ctx->ev_gs, ctx->ev_ge, ctx->ev_gt, ctx->ev_gra})
+  for (cudaEvent_t e : {ctx->ev_gs, ctx->ev_ge, ctx->ev_gt, ctx->ev_gra, ctx->ev_side_pre, ctx->ev_side_done})
     if (e) cudaEventDestroy(e);
   if (ctx->green_ctx[0] || ctx->green_ctx[1]) {
     PFN_cuGreenCtxDestroy p_destroy = nullptr;

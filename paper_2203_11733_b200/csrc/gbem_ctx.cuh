@@ -114,6 +114,8 @@ struct gbem_ctx {
   int green_state = 0;
   int green_side_sms = 0;
   cudaStream_t g_main = nullptr, g_main_hi = nullptr, g_side = nullptr;
+  cudaStream_t g_side_lo = nullptr;  // low-priority stream of the side partition: a share of the large updates
+  cudaEvent_t ev_side_pre = nullptr, ev_side_done = nullptr;
   cudaEvent_t ev_gs = nullptr, ev_ge = nullptr, ev_gt = nullptr, ev_gra = nullptr;
   void* green_ctx[2] = {nullptr, nullptr};  // CUgreenCtx (side, main)
 

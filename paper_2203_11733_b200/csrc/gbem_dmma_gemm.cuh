@@ -290,7 +290,7 @@ __device__ __forceinline__ void lower_tile_strips(long long t, int X, int& r, in
 template <int TBM, int TBN, int WMW, int WNW, int NSTG, int MINB>
 __global__ void __launch_bounds__(32 * WMW * WNW, MINB)
     k_syrk_gen(double* C, long long ldc, const double* A, long long lda, int M, int K, int split, int band,
-               unsigned* band_done = nullptr) {
+               unsigned* band_done = nullptr, long long /* t_off: k_syrk_bulk's signature */ = 0) {
   static_assert(TBM == TBN, "square tiles");
   using S = GenShape<TBM, TBN, WMW, WNW, NSTG>;
   extern __shared__ __align__(16) double smem[];
@@ -485,7 +485,7 @@ struct BulkShape {
 template <int BKS, int NST, int MINB, bool SPLIT = false, bool TRI_STORE = false>
 __global__ void __launch_bounds__(128, MINB)
     k_syrk_bulk(double* C, long long ldc, const double* A, long long lda, int M, int K, int split, int band,
-                unsigned* band_done = nullptr) {
+                unsigned* band_done = nullptr, long long t_off = 0) {
   using S = BulkShape<BKS, NST>;
   constexpr int T = S::T;
   extern __shared__ __align__(16) double smem[];
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(128, MINB)
   unsigned long long* empty = full + NST;
   int tm, tn;
   bool signal = false;
-  long long t = blockIdx.x;
+  long long t = blockIdx.x + t_off;  // t_off: this launch covers tiles [t_off, t_off + gridDim.x) of the enumeration
   if (band < 0) {
     const int nt = (M + T - 1) / T;
     if (t < (long long)nt * -band) {

@@ -1522,7 +1522,10 @@ static int init_green(gbem_ctx* ctx) {
   if (p_stream(&sm, g_main, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return ctx->green_state;
   CUstream sh;
   if (p_stream(&sh, g_main, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS) return ctx->green_state;
+  CUstream sl;
+  if (p_stream(&sl, g_side, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS) return ctx->green_state;
   ctx->g_side = (cudaStream_t)ss;
+  ctx->g_side_lo = (cudaStream_t)sl;
   ctx->g_main = (cudaStream_t)sm;
   ctx->g_main_hi = (cudaStream_t)sh;
   ctx->green_ctx[0] = (void*)g_side;
@@ -1531,7 +1534,9 @@ static int init_green(gbem_ctx* ctx) {
   if (cudaEventCreateWithFlags(&ctx->ev_gs, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_ge, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&ctx->ev_gt, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&ctx->ev_gra, cudaEventDisableTiming) != cudaSuccess)
+      cudaEventCreateWithFlags(&ctx->ev_gra, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_side_pre, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&ctx->ev_side_done, cudaEventDisableTiming) != cudaSuccess)
     return ctx->green_state;
   ctx->green_state = 1;
   return ctx->green_state;
@@ -1829,8 +1834,31 @@ int gbem_internal_factor(gbem_ctx* ctx, gbem_solve_stats* stats) {
             (long long)nt * bw + (nt > kBand2 ? (long long)(nt - kBand2) * (nt - kBand2 + 1) / 2 : 0);
         double* A21 = ctx->d_A + (long long)k0 * lda + k0 + kw;
         double* A22 = ctx->d_A + (long long)(k0 + kw) * lda + (k0 + kw);
-        launch_update(ctx, dim3((unsigned)tiles), false, lo, A22, lda, A21, lda, m, kw, 0, -bw, ctx->d_band_done);
+        // Experiment (off by default, GBEM_SIDE_SHARE=fraction): the 2 SMs reserved for the diagonal
+        // factor idle most of the time, so while the update is long against the chain (m >= 12,000,
+        // K >= 1,024) the last `side_share` of its tiles (far from the band) can run on them at low
+        // priority.  Measured on config 3: 0.006 -> factor 371.2 -> 369.6 ms, 0.009 -> 380.5 ms,
+        // 0.012 -> 500 ms: the diagonal factor does not get ahead of the share's queued CTAs, so as
+        // soon as the share outlasts the chain's slack the chain becomes the critical path.
+        static const double side_share = getenv("GBEM_SIDE_SHARE") ? atof(getenv("GBEM_SIDE_SHARE")) : 0.0;
+        long long t_side = 0;
+        if (side_share > 0 && ctx->g_side_lo && m >= 12000 && kw >= 1024 && kw % 16 == 0 && lda % 2 == 0 &&
+            ((m & 1) == 0 || k0 + kw + m < lda) && getenv("GBEM_UPDATE_CPASYNC") == nullptr)
+          t_side = std::min<long long>((long long)(side_share * (double)tiles), tiles - (long long)nt * bw - 1);
+        if (t_side > 0) {
+          GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_side_pre, lo));  // after evT and the previous update
+          GBEM_CUDA(ctx, cudaStreamWaitEvent(ctx->g_side_lo, ctx->ev_side_pre, 0));
+          kUpdateBulk<<<(unsigned)t_side, BulkUpd::THREADS, BulkUpd::SMEM, ctx->g_side_lo>>>(
+              A22, lda, A21, lda, m, kw, 0, -bw, ctx->d_band_done, tiles - t_side);
+          GBEM_LAUNCH_CHECK(ctx);
+          GBEM_CUDA(ctx, cudaEventRecord(ctx->ev_side_done, ctx->g_side_lo));
+        } else {
+          t_side = 0;
+        }
+        launch_update(ctx, dim3((unsigned)(tiles - t_side)), false, lo, A22, lda, A21, lda, m, kw, 0, -bw,
+                      ctx->d_band_done);
         GBEM_LAUNCH_CHECK(ctx);
+        if (t_side > 0) GBEM_CUDA(ctx, cudaStreamWaitEvent(lo, ctx->ev_side_done, 0));
         band_target += (unsigned)(nt * bw);
         if (!next_tail) {
           rc2 = stepA(next, nb_next, band_target);

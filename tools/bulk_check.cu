@@ -25,13 +25,13 @@ int run(KB kb, size_t smem_b, int m, int k, int lda, int reps, const char* name)
   cudaFuncSetAttribute(k_syrk_gen<64, 64, 2, 2, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GenShape<64, 64, 2, 2, 2>::SMEM);
   cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
   fill<<<(unsigned)(((long long)lda * m + 255) / 256), 256>>>(C1, (long long)lda * m, 1);
-  k_syrk_gen<64, 64, 2, 2, 2, 4><<<tiles, 128, GenShape<64, 64, 2, 2, 2>::SMEM>>>(C1, lda, A, lda, m, k, 0, 0, nullptr);
+  k_syrk_gen<64, 64, 2, 2, 2, 4><<<tiles, 128, GenShape<64, 64, 2, 2, 2>::SMEM>>>(C1, lda, A, lda, m, k, 0, 0, nullptr, 0LL);
   std::vector<double> h1((size_t)lda * m), h2((size_t)lda * m);
   cudaMemcpy(h1.data(), C1, sizeof(double) * h1.size(), cudaMemcpyDeviceToHost);
   int bad_total = 0;
   for (int rep = 0; rep < reps; ++rep) {
     fill<<<(unsigned)(((long long)lda * m + 255) / 256), 256>>>(C2, (long long)lda * m, 1);
-    kb<<<tiles, 128, smem_b>>>(C2, lda, A, lda, m, k, 0, 0, nullptr);
+    kb<<<tiles, 128, smem_b>>>(C2, lda, A, lda, m, k, 0, 0, nullptr, 0LL);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("%s m=%d k=%d: %s\n", name, m, k, cudaGetErrorString(e)); return 1; }
     cudaMemcpy(h2.data(), C2, sizeof(double) * h2.size(), cudaMemcpyDeviceToHost);

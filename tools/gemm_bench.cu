@@ -66,7 +66,7 @@ int main(int argc, char** argv) {
     long long nb = (long long)(TBM / TBN) * ntr * (ntr + 1) / 2;
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0);
-      for (int it = 0; it < 10; ++it) kern<<<(unsigned)nb, threads, smem>>>(C, ldc, A, m, m, k, 0, 0, nullptr);
+      for (int it = 0; it < 10; ++it) kern<<<(unsigned)nb, threads, smem>>>(C, ldc, A, m, m, k, 0, 0, nullptr, 0LL);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       cudaEventElapsedTime(&ms, e0, e1);
