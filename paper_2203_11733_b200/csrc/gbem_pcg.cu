@@ -516,6 +516,9 @@ int splits_for(gbem_ctx* ctx, long long tiles, long long Ktot) {
   tiles = std::max<long long>(1, tiles);
   const long long target = std::max<long long>(22 * slots / 10, 4 * tiles);
   long long s = (target + tiles - 1) / tiles;
+  // bulk-staged kernel, tools/pcg_gemm_bench.cu at Kp = 64, n = 96,200 (TFLOP/s at S = 4 / 7):
+  // 12,025 rows 29.9 / 34.7, 24,050 rows 32.4 / 35.0, 48,100 rows 34.5 / 35.5, 96,200 rows 35.6 / 35.6
+  if (tiles >= 150 && s < 7) s = 7;
   s = std::min<long long>(s, std::max<long long>(1, Ktot / 512));
   return (int)std::max<long long>(1, std::min<long long>(s, 8));
 }
